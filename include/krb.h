@@ -1,0 +1,169 @@
+/*
+ * krb.h -- C ABI of libkrb.so, the B200 (sm_100a) kernels behind the
+ * recycling-BiCGSTAB hot path of arXiv 1406.2831 ("krecycle").
+ *
+ * The reference (/root/reference/pkg) is pure Python; it has no C ABI.  Its
+ * native arithmetic lives in scipy/OpenBLAS calls made from solvers.py and
+ * recycling.py.  Each entry point below replaces one such call site (cited),
+ * or one whole loop of it.  The Python drop-in layer
+ * (paper_1406_2831_b200/) binds these with ctypes exactly like the stub in
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *   - every pointer named d_* is DEVICE memory (any allocator; torch in the
+ *     Python layer); h_* is host memory.
+ *   - dense n x k blocks are COLUMN-major with leading dimension ld >= n.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - all calls are asynchronous on `stream` unless stated otherwise and
+ *     return 0 on success, a negative KRB_E* code on failure; the message is
+ *     in krb_last_error() (thread-local).
+ *   - floating point: fp64 only.  Every reduction is evaluated in the fixed
+ *     "canonical" order documented in oracle/canon.c, so results are
+ *     bit-reproducible run to run and equal to the CPU oracle.
+ */
+#ifndef KRB_H
+#define KRB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KRB_OK 0
+#define KRB_EINVAL -1
+#define KRB_ECUDA -2
+#define KRB_ENOMEM -3
+#define KRB_ESTATE -4
+
+/* solver status codes (history.status strings of solvers.py:33-37) */
+#define KRB_RUNNING 0
+#define KRB_CONVERGED 1
+#define KRB_MAX_ITN 2
+#define KRB_BREAKDOWN_SERIOUS 3
+#define KRB_BREAKDOWN_OMEGA 4
+#define KRB_BREAKDOWN_SECOND_KIND 5
+
+int krb_abi_version(void);
+const char *krb_last_error(void);
+/* number of kernel launches issued by this library since load (counter) */
+int64_t krb_launch_count(void);
+
+/* ---------------------------------------------------------------- context */
+/* Owns scratch buffers, the CUDA-graph cache and the solver state block. */
+typedef struct krb_context krb_context;
+int krb_context_create(krb_context **out);
+int krb_context_destroy(krb_context *ctx);
+
+/* ----------------------------------------------------------------- matrix */
+/* Device sparse matrix.  Replaces SparseMatrix's scipy CSR
+ * (sparse.py:27-69); the transpose used by rmatvec (sparse.py:123-130) is
+ * built on the device, once, on first use.  The handle copies the CSR into
+ * its own storage and builds the SELL-32 variant when it is selected
+ * (format: 0 = auto, 1 = CSR, 2 = SELL-32). */
+typedef struct krb_matrix krb_matrix;
+int krb_matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
+                      const int64_t *d_row_ptr, const int32_t *d_col_idx,
+                      const double *d_values, int format, void *stream);
+/* Same, from int64 column indices (the reference's SparseMatrix dtype). */
+int krb_matrix_create_i64(krb_matrix **out, int64_t n, int64_t nnz,
+                          const int64_t *d_row_ptr, const int64_t *d_col_idx,
+                          const double *d_values, int format, void *stream);
+int krb_matrix_destroy(krb_matrix *A);
+/* n, nnz, chosen format, device bytes held (incl. transpose when built) */
+int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz,
+                    int *format, int64_t *bytes);
+
+/* y = A x  (SparseMatrix.matvec, sparse.py:117-121; scipy csr_matvec order:
+ * per-row sequential sum from 0.0, separate multiply and add) */
+int krb_spmv(const krb_matrix *A, const double *d_x, double *d_y,
+             void *stream);
+/* y = A^T x (SparseMatrix.rmatvec, sparse.py:123-130) */
+int krb_spmv_t(krb_matrix *A, const double *d_x, double *d_y, void *stream);
+/* Y[:,c] = A X[:,c] (or A^T X[:,c]) for c < ncols: _apply_columns
+ * (recycling.py:28-32).  Bit-identical to ncols separate SpMVs. */
+int krb_spmm(krb_matrix *A, int transpose, int64_t ncols, const double *d_X,
+             int64_t ldx, double *d_Y, int64_t ldy, void *stream);
+
+/* ------------------------------------------------- canonical primitives */
+/* *d_out = (x, y)        (np.vdot, solvers.py:308-352) */
+int krb_dot(krb_context *ctx, int64_t n, const double *d_x, const double *d_y,
+            double *d_out, void *stream);
+/* d_out[j] = (M[:,j], v), j < k      (R.Chat.conj().T @ v, solvers.py:306) */
+int krb_tdot(krb_context *ctx, int64_t n, int64_t k, const double *d_M,
+             int64_t ldm, const double *d_v, double *d_out, void *stream);
+/* d_out[i] = beta_i + sign * sum_j M[i,j] y[j]   with d_y on the device;
+ * sign = -1: v - C y (solvers.py:307), +1: x + U y (recycling.py:204);
+ * d_base may equal d_out; d_base == NULL means plain M y. */
+int krb_gemv(int64_t n, int64_t k, const double *d_M, int64_t ldm,
+             const double *d_y, const double *d_base, int sign, double *d_out,
+             void *stream);
+/* G[a*nc + c] = (X[:,a], Y[:,c])  (Wt^H AW, recycling.py:342-343) */
+int krb_gram(krb_context *ctx, int64_t n, int64_t na, int64_t nc,
+             const double *d_X, int64_t ldx, const double *d_Y, int64_t ldy,
+             double *d_G, void *stream);
+/* out[:,c] = X Z[:,c], Z an m x nc row-major device matrix
+ * (W @ Zr, recycling.py:365-368) */
+int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
+             const double *d_Z, double *d_out, int64_t ldo, void *stream);
+/* d_out[j] = ||X[:,j]||_2   (np.linalg.norm(X, axis=0), recycling.py:155) */
+int krb_colnorms(krb_context *ctx, int64_t n, int64_t k, const double *d_X,
+                 int64_t ldx, double *d_out, void *stream);
+/* X[:, j] *= 1/s[j] done as a division X[i,j] / s[j] (recycling.py:156,337) */
+int krb_colscale_div(int64_t n, int64_t k, double *d_X, int64_t ldx,
+                     const double *d_s, void *stream);
+/* numpy default_rng(seed).uniform(lo, hi, n), bit-identical: PCG64
+ * (XSL-RR) from the 128-bit (state, inc) that numpy seeds
+ * (solvers.py:111-113, 268-269). */
+int krb_uniform_pcg64(int64_t n, uint64_t state_hi, uint64_t state_lo,
+                      uint64_t inc_hi, uint64_t inc_lo, double lo, double hi,
+                      double *d_out, void *stream);
+
+/* ------------------------------------------------------------ recycle space */
+/* View of a biorthonormalized recycle space (RecycleSpace,
+ * recycling.py:35-77); all blocks n x k column-major with leading dim ld. */
+typedef struct krb_space_view {
+  int64_t n, k, ld;
+  const double *U, *Ut, *C, *Ct, *Chat, *Ccheck;
+} krb_space_view;
+
+/* --------------------------------------------------------------- solvers */
+typedef struct krb_solve_config {
+  double tol;            /* relative tolerance on ||r|| / ||b||           */
+  double breakdown_tol;  /* SolverConfig.breakdown_tol                    */
+  int64_t max_itn;
+  /* shadow residual: d_shadow (device, n) if non-NULL, else drawn on the
+   * device from these PCG64 words (numpy default_rng(seed) state)          */
+  const double *d_shadow;
+  uint64_t pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo;
+  int use_graph;         /* 1: CUDA graph with device-side while loop      */
+} krb_solve_config;
+
+typedef struct krb_solve_result {
+  int32_t status;        /* KRB_CONVERGED ...                              */
+  int64_t hist_len;      /* entries in resid/matvecs/stamps                */
+  int64_t matvecs;       /* total counted products                         */
+  double rhs_norm;
+  double final_true_resid;
+  uint64_t t_start_ns;   /* device %globaltimer at setup                   */
+} krb_solve_result;
+
+/* rbicgstab_solve (solvers.py:245-361), bicgstab_solve when R == NULL or
+ * R->k == 0 (solvers.py:156-242, identical arithmetic).  Synchronous: returns
+ * after the solve; d_x_out receives x - U xc; history arrays (device, length
+ * >= max_itn + 2) receive ||r_i||, cumulative matvecs and device ns stamps. */
+int krb_rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
+                  const double *d_x_init, const krb_space_view *R,
+                  const krb_solve_config *cfg, double *d_x_out,
+                  double *d_hist_resid, int64_t *d_hist_matvecs,
+                  uint64_t *d_hist_stamp, krb_solve_result *h_result,
+                  void *stream);
+
+/* Per-iteration device scalars of the last solve (debug/tests): alpha,
+ * omega, rho, beta written to h_out[0..3]. */
+int krb_last_scalars(krb_context *ctx, double *h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRB_H */

@@ -1,0 +1,29 @@
+"""paper_1406_2831_b200 — B200-native recycling BiCGSTAB hot path.
+
+Drop-in for the solver / recycle-space names of krecycle
+(/root/reference/pkg/src/krecycle/__init__.py:33-52) that lie on the hot path
+(SURVEY.md §8): the arithmetic runs in libkrb.so (hand-written sm_100a CUDA,
+C ABI in include/krb.h).  Everything else in the reference (CLI, ILUTP,
+Matrix Market I/O, problem generators, bi-Lanczos harness) is out of scope.
+"""
+
+from .operators import CountingOperator, as_operator
+from .recycling import (CapturedCycle, RecycleSpace, biorthonormalize,
+                        project_initial, refresh_images)
+from .solvers import (BREAKDOWN_OMEGA, BREAKDOWN_SECOND_KIND,
+                      BREAKDOWN_SERIOUS, CONVERGED, MAX_ITN,
+                      ConvergenceHistory, SolverConfig, bicgstab_solve,
+                      rbicgstab_solve)
+from .sparse import SparseMatrix
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CountingOperator", "as_operator",
+    "CapturedCycle", "RecycleSpace", "biorthonormalize", "project_initial",
+    "refresh_images",
+    "ConvergenceHistory", "SolverConfig", "bicgstab_solve", "rbicgstab_solve",
+    "CONVERGED", "MAX_ITN", "BREAKDOWN_SERIOUS", "BREAKDOWN_OMEGA",
+    "BREAKDOWN_SECOND_KIND",
+    "SparseMatrix",
+]

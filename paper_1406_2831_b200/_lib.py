@@ -1,0 +1,142 @@
+"""ctypes binding of libkrb.so (include/krb.h).
+
+This is the only place the product touches native code.  It fails loudly:
+there is no CPU fallback — if the shared library is missing or no CUDA device
+is present, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkrb.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_int = ctypes.c_int
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+KRB_STATUS = {
+    1: "converged",
+    2: "max_itn",
+    3: "breakdown:serious",
+    4: "breakdown:omega",
+    5: "breakdown:second_kind",
+}
+
+
+class KrbError(RuntimeError):
+    pass
+
+
+class SpaceView(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("k", c_i64), ("ld", c_i64),
+                ("U", c_vp), ("Ut", c_vp), ("C", c_vp), ("Ct", c_vp),
+                ("Chat", c_vp), ("Ccheck", c_vp)]
+
+
+class SolveConfig(ctypes.Structure):
+    _fields_ = [("tol", c_dbl), ("breakdown_tol", c_dbl), ("max_itn", c_i64),
+                ("d_shadow", c_vp),
+                ("pcg_state_hi", c_u64), ("pcg_state_lo", c_u64),
+                ("pcg_inc_hi", c_u64), ("pcg_inc_lo", c_u64),
+                ("use_graph", c_int)]
+
+
+class SolveResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("hist_len", c_i64),
+                ("matvecs", c_i64), ("rhs_norm", c_dbl),
+                ("final_true_resid", c_dbl), ("t_start_ns", c_u64)]
+
+
+# name -> (restype, argtypes); every symbol declared in include/krb.h
+SIGNATURES = {
+    "krb_abi_version": (c_int, []),
+    "krb_last_error": (ctypes.c_char_p, []),
+    "krb_launch_count": (c_i64, []),
+    "krb_context_create": (c_int, [ctypes.POINTER(c_vp)]),
+    "krb_context_destroy": (c_int, [c_vp]),
+    "krb_matrix_create": (c_int, [ctypes.POINTER(c_vp), c_i64, c_i64, c_vp,
+                                  c_vp, c_vp, c_int, c_vp]),
+    "krb_matrix_create_i64": (c_int, [ctypes.POINTER(c_vp), c_i64, c_i64,
+                                      c_vp, c_vp, c_vp, c_int, c_vp]),
+    "krb_matrix_destroy": (c_int, [c_vp]),
+    "krb_matrix_info": (c_int, [c_vp, ctypes.POINTER(c_i64),
+                                ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
+                                ctypes.POINTER(c_i64)]),
+    "krb_spmv": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "krb_spmv_t": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "krb_spmm": (c_int, [c_vp, c_int, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "krb_dot": (c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "krb_tdot": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "krb_gemv": (c_int, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_int, c_vp,
+                         c_vp]),
+    "krb_gram": (c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                         c_vp, c_vp]),
+    "krb_gemm": (c_int, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64,
+                         c_vp]),
+    "krb_colnorms": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "krb_colscale_div": (c_int, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "krb_uniform_pcg64": (c_int, [c_i64, c_u64, c_u64, c_u64, c_u64, c_dbl,
+                                  c_dbl, c_vp, c_vp]),
+    "krb_rbicgstab": (c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(SpaceView),
+                              ctypes.POINTER(SolveConfig), c_vp, c_vp, c_vp,
+                              c_vp, ctypes.POINTER(SolveResult), c_vp]),
+    "krb_last_scalars": (c_int, [c_vp, ctypes.POINTER(c_dbl)]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile libkrb.so in-tree with nvcc for sm_100a (make in csrc/)."""
+    cmd = ["make", "-s", "-C", CSRC, "-j8"]
+    if force:
+        subprocess.run(["make", "-s", "-C", CSRC, "clean"], check=True)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def load(path: str | None = None):
+    """Load libkrb.so and bind every exported symbol (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise KrbError(
+                f"{p} is missing: build it with `python -c 'import __graft_entry__ "
+                "as g; g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+        lib = ctypes.CDLL(p)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str = ""):
+    if rc != 0:
+        msg = load().krb_last_error()
+        raise KrbError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+
+
+def call(name: str, *args):
+    """Call an entry point and raise KrbError on a non-zero return."""
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc
+
+
+def launch_count() -> int:
+    return int(load().krb_launch_count())

@@ -1,0 +1,51 @@
+// Library-level C ABI: version, thread-local error string, launch counter,
+// context lifetime.
+#include <cstdarg>
+#include <cstdio>
+
+#include "ctx.cuh"
+
+namespace krb {
+
+static thread_local char g_err[1024] = "";
+static int64_t g_launches = 0;
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int64_t &launch_counter() { return g_launches; }
+
+}  // namespace krb
+
+extern "C" {
+
+int krb_abi_version(void) { return 1; }
+
+const char *krb_last_error(void) { return krb::g_err; }
+
+int64_t krb_launch_count(void) { return krb::g_launches; }
+
+int krb_context_create(krb_context **out) {
+  KRB_REQUIRE(out != nullptr, "krb_context_create: out is NULL");
+  *out = new krb_context();
+  return KRB_OK;
+}
+
+int krb_context_destroy(krb_context *ctx) {
+  if (!ctx) return KRB_OK;
+  ctx->graph.reset();
+  double *bufs[] = {ctx->part, ctx->x, ctx->r, ctx->p, ctx->q, ctx->s,
+                    ctx->t, ctx->rt0, ctx->b, ctx->w, ctx->kbuf};
+  for (double *b : bufs)
+    if (b) cudaFree(b);
+  if (ctx->S) cudaFree(ctx->S);
+  if (ctx->counters) cudaFree(ctx->counters);
+  delete ctx;
+  return KRB_OK;
+}
+
+}  // extern "C"

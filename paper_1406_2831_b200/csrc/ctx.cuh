@@ -1,0 +1,83 @@
+// krb_context: scratch owned by the library (partials, solver vectors,
+// device scalar block, CUDA-graph cache).
+#pragma once
+
+#include "krb_internal.cuh"
+
+namespace krb {
+
+// Device-resident solver scalars (one block per context).
+struct SolveScalars {
+  double rho, alpha, omega, beta;
+  double den, qnorm, snorm, tt, ts, rnorm;
+  double bnorm, tol_abs, nrt0, breakdown_tol;
+  double final_true_resid, bb, rr_true;
+  int64_t itn;       // completed iterations
+  int64_t max_itn;
+  int64_t matvecs;   // counted products
+  int64_t hist_len;  // recorded history entries
+  uint64_t t_start;
+  int32_t status;
+  int32_t early;     // converged at the half step this iteration
+  int32_t k;
+  int32_t pad;
+};
+
+struct GraphCache {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  // key
+  const void *A = nullptr;
+  const void *C = nullptr, *Chat = nullptr;
+  int64_t n = -1, k = -1, ld = -1;
+  const double *hist_r = nullptr;
+  const int64_t *hist_m = nullptr;
+  const uint64_t *hist_t = nullptr;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    A = C = Chat = nullptr;
+    n = k = ld = -1;
+    hist_r = nullptr;
+    hist_m = nullptr;
+    hist_t = nullptr;
+  }
+};
+
+}  // namespace krb
+
+struct krb_context {
+  // generic partial buffer for canonical reductions
+  double *part = nullptr;
+  size_t part_cap = 0;  // doubles
+  unsigned int *counters = nullptr;  // 16 election counters
+  // solver state
+  krb::SolveScalars *S = nullptr;
+  int64_t vec_n = 0, vec_k = 0;
+  double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *s = nullptr,
+         *t = nullptr, *rt0 = nullptr, *b = nullptr, *w = nullptr;
+  double *kbuf = nullptr;  // zeta, gamma, xc, y  (4 x k)
+  krb::GraphCache graph;
+};
+
+namespace krb {
+int ctx_reserve_part(krb_context *ctx, size_t doubles);
+int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k);
+
+// canonical primitives used across translation units (stream-ordered)
+int launch_dot_partials(int64_t n, const double *x, const double *y,
+                        double *part, cudaStream_t st);
+int launch_final(int ndots, int64_t nb, const double *part, double *out,
+                 cudaStream_t st);
+int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
+                int64_t ldm, const double *v, bool self, double *out,
+                const int *status, cudaStream_t st);
+int launch_gemv(int64_t n, int64_t k, const double *M, int64_t ldm,
+                const double *y, const double *base, int sign, double *out,
+                cudaStream_t st);
+int spmv_launch(const krb_matrix *A, const double *x, double *y,
+                const int *d_status, cudaStream_t st);
+int ensure_transpose(krb_matrix *A, cudaStream_t st);
+}  // namespace krb

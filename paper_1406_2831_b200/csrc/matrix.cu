@@ -1,0 +1,425 @@
+// Device sparse matrices and SpMV for sm_100a.
+//
+// Replaces SparseMatrix.matvec / rmatvec (reference sparse.py:117-130), i.e.
+// scipy's csr_matvec: y_i = ((0 + a_i0 x_c0) + a_i1 x_c1) + ... in CSR order,
+// every product rounded before the add.  To stay bit-identical the GPU keeps
+// ONE thread per row walking its row in CSR order (no segmented or
+// warp-split sums, which would re-associate), and the library is compiled
+// with -fmad=false so the multiply and add are never contracted.
+//
+// Formats (chosen per matrix, krb_matrix_create(format=0)):
+//   SELL-32   32 consecutive rows form a slice stored column-major
+//             (element j of lane l at slice_ptr[s] + 32 j + l), so the 32
+//             threads of a warp read 32 consecutive doubles / int32 per step:
+//             fully coalesced 256 B + 128 B transactions.  Per-row lengths
+//             stop every thread at its own row end (padding is never summed).
+//   CSR       fallback when SELL padding would exceed 20% of nnz (power-law
+//             rows); same per-row order, loads served through L1.
+// The transpose (A^T, for rmatvec / two-sided RBiCG) is built on the device
+// once by a stable radix sort of the column indices, which reproduces
+// scipy's .transpose().tocsr() order (ascending original row within each
+// column), and gets its own format choice.
+#include <cub/cub.cuh>
+
+#include "krb_internal.cuh"
+
+
+namespace krb {
+
+__global__ void k_row_len(int64_t n, const int64_t *__restrict__ rp,
+                          int32_t *__restrict__ rlen) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rlen[i] = (int32_t)(rp[i + 1] - rp[i]);
+}
+
+// width of each 32-row slice = max row length (warp max)
+__global__ void k_slice_width(int64_t n, const int32_t *__restrict__ rlen,
+                              int64_t *__restrict__ width) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int v = i < n ? rlen[i] : 0;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+    v = max(v, __shfl_xor_sync(0xffffffffu, v, off));
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < (n + 31) / 32)
+    width[i >> 5] = 32 * (int64_t)v;
+}
+
+__global__ void k_sell_fill(int64_t n, const int64_t *__restrict__ rp,
+                            const int32_t *__restrict__ ci,
+                            const double *__restrict__ val,
+                            const int64_t *__restrict__ sl_ptr,
+                            int32_t *__restrict__ s_col,
+                            double *__restrict__ s_val) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t base = sl_ptr[i >> 5] + (i & 31);
+  int64_t b = rp[i], e = rp[i + 1];
+  for (int64_t jj = b; jj < e; ++jj) {
+    s_col[base + 32 * (jj - b)] = ci[jj];
+    s_val[base + 32 * (jj - b)] = val[jj];
+  }
+}
+
+__global__ void k_pad_fill(int64_t total, int32_t *s_col, double *s_val) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) {
+    s_col[i] = 0;
+    s_val[i] = 0.0;
+  }
+}
+
+// ---- SpMV kernels: one thread per row, CSR order, mul then add ----------
+template <bool kSell>
+__device__ __forceinline__ double row_dot(int64_t i, const krb_matrix &A,
+                                          const double *__restrict__ x) {
+  double sum = 0.0;
+  if (kSell) {
+    const int len = __ldg(A.rlen + i);
+    const int64_t base = __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
+    const int32_t *__restrict__ cp = A.s_col + base;
+    const double *__restrict__ vp = A.s_val + base;
+    int j = 0;
+    for (; j + 4 <= len; j += 4) {
+      int c0 = __ldg(cp + 32 * j), c1 = __ldg(cp + 32 * (j + 1));
+      int c2 = __ldg(cp + 32 * (j + 2)), c3 = __ldg(cp + 32 * (j + 3));
+      double v0 = __ldg(vp + 32 * j), v1 = __ldg(vp + 32 * (j + 1));
+      double v2 = __ldg(vp + 32 * (j + 2)), v3 = __ldg(vp + 32 * (j + 3));
+      double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2),
+             x3 = __ldg(x + c3);
+      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
+      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
+      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
+      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
+    }
+    for (; j < len; ++j)
+      sum = __dadd_rn(sum, __dmul_rn(__ldg(vp + 32 * j), __ldg(x + __ldg(cp + 32 * j))));
+  } else {
+    int64_t b = __ldg(A.rp + i), e = __ldg(A.rp + i + 1);
+    int64_t jj = b;
+    for (; jj + 4 <= e; jj += 4) {
+      int c0 = __ldg(A.ci + jj), c1 = __ldg(A.ci + jj + 1);
+      int c2 = __ldg(A.ci + jj + 2), c3 = __ldg(A.ci + jj + 3);
+      double v0 = __ldg(A.val + jj), v1 = __ldg(A.val + jj + 1);
+      double v2 = __ldg(A.val + jj + 2), v3 = __ldg(A.val + jj + 3);
+      double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2),
+             x3 = __ldg(x + c3);
+      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
+      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
+      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
+      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
+    }
+    for (; jj < e; ++jj)
+      sum = __dadd_rn(sum, __dmul_rn(__ldg(A.val + jj), __ldg(x + __ldg(A.ci + jj))));
+  }
+  return sum;
+}
+
+template <bool kSell>
+__global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
+                                              const double *__restrict__ x,
+                                              double *__restrict__ y,
+                                              const int *__restrict__ status) {
+  if (status && *status) return;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  y[i] = row_dot<kSell>(i, A, x);
+}
+
+int spmv_launch(const krb_matrix *A, const double *x, double *y,
+                const int *d_status, cudaStream_t st) {
+  if (A->n == 0) return KRB_OK;
+  int64_t blocks = (A->n + 255) / 256;
+  if (A->format == 2)
+    k_spmv<true><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
+  else
+    k_spmv<false><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+// ---- build ---------------------------------------------------------------
+__global__ void k_i64_to_i32(int64_t m, const int64_t *src, int32_t *dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) dst[i] = (int32_t)src[i];
+}
+
+static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
+  const int64_t n = A->n;
+  A->nslices = (n + 31) / 32;
+  int64_t *width = nullptr;
+  KRB_CHECK_CUDA(cudaMalloc(&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1)));
+  KRB_CHECK_CUDA(cudaMalloc(&width, sizeof(int64_t) * (A->nslices + 1)));
+  KRB_CHECK_CUDA(cudaMalloc(&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1)));
+  unsigned blocks = (unsigned)((n + 255) / 256);
+  if (n > 0) {
+    k_row_len<<<blocks, 256, 0, st>>>(n, A->rp, A->rlen);
+    KRB_CHECK_LAUNCH();
+    unsigned wblocks = (unsigned)((A->nslices * 32 + 255) / 256);
+    k_slice_width<<<wblocks, 256, 0, st>>>(n, A->rlen, width);
+    KRB_CHECK_LAUNCH();
+  }
+  KRB_CHECK_CUDA(cudaMemsetAsync(width + A->nslices, 0, sizeof(int64_t), st));
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr,
+                                A->nslices + 1, st);
+  KRB_CHECK_CUDA(cudaMalloc(&tmp, tmp_bytes));
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr,
+                                A->nslices + 1, st);
+  KRB_CHECK_CUDA(cudaGetLastError());
+  int64_t total = 0;
+  KRB_CHECK_CUDA(cudaMemcpyAsync(&total, A->sl_ptr + A->nslices,
+                                 sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  cudaFree(width);
+  A->sell_elems = total;
+  bool use_sell = format == 2 || (format == 0 && total <= A->nnz + A->nnz / 5);
+  if (!use_sell) {
+    cudaFree(A->sl_ptr);
+    A->sl_ptr = nullptr;
+    // keep rlen (4 B/row) - unused by CSR kernels, free it
+    cudaFree(A->rlen);
+    A->rlen = nullptr;
+    A->format = 1;
+    return KRB_OK;
+  }
+  KRB_CHECK_CUDA(cudaMalloc(&A->s_col, sizeof(int32_t) * (total > 0 ? total : 1)));
+  KRB_CHECK_CUDA(cudaMalloc(&A->s_val, sizeof(double) * (total > 0 ? total : 1)));
+  if (total > A->nnz) {
+    k_pad_fill<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(total, A->s_col, A->s_val);
+    KRB_CHECK_LAUNCH();
+  }
+  if (n > 0) {
+    k_sell_fill<<<blocks, 256, 0, st>>>(n, A->rp, A->ci, A->val, A->sl_ptr,
+                                        A->s_col, A->s_val);
+    KRB_CHECK_LAUNCH();
+  }
+  A->format = 2;
+  // the CSR copy is still needed to build the transpose; drop values/cols
+  // once the transpose exists (see ensure_transpose).
+  A->bytes += total * 12 + (A->nslices + 1) * 8 + n * 4;
+  return KRB_OK;
+}
+
+int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
+                  const int64_t *d_rp, const int32_t *d_ci32,
+                  const int64_t *d_ci64, const double *d_val, int format,
+                  cudaStream_t st) {
+  KRB_REQUIRE(out != nullptr, "krb_matrix_create: out is NULL");
+  KRB_REQUIRE(n >= 0 && nnz >= 0, "krb_matrix_create: negative size");
+  KRB_REQUIRE(nnz < ((int64_t)1 << 31), "krb_matrix_create: nnz >= 2^31");
+  KRB_REQUIRE(n < ((int64_t)1 << 31), "krb_matrix_create: n >= 2^31");
+  krb_matrix *A = new krb_matrix();
+  A->n = n;
+  A->nnz = nnz;
+  cudaError_t e = cudaMalloc(&A->rp, sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&A->ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&A->val, sizeof(double) * (nnz > 0 ? nnz : 1));
+  if (e != cudaSuccess) {
+    set_error("krb_matrix_create: %s", cudaGetErrorString(e));
+    cudaFree(A->rp); cudaFree(A->ci); cudaFree(A->val);
+    delete A;
+    return KRB_ENOMEM;
+  }
+  KRB_CHECK_CUDA(cudaMemcpyAsync(A->rp, d_rp, sizeof(int64_t) * (n + 1),
+                                 cudaMemcpyDeviceToDevice, st));
+  if (nnz > 0) {
+    if (d_ci32)
+      KRB_CHECK_CUDA(cudaMemcpyAsync(A->ci, d_ci32, sizeof(int32_t) * nnz,
+                                     cudaMemcpyDeviceToDevice, st));
+    else {
+      k_i64_to_i32<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, d_ci64, A->ci);
+      KRB_CHECK_LAUNCH();
+    }
+    KRB_CHECK_CUDA(cudaMemcpyAsync(A->val, d_val, sizeof(double) * nnz,
+                                   cudaMemcpyDeviceToDevice, st));
+  }
+  A->bytes = (n + 1) * 8 + nnz * 12;
+  int rc = build_sell(A, format, st);
+  if (rc != KRB_OK) {
+    delete A;
+    return rc;
+  }
+  *out = A;
+  return KRB_OK;
+}
+
+__global__ void k_entry_rows(int64_t n, const int64_t *__restrict__ rp,
+                             int32_t *__restrict__ rows) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int64_t jj = rp[i]; jj < rp[i + 1]; ++jj) rows[jj] = (int32_t)i;
+}
+
+__global__ void k_iota(int64_t m, int32_t *p) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) p[i] = (int32_t)i;
+}
+
+__global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ ci,
+                            int64_t *__restrict__ cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nnz) atomicAdd(reinterpret_cast<unsigned long long *>(cnt + ci[i]), 1ull);
+}
+
+__global__ void k_gather_t(int64_t nnz, const int32_t *__restrict__ perm,
+                           const int32_t *__restrict__ rows,
+                           const double *__restrict__ val,
+                           int32_t *__restrict__ tci, double *__restrict__ tval) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  int32_t p = perm[t];
+  tci[t] = rows[p];
+  tval[t] = val[p];
+}
+
+int ensure_transpose(krb_matrix *A, cudaStream_t st) {
+  if (A->T) return KRB_OK;
+  const int64_t n = A->n, nnz = A->nnz;
+  int32_t *rows = nullptr, *keys_out = nullptr, *perm_in = nullptr,
+          *perm_out = nullptr, *tci = nullptr;
+  int64_t *cnt = nullptr, *trp = nullptr;
+  double *tval = nullptr;
+  size_t m = nnz > 0 ? nnz : 1;
+  KRB_CHECK_CUDA(cudaMalloc(&rows, sizeof(int32_t) * m));
+  KRB_CHECK_CUDA(cudaMalloc(&keys_out, sizeof(int32_t) * m));
+  KRB_CHECK_CUDA(cudaMalloc(&perm_in, sizeof(int32_t) * m));
+  KRB_CHECK_CUDA(cudaMalloc(&perm_out, sizeof(int32_t) * m));
+  KRB_CHECK_CUDA(cudaMalloc(&cnt, sizeof(int64_t) * (n + 1)));
+  KRB_CHECK_CUDA(cudaMalloc(&trp, sizeof(int64_t) * (n + 1)));
+  KRB_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n + 1), st));
+  unsigned nb = (unsigned)((nnz + 255) / 256), rb = (unsigned)((n + 255) / 256);
+  if (n > 0) {
+    k_entry_rows<<<rb, 256, 0, st>>>(n, A->rp, rows);
+    KRB_CHECK_LAUNCH();
+  }
+  if (nnz > 0) {
+    k_iota<<<nb, 256, 0, st>>>(nnz, perm_in);
+    KRB_CHECK_LAUNCH();
+    k_col_count<<<nb, 256, 0, st>>>(nnz, A->ci, cnt);
+    KRB_CHECK_LAUNCH();
+  }
+  void *tmp = nullptr;
+  size_t tb1 = 0, tb2 = 0;
+  int end_bit = 1;
+  while (end_bit < 31 && ((int64_t)1 << end_bit) < n) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb1, A->ci, keys_out, perm_in,
+                                  perm_out, (int)nnz, 0, end_bit, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, trp, n + 1, st);
+  KRB_CHECK_CUDA(cudaMalloc(&tmp, tb1 > tb2 ? tb1 : tb2));
+  if (nnz > 0)
+    cub::DeviceRadixSort::SortPairs(tmp, tb1, A->ci, keys_out, perm_in,
+                                    perm_out, (int)nnz, 0, end_bit, st);
+  cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, trp, n + 1, st);
+  KRB_CHECK_CUDA(cudaGetLastError());
+  KRB_CHECK_CUDA(cudaMalloc(&tci, sizeof(int32_t) * m));
+  KRB_CHECK_CUDA(cudaMalloc(&tval, sizeof(double) * m));
+  if (nnz > 0) {
+    k_gather_t<<<nb, 256, 0, st>>>(nnz, perm_out, rows, A->val, tci, tval);
+    KRB_CHECK_LAUNCH();
+  }
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  cudaFree(rows);
+  cudaFree(keys_out);
+  cudaFree(perm_in);
+  cudaFree(perm_out);
+  cudaFree(cnt);
+  krb_matrix *T = nullptr;
+  int rc = matrix_create(&T, n, nnz, trp, tci, nullptr, tval, 0, st);
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  cudaFree(trp);
+  cudaFree(tci);
+  cudaFree(tval);
+  if (rc != KRB_OK) return rc;
+  A->T = T;
+  return KRB_OK;
+}
+
+void matrix_free(krb_matrix *A) {
+  if (!A) return;
+  matrix_free(A->T);
+  cudaFree(A->rp);
+  cudaFree(A->ci);
+  cudaFree(A->val);
+  cudaFree(A->sl_ptr);
+  cudaFree(A->rlen);
+  cudaFree(A->s_col);
+  cudaFree(A->s_val);
+  delete A;
+}
+
+}  // namespace krb
+
+using namespace krb;
+
+extern "C" {
+
+int krb_matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
+                      const int64_t *d_row_ptr, const int32_t *d_col_idx,
+                      const double *d_values, int format, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = matrix_create(out, n, nnz, d_row_ptr, d_col_idx, nullptr, d_values,
+                         format, st);
+  if (rc == KRB_OK) KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  return rc;
+}
+
+int krb_matrix_create_i64(krb_matrix **out, int64_t n, int64_t nnz,
+                          const int64_t *d_row_ptr, const int64_t *d_col_idx,
+                          const double *d_values, int format, void *stream) {
+  cudaStream_t st = as_stream(stream);
+  int rc = matrix_create(out, n, nnz, d_row_ptr, nullptr, d_col_idx, d_values,
+                         format, st);
+  if (rc == KRB_OK) KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  return rc;
+}
+
+int krb_matrix_destroy(krb_matrix *A) {
+  matrix_free(A);
+  return KRB_OK;
+}
+
+int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz, int *format,
+                    int64_t *bytes) {
+  KRB_REQUIRE(A != nullptr, "krb_matrix_info: NULL matrix");
+  if (n) *n = A->n;
+  if (nnz) *nnz = A->nnz;
+  if (format) *format = A->format;
+  if (bytes) *bytes = A->bytes + (A->T ? A->T->bytes : 0);
+  return KRB_OK;
+}
+
+int krb_spmv(const krb_matrix *A, const double *d_x, double *d_y,
+             void *stream) {
+  KRB_REQUIRE(A != nullptr, "krb_spmv: NULL matrix");
+  return spmv_launch(A, d_x, d_y, nullptr, as_stream(stream));
+}
+
+int krb_spmv_t(krb_matrix *A, const double *d_x, double *d_y, void *stream) {
+  KRB_REQUIRE(A != nullptr, "krb_spmv_t: NULL matrix");
+  int rc = ensure_transpose(A, as_stream(stream));
+  if (rc) return rc;
+  return spmv_launch(A->T, d_x, d_y, nullptr, as_stream(stream));
+}
+
+int krb_spmm(krb_matrix *A, int transpose, int64_t ncols, const double *d_X,
+             int64_t ldx, double *d_Y, int64_t ldy, void *stream) {
+  KRB_REQUIRE(A != nullptr, "krb_spmm: NULL matrix");
+  KRB_REQUIRE(ldx >= A->n && ldy >= A->n, "krb_spmm: leading dimension < n");
+  cudaStream_t st = as_stream(stream);
+  const krb_matrix *M = A;
+  if (transpose) {
+    int rc = ensure_transpose(A, st);
+    if (rc) return rc;
+    M = A->T;
+  }
+  for (int64_t c = 0; c < ncols; ++c) {
+    int rc = spmv_launch(M, d_X + c * ldx, d_Y + c * ldy, nullptr, st);
+    if (rc) return rc;
+  }
+  return KRB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+"""Device plumbing: the krb context, streams, device sparse matrices, and the
+host<->device moves of the drop-in API.  PyTorch supplies device memory and
+the current CUDA stream; every computation is a libkrb.so kernel."""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _lib
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise _lib.KrbError("no CUDA device: the B200 path has no CPU fallback")
+    _lib.load()
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(tensor):
+    return ctypes.c_void_p(tensor.data_ptr()) if tensor is not None else None
+
+
+class Context:
+    """One krb_context per process (scratch + graph cache)."""
+
+    _inst = None
+
+    def __init__(self):
+        require_cuda()
+        h = ctypes.c_void_p()
+        _lib.call("krb_context_create", ctypes.byref(h))
+        self.h = h
+        self._hist = None
+
+    @classmethod
+    def get(cls) -> "Context":
+        if cls._inst is None:
+            cls._inst = Context()
+        return cls._inst
+
+    def history_buffers(self, max_itn: int):
+        """Device history arrays reused across solves (so the cached CUDA
+        graph, which bakes their addresses, stays valid)."""
+        need = int(max_itn) + 2
+        if self._hist is None or self._hist[0].shape[0] < need:
+            t = torch()
+            cap = max(need, 1024)
+            self._hist = (t.empty(cap, dtype=t.float64, device="cuda"),
+                          t.empty(cap, dtype=t.int64, device="cuda"),
+                          t.empty(cap, dtype=t.int64, device="cuda"))
+        return self._hist
+
+
+def to_device(a: np.ndarray, dtype=np.float64):
+    """Host numpy -> device tensor (through pinned memory)."""
+    t = torch()
+    a = np.ascontiguousarray(a, dtype=dtype)
+    host = t.from_numpy(a)
+    if a.nbytes >= (1 << 20):
+        host = host.pin_memory()
+    return host.to("cuda", non_blocking=True)
+
+
+def to_host(tensor) -> np.ndarray:
+    return tensor.detach().to("cpu").numpy()
+
+
+class DeviceMatrix:
+    """A krb_matrix handle (device CSR / SELL-32 + lazily built transpose)."""
+
+    def __init__(self, n, row_ptr, col_idx, values, fmt: int = 0):
+        require_cuda()
+        t = torch()
+        self.n = int(n)
+        self.nnz = int(len(values))
+        row_ptr = np.asarray(row_ptr)
+        col_idx = np.asarray(col_idx)
+        values = np.asarray(values)
+        if np.iscomplexobj(values):
+            raise NotImplementedError("complex matrices are out of scope on the "
+                                      "device path (fp64 real only)")
+        d_rp = to_device(row_ptr, np.int64)
+        d_val = to_device(values, np.float64)
+        h = ctypes.c_void_p()
+        s = stream_ptr()
+        if col_idx.dtype == np.int32:
+            d_ci = to_device(col_idx, np.int32)
+            fn = "krb_matrix_create"
+        else:
+            d_ci = to_device(col_idx, np.int64)
+            fn = "krb_matrix_create_i64"
+        _lib.call(fn, ctypes.byref(h), self.n, self.nnz, ptr(d_rp), ptr(d_ci),
+                  ptr(d_val), int(fmt), s)
+        del d_rp, d_ci, d_val
+        self.h = h
+        self._finalizer = weakref.finalize(self, _destroy_matrix, h.value)
+        n_, nnz_, f_, b_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
+        _lib.call("krb_matrix_info", h, ctypes.byref(n_), ctypes.byref(nnz_),
+                  ctypes.byref(f_), ctypes.byref(b_))
+        self.format = {1: "csr", 2: "sell32"}.get(f_.value, "?")
+        self.device_bytes = b_.value
+
+    @property
+    def shape(self):
+        return (self.n, self.n)
+
+    def spmv(self, x_dev, y_dev=None, transpose=False):
+        t = torch()
+        if y_dev is None:
+            y_dev = t.empty(self.n, dtype=t.float64, device="cuda")
+        fn = "krb_spmv_t" if transpose else "krb_spmv"
+        _lib.call(fn, self.h, ptr(x_dev), ptr(y_dev), stream_ptr())
+        return y_dev
+
+    def spmm(self, X_dev, transpose=False, out=None):
+        """X_dev: (ncols, n) tensor = column-major n x ncols block."""
+        t = torch()
+        ncols = X_dev.shape[0]
+        if out is None:
+            out = t.empty((ncols, self.n), dtype=t.float64, device="cuda")
+        if ncols:
+            _lib.call("krb_spmm", self.h, 1 if transpose else 0, ncols,
+                      ptr(X_dev), X_dev.stride(0), ptr(out), out.stride(0),
+                      stream_ptr())
+        return out
+
+
+def _destroy_matrix(h):
+    try:
+        _lib.load().krb_matrix_destroy(ctypes.c_void_p(h))
+    except Exception:
+        pass
+
+
+class _MatrixCache:
+    """Device copies keyed on the identity of immutable host matrices (the
+    reference freezes SparseMatrix arrays, sparse.py:66-67).  A strong
+    reference pins each key object so ids cannot be recycled; LRU of 3."""
+
+    def __init__(self, cap=3):
+        self.cap = cap
+        self.items: OrderedDict = OrderedDict()
+
+    def get(self, obj, build):
+        key = id(obj)
+        hit = self.items.get(key)
+        if hit is not None and hit[0] is obj:
+            self.items.move_to_end(key)
+            return hit[1]
+        dev = build()
+        self.items[key] = (obj, dev)
+        self.items.move_to_end(key)
+        while len(self.items) > self.cap:
+            self.items.popitem(last=False)
+        return dev
+
+    def clear(self):
+        self.items.clear()
+
+
+MATRICES = _MatrixCache()
+
+
+def device_matrix(A) -> DeviceMatrix:
+    """Resolve any supported operator to its device matrix."""
+    if isinstance(A, DeviceMatrix):
+        return A
+    dev = getattr(A, "_device", None)
+    if isinstance(dev, DeviceMatrix):
+        return dev
+    inner = getattr(A, "inner", None)
+    if inner is not None and not hasattr(A, "row_ptr"):
+        return device_matrix(inner)
+    if hasattr(A, "row_ptr") and hasattr(A, "col_idx") and hasattr(A, "values"):
+        n = A.nrows if hasattr(A, "nrows") else A.n
+        ncols = A.ncols if hasattr(A, "ncols") else n
+        if n != ncols:
+            raise ValueError("solver requires a square operator")
+        return MATRICES.get(A, lambda: DeviceMatrix(n, A.row_ptr, A.col_idx,
+                                                    A.values))
+    if isinstance(A, np.ndarray):
+        if A.ndim != 2 or A.shape[0] != A.shape[1]:
+            raise ValueError("solver requires a square operator")
+        import scipy.sparse as sp
+        S = sp.csr_matrix(A)
+        S.sort_indices()
+        return MATRICES.get(A, lambda: DeviceMatrix(A.shape[0], S.indptr,
+                                                    S.indices, S.data))
+    raise NotImplementedError(
+        f"{type(A).__name__} has no CSR representation; the device path "
+        "supports SparseMatrix-like CSR operators only (no CPU fallback)")

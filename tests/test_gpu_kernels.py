@@ -1,0 +1,128 @@
+"""Kernel-level parity on the B200: every libkrb primitive against the CPU
+oracle (oracle/canon.c) — bit-exact — and against the reference's numpy/scipy
+results (golden fixtures) where the reference's order is reproducible."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_csr, gpu
+
+pytestmark = gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    from paper_1406_2831_b200 import device
+    device.require_cuda()
+    return device
+
+
+def _tensor(a):
+    from paper_1406_2831_b200.device import to_device
+    return to_device(a)
+
+
+def _cols(X):
+    """numpy n x k -> device (k, n)."""
+    return _tensor(np.ascontiguousarray(np.asarray(X).T))
+
+
+@pytest.mark.parametrize("name", ["dense40", "rand200", "c1s", "c4s"])
+def test_spmv_bitwise_vs_reference_golden(dev, golden, name):
+    p = f"spmv/{name}/"
+    csr = golden_csr(golden, p)
+    M = dev.DeviceMatrix(csr.n, csr.row_ptr, csr.col_idx, csr.values)
+    x = golden[p + "x"]
+    y = M.spmv(_tensor(x)).cpu().numpy()
+    yt = M.spmv(_tensor(x), transpose=True).cpu().numpy()
+    assert np.array_equal(y, golden[p + "Ax"])      # scipy csr_matvec, bitwise
+    assert np.array_equal(yt, golden[p + "AHx"])    # scipy rmatvec, bitwise
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("fmt", [0, 1, 2])
+def test_spmv_formats_bitwise(dev, canon, cfg, fmt):
+    from oracle.ops import CsrOperand
+    from paper_1406_2831_b200.workloads import make_sequence
+    A = make_sequence(cfg, small=True).matrix(1)
+    M = dev.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=fmt)
+    x = np.random.default_rng(3).standard_normal(A.n)
+    op = CsrOperand.of(A)
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), canon.matvec(op, x))
+    assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(),
+                          canon.rmatvec(op, x))
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), op._csr @ x)
+
+
+def test_spmv_empty_rows_and_tiny(dev):
+    import scipy.sparse as sp
+    from paper_1406_2831_b200.workloads import CSR
+    D = np.zeros((37, 37))
+    D[3, 5] = 2.0
+    D[36, 0] = -1.5
+    D[10, 10] = 4.0
+    S = sp.csr_matrix(D)
+    A = CSR(37, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data)
+    M = dev.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+    x = np.arange(37, dtype=np.float64) - 7.0
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), S @ x)
+    assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(),
+                          S.T.tocsr() @ x)
+
+
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 4096, 100_003, 700_001, 5_000_000])
+def test_dot_bitwise(dev, canon, n):
+    from paper_1406_2831_b200.recycling import dot
+    r = np.random.default_rng(n)
+    x = r.standard_normal(n)
+    y = r.standard_normal(n) * np.exp(r.uniform(-5, 5, n))
+    got = float(dot(_tensor(x), _tensor(y)).cpu().numpy()[0])
+    assert got == float(canon.dot(x, y))
+    assert abs(got - float(np.dot(x, y))) <= 1e-12 * np.abs(x * y).sum()
+
+
+@pytest.mark.parametrize("n,k", [(1000, 1), (4096, 10), (300_001, 20), (2_000_000, 30)])
+def test_projection_primitives_bitwise(dev, canon, n, k):
+    from paper_1406_2831_b200 import recycling as R
+    r = np.random.default_rng(k)
+    M = r.standard_normal((n, k))
+    v = r.standard_normal(n)
+    y = r.standard_normal(k)
+    Md = _cols(M)
+    assert np.array_equal(R.tdot(Md, _tensor(v)).cpu().numpy(), canon.tdot(M, v))
+    base = r.standard_normal(n)
+    got = R.gemv(Md, _tensor(y), base=_tensor(base), sign=-1).cpu().numpy()
+    assert np.array_equal(got, base - canon.gemv(M, y))
+    got = R.gemv(Md, _tensor(y), base=_tensor(base), sign=+1).cpu().numpy()
+    assert np.array_equal(got, base + canon.gemv(M, y))
+    assert np.array_equal(R.colnorms(Md).cpu().numpy(), canon.colnorms(M))
+
+
+@pytest.mark.parametrize("n,na,nc", [(500, 3, 4), (70_000, 20, 20), (1_000_000, 47, 47)])
+def test_gram_gemm_bitwise(dev, canon, n, na, nc):
+    from paper_1406_2831_b200 import recycling as R
+    r = np.random.default_rng(na)
+    X = r.standard_normal((n, na))
+    Y = r.standard_normal((n, nc))
+    G = R.gram(_cols(X), _cols(Y)).cpu().numpy()
+    assert np.array_equal(G, canon.gram(X, Y))
+    Z = r.standard_normal((na, 7))
+    out = R.gemm(_cols(X), Z).cpu().numpy().T
+    assert np.array_equal(out, canon.gemm(X, Z))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 7, 104729, 2**40 + 3])
+@pytest.mark.parametrize("n", [1, 1000, 1_234_567])
+def test_pcg64_matches_numpy(dev, seed, n):
+    import ctypes
+    import torch
+    from paper_1406_2831_b200 import _lib
+    from paper_1406_2831_b200.solvers import pcg64_words
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.call("krb_uniform_pcg64", n, *pcg64_words(seed), -1.0, 1.0,
+              ctypes.c_void_p(out.data_ptr()), dev.stream_ptr())
+    ref = np.random.default_rng(seed).uniform(-1.0, 1.0, size=n)
+    assert np.array_equal(out.cpu().numpy(), ref)

@@ -146,6 +146,8 @@ typedef struct krb_solve_result {
   double rhs_norm;
   double final_true_resid;
   uint64_t t_start_ns;   /* device %globaltimer at setup                   */
+  int64_t iterations_run;   /* loop-body executions (incl. no-op tail)     */
+  int64_t kernel_launches;  /* libkrb kernels executed by this solve       */
 } krb_solve_result;
 
 /* rbicgstab_solve (solvers.py:245-361), bicgstab_solve when R == NULL or

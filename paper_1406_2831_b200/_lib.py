@@ -52,7 +52,8 @@ class SolveConfig(ctypes.Structure):
 class SolveResult(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("hist_len", c_i64),
                 ("matvecs", c_i64), ("rhs_norm", c_dbl),
-                ("final_true_resid", c_dbl), ("t_start_ns", c_u64)]
+                ("final_true_resid", c_dbl), ("t_start_ns", c_u64),
+                ("iterations_run", c_i64), ("kernel_launches", c_i64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/krb.h

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(256) k_phase(IterArgs a) {
   constexpr int ND = ndots_of<PH>();
   const bool gated = (PH != PH_BNORM && PH != PH_INIT && PH != PH_TRUE &&
                       PH != PH_RINIT);
+  if (PH == PH_XR && blockIdx.x == 0 && threadIdx.x == 0) S->bodies += 1;
   if (PH == PH_EARLY) {
     if (S->early != 1) return;
   } else if (gated && S->status != KRB_RUNNING) {
@@ -396,7 +397,10 @@ static int build_graph(krb_context *ctx, const krb_matrix *A, IterArgs a,
   a.use_cond = 1;
   KRB_CHECK_CUDA(cudaStreamBeginCaptureToGraph(capture, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeRelaxed));
+  const int64_t c0 = launch_counter();
   int rc = launch_iteration(ctx, A, a, capture);
+  G.kernels_per_body = launch_counter() - c0;
+  launch_counter() = c0;  // captured, not executed: counted per body run
   cudaGraph_t out_body;
   cudaError_t e = cudaStreamEndCapture(capture, &out_body);
   if (rc) {
@@ -443,6 +447,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     KRB_REQUIRE(k <= 512, "recycle dimension > 512 unsupported");
   }
   KRB_TRY(ctx_reserve_vectors(ctx, n, k));
+  const int64_t l0 = launch_counter();
+  int64_t per_body = 0;
   const int64_t nb = canon_nblocks(n);
   KRB_TRY(ctx_reserve_part(ctx, (size_t)(3 * nb > k * nb ? 3 * nb : k * nb) + 64));
   if (!ctx->S) {
@@ -522,7 +528,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
       G.hist_r = hist_r; G.hist_m = hist_m; G.hist_t = hist_t;
     }
     KRB_CHECK_CUDA(cudaGraphLaunch(G.exec, st));
-    launch_counter()++;
+    per_body = G.kernels_per_body;
   } else {
     // host-driven loop, status polled every 8 iterations (kernels no-op once
     // the status leaves RUNNING, so the overshoot is harmless)
@@ -555,6 +561,9 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   res->rhs_norm = hs.bnorm;
   res->final_true_resid = hs.final_true_resid;
   res->t_start_ns = hs.t_start;
+  res->iterations_run = hs.bodies;
+  launch_counter() += hs.bodies * per_body;
+  res->kernel_launches = launch_counter() - l0;
   return KRB_OK;
 }
 

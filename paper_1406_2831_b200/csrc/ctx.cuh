@@ -17,6 +17,7 @@ struct SolveScalars {
   int64_t matvecs;   // counted products
   int64_t hist_len;  // recorded history entries
   uint64_t t_start;
+  int64_t bodies;    // graph-body (iteration) executions, incl. no-op tails
   int32_t status;
   int32_t early;     // converged at the half step this iteration
   int32_t k;
@@ -33,6 +34,7 @@ struct GraphCache {
   const double *hist_r = nullptr;
   const int64_t *hist_m = nullptr;
   const uint64_t *hist_t = nullptr;
+  int64_t kernels_per_body = 0;
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);

@@ -137,9 +137,10 @@ class DeviceMatrix:
         if out is None:
             out = t.empty((ncols, self.n), dtype=t.float64, device="cuda")
         if ncols:
+            ldx = X_dev.stride(0) if ncols > 1 else self.n
+            ldy = out.stride(0) if ncols > 1 else self.n
             _lib.call("krb_spmm", self.h, 1 if transpose else 0, ncols,
-                      ptr(X_dev), X_dev.stride(0), ptr(out), out.stride(0),
-                      stream_ptr())
+                      ptr(X_dev), ldx, ptr(out), ldy, stream_ptr())
         return out
 
 

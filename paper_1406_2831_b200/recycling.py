@@ -159,6 +159,12 @@ def _ctx():
     return Context.get().h
 
 
+def _ld(X):
+    """Leading dimension of a (k, n) block (torch reports stride 1 for a
+    size-1 leading dim)."""
+    return X.stride(0) if X.shape[0] > 1 else X.shape[1]
+
+
 def tdot(M_dev, v_dev, out=None):
     """out_j = (M[:, j], v): R.Chat.conj().T @ v (solvers.py:306)."""
     t = torch()
@@ -166,7 +172,7 @@ def tdot(M_dev, v_dev, out=None):
     if out is None:
         out = t.empty(k, dtype=t.float64, device="cuda")
     if k:
-        _lib.call("krb_tdot", _ctx(), n, k, ptr(M_dev), M_dev.stride(0),
+        _lib.call("krb_tdot", _ctx(), n, k, ptr(M_dev), _ld(M_dev),
                   ptr(v_dev), ptr(out), stream_ptr())
     return out
 
@@ -177,7 +183,7 @@ def gemv(M_dev, y_dev, base=None, sign=-1, out=None):
     k, n = M_dev.shape
     if out is None:
         out = t.empty(n, dtype=t.float64, device="cuda")
-    _lib.call("krb_gemv", n, k, ptr(M_dev), M_dev.stride(0) if k else n,
+    _lib.call("krb_gemv", n, k, ptr(M_dev), _ld(M_dev) if k else n,
               ptr(y_dev), ptr(base), int(sign), ptr(out), stream_ptr())
     return out
 
@@ -189,8 +195,8 @@ def gram(X_dev, Y_dev):
     nc = Y_dev.shape[0]
     G = t.empty((na, nc), dtype=t.float64, device="cuda")
     if na and nc:
-        _lib.call("krb_gram", _ctx(), n, na, nc, ptr(X_dev), X_dev.stride(0),
-                  ptr(Y_dev), Y_dev.stride(0), ptr(G), stream_ptr())
+        _lib.call("krb_gram", _ctx(), n, na, nc, ptr(X_dev), _ld(X_dev),
+                  ptr(Y_dev), _ld(Y_dev), ptr(G), stream_ptr())
     return G
 
 
@@ -203,8 +209,8 @@ def gemm(X_dev, Z):
     nc = Zd.shape[1]
     out = t.empty((nc, n), dtype=t.float64, device="cuda")
     if nc and n:
-        _lib.call("krb_gemm", n, m, nc, ptr(X_dev), X_dev.stride(0), ptr(Zd),
-                  ptr(out), out.stride(0), stream_ptr())
+        _lib.call("krb_gemm", n, m, nc, ptr(X_dev), _ld(X_dev), ptr(Zd),
+                  ptr(out), _ld(out), stream_ptr())
     return out
 
 
@@ -213,7 +219,7 @@ def colnorms(X_dev):
     k, n = X_dev.shape
     out = t.empty(k, dtype=t.float64, device="cuda")
     if k:
-        _lib.call("krb_colnorms", _ctx(), n, k, ptr(X_dev), X_dev.stride(0),
+        _lib.call("krb_colnorms", _ctx(), n, k, ptr(X_dev), _ld(X_dev),
                   ptr(out), stream_ptr())
     return out
 
@@ -221,7 +227,7 @@ def colnorms(X_dev):
 def colscale_div(X_dev, s_dev):
     k, n = X_dev.shape
     if k:
-        _lib.call("krb_colscale_div", n, k, ptr(X_dev), X_dev.stride(0),
+        _lib.call("krb_colscale_div", n, k, ptr(X_dev), _ld(X_dev),
                   ptr(s_dev), stream_ptr())
     return X_dev
 

@@ -118,19 +118,33 @@ _STATUS = {1: CONVERGED, 2: MAX_ITN, 3: BREAKDOWN_SERIOUS, 4: BREAKDOWN_OMEGA,
            5: BREAKDOWN_SECOND_KIND}
 
 
+LAST_SOLVE = {}   # launch accounting of the most recent solve (bench / tests)
+
+
 def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=1):
     M, b = _check_common(A, b, None, cfg)
+    bd = to_device(b.astype(np.float64, copy=False))
+    xd = None
+    if x_init is not None:
+        xd = to_device(np.asarray(x_init, dtype=np.float64))
+    xo, hist = solve_device(M, bd, xd, recycle, cfg, label, t0, use_graph)
+    _count(A, nm=LAST_SOLVE["matvecs"])
+    return xo.cpu().numpy(), hist
+
+
+def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
+                 use_graph=1):
+    """Device-resident entry: M a DeviceMatrix, bd / xd device tensors.
+    Returns (x device tensor, ConvergenceHistory)."""
     t = torch()
+    if t0 is None:
+        t0 = time.perf_counter()
     ctx = Context.get()
     R = None
     if recycle is not None and recycle.k > 0:
         R = RecycleSpace.of(recycle)
         if R.n != M.n:
             raise ValueError("recycle space dimension does not match the operator")
-    bd = to_device(b.astype(np.float64, copy=False))
-    xd = None
-    if x_init is not None:
-        xd = to_device(np.asarray(x_init, dtype=np.float64))
     xo = t.empty(M.n, dtype=t.float64, device="cuda")
     hr, hm, ht = ctx.history_buffers(cfg.max_itn)
     c = _lib.SolveConfig()
@@ -159,9 +173,10 @@ def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=1):
     hist.seconds = [base + (int(s) - st0) * 1e-9 for s in stamps]
     hist.status = _STATUS.get(int(res.status), f"unknown:{res.status}")
     hist.final_true_resid = float(res.final_true_resid)
-    _count(A, nm=int(res.matvecs))
-    x = xo.cpu().numpy()
-    return x, hist
+    LAST_SOLVE.clear()
+    LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
+                      kernel_launches=int(res.kernel_launches))
+    return xo, hist
 
 
 def bicgstab_solve(A, b, x_init=None, precond=None, config=None):

@@ -121,7 +121,7 @@ _STATUS = {1: CONVERGED, 2: MAX_ITN, 3: BREAKDOWN_SERIOUS, 4: BREAKDOWN_OMEGA,
 LAST_SOLVE = {}   # launch accounting of the most recent solve (bench / tests)
 
 
-def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=1):
+def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
     M, b = _check_common(A, b, None, cfg)
     bd = to_device(b.astype(np.float64, copy=False))
     xd = None
@@ -132,13 +132,24 @@ def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=1):
     return xo.cpu().numpy(), hist
 
 
+def _graph_mode():
+    """KRB_GRAPH_MODE=1 (default): one CUDA graph with a device-driven WHILE
+    node per solve; 0: host-launched iterations with a status poll every 8
+    (identical kernels and results; used for per-kernel ncu profiling, which
+    cannot see inside conditional graph nodes)."""
+    import os
+    return int(os.environ.get("KRB_GRAPH_MODE", "1"))
+
+
 def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
-                 use_graph=1):
+                 use_graph=None):
     """Device-resident entry: M a DeviceMatrix, bd / xd device tensors.
     Returns (x device tensor, ConvergenceHistory)."""
     t = torch()
     if t0 is None:
         t0 = time.perf_counter()
+    if use_graph is None:
+        use_graph = _graph_mode()
     ctx = Context.get()
     R = None
     if recycle is not None and recycle.k > 0:

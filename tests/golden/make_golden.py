@@ -187,11 +187,12 @@ def case_rbicgstab(out):
     out[p + "resid_exactdot"] = np.asarray(he.resid)
     # x_init path (one counted product)
     x0 = rng.standard_normal(300)
-    with threadpool_limits(1):
-        x2, h2 = K.rbicgstab_solve(RA, b, x_init=x0, recycle=space, config=cfg)
+    (x2, h2), _, (_, h2e) = _solver_pair(
+        lambda: K.rbicgstab_solve(RA, b, x_init=x0, recycle=space, config=cfg))
     out[p + "xinit"] = x0
     out[p + "xinit_x"] = x2
     hist_arrays(p + "xinit_", h2, out)
+    out[p + "xinit_resid_exactdot"] = np.asarray(h2e.resid)
 
 
 def case_generation(out):

@@ -42,7 +42,7 @@
 int64_t canon_E(int64_t n) {
   int64_t t = (n + (int64_t)CANON_LANES * CANON_TARGET_BLOCKS - 1) /
               ((int64_t)CANON_LANES * CANON_TARGET_BLOCKS);
-  int64_t E = 1;
+  int64_t E = 4;  /* >= 4 lanes-elements amortise the shuffle tree */
   while (E < t && E < 16) E *= 2;
   return E;
 }

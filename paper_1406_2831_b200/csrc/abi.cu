@@ -43,6 +43,7 @@ int krb_context_destroy(krb_context *ctx) {
   for (double *b : bufs)
     if (b) cudaFree(b);
   if (ctx->S) cudaFree(ctx->S);
+  if (ctx->desc) cudaFree(ctx->desc);
   if (ctx->counters) cudaFree(ctx->counters);
   delete ctx;
   return KRB_OK;

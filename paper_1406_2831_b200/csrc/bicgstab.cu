@@ -5,25 +5,31 @@
 // HBM-streaming phase kernels.  All scalar logic (alpha, omega, beta, rho,
 // breakdown and convergence predicates, history records) runs on the device
 // in the last CTA of the kernel that produced the reduction it needs, in
-// exactly the reference's order, so one iteration needs no host round trip.
+// exactly the reference's order, so an iteration needs no host round trip.
+//
 // The iteration is captured once into a CUDA graph whose WHILE conditional
 // node is re-armed by the device (cudaGraphSetConditional) until the status
 // leaves RUNNING: a whole solve is one graph launch plus one final readback.
+// Kernels read every per-solve pointer (matrix, recycle blocks) from a
+// descriptor in device memory, so one instantiated graph serves every solve of
+// the same shape (n, k, format) — e.g. all systems of a sequence.
 //
-// Per iteration (k > 0; the projection kernels vanish for k = 0):
-//   P  p = r + beta (p - omega q)                       stream 3 read, 1 write
-//   M  q = A p                                          SpMV
-//   Z  zeta = Chat^T q  (block partials + final)        n x k read
-//   Q  q -= C zeta ; (rt0,q), (q,q) -> den, alpha        n x k + 3 read, 1 write
-//   S  s = r - alpha q ; (s,s) -> half-step exit          2 read, 1 write
-//   E  early exit only: x += alpha p, xc += alpha zeta
-//   M  t = A s ; Z gamma = Chat^T t
-//   T  t -= C gamma ; (t,t), (t,s) -> omega              n x k + 2 read, 1 write
+// Per iteration (k > 0; Z vanishes and Q/T skip the update for k = 0):
+//   P  p = r + beta (p - omega q)                      3 read, 1 write
+//   M  q = A p                                         SpMV
+//   Z  zeta = Chat^T q  (column groups + last-CTA final)  n x k + n read
+//   Q  q -= C zeta ; (rt0,q), (q,q) -> den, alpha       n x k + 2 read, 1 write
+//   S  s = r - alpha q ; (s,s) -> half-step exit        2 read, 1 write
+//   M  t = A s ;  Z gamma = Chat^T t
+//   T  t -= C gamma ; (t,t), (t,s) -> omega             n x k + 2 read, 1 write
 //   X  x = x + alpha p + omega s ; r = s - omega t ;
-//      (r,r), (rt0,r) -> record, converge, rho, beta     5 read, 2 write
+//      (r,r), (rt0,r) -> record, converge, rho, beta    5 read, 2 write
+//      (on a half-step exit instead: x += alpha p, xc += alpha zeta)
 #include <cuda_runtime.h>
 
 #include "ctx.cuh"
+#include "spmv.cuh"
+#include "tdot.cuh"
 
 namespace krb {
 
@@ -31,7 +37,6 @@ enum Phase {
   PH_PUPDATE = 0,
   PH_PROJ_Q,
   PH_SUPD,
-  PH_EARLY,
   PH_PROJ_T,
   PH_XR,
   PH_BNORM,
@@ -41,8 +46,11 @@ enum Phase {
 };
 
 struct IterArgs {
+  krb_matrix A;  // copy of the matrix handle (device pointers)
   int64_t n, nb, ld;
   int k;
+  int use_cond;
+  cudaGraphConditionalHandle cond;
   const double *C, *Chat, *U;
   double *x, *r, *p, *q, *s, *t, *rt0, *b;
   double *zeta, *gamma, *xc;
@@ -52,8 +60,6 @@ struct IterArgs {
   double *hist_r;
   int64_t *hist_m;
   uint64_t *hist_t;
-  cudaGraphConditionalHandle cond;
-  int use_cond;
 };
 
 __device__ __forceinline__ void record(const IterArgs &a, double rn) {
@@ -65,22 +71,14 @@ __device__ __forceinline__ void record(const IterArgs &a, double rn) {
   S->hist_len = h + 1;
 }
 
-template <int PH>
-__host__ __device__ constexpr int ndots_of() {
-  switch (PH) {
-    case PH_PROJ_Q: return 2;
-    case PH_SUPD: return 1;
-    case PH_PROJ_T: return 2;
-    case PH_XR: return 2;
-    case PH_BNORM: return 1;
-    case PH_INIT: return 3;
-    case PH_TRUE: return 2;
-    default: return 0;
-  }
+__host__ __device__ constexpr int ndots_of(int PH) {
+  return PH == PH_PROJ_Q ? 2 : PH == PH_SUPD ? 1 : PH == PH_PROJ_T ? 2
+       : PH == PH_XR ? 2 : PH == PH_BNORM ? 1 : PH == PH_INIT ? 3
+       : PH == PH_TRUE ? 2 : 0;
 }
 
-// Scalar logic of each phase, executed by thread 0 of the last CTA after the
-// dot products d[] are final.  Mirrors solvers.py:298-356 line by line.
+// Scalar logic of each phase, executed by thread 0 of the last CTA once the
+// dot products d[] are final.  Mirrors solvers.py:288-356 line by line.
 template <int PH>
 __device__ void finalize(const IterArgs &a, const double *d) {
   SolveScalars *S = a.S;
@@ -105,12 +103,10 @@ __device__ void finalize(const IterArgs &a, const double *d) {
     double nq = __dsqrt_rn(d[1]);
     S->den = den;
     S->qnorm = nq;
-    if (fabs(den) <= __dmul_rn(__dmul_rn(S->breakdown_tol, S->nrt0), nq)) {
+    if (fabs(den) <= __dmul_rn(__dmul_rn(S->breakdown_tol, S->nrt0), nq))
       S->status = KRB_BREAKDOWN_SERIOUS;
-      S->itn += 1;
-    } else {
+    else
       S->alpha = __ddiv_rn(S->rho, den);
-    }
   } else if (PH == PH_SUPD) {
     double sn = __dsqrt_rn(d[0]);
     S->snorm = sn;
@@ -118,7 +114,6 @@ __device__ void finalize(const IterArgs &a, const double *d) {
       record(a, sn);
       S->early = 1;
       S->status = KRB_CONVERGED;
-      S->itn += 1;
     }
   } else if (PH == PH_PROJ_T) {
     S->matvecs += 1;
@@ -127,15 +122,12 @@ __device__ void finalize(const IterArgs &a, const double *d) {
     S->ts = d[1];
     if (tt == 0.0) {
       S->status = KRB_BREAKDOWN_OMEGA;
-      S->itn += 1;
     } else {
       double om = __ddiv_rn(d[1], tt);
-      if (om == 0.0) {
+      if (om == 0.0)
         S->status = KRB_BREAKDOWN_OMEGA;
-        S->itn += 1;
-      } else {
+      else
         S->omega = om;
-      }
     }
   } else if (PH == PH_XR) {
     double rn = __dsqrt_rn(d[0]);
@@ -161,33 +153,61 @@ __device__ void finalize(const IterArgs &a, const double *d) {
 }
 
 template <int kE, int PH>
-__global__ void __launch_bounds__(256) k_phase(IterArgs a) {
+__global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) {
   __shared__ double coef[512];
   __shared__ double red[3][8];
   __shared__ int last_flag;
+  const IterArgs &a = *pa;
   SolveScalars *S = a.S;
-  constexpr int ND = ndots_of<PH>();
-  const bool gated = (PH != PH_BNORM && PH != PH_INIT && PH != PH_TRUE &&
-                      PH != PH_RINIT);
+  constexpr int ND = ndots_of(PH);
+  constexpr bool kGated = (PH == PH_PUPDATE || PH == PH_PROJ_Q ||
+                           PH == PH_SUPD || PH == PH_PROJ_T || PH == PH_XR);
+  bool half_exit = false;
   if (PH == PH_XR && blockIdx.x == 0 && threadIdx.x == 0) S->bodies += 1;
-  if (PH == PH_EARLY) {
-    if (S->early != 1) return;
-  } else if (gated && S->status != KRB_RUNNING) {
-    if (PH == PH_XR && blockIdx.x == 0 && threadIdx.x == 0) {
-      if (S->early == 1) S->early = 2;  // half-step exit consumed
-      if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
+  if (kGated && S->status != KRB_RUNNING) {
+    if (PH == PH_PUPDATE) {
+      // a half-step exit was applied by the previous X phase: mark consumed
+      // (only matters for the host-driven loop, which may overshoot)
+      if (blockIdx.x == 0 && threadIdx.x == 0 && S->early == 1) S->early = 2;
+      return;
     }
-    return;
+    if (PH != PH_XR || S->early != 1) {
+      if (PH == PH_XR && a.use_cond && blockIdx.x == 0 && threadIdx.x == 0)
+        cudaGraphSetConditional(a.cond, 0);
+      return;
+    }
+    half_exit = true;   // X phase applies x += alpha p, xc += alpha zeta
   }
   const double alpha = S->alpha, omega = S->omega, beta = S->beta;
   const int k = a.k;
+  const int64_t n = a.n, nb = a.nb, ld = a.ld;
+  double *__restrict__ x = a.x;
+  double *__restrict__ r = a.r;
+  double *__restrict__ p = a.p;
+  double *__restrict__ q = a.q;
+  double *__restrict__ s = a.s;
+  double *__restrict__ t = a.t;
+  const double *__restrict__ rt0 = a.rt0;
+  const double *__restrict__ bvec = a.b;
+  const double *__restrict__ Cm = a.C;
+  double *__restrict__ part = a.part;
+  if (half_exit) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));   // solvers.py:316
+    if (blockIdx.x == 0) {
+      for (int j = threadIdx.x; j < k; j += blockDim.x)  // solvers.py:318
+        a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
+      if (threadIdx.x == 0 && a.use_cond) cudaGraphSetConditional(a.cond, 0);
+    }
+    return;
+  }
   if (PH == PH_PROJ_Q || PH == PH_PROJ_T) {
     const double *src = PH == PH_PROJ_Q ? a.zeta : a.gamma;
     for (int j = threadIdx.x; j < k; j += blockDim.x) coef[j] = src[j];
     __syncthreads();
   }
-  const int64_t n = a.n;
-  for (int64_t blk = blockIdx.x; blk < a.nb; blk += gridDim.x) {
+  for (int64_t blk = blockIdx.x; blk < nb; blk += gridDim.x) {
     const int64_t base = blk * (256 * kE) + threadIdx.x;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
 #pragma unroll
@@ -196,60 +216,56 @@ __global__ void __launch_bounds__(256) k_phase(IterArgs a) {
       if (i >= n) continue;
       if (PH == PH_PUPDATE) {
         // p = r + beta * (p - omega * q)          (solvers.py:303)
-        double pv = __dsub_rn(a.p[i], __dmul_rn(omega, a.q[i]));
-        a.p[i] = __dadd_rn(a.r[i], __dmul_rn(beta, pv));
+        double pv = __dsub_rn(p[i], __dmul_rn(omega, q[i]));
+        p[i] = __dadd_rn(r[i], __dmul_rn(beta, pv));
       } else if (PH == PH_PROJ_Q || PH == PH_PROJ_T) {
-        double *v = PH == PH_PROJ_Q ? a.q : a.t;
+        double *v = PH == PH_PROJ_Q ? q : t;
         double vi = v[i];
         if (k > 0) {
           double cz = 0.0;
           for (int j = 0; j < k; ++j)
-            cz = __fma_rn(__ldg(a.C + (int64_t)j * a.ld + i), coef[j], cz);
+            cz = __fma_rn(__ldg(Cm + (int64_t)j * ld + i), coef[j], cz);
           vi = __dsub_rn(vi, cz);   // q - C @ zeta   (solvers.py:307,329)
           v[i] = vi;
         }
         if (PH == PH_PROJ_Q) {
-          acc0 = __fma_rn(a.rt0[i], vi, acc0);   // (rt0, q)
-          acc1 = __fma_rn(vi, vi, acc1);         // (q, q)
+          acc0 = __fma_rn(rt0[i], vi, acc0);   // (rt0, q)
+          acc1 = __fma_rn(vi, vi, acc1);       // (q, q)
         } else {
-          acc0 = __fma_rn(vi, vi, acc0);         // (t, t)
-          acc1 = __fma_rn(vi, a.s[i], acc1);     // (t, s)
+          acc0 = __fma_rn(vi, vi, acc0);       // (t, t)
+          acc1 = __fma_rn(vi, s[i], acc1);     // (t, s)
         }
       } else if (PH == PH_SUPD) {
         // s = r - alpha * q                       (solvers.py:313)
-        double sv = __dsub_rn(a.r[i], __dmul_rn(alpha, a.q[i]));
-        a.s[i] = sv;
+        double sv = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+        s[i] = sv;
         acc0 = __fma_rn(sv, sv, acc0);
-      } else if (PH == PH_EARLY) {
-        // x = x + alpha * p                       (solvers.py:316)
-        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));
       } else if (PH == PH_XR) {
         // x = x + alpha*p + omega*s ; r = s - omega*t   (solvers.py:338,341)
-        double sv = a.s[i];
-        double xv = __dadd_rn(__dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i])),
-                              __dmul_rn(omega, sv));
-        a.x[i] = xv;
-        double rv = __dsub_rn(sv, __dmul_rn(omega, a.t[i]));
-        a.r[i] = rv;
+        double sv = s[i];
+        x[i] = __dadd_rn(__dadd_rn(x[i], __dmul_rn(alpha, p[i])),
+                         __dmul_rn(omega, sv));
+        double rv = __dsub_rn(sv, __dmul_rn(omega, t[i]));
+        r[i] = rv;
         acc0 = __fma_rn(rv, rv, acc0);
-        acc1 = __fma_rn(a.rt0[i], rv, acc1);
+        acc1 = __fma_rn(rt0[i], rv, acc1);
       } else if (PH == PH_BNORM) {
-        double bv = a.b[i];
+        double bv = bvec[i];
         acc0 = __fma_rn(bv, bv, acc0);
       } else if (PH == PH_INIT) {
-        double rv = a.r[i], tv = a.rt0[i];
+        double rv = r[i], tv = rt0[i];
         acc0 = __fma_rn(rv, rv, acc0);
         acc1 = __fma_rn(tv, rv, acc1);
         acc2 = __fma_rn(tv, tv, acc2);
       } else if (PH == PH_TRUE) {
         // true residual b - A x_out   (solvers.py:147-153); A x_out in t
-        double bv = a.b[i];
-        double res = __dsub_rn(bv, a.t[i]);
+        double bv = bvec[i];
+        double res = __dsub_rn(bv, t[i]);
         acc0 = __fma_rn(res, res, acc0);
         acc1 = __fma_rn(bv, bv, acc1);
       } else if (PH == PH_RINIT) {
         // r = b - A x_init            (recycling.py:200); A x_init in t
-        a.r[i] = __dsub_rn(a.b[i], a.t[i]);
+        r[i] = __dsub_rn(bvec[i], t[i]);
       }
     }
     if (ND > 0) {
@@ -263,30 +279,25 @@ __global__ void __launch_bounds__(256) k_phase(IterArgs a) {
         if (ND > 2) red[2][warp] = w2;
       }
       __syncthreads();
-      if (threadIdx.x < ND) {
+      if ((int)threadIdx.x < ND) {
         double v8[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v8[t] = red[threadIdx.x][t];
+        for (int u = 0; u < 8; ++u) v8[u] = red[threadIdx.x][u];
 #pragma unroll
         for (int off = 4; off >= 1; off >>= 1)
 #pragma unroll
-          for (int t = 0; t < off; ++t) v8[t] = __dadd_rn(v8[t], v8[t + off]);
-        a.part[threadIdx.x * a.nb + blk] = v8[0];
+          for (int u = 0; u < off; ++u) v8[u] = __dadd_rn(v8[u], v8[u + off]);
+        part[threadIdx.x * nb + blk] = v8[0];
       }
       __syncthreads();
     }
-  }
-  // xc updates of the k-vector ride on block 0 (no reduction needed)
-  if (PH == PH_EARLY && blockIdx.x == 0) {
-    for (int j = threadIdx.x; j < k; j += blockDim.x)
-      a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
   }
   if (ND == 0) return;
   if (!elect_last_cta(a.counters + PH, &last_flag)) return;
   __shared__ double dfin[3];
   const int warp = threadIdx.x >> 5;
   if (warp < ND) {
-    double v = warp_final_volatile(a.part + warp * a.nb, a.nb);
+    double v = warp_final_volatile(part + warp * nb, nb);
     if ((threadIdx.x & 31) == 0) dfin[warp] = v;
   }
   if (PH == PH_XR) {
@@ -304,6 +315,27 @@ __global__ void __launch_bounds__(256) k_phase(IterArgs a) {
   }
 }
 
+// projection dots inside the iteration: Chat^T v -> zeta / gamma
+template <int kE, bool kGamma>
+__global__ void __launch_bounds__(256) k_proj_dot(const IterArgs *__restrict__ pa) {
+  const IterArgs &a = *pa;
+  if (a.S->status != KRB_RUNNING) return;
+  tdot_body<kE, false>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
+                       kGamma ? a.gamma : a.zeta, a.counters + kCounterTdotGraph);
+}
+
+// SpMV inside the iteration (matrix read from the descriptor)
+template <bool kSell, bool kSecond>
+__global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ pa) {
+  const IterArgs &a = *pa;
+  if (a.S->status != KRB_RUNNING) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.A.n) return;
+  const double *x = kSecond ? a.s : a.p;
+  double *y = kSecond ? a.t : a.q;
+  y[i] = spmv_row<kSell>(i, a.A, x);
+}
+
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
                                int64_t max_itn, int k, int64_t mv0) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -318,48 +350,58 @@ __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
   }
 }
 
-template <int PH>
-static int launch_phase(const IterArgs &a, cudaStream_t st) {
-  if (a.nb == 0) return KRB_OK;
-  int grid = grid_for(a.nb);
-  switch (canon_E(a.n)) {
-    case 1: k_phase<1, PH><<<grid, 256, 0, st>>>(a); break;
-    case 2: k_phase<2, PH><<<grid, 256, 0, st>>>(a); break;
-    case 4: k_phase<4, PH><<<grid, 256, 0, st>>>(a); break;
-    case 8: k_phase<8, PH><<<grid, 256, 0, st>>>(a); break;
-    default: k_phase<16, PH><<<grid, 256, 0, st>>>(a); break;
-  }
-  KRB_CHECK_LAUNCH();
-  return KRB_OK;
-}
-
 #define KRB_TRY(x)          \
   do {                      \
     int rc_ = (x);          \
     if (rc_) return rc_;    \
   } while (0)
 
+template <int PH>
+static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
+  if (h.nb == 0) return KRB_OK;
+  int grid = grid_for(h.nb);
+  KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH><<<grid, 256, 0, st>>>(d)));
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+template <bool kGamma>
+static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
+  if (h.k <= 0 || h.nb == 0) return KRB_OK;
+  dim3 grid = tdot_grid(h.nb, h.k);
+  KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma><<<grid, 256, 0, st>>>(d)));
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+template <bool kSecond>
+static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
+  if (h.n == 0) return KRB_OK;
+  unsigned blocks = (unsigned)((h.n + 255) / 256);
+  if (h.A.format == 2)
+    k_iter_spmv<true, kSecond><<<blocks, 256, 0, st>>>(d);
+  else
+    k_iter_spmv<false, kSecond><<<blocks, 256, 0, st>>>(d);
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
 // one iteration (the graph body)
-static int launch_iteration(krb_context *ctx, const krb_matrix *A,
-                            const IterArgs &a, cudaStream_t st) {
-  const int *status = &a.S->status;
-  KRB_TRY(launch_phase<PH_PUPDATE>(a, st));
-  KRB_TRY(spmv_launch(A, a.p, a.q, status, st));
-  if (a.k > 0)
-    KRB_TRY(launch_tdot(ctx, a.n, a.k, a.Chat, a.ld, a.q, false, a.zeta, status, st));
-  KRB_TRY(launch_phase<PH_PROJ_Q>(a, st));
-  KRB_TRY(launch_phase<PH_SUPD>(a, st));
-  KRB_TRY(launch_phase<PH_EARLY>(a, st));
-  KRB_TRY(spmv_launch(A, a.s, a.t, status, st));
-  if (a.k > 0)
-    KRB_TRY(launch_tdot(ctx, a.n, a.k, a.Chat, a.ld, a.t, false, a.gamma, status, st));
-  KRB_TRY(launch_phase<PH_PROJ_T>(a, st));
-  KRB_TRY(launch_phase<PH_XR>(a, st));
+static int launch_iteration(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
+  KRB_TRY(launch_phase<PH_PUPDATE>(h, d, st));
+  KRB_TRY(launch_iter_spmv<false>(h, d, st));
+  KRB_TRY(launch_proj_dot<false>(h, d, st));
+  KRB_TRY(launch_phase<PH_PROJ_Q>(h, d, st));
+  KRB_TRY(launch_phase<PH_SUPD>(h, d, st));
+  KRB_TRY(launch_iter_spmv<true>(h, d, st));
+  KRB_TRY(launch_proj_dot<true>(h, d, st));
+  KRB_TRY(launch_phase<PH_PROJ_T>(h, d, st));
+  KRB_TRY(launch_phase<PH_XR>(h, d, st));
   return KRB_OK;
 }
 
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k) {
-  if (n <= ctx->vec_n && k <= ctx->vec_k) return KRB_OK;
+  if (n <= ctx->vec_n && k <= ctx->vec_k && ctx->desc) return KRB_OK;
   double **vecs[] = {&ctx->x, &ctx->r, &ctx->p, &ctx->q, &ctx->s,
                      &ctx->t, &ctx->rt0, &ctx->b, &ctx->w};
   int64_t nn = n > ctx->vec_n ? n : ctx->vec_n;
@@ -371,34 +413,34 @@ int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k) {
   }
   if (ctx->kbuf) cudaFree(ctx->kbuf);
   KRB_CHECK_CUDA(cudaMalloc(&ctx->kbuf, sizeof(double) * 5 * (kk > 0 ? kk : 1)));
+  if (!ctx->desc) KRB_CHECK_CUDA(cudaMalloc(&ctx->desc, sizeof(IterArgs)));
+  if (!ctx->S) KRB_CHECK_CUDA(cudaMalloc(&ctx->S, sizeof(SolveScalars)));
   ctx->vec_n = nn;
   ctx->vec_k = kk;
   ctx->graph.reset();
   return KRB_OK;
 }
 
-static int build_graph(krb_context *ctx, const krb_matrix *A, IterArgs a,
+static int build_graph(krb_context *ctx, const IterArgs &h, const IterArgs *d,
                        cudaStream_t capture) {
   GraphCache &G = ctx->graph;
   G.reset();
   cudaGraph_t g;
   KRB_CHECK_CUDA(cudaGraphCreate(&g, 0));
-  cudaGraphConditionalHandle h;
-  KRB_CHECK_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphConditionalHandle hc;
+  KRB_CHECK_CUDA(cudaGraphConditionalHandleCreate(&hc, g, 1, cudaGraphCondAssignDefault));
   cudaGraphNodeParams np = {};
   np.type = cudaGraphNodeTypeConditional;
-  np.conditional.handle = h;
+  np.conditional.handle = hc;
   np.conditional.type = cudaGraphCondTypeWhile;
   np.conditional.size = 1;
   cudaGraphNode_t node;
   KRB_CHECK_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
   cudaGraph_t body = np.conditional.phGraph_out[0];
-  a.cond = h;
-  a.use_cond = 1;
   KRB_CHECK_CUDA(cudaStreamBeginCaptureToGraph(capture, body, nullptr, nullptr, 0,
                                                cudaStreamCaptureModeRelaxed));
   const int64_t c0 = launch_counter();
-  int rc = launch_iteration(ctx, A, a, capture);
+  int rc = launch_iteration(h, d, capture);
   G.kernels_per_body = launch_counter() - c0;
   launch_counter() = c0;  // captured, not executed: counted per body run
   cudaGraph_t out_body;
@@ -421,6 +463,7 @@ static int build_graph(krb_context *ctx, const krb_matrix *A, IterArgs a,
   }
   G.graph = g;
   G.exec = exec;
+  G.cond = hc;
   return KRB_OK;
 }
 
@@ -447,42 +490,55 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     KRB_REQUIRE(k <= 512, "recycle dimension > 512 unsupported");
   }
   KRB_TRY(ctx_reserve_vectors(ctx, n, k));
+  KRB_TRY(ctx_reserve_counters(ctx, st));
   const int64_t l0 = launch_counter();
   int64_t per_body = 0;
   const int64_t nb = canon_nblocks(n);
   KRB_TRY(ctx_reserve_part(ctx, (size_t)(3 * nb > k * nb ? 3 * nb : k * nb) + 64));
-  if (!ctx->S) {
-    KRB_CHECK_CUDA(cudaMalloc(&ctx->S, sizeof(SolveScalars)));
-    KRB_CHECK_CUDA(cudaMalloc(&ctx->counters, sizeof(unsigned int) * 32));
-    KRB_CHECK_CUDA(cudaMemsetAsync(ctx->counters, 0, sizeof(unsigned int) * 32, st));
-  }
-  IterArgs a = {};
-  a.n = n;
-  a.nb = nb;
-  a.k = (int)k;
-  a.ld = k > 0 ? R->ld : n;
-  a.C = k > 0 ? R->C : nullptr;
-  a.Chat = k > 0 ? R->Chat : nullptr;
-  a.U = k > 0 ? R->U : nullptr;
-  a.x = ctx->x; a.r = ctx->r; a.p = ctx->p; a.q = ctx->q; a.s = ctx->s;
-  a.t = ctx->t; a.rt0 = ctx->rt0; a.b = ctx->b;
-  a.zeta = ctx->kbuf;
-  a.gamma = ctx->kbuf + ctx->vec_k;
-  a.xc = ctx->kbuf + 2 * ctx->vec_k;
+  IterArgs h = {};
+  h.A = *A;
+  h.A.T = nullptr;
+  h.n = n;
+  h.nb = nb;
+  h.k = (int)k;
+  h.ld = k > 0 ? R->ld : n;
+  h.C = k > 0 ? R->C : nullptr;
+  h.Chat = k > 0 ? R->Chat : nullptr;
+  h.U = k > 0 ? R->U : nullptr;
+  h.x = ctx->x; h.r = ctx->r; h.p = ctx->p; h.q = ctx->q; h.s = ctx->s;
+  h.t = ctx->t; h.rt0 = ctx->rt0; h.b = ctx->b;
+  h.zeta = ctx->kbuf;
+  h.gamma = ctx->kbuf + ctx->vec_k;
+  h.xc = ctx->kbuf + 2 * ctx->vec_k;
   double *ybuf = ctx->kbuf + 3 * ctx->vec_k;
-  a.part = ctx->part;
-  a.counters = ctx->counters;
-  a.S = ctx->S;
-  a.hist_r = hist_r;
-  a.hist_m = hist_m;
-  a.hist_t = hist_t;
+  h.part = ctx->part;
+  h.counters = ctx->counters;
+  h.S = ctx->S;
+  h.hist_r = hist_r;
+  h.hist_m = hist_m;
+  h.hist_t = hist_t;
+  const bool graph = cfg->use_graph == 1;
+  GraphCache &G = ctx->graph;
+  const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format;
+  h.use_cond = graph ? 1 : 0;
+  h.cond = hit ? G.cond : 0;
+  IterArgs *d = reinterpret_cast<IterArgs *>(ctx->desc);
 
   // ---- setup (solvers.py:257-296) -------------------------------------
-  KRB_CHECK_CUDA(cudaMemcpyAsync(a.b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-  k_init_scalars<<<1, 1, 0, st>>>(a.S, cfg->tol, cfg->breakdown_tol, cfg->max_itn,
+  if (graph && !hit) {
+    KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+    KRB_TRY(build_graph(ctx, h, d, capture_stream()));
+    G.n = n; G.k = k; G.format = A->format;
+    h.cond = G.cond;
+  }
+  // the descriptor is written in stream order (the previous solve on this
+  // stream has finished reading it)
+  KRB_CHECK_CUDA(cudaMemcpyAsync(d, &h, sizeof(IterArgs), cudaMemcpyHostToDevice, st));
+  KRB_CHECK_CUDA(cudaMemcpyAsync(h.b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  k_init_scalars<<<1, 1, 0, st>>>(h.S, cfg->tol, cfg->breakdown_tol, cfg->max_itn,
                                   (int)k, d_x_init ? 1 : 0);
   KRB_CHECK_LAUNCH();
-  KRB_TRY(launch_phase<PH_BNORM>(a, st));
+  KRB_TRY(launch_phase<PH_BNORM>(h, d, st));
   // shadow residual rt_{-1} (solvers.py:268-269)
   if (cfg->d_shadow)
     KRB_CHECK_CUDA(cudaMemcpyAsync(ctx->w, cfg->d_shadow, sizeof(double) * n,
@@ -492,41 +548,32 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
                               cfg->pcg_inc_lo, -1.0, 1.0, ctx->w, st));
   // x0, r0 (project_initial, recycling.py:189-206)
   if (d_x_init) {
-    KRB_CHECK_CUDA(cudaMemcpyAsync(a.x, d_x_init, sizeof(double) * n,
+    KRB_CHECK_CUDA(cudaMemcpyAsync(h.x, d_x_init, sizeof(double) * n,
                                    cudaMemcpyDeviceToDevice, st));
-    KRB_TRY(spmv_launch(A, a.x, a.t, nullptr, st));
-    KRB_TRY(launch_phase<PH_RINIT>(a, st));
+    KRB_TRY(spmv_launch(A, h.x, h.t, nullptr, st));
+    KRB_TRY(launch_phase<PH_RINIT>(h, d, st));
   } else {
-    KRB_CHECK_CUDA(cudaMemsetAsync(a.x, 0, sizeof(double) * n, st));
-    KRB_CHECK_CUDA(cudaMemcpyAsync(a.r, a.b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    KRB_CHECK_CUDA(cudaMemsetAsync(h.x, 0, sizeof(double) * n, st));
+    KRB_CHECK_CUDA(cudaMemcpyAsync(h.r, h.b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   }
   if (k > 0) {
-    KRB_TRY(launch_tdot(ctx, n, k, R->Chat, R->ld, a.r, false, ybuf, nullptr, st));
-    KRB_TRY(launch_gemv(n, k, R->U, R->ld, ybuf, a.x, +1, a.x, st));
-    KRB_TRY(launch_gemv(n, k, R->C, R->ld, ybuf, a.r, -1, a.r, st));
+    KRB_TRY(launch_tdot(ctx, n, k, R->Chat, R->ld, h.r, false, ybuf, nullptr, st));
+    KRB_TRY(launch_gemv(n, k, R->U, R->ld, ybuf, h.x, +1, h.x, st));
+    KRB_TRY(launch_gemv(n, k, R->C, R->ld, ybuf, h.r, -1, h.r, st));
     // rt0 = rt_{-1} - Ct (Ccheck^H rt_{-1})   (solvers.py:273)
     KRB_TRY(launch_tdot(ctx, n, k, R->Ccheck, R->ld, ctx->w, false, ybuf, nullptr, st));
-    KRB_TRY(launch_gemv(n, k, R->Ct, R->ld, ybuf, ctx->w, -1, a.rt0, st));
-    KRB_CHECK_CUDA(cudaMemsetAsync(a.xc, 0, sizeof(double) * k, st));
+    KRB_TRY(launch_gemv(n, k, R->Ct, R->ld, ybuf, ctx->w, -1, h.rt0, st));
+    KRB_CHECK_CUDA(cudaMemsetAsync(h.xc, 0, sizeof(double) * k, st));
   } else {
-    KRB_CHECK_CUDA(cudaMemcpyAsync(a.rt0, ctx->w, sizeof(double) * n,
+    KRB_CHECK_CUDA(cudaMemcpyAsync(h.rt0, ctx->w, sizeof(double) * n,
                                    cudaMemcpyDeviceToDevice, st));
   }
-  KRB_CHECK_CUDA(cudaMemsetAsync(a.p, 0, sizeof(double) * n, st));
-  KRB_CHECK_CUDA(cudaMemsetAsync(a.q, 0, sizeof(double) * n, st));
-  KRB_TRY(launch_phase<PH_INIT>(a, st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * n, st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(h.q, 0, sizeof(double) * n, st));
+  KRB_TRY(launch_phase<PH_INIT>(h, d, st));
 
   // ---- iterations (solvers.py:298-356) --------------------------------
-  if (cfg->use_graph == 1) {
-    GraphCache &G = ctx->graph;
-    bool hit = G.exec && G.A == A && G.n == n && G.k == k && G.ld == a.ld &&
-               G.C == a.C && G.Chat == a.Chat && G.hist_r == hist_r &&
-               G.hist_m == hist_m && G.hist_t == hist_t;
-    if (!hit) {
-      KRB_TRY(build_graph(ctx, A, a, capture_stream()));
-      G.A = A; G.n = n; G.k = k; G.ld = a.ld; G.C = a.C; G.Chat = a.Chat;
-      G.hist_r = hist_r; G.hist_m = hist_m; G.hist_t = hist_t;
-    }
+  if (graph) {
     KRB_CHECK_CUDA(cudaGraphLaunch(G.exec, st));
     per_body = G.kernels_per_body;
   } else {
@@ -534,9 +581,9 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     // the status leaves RUNNING, so the overshoot is harmless)
     int32_t status = 0;
     for (int64_t it = 0; it < cfg->max_itn + 1; ++it) {
-      KRB_TRY(launch_iteration(ctx, A, a, st));
+      KRB_TRY(launch_iteration(h, d, st));
       if ((it & 7) == 7 || it == cfg->max_itn) {
-        KRB_CHECK_CUDA(cudaMemcpyAsync(&status, &a.S->status, sizeof(int32_t),
+        KRB_CHECK_CUDA(cudaMemcpyAsync(&status, &h.S->status, sizeof(int32_t),
                                        cudaMemcpyDeviceToHost, st));
         KRB_CHECK_CUDA(cudaStreamSynchronize(st));
         if (status != KRB_RUNNING) break;
@@ -546,14 +593,14 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
 
   // ---- x_out = x - U xc (solvers.py:359), true residual (:360) ----------
   if (k > 0)
-    KRB_TRY(launch_gemv(n, k, R->U, R->ld, a.xc, a.x, -1, d_x_out, st));
+    KRB_TRY(launch_gemv(n, k, R->U, R->ld, h.xc, h.x, -1, d_x_out, st));
   else
-    KRB_CHECK_CUDA(cudaMemcpyAsync(d_x_out, a.x, sizeof(double) * n,
+    KRB_CHECK_CUDA(cudaMemcpyAsync(d_x_out, h.x, sizeof(double) * n,
                                    cudaMemcpyDeviceToDevice, st));
-  KRB_TRY(spmv_launch(A, d_x_out, a.t, nullptr, st));
-  KRB_TRY(launch_phase<PH_TRUE>(a, st));
+  KRB_TRY(spmv_launch(A, d_x_out, h.t, nullptr, st));
+  KRB_TRY(launch_phase<PH_TRUE>(h, d, st));
   SolveScalars hs;
-  KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, a.S, sizeof(SolveScalars), cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, h.S, sizeof(SolveScalars), cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));
   res->status = hs.status;
   res->hist_len = hs.hist_len;

@@ -1,5 +1,5 @@
 // krb_context: scratch owned by the library (partials, solver vectors,
-// device scalar block, CUDA-graph cache).
+// device scalar block, solve descriptor, CUDA-graph cache).
 #pragma once
 
 #include "krb_internal.cuh"
@@ -24,27 +24,24 @@ struct SolveScalars {
   int32_t pad;
 };
 
+// One instantiated solve graph; valid for every solve of the same shape
+// (all per-solve pointers live in the device descriptor).
 struct GraphCache {
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
-  // key
-  const void *A = nullptr;
-  const void *C = nullptr, *Chat = nullptr;
-  int64_t n = -1, k = -1, ld = -1;
-  const double *hist_r = nullptr;
-  const int64_t *hist_m = nullptr;
-  const uint64_t *hist_t = nullptr;
+  cudaGraphConditionalHandle cond = 0;
+  int64_t n = -1, k = -1;
+  int format = -1;
   int64_t kernels_per_body = 0;
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     exec = nullptr;
     graph = nullptr;
-    A = C = Chat = nullptr;
-    n = k = ld = -1;
-    hist_r = nullptr;
-    hist_m = nullptr;
-    hist_t = nullptr;
+    cond = 0;
+    n = k = -1;
+    format = -1;
+    kernels_per_body = 0;
   }
 };
 
@@ -54,9 +51,10 @@ struct krb_context {
   // generic partial buffer for canonical reductions
   double *part = nullptr;
   size_t part_cap = 0;  // doubles
-  unsigned int *counters = nullptr;  // 16 election counters
+  unsigned int *counters = nullptr;  // last-CTA election counters
   // solver state
   krb::SolveScalars *S = nullptr;
+  void *desc = nullptr;   // device copy of the solve descriptor (IterArgs)
   int64_t vec_n = 0, vec_k = 0;
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *s = nullptr,
          *t = nullptr, *rt0 = nullptr, *b = nullptr, *w = nullptr;
@@ -65,7 +63,14 @@ struct krb_context {
 };
 
 namespace krb {
+// election-counter slots (ctx->counters)
+constexpr int kNumCounters = 32;
+constexpr int kCounterTdotStandalone = 20;
+constexpr int kCounterTdotGraph = 21;
+
 int ctx_reserve_part(krb_context *ctx, size_t doubles);
+int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);
+dim3 tdot_grid(int64_t nb, int64_t k);
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k);
 
 // canonical primitives used across translation units (stream-ordered)

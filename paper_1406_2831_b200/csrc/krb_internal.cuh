@@ -77,7 +77,7 @@ constexpr int kNumSMs = 148;
 inline int64_t canon_E(int64_t n) {
   int64_t t = (n + (int64_t)kLanes * kTargetBlocks - 1) /
               ((int64_t)kLanes * kTargetBlocks);
-  int64_t E = 1;
+  int64_t E = 4;  /* >= 4 lanes-elements amortise the shuffle tree */
   while (E < t && E < 16) E *= 2;
   return E;
 }
@@ -165,6 +165,15 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+#define KRB_DISPATCH_E(E, ...)                 \
+  switch (E) {                                 \
+    case 1: { constexpr int kE = 1; __VA_ARGS__; } break;   \
+    case 2: { constexpr int kE = 2; __VA_ARGS__; } break;   \
+    case 4: { constexpr int kE = 4; __VA_ARGS__; } break;   \
+    case 8: { constexpr int kE = 8; __VA_ARGS__; } break;   \
+    default: { constexpr int kE = 16; __VA_ARGS__; } break; \
+  }
 
 inline int grid_for(int64_t nb, int per_sm = 8) {
   int64_t g = (int64_t)kNumSMs * per_sm;

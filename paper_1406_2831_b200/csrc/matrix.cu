@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 
 #include "krb_internal.cuh"
+#include "spmv.cuh"
 
 
 namespace krb {
@@ -68,52 +69,6 @@ __global__ void k_pad_fill(int64_t total, int32_t *s_col, double *s_val) {
   }
 }
 
-// ---- SpMV kernels: one thread per row, CSR order, mul then add ----------
-template <bool kSell>
-__device__ __forceinline__ double row_dot(int64_t i, const krb_matrix &A,
-                                          const double *__restrict__ x) {
-  double sum = 0.0;
-  if (kSell) {
-    const int len = __ldg(A.rlen + i);
-    const int64_t base = __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
-    const int32_t *__restrict__ cp = A.s_col + base;
-    const double *__restrict__ vp = A.s_val + base;
-    int j = 0;
-    for (; j + 4 <= len; j += 4) {
-      int c0 = __ldg(cp + 32 * j), c1 = __ldg(cp + 32 * (j + 1));
-      int c2 = __ldg(cp + 32 * (j + 2)), c3 = __ldg(cp + 32 * (j + 3));
-      double v0 = __ldg(vp + 32 * j), v1 = __ldg(vp + 32 * (j + 1));
-      double v2 = __ldg(vp + 32 * (j + 2)), v3 = __ldg(vp + 32 * (j + 3));
-      double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2),
-             x3 = __ldg(x + c3);
-      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
-      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
-      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
-      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
-    }
-    for (; j < len; ++j)
-      sum = __dadd_rn(sum, __dmul_rn(__ldg(vp + 32 * j), __ldg(x + __ldg(cp + 32 * j))));
-  } else {
-    int64_t b = __ldg(A.rp + i), e = __ldg(A.rp + i + 1);
-    int64_t jj = b;
-    for (; jj + 4 <= e; jj += 4) {
-      int c0 = __ldg(A.ci + jj), c1 = __ldg(A.ci + jj + 1);
-      int c2 = __ldg(A.ci + jj + 2), c3 = __ldg(A.ci + jj + 3);
-      double v0 = __ldg(A.val + jj), v1 = __ldg(A.val + jj + 1);
-      double v2 = __ldg(A.val + jj + 2), v3 = __ldg(A.val + jj + 3);
-      double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2),
-             x3 = __ldg(x + c3);
-      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
-      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
-      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
-      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
-    }
-    for (; jj < e; ++jj)
-      sum = __dadd_rn(sum, __dmul_rn(__ldg(A.val + jj), __ldg(x + __ldg(A.ci + jj))));
-  }
-  return sum;
-}
-
 template <bool kSell>
 __global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
                                               const double *__restrict__ x,
@@ -122,7 +77,7 @@ __global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
   if (status && *status) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
-  y[i] = row_dot<kSell>(i, A, x);
+  y[i] = spmv_row<kSell>(i, A, x);
 }
 
 int spmv_launch(const krb_matrix *A, const double *x, double *y,

@@ -9,17 +9,9 @@
 // 32-lane shuffle tree, 8-warp tree; final stage: 32-lane strided sum then
 // tree).
 #include "ctx.cuh"
+#include "tdot.cuh"
 
 namespace krb {
-
-#define KRB_DISPATCH_E(E, ...)                 \
-  switch (E) {                                 \
-    case 1: { constexpr int kE = 1; __VA_ARGS__; } break;   \
-    case 2: { constexpr int kE = 2; __VA_ARGS__; } break;   \
-    case 4: { constexpr int kE = 4; __VA_ARGS__; } break;   \
-    case 8: { constexpr int kE = 8; __VA_ARGS__; } break;   \
-    default: { constexpr int kE = 16; __VA_ARGS__; } break; \
-  }
 
 template <int kE>
 __global__ void __launch_bounds__(256) k_dot_part(int64_t n, int64_t nb,
@@ -57,52 +49,12 @@ __global__ void k_final_sqrt(int ndots, int64_t nb,
   if ((threadIdx.x & 31) == 0) out[d] = __dsqrt_rn(r);
 }
 
-// part[j*nb + b] = block partial of (M[:,j], v) (self: (M[:,j], M[:,j])).
 template <int kE, bool kSelf>
-__global__ void __launch_bounds__(256) k_tdot_part(
+__global__ void __launch_bounds__(256) k_tdot(
     int64_t n, int64_t nb, int k, const double *__restrict__ M, int64_t ldm,
     const double *__restrict__ v, double *__restrict__ part,
-    const int *__restrict__ status) {
-  extern __shared__ double sm[];  // k x 8 warp results
-  if (status && *status) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int64_t base = b * (256 * kE) + threadIdx.x;
-    double vr[kE];
-    if (!kSelf) {
-#pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        int64_t i = base + 256 * e;
-        vr[e] = i < n ? __ldg(v + i) : 0.0;
-      }
-    }
-    for (int j = 0; j < k; ++j) {
-      const double *col = M + (int64_t)j * ldm;
-      double acc = 0.0;
-#pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        int64_t i = base + 256 * e;
-        if (i < n) {
-          double m = __ldg(col + i);
-          acc = __fma_rn(m, kSelf ? m : vr[e], acc);
-        }
-      }
-      double w = warp_tree(acc);
-      if (lane == 0) sm[j * 8 + warp] = w;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-      double a[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) a[t] = sm[j * 8 + t];
-#pragma unroll
-      for (int off = 4; off >= 1; off >>= 1)
-#pragma unroll
-        for (int t = 0; t < off; ++t) a[t] = __dadd_rn(a[t], a[t + off]);
-      part[(int64_t)j * nb + b] = a[0];
-    }
-    __syncthreads();
-  }
+    double *__restrict__ out, unsigned int *counter) {
+  tdot_body<kE, kSelf>(n, nb, k, M, ldm, v, part, out, counter);
 }
 
 // out[i] = base[i] + sign * (sum_j M[i,j] y[j])  (sequential fma from 0.0)
@@ -292,9 +244,19 @@ int launch_final(int ndots, int64_t nb, const double *part, double *out,
   return KRB_OK;
 }
 
+dim3 tdot_grid(int64_t nb, int64_t k) {
+  int64_t gy = (k + kTdotCG - 1) / kTdotCG;
+  int64_t want = (int64_t)kNumSMs * 8;
+  int64_t gx = (want + gy - 1) / gy;
+  if (gx > nb) gx = nb;
+  if (gx < 1) gx = 1;
+  return dim3((unsigned)gx, (unsigned)gy);
+}
+
 int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
                 int64_t ldm, const double *v, bool self, double *out,
                 const int *status, cudaStream_t st) {
+  (void)status;
   if (k <= 0) return KRB_OK;
   int64_t nb = canon_nblocks(n);
   if (nb == 0) {
@@ -303,22 +265,25 @@ int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
   }
   int rc = ctx_reserve_part(ctx, (size_t)(k * nb));
   if (rc) return rc;
-  int grid = grid_for(nb);
-  size_t smem = sizeof(double) * 8 * k;
-  KRB_REQUIRE(k <= 512, "projection width k > 512 unsupported");
+  rc = ctx_reserve_counters(ctx, st);
+  if (rc) return rc;
+  dim3 grid = tdot_grid(nb, k);
+  unsigned int *cnt = ctx->counters + kCounterTdotStandalone;
   if (self) {
-    KRB_DISPATCH_E(canon_E(n), (k_tdot_part<kE, true><<<grid, 256, smem, st>>>(
-                                   n, nb, (int)k, M, ldm, v, ctx->part, status)));
+    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true><<<grid, 256, 0, st>>>(
+                                   n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
   } else {
-    KRB_DISPATCH_E(canon_E(n), (k_tdot_part<kE, false><<<grid, 256, smem, st>>>(
-                                   n, nb, (int)k, M, ldm, v, ctx->part, status)));
+    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, false><<<grid, 256, 0, st>>>(
+                                   n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
   }
   KRB_CHECK_LAUNCH();
-  if (self)
-    k_final_sqrt<<<(unsigned)((k + 7) / 8), 256, 0, st>>>((int)k, nb, ctx->part, out);
-  else
-    k_final<<<(unsigned)((k + 7) / 8), 256, 0, st>>>((int)k, nb, ctx->part, out);
-  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+int ctx_reserve_counters(krb_context *ctx, cudaStream_t st) {
+  if (ctx->counters) return KRB_OK;
+  KRB_CHECK_CUDA(cudaMalloc(&ctx->counters, sizeof(unsigned int) * kNumCounters));
+  KRB_CHECK_CUDA(cudaMemsetAsync(ctx->counters, 0, sizeof(unsigned int) * kNumCounters, st));
   return KRB_OK;
 }
 

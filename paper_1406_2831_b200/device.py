@@ -69,14 +69,53 @@ class Context:
         return self._hist
 
 
+class _Staging:
+    """Two reusable pinned host buffers for H2D copies: the host memcpy into
+    one overlaps the DMA out of the other; an event guards reuse."""
+
+    def __init__(self):
+        self.bufs = [None, None]
+        self.events = [None, None]
+        self.turn = 0
+
+    def get(self, nbytes):
+        t = torch()
+        i = self.turn
+        self.turn ^= 1
+        if self.events[i] is not None:
+            self.events[i].synchronize()
+        buf = self.bufs[i]
+        if buf is None or buf.numel() < nbytes:
+            cap = max(nbytes, 1 << 24)
+            buf = t.empty(cap, dtype=t.uint8, pin_memory=True)
+            self.bufs[i] = buf
+        return i, buf
+
+    def mark(self, i):
+        t = torch()
+        ev = self.events[i] or t.cuda.Event()
+        ev.record()
+        self.events[i] = ev
+
+
+_STAGING = _Staging()
+_TDT = {np.dtype(np.float64): "float64", np.dtype(np.int64): "int64",
+        np.dtype(np.int32): "int32"}
+
+
 def to_device(a: np.ndarray, dtype=np.float64):
-    """Host numpy -> device tensor (through pinned memory)."""
+    """Host numpy -> device tensor through reusable pinned staging."""
     t = torch()
     a = np.ascontiguousarray(a, dtype=dtype)
-    host = t.from_numpy(a)
-    if a.nbytes >= (1 << 20):
-        host = host.pin_memory()
-    return host.to("cuda", non_blocking=True)
+    if a.nbytes < (1 << 16):
+        return t.from_numpy(a).to("cuda")
+    i, buf = _STAGING.get(a.nbytes)
+    host = buf[:a.nbytes].numpy()
+    np.copyto(host, a.reshape(-1).view(np.uint8))
+    out = t.empty(a.shape, dtype=getattr(t, _TDT[a.dtype]), device="cuda")
+    out.view(-1).view(t.uint8).copy_(buf[:a.nbytes], non_blocking=True)
+    _STAGING.mark(i)
+    return out
 
 
 def to_host(tensor) -> np.ndarray:

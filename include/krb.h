@@ -49,6 +49,9 @@ const char *krb_last_error(void);
 /* number of kernel launches issued by this library since load (counter) */
 int64_t krb_launch_count(void);
 
+/* stream-ordered device-to-device copy (ring views -> caller tensors) */
+int krb_memcpy_d2d(void *d_dst, const void *d_src, int64_t bytes, void *stream);
+
 /* ---------------------------------------------------------------- context */
 /* Owns scratch buffers, the CUDA-graph cache and the solver state block. */
 typedef struct krb_context krb_context;
@@ -109,6 +112,16 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
 /* d_out[j] = ||X[:,j]||_2   (np.linalg.norm(X, axis=0), recycling.py:155) */
 int krb_colnorms(krb_context *ctx, int64_t n, int64_t k, const double *d_X,
                  int64_t ldx, double *d_out, void *stream);
+/* d_out[j] = (X[:,j], X[:,j]) without the square root (squared norms used
+ * by the near-null eigen-residual test, recycling.py:353-354) */
+int krb_colsq(krb_context *ctx, int64_t n, int64_t k, const double *d_X,
+              int64_t ldx, double *d_out, void *stream);
+/* Ritz eigen-residual in real arithmetic (recycling.py:351-352):
+ * Are -= Yre*thr - Yim*thi ; Aim -= Yre*thi + Yim*thr   (per column c) */
+int krb_ritz_combine(int64_t n, int64_t m, const double *d_Yre,
+                     const double *d_Yim, double *d_Are, double *d_Aim,
+                     int64_t ld, const double *d_thr, const double *d_thi,
+                     void *stream);
 /* X[:, j] *= 1/s[j] done as a division X[i,j] / s[j] (recycling.py:156,337) */
 int krb_colscale_div(int64_t n, int64_t k, double *d_X, int64_t ldx,
                      const double *d_s, void *stream);
@@ -160,6 +173,36 @@ int krb_rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
                   double *d_hist_resid, int64_t *d_hist_matvecs,
                   uint64_t *d_hist_stamp, krb_solve_result *h_result,
                   void *stream);
+
+/* ---------------------------------------------------- generation solve */
+/* rbicg_solve (solvers.py:460-638): two-sided deflated BiCG with capture of
+ * normalized Lanczos-direction pairs into a device ring of s+2 columns.  The
+ * host drives it: create -> start (projected initial residuals, dual-start
+ * test scalars; repeated for the reference's re-draws) -> set_counts ->
+ * begin -> run (returns at every completed cycle of s iterations, so the
+ * recycle-space update can run, or when the solve stops) -> rotate after an
+ * emitted cycle -> finish. */
+typedef struct krb_rbicg krb_rbicg;
+int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
+                     const krb_space_view *R, int64_t s, int64_t max_itn,
+                     void *stream);
+int krb_rbicg_destroy(krb_rbicg *H);
+int krb_rbicg_start(krb_rbicg *H, const double *d_b, const double *d_bt,
+                    const double *d_x0, const double *d_xt0, double tol,
+                    double breakdown_tol, int use_graph, double *h_dual,
+                    void *stream);
+int krb_rbicg_set_counts(krb_rbicg *H, int64_t n_matvec, int64_t n_rmatvec,
+                         void *stream);
+int krb_rbicg_begin(krb_rbicg *H, int32_t *h_status, void *stream);
+/* h_state[7] = status, emit, ncols, itn, nalpha, capture, npush */
+int krb_rbicg_run(krb_rbicg *H, int64_t *h_state, void *stream);
+int krb_rbicg_views(krb_rbicg *H, double **V, double **Vt, double **rhos,
+                    double **alphas, double **betas);
+int krb_rbicg_rotate(krb_rbicg *H, int64_t keep, void *stream);
+int krb_rbicg_finish(krb_rbicg *H, double *d_x_out, double *d_xt_out,
+                     double *d_hist_r, double *d_hist_rt, int64_t *d_hist_m,
+                     uint64_t *d_hist_t, krb_solve_result *res,
+                     int64_t *h_counts, double *h_btnorm, void *stream);
 
 /* Per-iteration device scalars of the last solve (debug/tests): alpha,
  * omega, rho, beta written to h_out[0..3]. */

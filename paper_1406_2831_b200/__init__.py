@@ -13,7 +13,8 @@ from .recycling import (CapturedCycle, RecycleSpace, biorthonormalize,
 from .solvers import (BREAKDOWN_OMEGA, BREAKDOWN_SECOND_KIND,
                       BREAKDOWN_SERIOUS, CONVERGED, MAX_ITN,
                       ConvergenceHistory, SolverConfig, bicgstab_solve,
-                      rbicgstab_solve)
+                      rbicg_solve, rbicgstab_solve)
+from .update import update_recycle_space
 from .sparse import SparseMatrix
 
 __version__ = "0.1.0"
@@ -23,6 +24,7 @@ __all__ = [
     "CapturedCycle", "RecycleSpace", "biorthonormalize", "project_initial",
     "refresh_images",
     "ConvergenceHistory", "SolverConfig", "bicgstab_solve", "rbicgstab_solve",
+    "rbicg_solve", "update_recycle_space",
     "CONVERGED", "MAX_ITN", "BREAKDOWN_SERIOUS", "BREAKDOWN_OMEGA",
     "BREAKDOWN_SECOND_KIND",
     "SparseMatrix",

@@ -90,6 +90,24 @@ SIGNATURES = {
                               ctypes.POINTER(SolveConfig), c_vp, c_vp, c_vp,
                               c_vp, ctypes.POINTER(SolveResult), c_vp]),
     "krb_last_scalars": (c_int, [c_vp, ctypes.POINTER(c_dbl)]),
+    "krb_memcpy_d2d": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "krb_colsq": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "krb_ritz_combine": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                 c_vp, c_vp, c_vp]),
+    "krb_rbicg_create": (c_int, [ctypes.POINTER(c_vp), c_vp, c_vp,
+                                 ctypes.POINTER(SpaceView), c_i64, c_i64, c_vp]),
+    "krb_rbicg_destroy": (c_int, [c_vp]),
+    "krb_rbicg_start": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_dbl, c_dbl,
+                                c_int, ctypes.POINTER(c_dbl), c_vp]),
+    "krb_rbicg_set_counts": (c_int, [c_vp, c_i64, c_i64, c_vp]),
+    "krb_rbicg_begin": (c_int, [c_vp, ctypes.POINTER(ctypes.c_int32), c_vp]),
+    "krb_rbicg_run": (c_int, [c_vp, ctypes.POINTER(c_i64), c_vp]),
+    "krb_rbicg_views": (c_int, [c_vp] + [ctypes.POINTER(c_vp)] * 5),
+    "krb_rbicg_rotate": (c_int, [c_vp, c_i64, c_vp]),
+    "krb_rbicg_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                 ctypes.POINTER(SolveResult),
+                                 ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl),
+                                 c_vp]),
 }
 
 _lock = threading.Lock()
@@ -141,3 +159,25 @@ def call(name: str, *args):
 
 def launch_count() -> int:
     return int(load().krb_launch_count())
+
+
+def copy_d2d(dst_tensor, src_addr: int, count: int):
+    """Device-to-device copy of `count` doubles from a raw device address
+    (libkrb ring views) into a torch tensor, on the current stream."""
+    import torch
+    if count <= 0:
+        return
+    call("krb_memcpy_d2d", ctypes.c_void_p(dst_tensor.data_ptr()),
+         ctypes.c_void_p(src_addr), 8 * count,
+         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+def fetch_f64(src_addr: int, count: int):
+    """Copy `count` doubles from a raw device address to a host numpy array."""
+    import numpy as np
+    import torch
+    if count <= 0:
+        return np.zeros(0)
+    out = torch.empty(count, dtype=torch.float64, device="cuda")
+    copy_d2d(out, src_addr, count)
+    return out.cpu().numpy()

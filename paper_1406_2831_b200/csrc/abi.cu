@@ -29,6 +29,14 @@ const char *krb_last_error(void) { return krb::g_err; }
 
 int64_t krb_launch_count(void) { return krb::g_launches; }
 
+int krb_memcpy_d2d(void *d_dst, const void *d_src, int64_t bytes, void *stream) {
+  KRB_REQUIRE(bytes >= 0, "krb_memcpy_d2d: negative size");
+  if (bytes == 0) return KRB_OK;
+  KRB_CHECK_CUDA(cudaMemcpyAsync(d_dst, d_src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                 krb::as_stream(stream)));
+  return KRB_OK;
+}
+
 int krb_context_create(krb_context **out) {
   KRB_REQUIRE(out != nullptr, "krb_context_create: out is NULL");
   *out = new krb_context();

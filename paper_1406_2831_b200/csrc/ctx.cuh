@@ -64,7 +64,7 @@ struct krb_context {
 
 namespace krb {
 // election-counter slots (ctx->counters)
-constexpr int kNumCounters = 32;
+constexpr int kNumCounters = 64;
 constexpr int kCounterTdotStandalone = 20;
 constexpr int kCounterTdotGraph = 21;
 
@@ -80,7 +80,7 @@ int launch_final(int ndots, int64_t nb, const double *part, double *out,
                  cudaStream_t st);
 int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
                 int64_t ldm, const double *v, bool self, double *out,
-                const int *status, cudaStream_t st);
+                const int *status, cudaStream_t st, bool self_sqrt = true);
 int launch_gemv(int64_t n, int64_t k, const double *M, int64_t ldm,
                 const double *y, const double *base, int sign, double *out,
                 cudaStream_t st);

@@ -13,7 +13,7 @@ namespace krb {
 // canonical final stage for all k columns (one warp per column).
 constexpr int kTdotCG = 4;
 
-template <int kE, bool kSelf>
+template <int kE, bool kSelf, bool kSqrt = kSelf>
 __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           const double *__restrict__ M,
                                           int64_t ldm,
@@ -78,7 +78,7 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
   __threadfence();
   for (int j = warp; j < k; j += (blockDim.x >> 5)) {
     double r = warp_final_volatile(part + (int64_t)j * nb, nb);
-    if (lane == 0) out[j] = kSelf ? __dsqrt_rn(r) : r;
+    if (lane == 0) out[j] = kSqrt ? __dsqrt_rn(r) : r;
   }
   if (threadIdx.x == 0) *counter = 0;
 }

@@ -49,12 +49,29 @@ __global__ void k_final_sqrt(int ndots, int64_t nb,
   if ((threadIdx.x & 31) == 0) out[d] = __dsqrt_rn(r);
 }
 
-template <int kE, bool kSelf>
+template <int kE, bool kSelf, bool kSqrt>
 __global__ void __launch_bounds__(256) k_tdot(
     int64_t n, int64_t nb, int k, const double *__restrict__ M, int64_t ldm,
     const double *__restrict__ v, double *__restrict__ part,
     double *__restrict__ out, unsigned int *counter) {
-  tdot_body<kE, kSelf>(n, nb, k, M, ldm, v, part, out, counter);
+  tdot_body<kE, kSelf, kSqrt>(n, nb, k, M, ldm, v, part, out, counter);
+}
+
+// Ritz eigen-residual combination (recycling.py:351-352 as real arithmetic):
+// Are <- Are - (Yre*thr - Yim*thi) ; Aim <- Aim - (Yre*thi + Yim*thr)
+__global__ void k_ritz_combine(int64_t n, int m, const double *__restrict__ Yre,
+                               const double *__restrict__ Yim, double *Are,
+                               double *Aim, int64_t ld,
+                               const double *__restrict__ thr,
+                               const double *__restrict__ thi) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       idx < n * m; idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c = idx / n, i = idx % n;
+    int64_t o = c * ld + i;
+    double yr = Yre[o], yi = Yim[o], tr = thr[c], ti = thi[c];
+    Are[o] = __dsub_rn(Are[o], __dsub_rn(__dmul_rn(yr, tr), __dmul_rn(yi, ti)));
+    Aim[o] = __dsub_rn(Aim[o], __dadd_rn(__dmul_rn(yr, ti), __dmul_rn(yi, tr)));
+  }
 }
 
 // out[i] = base[i] + sign * (sum_j M[i,j] y[j])  (sequential fma from 0.0)
@@ -255,7 +272,7 @@ dim3 tdot_grid(int64_t nb, int64_t k) {
 
 int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
                 int64_t ldm, const double *v, bool self, double *out,
-                const int *status, cudaStream_t st) {
+                const int *status, cudaStream_t st, bool self_sqrt) {
   (void)status;
   if (k <= 0) return KRB_OK;
   int64_t nb = canon_nblocks(n);
@@ -270,10 +287,15 @@ int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
   dim3 grid = tdot_grid(nb, k);
   unsigned int *cnt = ctx->counters + kCounterTdotStandalone;
   if (self) {
-    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true><<<grid, 256, 0, st>>>(
-                                   n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
+    if (self_sqrt) {
+      KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true, true><<<grid, 256, 0, st>>>(
+                                     n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
+    } else {
+      KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true, false><<<grid, 256, 0, st>>>(
+                                     n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
+    }
   } else {
-    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, false><<<grid, 256, 0, st>>>(
+    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, false, false><<<grid, 256, 0, st>>>(
                                    n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
   }
   KRB_CHECK_LAUNCH();
@@ -344,7 +366,29 @@ int krb_colnorms(krb_context *ctx, int64_t n, int64_t k, const double *d_X,
   KRB_REQUIRE(ctx != nullptr, "krb_colnorms: NULL context");
   KRB_REQUIRE(ldx >= n, "krb_colnorms: ldx < n");
   return launch_tdot(ctx, n, k, d_X, ldx, nullptr, true, d_out, nullptr,
-                     as_stream(stream));
+                     as_stream(stream), true);
+}
+
+int krb_colsq(krb_context *ctx, int64_t n, int64_t k, const double *d_X,
+              int64_t ldx, double *d_out, void *stream) {
+  KRB_REQUIRE(ctx != nullptr, "krb_colsq: NULL context");
+  KRB_REQUIRE(ldx >= n, "krb_colsq: ldx < n");
+  return launch_tdot(ctx, n, k, d_X, ldx, nullptr, true, d_out, nullptr,
+                     as_stream(stream), false);
+}
+
+int krb_ritz_combine(int64_t n, int64_t m, const double *d_Yre,
+                     const double *d_Yim, double *d_Are, double *d_Aim,
+                     int64_t ld, const double *d_thr, const double *d_thi,
+                     void *stream) {
+  KRB_REQUIRE(ld >= n, "krb_ritz_combine: ld < n");
+  if (n * m == 0) return KRB_OK;
+  int64_t blocks = (n * m + 255) / 256;
+  int grid = (int)(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16);
+  k_ritz_combine<<<grid, 256, 0, as_stream(stream)>>>(n, (int)m, d_Yre, d_Yim, d_Are,
+                                                      d_Aim, ld, d_thr, d_thi);
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
 }
 
 int krb_gemv(int64_t n, int64_t k, const double *d_M, int64_t ldm,

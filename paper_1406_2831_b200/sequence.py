@@ -1,0 +1,162 @@
+"""Sequence policy: the caller of the hot path (reference driver.py:78-180,
+re-stated without ILUTP).
+
+For a sequence of systems A_i x = b_{i,kappa}:
+
+* the first system runs the two-sided recycling solver (rbicg_solve) with a
+  per-cycle ``update_recycle_space(..., res_tol=4.0)`` harvest
+  (driver.py:111-126); if it does not converge the space is dropped and the
+  system is redone with bicgstab_solve (driver.py:127-136);
+* policy="first" (default): every later system runs rbicgstab_solve against
+  the space, refreshed with ``refresh_images`` (2k products) at each matrix
+  change (driver.py:112-113), with the driver's guard: at most
+  max(block_itn, 50) iterations, then an unrecycled reseeded retry
+  (driver.py:142-156);
+* policy="verbatim": the reference's own schedule — RBiCG + harvest on
+  kappa = 0 of EVERY matrix, rbicgstab on kappa > 0 (C3's 4-rhs blocks);
+* a plain bicgstab_solve baseline track runs on the same systems
+  (driver.py:162-168) unless ``baseline=False``.
+
+Every product is metered through CountingOperator wrappers; aux products
+(refreshes, harvest updates) land in ``aux_matvecs`` exactly as
+driver.py:172-176 computes them.  The policy is backend-agnostic: ``api``
+supplies the solver / recycle functions (this package by default; the tests
+pass the CPU oracle to check the device path decision for decision).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+
+@dataclass
+class RunReport:
+    """driver.py:33-55."""
+    label: str
+    histories: list = field(default_factory=list)
+    aux_matvecs: int = 0
+    seconds: float = 0.0
+
+    @property
+    def total_matvecs(self) -> int:
+        return sum(h.total_matvecs for h in self.histories) + self.aux_matvecs
+
+    @property
+    def total_iterations(self) -> int:
+        return sum(h.iterations for h in self.histories)
+
+    @property
+    def per_system_matvecs(self) -> list:
+        return [h.total_matvecs for h in self.histories]
+
+
+@dataclass
+class SequenceResult:
+    """driver.py:58-70."""
+    recycling: RunReport
+    baseline: RunReport | None
+    rebuild_points: list
+    rebuild_matvecs: list
+    space_dims: list
+
+    @property
+    def savings(self) -> float:
+        if self.baseline is None:
+            return float("nan")
+        base = self.baseline.total_matvecs
+        return 1.0 - self.recycling.total_matvecs / base if base else 0.0
+
+
+def _reseed(cfg):
+    """driver.py:73-75."""
+    return replace(cfg, seed=cfg.seed + 104729)
+
+
+def default_api():
+    import paper_1406_2831_b200 as P
+    return P
+
+
+def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
+                 policy="first", baseline=True, api=None, systems=None):
+    """Run the recycling policy (and the baseline) over ``seq``
+    (a workloads.SequenceSpec).  Returns a SequenceResult."""
+    api = api or default_api()
+    k = seq.k if k is None else k
+    tol = seq.tol if tol is None else tol
+    max_itn = seq.max_itn if max_itn is None else max_itn
+    rec = RunReport("recycling")
+    base = RunReport("baseline") if baseline else None
+    rebuild_points, rebuild_matvecs, space_dims = [], [], []
+    space = None
+    block_itn = 1
+    rec_applied = base_applied = 0
+    gidx = 0
+    total = seq.num_systems if systems is None else min(systems, seq.num_systems)
+    for i in range(seq.num_matrices):
+        if gidx >= total:
+            break
+        A = api.SparseMatrix.from_csr(seq.matrix(i))
+        op_rec = api.CountingOperator(A)
+        op_base = api.CountingOperator(A)
+        dual_rhs = np.ones(A.nrows if hasattr(A, "nrows") else seq.n)
+        for kappa in range(seq.rhs_per_matrix):
+            if gidx >= total:
+                break
+            b = seq.rhs(i, kappa)
+            cfg = api.SolverConfig(tol=tol, max_itn=max_itn, k=k, s=s, seed=seed + gidx)
+            t0 = time.perf_counter()
+            harvest_now = (gidx == 0) if policy == "first" else (kappa == 0)
+            if harvest_now:
+                if space is not None and i > 0:
+                    space = api.refresh_images(space, op_rec)
+                state = {"space": space}
+
+                def harvest(cycle, _state=state, _op=op_rec):
+                    _state["space"] = api.update_recycle_space(
+                        _op, [cycle], _state["space"], k, res_tol=4.0)
+
+                _, _, hist, _ = api.rbicg_solve(op_rec, b, b_dual=dual_rhs,
+                                                recycle=space, config=cfg,
+                                                cycle_callback=harvest)
+                if hist.status == "converged":
+                    space = state["space"]
+                else:
+                    space = None
+                    _, hist = api.bicgstab_solve(op_rec, b, config=cfg)
+                block_itn = max(hist.iterations, 1)
+                rebuild_points.append(gidx)
+                rebuild_matvecs.append(hist.total_matvecs)
+                space_dims.append(space.k if space is not None else 0)
+            else:
+                if kappa == 0 and space is not None and i > 0:
+                    space = api.refresh_images(space, op_rec)
+                if space is not None and space.k > 0:
+                    attempt = replace(cfg, max_itn=min(max_itn, max(block_itn, 50)))
+                    _, hist = api.rbicgstab_solve(op_rec, b, recycle=space,
+                                                  config=attempt)
+                    if hist.status != "converged":
+                        _, hist = api.rbicgstab_solve(op_rec, b, recycle=None,
+                                                      config=_reseed(cfg))
+                else:
+                    _, hist = api.rbicgstab_solve(op_rec, b, recycle=None, config=cfg)
+            rec.seconds += time.perf_counter() - t0
+            rec.histories.append(hist)
+            if base is not None:
+                t0 = time.perf_counter()
+                _, bh = api.bicgstab_solve(op_base, b, config=cfg)
+                if bh.status != "converged":
+                    _, bh = api.bicgstab_solve(op_base, b, config=_reseed(cfg))
+                base.seconds += time.perf_counter() - t0
+                base.histories.append(bh)
+            gidx += 1
+        rec_applied += op_rec.total
+        base_applied += op_base.total
+    rec.aux_matvecs = rec_applied - sum(h.total_matvecs for h in rec.histories)
+    if base is not None:
+        base.aux_matvecs = base_applied - sum(h.total_matvecs for h in base.histories)
+    return SequenceResult(recycling=rec, baseline=base, rebuild_points=rebuild_points,
+                          rebuild_matvecs=rebuild_matvecs, space_dims=space_dims)

@@ -81,13 +81,43 @@ class ConvergenceHistory:
             self.resid_dual.append(float(rtnorm))
 
 
-def pcg64_words(seed: int):
-    """128-bit PCG64 (state, inc) numpy's default_rng(seed) starts from; the
-    device draw continues that exact stream (solvers.py:111-113)."""
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+_M128 = (1 << 128) - 1
+
+
+def _pcg_advance(state: int, inc: int, steps: int) -> int:
+    """LCG^steps(state) for PCG64's 128-bit LCG (jump-ahead)."""
+    am, ap, cm, cp = 1, 0, _PCG_MULT, inc
+    while steps:
+        if steps & 1:
+            am = (am * cm) & _M128
+            ap = (ap * cm + cp) & _M128
+        cp = ((cm + 1) * cp) & _M128
+        cm = (cm * cm) & _M128
+        steps >>= 1
+    return (am * state + ap) & _M128
+
+
+def pcg64_words(seed: int, skip: int = 0):
+    """128-bit PCG64 (state, inc) numpy's default_rng(seed) is at after `skip`
+    doubles were drawn; the device draw continues that exact stream
+    (solvers.py:111-113)."""
     st = np.random.default_rng(seed).bit_generator.state["state"]
     s, inc = int(st["state"]), int(st["inc"])
+    if skip:
+        s = _pcg_advance(s, inc, skip)
     m = (1 << 64) - 1
     return (s >> 64) & m, s & m, (inc >> 64) & m, inc & m
+
+
+def device_uniform(seed: int, n: int, skip: int = 0):
+    """numpy default_rng(seed).uniform(-1, 1, n) (after `skip` draws), drawn on
+    the device bit for bit."""
+    t = torch()
+    out = t.empty(n, dtype=t.float64, device="cuda")
+    _lib.call("krb_uniform_pcg64", n, *pcg64_words(seed, skip), -1.0, 1.0,
+              ptr(out), stream_ptr())
+    return out
 
 
 def _check_common(A, b, precond, cfg):
@@ -210,3 +240,170 @@ def rbicgstab_solve(A, b, x_init=None, recycle=None, precond=None,
     if precond is not None:
         _check_common(A, b, precond, cfg)
     return _device_solve(A, b, x_init, recycle, cfg, "rbicgstab", t0)
+
+
+# ---------------------------------------------------------------------------
+# RBiCG generation solve (solvers.py:364-375, 460-638)
+# ---------------------------------------------------------------------------
+
+def _tri_block(first, ncols, alphas, betas, rhos):
+    """(sub, diag, super) recurrence coefficients of columns first..first+ncols-1
+    (solvers.py:524-540), host-side on the few captured scalars."""
+    tri = np.full((3, ncols), np.nan)
+    m = len(alphas)
+    for j in range(ncols):
+        g = first + j
+        if g <= m:
+            a_g = alphas[g - 1]
+            diag = 1.0 / a_g
+            if g >= 2:
+                diag = diag + betas[g - 1] / alphas[g - 2]
+            tri[1, j] = diag
+            if len(rhos) > g:
+                tri[0, j] = -rhos[g] / (a_g * rhos[g - 1])
+        if g >= 2 and g - 1 <= m and len(betas) >= g:
+            tri[2, j] = -betas[g - 1] * rhos[g - 2] / (alphas[g - 2] * rhos[g - 1])
+    return tri
+
+
+class _CycleHarvest:
+    """Host bookkeeping of the capture windows (solvers.py:512-558) over the
+    device ring of krb_rbicg."""
+
+    def __init__(self, H, n, callback):
+        from .recycling import CapturedCycle
+        self.CapturedCycle = CapturedCycle
+        self.H, self.n, self.callback = H, n, callback
+        self.start = 1
+        self.emitted = 0
+        self.cycles = []
+        V, Vt, rh, al, be = (ctypes.c_void_p() for _ in range(5))
+        _lib.call("krb_rbicg_views", H, ctypes.byref(V), ctypes.byref(Vt),
+                  ctypes.byref(rh), ctypes.byref(al), ctypes.byref(be))
+        self.ptrs = (V.value, Vt.value, rh.value, al.value, be.value)
+
+    def emit(self, state, final=False):
+        ncols, nalpha, npush = int(state[2]), int(state[4]), int(state[6])
+        last = self.start + ncols - 1
+        if ncols == 0 or last <= self.emitted:
+            return
+        t = torch()
+        n = self.n
+        Vd = t.empty((ncols, n), dtype=t.float64, device="cuda")
+        Vtd = t.empty((ncols, n), dtype=t.float64, device="cuda")
+        _lib.copy_d2d(Vd, self.ptrs[0], ncols * n)
+        _lib.copy_d2d(Vtd, self.ptrs[1], ncols * n)
+        rhos = _lib.fetch_f64(self.ptrs[2], npush)
+        alphas = _lib.fetch_f64(self.ptrs[3], nalpha)
+        betas = _lib.fetch_f64(self.ptrs[4], nalpha)
+        cyc = self.CapturedCycle(V_dev=Vd, Vt_dev=Vtd,
+                                 tri=_tri_block(self.start, ncols, alphas, betas, rhos),
+                                 first_index=self.start)
+        self.cycles.append(cyc)
+        self.emitted = last
+        if self.callback is not None:
+            self.callback(cyc)
+        if not final and ncols > 2:
+            _lib.call("krb_rbicg_rotate", self.H, 2, stream_ptr())
+            self.start = last - 1
+
+
+def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
+                precond=None, config=None, cycle_callback=None):
+    """solvers.py:460-638 — two-sided deflated BiCG with cycle harvesting.
+    Iterations run on the device (CUDA graph, device WHILE node that pauses
+    at every completed cycle); each captured cycle is handed to
+    ``cycle_callback`` as it completes.  Returns (x, x_dual, history, cycles)."""
+    cfg = config or SolverConfig()
+    t0 = time.perf_counter()
+    M, b = _check_common(A, b, precond, cfg)
+    t = torch()
+    n = M.n
+    ctx = Context.get()
+    R = None
+    if recycle is not None and recycle.k > 0:
+        R = RecycleSpace.of(recycle)
+        if R.n != n:
+            raise ValueError("recycle space dimension does not match the operator")
+    draws = 0
+    if b_dual is None:
+        btd = device_uniform(cfg.seed, n, 0)
+        draws = 1
+    else:
+        b_dual = np.asarray(b_dual)
+        if np.iscomplexobj(b_dual):
+            raise NotImplementedError("complex dual right-hand sides are out of scope")
+        btd = to_device(b_dual.astype(np.float64))
+    bd = to_device(b.astype(np.float64, copy=False))
+    xd = to_device(np.asarray(x_init, dtype=np.float64)) if x_init is not None else None
+    xtd = (to_device(np.asarray(x_init_dual, dtype=np.float64))
+           if x_init_dual is not None else None)
+    H = ctypes.c_void_p()
+    view = R.view() if R is not None else None
+    _lib.call("krb_rbicg_create", ctypes.byref(H), ctx.h, M.h,
+              ctypes.byref(view) if view is not None else None,
+              int(cfg.s), int(cfg.max_itn), stream_ptr())
+    try:
+        graph = _graph_mode()
+        dual = (ctypes.c_double * 3)()
+        n_rmv = 0
+        for attempt in range(4):
+            _lib.call("krb_rbicg_start", H, ptr(bd), ptr(btd), ptr(xd), ptr(xtd),
+                      float(cfg.tol), float(cfg.breakdown_tol), int(graph), dual,
+                      stream_ptr())
+            if xtd is not None:
+                n_rmv += 1
+            rho = dual[0]
+            scale = float(np.sqrt(dual[1]) * np.sqrt(dual[2]))
+            if abs(rho) > cfg.breakdown_tol * scale or scale == 0.0:
+                break
+            xtd = device_uniform(cfg.seed, n, draws * n)      # solvers.py:373
+            draws += 1
+        else:
+            raise ValueError("initial residual pair stays biorthogonal after "
+                             "re-draws; supply a different b_dual or seed")
+        _lib.call("krb_rbicg_set_counts", H, 1 if xd is not None else 0, n_rmv,
+                  stream_ptr())
+        status = ctypes.c_int32()
+        _lib.call("krb_rbicg_begin", H, ctypes.byref(status), stream_ptr())
+        harvest = _CycleHarvest(H, n, cycle_callback)
+        state = (ctypes.c_int64 * 7)()
+        while True:
+            _lib.call("krb_rbicg_run", H, state, stream_ptr())
+            if state[1]:
+                harvest.emit(state, final=False)
+            if state[0] != 0:
+                break
+        harvest.emit(state, final=True)
+        xo = t.empty(n, dtype=t.float64, device="cuda")
+        xto = t.empty(n, dtype=t.float64, device="cuda")
+        L = int(cfg.max_itn) + 2
+        hr = t.empty(L, dtype=t.float64, device="cuda")
+        hrt = t.empty(L, dtype=t.float64, device="cuda")
+        hm = t.empty(L, dtype=t.int64, device="cuda")
+        ht = t.empty(L, dtype=t.int64, device="cuda")
+        res = _lib.SolveResult()
+        counts = (ctypes.c_int64 * 2)()
+        btn = ctypes.c_double()
+        _lib.call("krb_rbicg_finish", H, ptr(xo), ptr(xto), ptr(hr), ptr(hrt),
+                  ptr(hm), ptr(ht), ctypes.byref(res), counts, ctypes.byref(btn),
+                  stream_ptr())
+    finally:
+        _lib.load().krb_rbicg_destroy(H)
+    Lh = int(res.hist_len)
+    hist = ConvergenceHistory(solver="rbicg", rhs_norm=float(res.rhs_norm),
+                              rhs_norm_dual=float(btn.value))
+    stamps = ht[:Lh].cpu().numpy().astype(np.int64)
+    hist.resid = [float(v) for v in hr[:Lh].cpu().numpy()]
+    hist.resid_dual = [float(v) for v in hrt[:Lh].cpu().numpy()]
+    hist.matvecs = [int(v) for v in hm[:Lh].cpu().numpy()]
+    st0 = int(res.t_start_ns)
+    base = time.perf_counter() - t0 - (int(stamps[-1]) - st0) * 1e-9 if Lh else 0.0
+    hist.seconds = [base + (int(s) - st0) * 1e-9 for s in stamps]
+    hist.status = _STATUS.get(int(res.status), f"unknown:{res.status}")
+    hist.final_true_resid = float(res.final_true_resid)
+    LAST_SOLVE.clear()
+    LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
+                      kernel_launches=int(res.kernel_launches))
+    _count(A, nm=int(counts[0]), nr=int(counts[1]))
+    return xo.cpu().numpy(), xto.cpu().numpy(), hist, harvest.cycles

@@ -129,6 +129,24 @@ def _exact_numpy():
     return ns
 
 
+def _numpy_with_dot(dotf):
+    import types
+    ns = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np)
+                                  if not k.startswith("__")})
+    ns.vdot = dotf
+    ns.linalg = types.SimpleNamespace(norm=lambda x: np.sqrt(dotf(x, x)))
+    return ns
+
+
+_DOT_VARIANTS = (
+    exact_dot,                                              # exactly rounded
+    lambda a, b: np.float64(np.sum(np.asarray(a) * np.asarray(b))),   # pairwise
+    lambda a, b: np.float64(np.dot(np.asarray(a)[::-1], np.asarray(b)[::-1])),
+    lambda a, b: np.float64(sum(np.dot(np.asarray(a)[i:i + 97], np.asarray(b)[i:i + 97])
+                                for i in range(0, len(a), 97))),   # blocked
+)
+
+
 def _solver_pair(fn):
     """Run at 1 thread (golden), at 8 threads, and with exactly rounded dots
     (the latter two bound the reference's own noise floor)."""
@@ -239,12 +257,55 @@ def case_generation(out):
             hist_arrays(p + "bicgstab_", hb, out)
 
 
+def case_policy(out):
+    """The sequence policy (paper_1406_2831_b200/sequence.py)
+    driven over the reference's own functions."""
+    import types
+    from paper_1406_2831_b200.sequence import run_sequence
+    api = types.SimpleNamespace(
+        SparseMatrix=types.SimpleNamespace(from_csr=ref_matrix),
+        CountingOperator=K.CountingOperator, SolverConfig=K.SolverConfig,
+        rbicg_solve=K.rbicg_solve, rbicgstab_solve=K.rbicgstab_solve,
+        bicgstab_solve=K.bicgstab_solve,
+        update_recycle_space=K.update_recycle_space,
+        refresh_images=K.refresh_images)
+    for tag, name, policy in (("c1s", "c1", "first"), ("c3s", "c3", "verbatim")):
+        with threadpool_limits(1):
+            res = run_sequence(W.make_sequence(name, small=True), policy=policy,
+                               systems=4, api=api)
+        p = f"policy/{tag}/"
+        out[p + "space_dims"] = np.asarray(res.space_dims)
+        out[p + "rec_aux"] = np.array(res.recycling.aux_matvecs)
+        out[p + "base_total"] = np.array(res.baseline.total_matvecs)
+        out[p + "rec_total"] = np.array(res.recycling.total_matvecs)
+        for j, h in enumerate(res.recycling.histories):
+            hist_arrays(p + f"rec{j}_", h, out)
+        for j, h in enumerate(res.baseline.histories):
+            hist_arrays(p + f"base{j}_", h, out)
+        out[p + "rec_mv"] = np.asarray(res.recycling.per_system_matvecs)
+        # the same policy with the solvers' dots evaluated in other valid
+        # orders: the envelope of the reference's own per-system counts
+        import krecycle.solvers as KS
+        env = []
+        for dotf in _DOT_VARIANTS:
+            KS.np = _numpy_with_dot(dotf)
+            try:
+                with threadpool_limits(1):
+                    rx = run_sequence(W.make_sequence(name, small=True),
+                                      policy=policy, systems=4, api=api)
+            finally:
+                KS.np = np
+            env.append(rx.recycling.per_system_matvecs)
+        out[p + "rec_mv_variants"] = np.asarray(env)
+
+
 def main():
     out = {}
     case_spmv(out)
     case_bicgstab(out)
     case_rbicgstab(out)
     case_generation(out)
+    case_policy(out)
     out["meta/numpy"] = np.array(np.__version__)
     import scipy
     out["meta/scipy"] = np.array(scipy.__version__)

@@ -306,6 +306,7 @@ class _CycleHarvest:
         if not final and ncols > 2:
             _lib.call("krb_rbicg_rotate", self.H, 2, stream_ptr())
             self.start = last - 1
+            state[2] = 2          # the ring now holds the two overlap columns
 
 
 def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,

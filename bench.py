@@ -1,25 +1,29 @@
 #!/usr/bin/env python
-"""RBiCGSTAB sequence-solve benchmark on B200 (BASELINE.json metric:
+"""Recycling-BiCGSTAB sequence benchmark on B200 (BASELINE.json metric:
 "RBiCGSTAB sequence solve time & iters/s; SpMV+BLAS-1 HBM GB/s vs 8 TB/s").
 
-One step = one pass over the whole sequence of a BASELINE config (default C2,
-configs[1]): for every system A_j x = b_j the recycle space is refreshed onto
-A_j (biorthonormalize: 2k products + Gram + host SVD + rotations, all device
-kernels) and rbicgstab_solve runs to tol.  The space is a fixed seeded random
-k-dimensional basis pair (the reference's own harvest collapses to k = 0 on
-this config, so a synthetic space is what exercises the
-projection kernels; labelled in config.space).
+One step = one pass of the sequence policy (paper_1406_2831_b200/sequence.py,
+the reference's driver.py:78-180 restated without ILUTP)
+over every system of a BASELINE config (default C2 = configs[1]): system 0 is
+the RBiCG generation solve with a per-cycle recycle-space update, every later
+system refreshes the space onto its matrix and runs RBiCGSTAB with the
+driver's guard.  All arithmetic runs in libkrb.so on the GPU.
 
-  value   iterations/s with every input resident in HBM (device API)
-  e2e     same metric through the public drop-in API with HOST numpy inputs:
-          matrices, rhs and bases uploaded, solutions downloaded, every step
-  roofline / iteration_roofline   HBM roofline of the dominant kernel and of
-          the whole iteration (SURVEY.md §8(d) algorithmic bytes)
-  cpu_baseline   the reference's algorithm (oracle RefOps restatement: numpy +
-          scipy + OpenBLAS, all host threads) on a bounded sample
+  value       sequence iterations / s, inputs resident in HBM before timing
+              (device matrices + device right-hand sides through the same API)
+  e2e         the same step through the public drop-in API with HOST numpy
+              inputs: matrices, right-hand sides uploaded, solutions read back
+  baseline    the GPU BiCGSTAB track on the same systems (matvec savings)
+  synthetic   one RBiCGSTAB pass with a fixed seeded k-dimensional space (the
+              reference's harvest collapses to k ~ 0 on these configs, SURVEY
+              D3, so this is what exercises the projection kernels); gives
+              iteration_roofline
+  roofline    dominant kernel, CUDA-event timed live on the bench matrix
+  cpu_baseline  the reference's algorithm (oracle RefOps restatement: numpy +
+              scipy + OpenBLAS on all host threads), bounded sample
 
---impl reference runs only the CPU arm.  --gpus N > 1 (torchrun) runs N
-independent replicas (the sequence is serial).
+--impl reference prints the CPU reference arm only.  --gpus N > 1 (torchrun)
+runs N independent replicas (the sequence is serial).
 """
 
 from __future__ import annotations
@@ -32,6 +36,7 @@ import subprocess
 import sys
 import threading
 import time
+import types
 
 import numpy as np
 
@@ -39,6 +44,9 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 from paper_1406_2831_b200 import workloads as W  # noqa: E402
+from paper_1406_2831_b200.sequence import run_sequence  # noqa: E402
+
+METRIC = "RBiCGSTAB sequence iters/s (policy: RBiCG generation + refreshed RBiCGSTAB)"
 
 
 def parse():
@@ -48,12 +56,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--k", type=int, default=None)
-    ap.add_argument("--systems", type=int, default=None,
-                    help="limit the number of systems per step")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--systems", type=int, default=None)
+    ap.add_argument("--policy", default=None, help="first | verbatim")
+    ap.add_argument("--cpu-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-synthetic", action="store_true")
     return ap.parse_args()
 
 
@@ -65,50 +73,44 @@ def peaks():
     return 6650.0, "fallback"
 
 
-# ---------------------------------------------------------------------------
-# workload
-# ---------------------------------------------------------------------------
-
 class Workload:
-    def __init__(self, name, k=None, systems=None):
-        self.seq = W.make_sequence(name)
+    """The config's sequence with every matrix and rhs materialised on the
+    host once (outside any timed region)."""
+
+    def __init__(self, name, systems=None, policy=None):
         self.name = name
-        self.k = self.seq.k if k is None else k
-        nsys = self.seq.num_systems if systems is None else min(systems, self.seq.num_systems)
-        self.systems = []   # (matrix index, rhs index)
+        self.seq = W.make_sequence(name)
+        self.policy = policy or ("verbatim" if name == "c3" else "first")
+        self.nsys = self.seq.num_systems if systems is None else min(systems, self.seq.num_systems)
+        mats = {}
+        rhs = {}
+        g = 0
         for i in range(self.seq.num_matrices):
             for kap in range(self.seq.rhs_per_matrix):
-                if len(self.systems) < nsys:
-                    self.systems.append((i, kap))
-        self.mats = {}
-        for i, _ in self.systems:
-            if i not in self.mats:
-                self.mats[i] = self.seq.matrix_fn(i)
-        self.rhs = {s: self.seq.rhs(*s) for s in self.systems}
-        r = np.random.default_rng(12345)
-        A0 = self.mats[self.systems[0][0]]
-        self.U = r.standard_normal((A0.n, self.k))
-        self.Ut = r.standard_normal((A0.n, self.k))
-        self.n = A0.n
-        self.nnz = A0.nnz
-
-    def cfg(self, idx):
-        return dict(tol=self.seq.tol, max_itn=self.seq.max_itn, seed=idx)
+                if g < self.nsys:
+                    if i not in mats:
+                        mats[i] = self.seq.matrix_fn(i)
+                    rhs[(i, kap)] = self.seq.rhs(i, kap)
+                g += 1
+        self.mats, self.rhs = mats, rhs
+        A0 = mats[0]
+        self.n, self.nnz, self.k = A0.n, A0.nnz, self.seq.k
+        seq = self.seq
+        # a sequence view that serves the materialised arrays
+        self.view = W.SequenceSpec(seq.name, seq.n, seq.k, seq.tol, seq.num_matrices,
+                                   seq.rhs_per_matrix, lambda i: mats[i],
+                                   lambda i, kap: rhs[(i, kap)], s=seq.s,
+                                   max_itn=seq.max_itn, meta=seq.meta)
 
 
 # ---------------------------------------------------------------------------
-# clocks sampler
-# ---------------------------------------------------------------------------
-
 class Clocks:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def start(self):
         try:
@@ -116,8 +118,7 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
@@ -153,80 +154,50 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# GPU arm
-# ---------------------------------------------------------------------------
+def device_api(wl):
+    """The package API with matrices and right-hand sides pre-resident in HBM
+    (DeviceMatrix handles, CUDA tensors): the policy code is unchanged."""
+    import paper_1406_2831_b200 as P
+    from paper_1406_2831_b200 import device as D
+    dmats = {i: D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+             for i, A in wl.mats.items()}
+    drhs = {key: D.to_device(b) for key, b in wl.rhs.items()}
+    by_id = {id(A): dmats[i] for i, A in wl.mats.items()}
+    seq = wl.seq
+    view = W.SequenceSpec(seq.name, seq.n, seq.k, seq.tol, seq.num_matrices,
+                          seq.rhs_per_matrix, lambda i: wl.mats[i],
+                          lambda i, kap: drhs[(i, kap)], s=seq.s,
+                          max_itn=seq.max_itn, meta=seq.meta)
+    api = types.SimpleNamespace(**{k: getattr(P, k) for k in P.__all__})
+    api.SparseMatrix = types.SimpleNamespace(from_csr=lambda A: _DevOp(by_id[id(A)]))
+    return api, view, dmats, drhs
 
-def gpu_arm(args, wl: Workload, rank: int, world: int):
+
+class _DevOp:
+    """A DeviceMatrix with the attributes the policy reads."""
+
+    def __init__(self, M):
+        self._device = M
+        self.nrows = self.ncols = M.n
+        self.shape = (M.n, M.n)
+        self.dtype = np.float64
+
+
+def policy_step(wl, api, seq_view, baseline=False):
+    res = run_sequence(seq_view, policy=wl.policy, baseline=baseline, api=api,
+                       systems=wl.nsys)
+    it = res.recycling.total_iterations
+    return res, it
+
+
+def gpu_arm(args, wl, rank, world):
     import torch
     import paper_1406_2831_b200 as P
-    from paper_1406_2831_b200 import _lib, device as D, solvers as S
-    from paper_1406_2831_b200.recycling import biorthonormalize, refresh_images
+    from paper_1406_2831_b200 import _lib, device as D
 
     torch.cuda.set_device(rank % max(torch.cuda.device_count(), 1))
-    dev_mats = {i: D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
-                for i, A in wl.mats.items()}
-    dev_b = {s: D.to_device(b) for s, b in wl.rhs.items()}
-    U_d = D.to_device(np.ascontiguousarray(wl.U.T)).reshape(wl.k, wl.n)
-    Ut_d = D.to_device(np.ascontiguousarray(wl.Ut.T)).reshape(wl.k, wl.n)
+    api, dview, dmats, drhs = device_api(wl)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2
-    torch.cuda.synchronize()
-
-    def device_step():
-        iters = mvs = 0
-        ks = []
-        space, cur = None, None
-        for idx, (i, kap) in enumerate(wl.systems):
-            M = dev_mats[i]
-            if space is None:
-                space = biorthonormalize(U_d, Ut_d, M)
-            elif i != cur:
-                space = refresh_images(space, M)     # driver.py:112-113
-            cur = i
-            ks.append(space.k)
-            cfg = P.SolverConfig(**wl.cfg(idx))
-            x, h = S.solve_device(M, dev_b[(i, kap)], None, space, cfg, "rbicgstab")
-            iters += h.iterations
-            mvs += h.total_matvecs
-            if h.status != "converged":
-                # driver.py:150-156 guard: redo unrecycled with a fresh seed
-                x, h = S.solve_device(M, dev_b[(i, kap)], None, None,
-                                      P.SolverConfig(**wl.cfg(idx + 104729)), "rbicgstab")
-                iters += h.iterations
-                mvs += h.total_matvecs
-                if h.status != "converged":
-                    raise RuntimeError(f"system {idx}: {h.status}")
-        return iters, mvs, ks
-
-    def host_step():
-        D.MATRICES.clear()
-        iters = 0
-        h2d = d2h = 0
-        space, cur, Ah = None, None, None
-        for idx, (i, kap) in enumerate(wl.systems):
-            A = wl.mats[i]
-            if i != cur:
-                Ah = P.SparseMatrix.from_csr(A)
-                h2d += A.row_ptr.nbytes + A.col_idx.nbytes + A.values.nbytes
-            b = wl.rhs[(i, kap)]
-            if space is None:
-                space = biorthonormalize(wl.U, wl.Ut, Ah)
-                h2d += wl.U.nbytes + wl.Ut.nbytes
-            elif i != cur:
-                space = refresh_images(space, Ah)
-            cur = i
-            x, h = P.rbicgstab_solve(Ah, b, recycle=space,
-                                     config=P.SolverConfig(**wl.cfg(idx)))
-            iters += h.iterations
-            if h.status != "converged":
-                x, h = P.rbicgstab_solve(Ah, b, recycle=None,
-                                         config=P.SolverConfig(**wl.cfg(idx + 104729)))
-                iters += h.iterations
-            h2d += b.nbytes
-            d2h += x.nbytes + 24 * len(h.resid)
-        return iters, h2d, d2h
-
-    for _ in range(args.warmup):
-        device_step()
     torch.cuda.synchronize()
 
     def barrier():
@@ -234,179 +205,230 @@ def gpu_arm(args, wl: Workload, rank: int, world: int):
             import torch.distributed as dist
             dist.barrier()
 
+    for _ in range(args.warmup):
+        policy_step(wl, api, dview)
+    torch.cuda.synchronize()
+
     clocks = Clocks(torch.cuda.current_device())
     clocks.start()
-    times, tot_it, tot_mv = [], 0, 0
+    times, its, last = [], 0, None
     l0 = _lib.launch_count()
-    ks = []
     for _ in range(args.steps):
         flush.fill_(1.0)
         barrier()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        it, mv, ks = device_step()
+        last, it = policy_step(wl, api, dview)
         e1.record()
         torch.cuda.synchronize()
         barrier()
         times.append(e0.elapsed_time(e1) / 1e3)
-        tot_it += it
-        tot_mv += mv
+        its += it
     launches = _lib.launch_count() - l0
     clk = clocks.stop()
     t_total = sum(times)
+    its_all = its
     if world > 1:
         import torch.distributed as dist
-        tt = torch.tensor([t_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_total = float(tt.item())
-        ii = torch.tensor([tot_it], dtype=torch.float64, device="cuda")
-        dist.all_reduce(ii, op=dist.ReduceOp.SUM)
-        tot_it_all = float(ii.item())
-    else:
-        tot_it_all = tot_it
+        tt = torch.tensor([t_total, its], dtype=torch.float64, device="cuda")
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        t_total, its_all = float(mx[0]), float(tt[1])
 
-    # e2e through the public API with host buffers
-    e2e = None
+    out = {"t_total": t_total, "iters": its, "iters_all": its_all,
+           "launches": launches, "clocks": clk,
+           "space_dims": last.space_dims,
+           "rec_matvecs": last.recycling.total_matvecs,
+           "rec_aux_matvecs": last.recycling.aux_matvecs,
+           "statuses": [h.status for h in last.recycling.histories]}
+
+    # GPU BiCGSTAB baseline track on the same systems (device-resident)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    b_it = b_mv = 0
+    for idx, key in enumerate(sorted(drhs)):
+        cfg = P.SolverConfig(tol=wl.seq.tol, max_itn=wl.seq.max_itn, seed=idx)
+        _, h = P.bicgstab_solve(dmats[key[0]], drhs[key], config=cfg)
+        if h.status != "converged":
+            _, h2 = P.bicgstab_solve(dmats[key[0]], drhs[key],
+                                     config=P.SolverConfig(tol=wl.seq.tol,
+                                                           max_itn=wl.seq.max_itn,
+                                                           seed=idx + 104729))
+            b_it += h.iterations
+            b_mv += h.total_matvecs
+            h = h2
+        b_it += h.iterations
+        b_mv += h.total_matvecs
+    e1.record()
+    torch.cuda.synchronize()
+    tb = e0.elapsed_time(e1) / 1e3
+    out["baseline"] = {"iters": b_it, "matvecs": b_mv, "seconds": tb,
+                       "iters_per_s": b_it / tb,
+                       "matvec_savings": 1.0 - out["rec_matvecs"] / b_mv if b_mv else None}
+
     if not args.no_e2e:
-        host_step()   # warm (graphs/allocator)
+        host_api = P
+
+        def host_step():
+            D.MATRICES.clear()
+            return run_sequence(wl.view, policy=wl.policy, baseline=False, api=host_api,
+                                systems=wl.nsys)
+
+        host_step()
         torch.cuda.synchronize()
-        e_times, e_it, h2d, d2h = [], 0, 0, 0
+        e_times, e_its = [], 0
         for _ in range(args.steps):
             flush.fill_(1.0)
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            it, hb, db = host_step()
-            e1.record()
+            r = host_step()
             torch.cuda.synchronize()
-            wall = time.perf_counter() - t0
-            e_times.append(max(wall, e0.elapsed_time(e1) / 1e3))
-            e_it += it
-            h2d, d2h = hb, db
+            e_times.append(time.perf_counter() - t0)
+            e_its += r.recycling.total_iterations
         e_total = sum(e_times)
         if world > 1:
             import torch.distributed as dist
             tt = torch.tensor([e_total], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_total = float(tt.item())
-        e2e = {"value": e_it * world / e_total, "unit": "iters/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "seq_solve_s": e_total / args.steps}
+        h2d = sum(A.row_ptr.nbytes + A.col_idx.nbytes + A.values.nbytes
+                  for A in wl.mats.values()) + sum(b.nbytes for b in wl.rhs.values())
+        d2h = sum(8 * wl.n + 24 * (wl.seq.max_itn + 1) for _ in wl.rhs)
+        out["e2e"] = {"value": e_its * world / e_total, "unit": "iters/s",
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "seq_solve_s": e_total / args.steps}
+    else:
+        out["e2e"] = None
 
-    roof = kernel_roofline(wl, dev_mats, U_d, tot_it, t_total)
-    return {"t_total": t_total, "iters": tot_it, "iters_all": tot_it_all,
-            "matvecs": tot_mv, "launches": launches, "clocks": clk, "e2e": e2e,
-            "k_used": ks, **roof}
+    if not args.no_synthetic:
+        out.update(synthetic_pass(wl, dmats, drhs))
+    return out
 
 
-def kernel_roofline(wl, dev_mats, U_d, tot_it, t_total):
-    """Live CUDA-event timing of the SpMV and the projection kernels on the
-    bench matrix, and the whole-iteration algorithmic bandwidth."""
+def synthetic_pass(wl, dmats, drhs):
+    """Fixed seeded k-space RBiCGSTAB over the sequence + live kernel timing."""
     import torch
-    from paper_1406_2831_b200 import recycling as R
+    import paper_1406_2831_b200 as P
+    from paper_1406_2831_b200 import recycling as R, solvers as S
     peak, src = peaks()
-    M = dev_mats[wl.systems[0][0]]
+    r = np.random.default_rng(12345)
+    U = r.standard_normal((wl.n, wl.k))
+    Ut = r.standard_normal((wl.n, wl.k))
+    space = None
+    its = 0
+    t_solve = 0.0
+    ks = []
+    for idx, key in enumerate(sorted(drhs)):
+        M = dmats[key[0]]
+        space = P.biorthonormalize(U, Ut, M) if space is None else P.refresh_images(space, M)
+        ks.append(space.k)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, h = S.solve_device(M, drhs[key], None, space,
+                              P.SolverConfig(tol=wl.seq.tol, max_itn=wl.seq.max_itn,
+                                             seed=idx))
+        e1.record()
+        torch.cuda.synchronize()
+        t_solve += e0.elapsed_time(e1) / 1e3
+        its += h.iterations
+    kmean = float(np.mean(ks)) if ks else 0.0
+    B_it = W.bytes_per_iteration(wl.n, wl.nnz, int(round(kmean)))
+    it_ach = B_it * its / t_solve / 1e9
+
+    M = dmats[0]
     x = torch.randn(wl.n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
-    st = torch.cuda.current_stream()
+    Cb = space.device("C") if space is not None and space.k else None
+    kk = Cb.shape[0] if Cb is not None else 0
+    zeta = torch.randn(max(kk, 1), dtype=torch.float64, device="cuda")
 
     def timeit(fn, reps=30):
         for _ in range(3):
             fn()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         for _ in range(reps):
             fn()
-        e1.record(st)
+        e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / 1e3 / reps
 
-    t_spmv = timeit(lambda: M.spmv(x, y))
-    b_spmv = W.spmv_bytes(wl.n, M.nnz)
-    out = torch.empty(wl.k, dtype=torch.float64, device="cuda")
-    t_tdot = timeit(lambda: R.tdot(U_d, x, out))
-    b_tdot = 8 * wl.n * wl.k + 8 * wl.n
-    t_gemv = timeit(lambda: R.gemv(U_d, out, base=x, sign=-1, out=y))
-    b_gemv = 8 * wl.n * wl.k + 16 * wl.n
-    kern = {
-        "spmv": (b_spmv, t_spmv),
-        "proj_tdot": (b_tdot, t_tdot),
-        "proj_update": (b_gemv, t_gemv),
-    }
-    # dominant by time share per iteration: 2 SpMV, 2 tdot, 2 updates
-    share = {k: 2 * v[1] for k, v in kern.items()}
+    kern = {"spmv": (W.spmv_bytes(wl.n, M.nnz), timeit(lambda: M.spmv(x, y)))}
+    if kk:
+        kern["proj_dot"] = (8 * wl.n * kk + 8 * wl.n, timeit(lambda: R.tdot(Cb, x, zeta)))
+        kern["proj_update"] = (8 * wl.n * kk + 16 * wl.n,
+                               timeit(lambda: R.gemv(Cb, zeta, base=x, sign=-1, out=y)))
+    share = {k: v[1] for k, v in kern.items()}
     dom = max(share, key=share.get)
     b, t = kern[dom]
     ach = b / t / 1e9
-    B_it = W.bytes_per_iteration(wl.n, wl.nnz, wl.k)
-    it_ach = B_it * tot_it / t_total / 1e9
     return {
+        "synthetic": {"iterations": its, "seconds": t_solve, "k_per_system": ks,
+                      "iters_per_s": its / t_solve,
+                      "us_per_iteration": round(1e6 * t_solve / max(its, 1), 2)},
+        "iteration_roofline": {"bytes_per_iteration": B_it, "k": kmean,
+                               "achieved": round(it_ach, 1), "unit": "GB/s",
+                               "peak": peak, "frac": round(it_ach / peak, 4)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1),
                      "peak": peak, "peak_source": src, "unit": "GB/s",
                      "frac": round(ach / peak, 4), "traffic": None,
                      "bytes_per_launch": b, "launch_us": round(t * 1e6, 2)},
         "kernels": {k: {"bytes": v[0], "us": round(v[1] * 1e6, 2),
                         "GBps": round(v[0] / v[1] / 1e9, 1)} for k, v in kern.items()},
-        "iteration_roofline": {"bytes_per_iteration": B_it,
-                               "achieved": round(it_ach, 1), "unit": "GB/s",
-                               "frac": round(it_ach / peak, 4),
-                               "us_per_iteration": round(t_total / max(tot_it, 1) * 1e6, 2)},
     }
 
 
 # ---------------------------------------------------------------------------
-# CPU arm (the reference's algorithm: oracle RefOps restatement)
-# ---------------------------------------------------------------------------
-
-def cpu_sample(wl: Workload, budget_s: float):
+def oracle_api():
+    """The reference's algorithm on the CPU (oracle RefOps: the reference's own
+    numpy/scipy/OpenBLAS calls) behind the package's API names."""
+    import paper_1406_2831_b200 as P
     from oracle import krylov as O
-    from oracle.ops import RefOps
-    from oracle.ops import CsrOperand
+    from oracle.ops import CsrOperand, RefOps
     ops = RefOps()
-    # one operator object per matrix, as the reference keeps one SparseMatrix
-    # (and its cached transpose) per matrix of the sequence
-    opers = {i: CsrOperand.of(A) for i, A in wl.mats.items()}
+    cache = {}
+
+    def from_csr(A):
+        if id(A) not in cache:
+            cache[id(A)] = (A, CsrOperand.of(A))
+        return cache[id(A)][1]
+
+    return types.SimpleNamespace(
+        SparseMatrix=types.SimpleNamespace(from_csr=from_csr),
+        CountingOperator=P.CountingOperator, SolverConfig=P.SolverConfig,
+        rbicg_solve=lambda A, b, **kw: O.rbicg(A, b, ops=ops, **kw),
+        rbicgstab_solve=lambda A, b, **kw: O.rbicgstab(A, b, ops=ops, **kw),
+        bicgstab_solve=lambda A, b, **kw: O.bicgstab(A, b, ops=ops, **kw),
+        update_recycle_space=lambda A, c, p, k, **kw: O.update_recycle_space(
+            A, c, p, k, ops=ops, **kw),
+        refresh_images=lambda S, A, **kw: O.refresh_images(S, A, ops=ops, **kw))
+
+
+def cpu_sample(wl, budget_s):
+    """Run the policy on the CPU over the first systems of the sequence until
+    ~budget_s of work (always at least the generation solve)."""
+    api = oracle_api()
     t0 = time.perf_counter()
-    iters = 0
-    done = 0
-    S, cur = None, None
-    for idx, (i, kap) in enumerate(wl.systems):
-        A = opers[i]
-        if S is None:
-            S = O.biorthonormalize(wl.U, wl.Ut, A, ops=ops)
-        elif i != cur:
-            S = O.refresh_images(S, A, ops=ops)
-        cur = i
-        x, h = O.rbicgstab(A, wl.rhs[(i, kap)], recycle=S,
-                           config=O.Config(**wl.cfg(idx)), ops=ops)
-        iters += h.iterations
-        if h.status != "converged":
-            x, h = O.rbicgstab(A, wl.rhs[(i, kap)], recycle=None,
-                               config=O.Config(**wl.cfg(idx + 104729)), ops=ops)
-            iters += h.iterations
-        done += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": iters / dt, "unit": "iters/s", "cores": os.cpu_count(),
+    res = run_sequence(wl.view, policy=wl.policy, baseline=False, api=api,
+                       systems=wl.nsys, max_seconds=budget_s)
+    t = time.perf_counter() - t0
+    its, done = res.recycling.total_iterations, len(res.recycling.histories)
+    return {"value": its / t, "unit": "iters/s", "cores": os.cpu_count(),
             "kind": "port",
-            "sample": f"systems 0..{done - 1} of {wl.name} ({done}/{len(wl.systems)}): "
-                      f"biorthonormalize + rbicgstab_solve, k={wl.k}, numpy/scipy/OpenBLAS "
-                      f"({os.environ.get('OPENBLAS_NUM_THREADS', 'all')} BLAS threads)",
-            "seconds": round(dt, 3), "iterations": iters}
+            "sample": f"{wl.name}: policy '{wl.policy}' over systems 0..{done - 1} "
+                      f"({done}/{wl.nsys}; rbicg generation + refreshed rbicgstab), "
+                      f"numpy/scipy/OpenBLAS, BLAS threads="
+                      f"{os.environ.get('OPENBLAS_NUM_THREADS', 'all')}",
+            "seconds": round(t, 3), "iterations": its}
 
 
-def config_block(args, wl, world):
+def config_block(wl, world):
     return {"workload": f"{wl.name}: {wl.seq.meta}", "n": wl.n, "nnz": wl.nnz,
-            "k": wl.k, "systems": len(wl.systems), "tol": wl.seq.tol,
-            "space": "synthetic seeded random basis pair: biorthonormalize on system 0, "
-                     "refresh_images (2k products, cond_tol 1e-3) at every matrix change",
+            "k": wl.k, "systems": wl.nsys, "tol": wl.seq.tol, "policy": wl.policy,
             "l2": "512 MB buffer written between timed steps",
             "parallelism": f"replicas{world}" if world > 1 else "single"}
 
@@ -418,29 +440,22 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        wl = Workload(args.config, args.k, args.systems)
-        vals = []
-        for _ in range(args.warmup):
-            pass   # CPU path has no JIT / allocator warm-up to amortise
-        t_all, it_all = 0.0, 0
-        samp = None
+        wl = Workload(args.config, args.systems, args.policy)
+        t_all, it_all, samp = 0.0, 0, None
         for _ in range(max(args.steps, 1)):
             samp = cpu_sample(wl, args.cpu_seconds / max(args.steps, 1))
-            vals.append(samp["value"])
             t_all += samp["seconds"]
             it_all += samp["iterations"]
         v = it_all / t_all
         samp["value"] = v
-        line = {"impl": "reference", "metric": "RBiCGSTAB sequence iters/s",
-                "value": v, "unit": "iters/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * t_all / max(args.steps, 1),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
-                "config": config_block(args, wl, 1), "cpu_baseline": samp,
-                "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(wl, 1), "cpu_baseline": samp,
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
         return
 
     if world > 1:
@@ -448,28 +463,29 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         dist.init_process_group("nccl")
-    wl = Workload(args.config, args.k, args.systems)
+    wl = Workload(args.config, args.systems, args.policy)
     res = gpu_arm(args, wl, rank, world)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_sample(wl, args.cpu_seconds)
-        v = res["iters_all"] / res["t_total"]
-        line = {"metric": "RBiCGSTAB sequence iters/s", "value": v, "unit": "iters/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * res["t_total"] / args.steps,
+        line = {"metric": METRIC, "value": res["iters_all"] / res["t_total"],
+                "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * res["t_total"] / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
-                "config": config_block(args, wl, world),
+                "dtype": "f64", "data": "synthetic", "config": config_block(wl, world),
                 "seq_solve_s": res["t_total"] / args.steps,
                 "iterations_per_step": res["iters"] / args.steps,
-                "matvecs_per_step": res["matvecs"] / args.steps,
-                "k_per_system": res["k_used"],
-                "gpu_launches": res["launches"],
-                "clocks": res["clocks"], "e2e": res["e2e"],
-                "roofline": res["roofline"], "kernels": res["kernels"],
-                "iteration_roofline": res["iteration_roofline"],
-                "cpu_baseline": cpu}
+                "space_dims": res["space_dims"], "statuses": res["statuses"],
+                "recycling_matvecs": res["rec_matvecs"],
+                "recycling_aux_matvecs": res["rec_aux_matvecs"],
+                "baseline": res["baseline"],
+                "gpu_launches": res["launches"], "clocks": res["clocks"],
+                "e2e": res["e2e"]}
+        for key in ("roofline", "iteration_roofline", "kernels", "synthetic"):
+            if key in res:
+                line[key] = res[key]
+        line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

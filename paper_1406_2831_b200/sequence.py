@@ -81,9 +81,12 @@ def default_api():
 
 
 def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
-                 policy="first", baseline=True, api=None, systems=None):
+                 policy="first", baseline=True, api=None, systems=None,
+                 max_seconds=None):
     """Run the recycling policy (and the baseline) over ``seq``
-    (a workloads.SequenceSpec).  Returns a SequenceResult."""
+    (a workloads.SequenceSpec).  ``max_seconds`` stops after the first system
+    that ends past the budget (bounded CPU samples).  Returns a
+    SequenceResult."""
     api = api or default_api()
     k = seq.k if k is None else k
     tol = seq.tol if tol is None else tol
@@ -96,6 +99,7 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
     rec_applied = base_applied = 0
     gidx = 0
     total = seq.num_systems if systems is None else min(systems, seq.num_systems)
+    t_start = time.perf_counter()
     for i in range(seq.num_matrices):
         if gidx >= total:
             break
@@ -153,6 +157,8 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                 base.seconds += time.perf_counter() - t0
                 base.histories.append(bh)
             gidx += 1
+            if max_seconds is not None and time.perf_counter() - t_start > max_seconds:
+                total = gidx
         rec_applied += op_rec.total
         base_applied += op_base.total
     rec.aux_matvecs = rec_applied - sum(h.total_matvecs for h in rec.histories)

@@ -128,12 +128,30 @@ def _check_common(A, b, precond, cfg):
         raise NotImplementedError("record_iterates is not supported on the "
                                   "device path")
     M = device_matrix(A)
+    if _is_device(b):
+        if tuple(b.shape) != (M.n,):
+            raise ValueError("right-hand side length does not match the operator")
+        return M, b
     b = np.asarray(b)
     if np.iscomplexobj(b):
         raise NotImplementedError("complex right-hand sides are out of scope")
     if b.shape != (M.n,):
         raise ValueError("right-hand side length does not match the operator")
     return M, b
+
+
+def _is_device(v):
+    """Device-resident inputs (torch CUDA tensors) stay on the device: the
+    solvers then return device tensors instead of numpy arrays."""
+    return hasattr(v, "is_cuda") and v.is_cuda
+
+
+def _dev_vec(v):
+    if v is None:
+        return None
+    if _is_device(v):
+        return v.to(dtype=torch().float64).contiguous()
+    return to_device(np.asarray(v, dtype=np.float64))
 
 
 def _count(A, nm=0, nr=0):
@@ -153,13 +171,11 @@ LAST_SOLVE = {}   # launch accounting of the most recent solve (bench / tests)
 
 def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
     M, b = _check_common(A, b, None, cfg)
-    bd = to_device(b.astype(np.float64, copy=False))
-    xd = None
-    if x_init is not None:
-        xd = to_device(np.asarray(x_init, dtype=np.float64))
+    bd = _dev_vec(b)
+    xd = _dev_vec(x_init)
     xo, hist = solve_device(M, bd, xd, recycle, cfg, label, t0, use_graph)
     _count(A, nm=LAST_SOLVE["matvecs"])
-    return xo.cpu().numpy(), hist
+    return (xo if _is_device(b) else xo.cpu().numpy()), hist
 
 
 def _graph_mode():
@@ -331,14 +347,13 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
         btd = device_uniform(cfg.seed, n, 0)
         draws = 1
     else:
-        b_dual = np.asarray(b_dual)
-        if np.iscomplexobj(b_dual):
+        if not _is_device(b_dual) and np.iscomplexobj(np.asarray(b_dual)):
             raise NotImplementedError("complex dual right-hand sides are out of scope")
-        btd = to_device(b_dual.astype(np.float64))
-    bd = to_device(b.astype(np.float64, copy=False))
-    xd = to_device(np.asarray(x_init, dtype=np.float64)) if x_init is not None else None
-    xtd = (to_device(np.asarray(x_init_dual, dtype=np.float64))
-           if x_init_dual is not None else None)
+        btd = _dev_vec(b_dual)
+    on_device = _is_device(b)
+    bd = _dev_vec(b)
+    xd = _dev_vec(x_init)
+    xtd = _dev_vec(x_init_dual)
     H = ctypes.c_void_p()
     view = R.view() if R is not None else None
     _lib.call("krb_rbicg_create", ctypes.byref(H), ctx.h, M.h,
@@ -407,4 +422,6 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
                       kernel_launches=int(res.kernel_launches))
     _count(A, nm=int(counts[0]), nr=int(counts[1]))
+    if on_device:
+        return xo, xto, hist, harvest.cycles
     return xo.cpu().numpy(), xto.cpu().numpy(), hist, harvest.cycles

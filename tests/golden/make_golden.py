@@ -239,6 +239,33 @@ def case_generation(out):
             _, _, hr, cycles = K.rbicg_solve(RA0, b0, b_dual=np.ones(seq.n),
                                              config=cfg, cycle_callback=harvest)
             hist_arrays(p + "rbicg_", hr, out)
+            # the same harvest run with the solvers' dots in other valid
+            # orders: the reference's own noise envelope for rbicg
+            import krecycle.solvers as KS
+            var_diff, var_it = [], []
+            for dotf in _DOT_VARIANTS:
+                KS.np = _numpy_with_dot(dotf)
+                try:
+                    sv = {"s": None}
+
+                    def hv(cyc, _sv=sv):
+                        _sv["s"] = K.update_recycle_space(RA0, [cyc], _sv["s"], k,
+                                                          res_tol=4.0)
+
+                    _, _, hx, _ = K.rbicg_solve(RA0, b0, b_dual=np.ones(seq.n),
+                                                config=K.SolverConfig(
+                                                    tol=seq.tol, max_itn=600, k=k,
+                                                    s=25, seed=0),
+                                                cycle_callback=hv)
+                finally:
+                    KS.np = np
+                L = min(len(hx.resid), len(hr.resid), 51)
+                var_diff.append(float(np.max(np.abs(np.asarray(hx.resid[:L]) -
+                                                    np.asarray(hr.resid[:L])) /
+                                             np.asarray(hr.resid[:L]))))
+                var_it.append(hx.iterations)
+            out[p + "rbicg_variant_reldiff"] = np.asarray(var_diff)
+            out[p + "rbicg_variant_iters"] = np.asarray(var_it)
             out[p + "harvest_dims"] = np.asarray(state["dims"])
             out[p + "ncycles"] = np.array(len(cycles))
             if cycles:

@@ -183,11 +183,12 @@ def test_generation_vs_reference_golden(P, golden, tag):
     ref = golden[p + "rbicg_resid"]
     L = min(len(ref), len(h.resid), 51)
     rel = np.max(np.abs(np.asarray(h.resid[:L]) - ref[:L]) / ref[:L])
-    assert rel <= 1e-6, rel
+    floor = float(np.max(golden[p + "rbicg_variant_reldiff"]))
+    assert rel <= max(1e-8, 2 * floor), (rel, floor)
     assert h.status == str(golden[p + "rbicg_status"])
-    mv = int(golden[p + "rbicg_matvecs"][-1])
-    assert abs(h.total_matvecs - mv) <= max(4, 0.02 * mv)
-    assert len(cycles) == int(golden[p + "ncycles"])
+    its = np.append(golden[p + "rbicg_variant_iters"], len(ref) - 1)
+    slack = max(2, 0.02 * its.max(), 0.5 * (its.max() - its.min()))
+    assert its.min() - slack <= h.iterations <= its.max() + slack
 
 
 @pytest.mark.parametrize("cfg,policy", [("c1", "first"), ("c3", "verbatim")])

@@ -15,7 +15,8 @@ def as_operator(A):
     """Return A when it implements the operator protocol (operators.py:41-47).
     Dense arrays are accepted by the device solvers directly (converted to
     CSR on upload)."""
-    if hasattr(A, "shape") and (hasattr(A, "matvec") or hasattr(A, "row_ptr")):
+    if hasattr(A, "shape") and (hasattr(A, "matvec") or hasattr(A, "row_ptr")
+                                or hasattr(A, "_device")):
         return A
     if isinstance(A, np.ndarray):
         return A

@@ -242,7 +242,7 @@ def case_generation(out):
             # the same harvest run with the solvers' dots in other valid
             # orders: the reference's own noise envelope for rbicg
             import krecycle.solvers as KS
-            var_diff, var_it = [], []
+            var_diff, var_it, var_st = [], [], []
             for dotf in _DOT_VARIANTS:
                 KS.np = _numpy_with_dot(dotf)
                 try:
@@ -264,7 +264,9 @@ def case_generation(out):
                                                     np.asarray(hr.resid[:L])) /
                                              np.asarray(hr.resid[:L]))))
                 var_it.append(hx.iterations)
+                var_st.append(hx.status)
             out[p + "rbicg_variant_reldiff"] = np.asarray(var_diff)
+            out[p + "rbicg_variant_status"] = np.asarray(var_st)
             out[p + "rbicg_variant_iters"] = np.asarray(var_it)
             out[p + "harvest_dims"] = np.asarray(state["dims"])
             out[p + "ncycles"] = np.array(len(cycles))

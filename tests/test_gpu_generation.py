@@ -185,7 +185,8 @@ def test_generation_vs_reference_golden(P, golden, tag):
     rel = np.max(np.abs(np.asarray(h.resid[:L]) - ref[:L]) / ref[:L])
     floor = float(np.max(golden[p + "rbicg_variant_reldiff"]))
     assert rel <= max(1e-8, 2 * floor), (rel, floor)
-    assert h.status == str(golden[p + "rbicg_status"])
+    statuses = {str(golden[p + "rbicg_status"])} | set(map(str, golden[p + "rbicg_variant_status"]))
+    assert h.status in statuses, (h.status, statuses)
     its = np.append(golden[p + "rbicg_variant_iters"], len(ref) - 1)
     slack = max(2, 0.02 * its.max(), 0.5 * (its.max() - its.min()))
     assert its.min() - slack <= h.iterations <= its.max() + slack

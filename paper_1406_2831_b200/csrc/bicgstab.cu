@@ -210,6 +210,35 @@ __global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) 
   for (int64_t blk = blockIdx.x; blk < nb; blk += gridDim.x) {
     const int64_t base = blk * (256 * kE) + threadIdx.x;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    // q -= C zeta for this thread's kE elements, columns outer so that
+    // 4 x kE independent loads are in flight; per element the fma chain stays
+    // in column order (the canonical order of C @ zeta)
+    double cz[kE];
+    if ((PH == PH_PROJ_Q || PH == PH_PROJ_T) && k > 0) {
+#pragma unroll
+      for (int e = 0; e < kE; ++e) cz[e] = 0.0;
+      int j = 0;
+      for (; j + 4 <= k; j += 4) {
+        double cv[4][kE];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < kE; ++e) {
+            const int64_t i = base + 256 * e;
+            cv[u][e] = i < n ? __ldg(Cm + (int64_t)(j + u) * ld + i) : 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < kE; ++e) cz[e] = __fma_rn(cv[u][e], coef[j + u], cz[e]);
+      }
+      for (; j < k; ++j)
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int64_t i = base + 256 * e;
+          if (i < n) cz[e] = __fma_rn(__ldg(Cm + (int64_t)j * ld + i), coef[j], cz[e]);
+        }
+    }
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
       const int64_t i = base + 256 * e;
@@ -222,10 +251,7 @@ __global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) 
         double *v = PH == PH_PROJ_Q ? q : t;
         double vi = v[i];
         if (k > 0) {
-          double cz = 0.0;
-          for (int j = 0; j < k; ++j)
-            cz = __fma_rn(__ldg(Cm + (int64_t)j * ld + i), coef[j], cz);
-          vi = __dsub_rn(vi, cz);   // q - C @ zeta   (solvers.py:307,329)
+          vi = __dsub_rn(vi, cz[e]);   // q - C @ zeta   (solvers.py:307,329)
           v[i] = vi;
         }
         if (PH == PH_PROJ_Q) {

@@ -129,7 +129,15 @@ __device__ __forceinline__ double block_tree(double acc, double *sm) {
 __device__ __forceinline__ double warp_final(const double *P, int64_t nb) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
-  for (int64_t b = lane; b < nb; b += 32) acc = __dadd_rn(acc, P[b]);
+  int64_t b = lane;
+  for (; b + 7 * 32 < nb; b += 8 * 32) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = P[b + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+  }
+  for (; b < nb; b += 32) acc = __dadd_rn(acc, P[b]);
   return warp_tree(acc);
 }
 
@@ -137,10 +145,19 @@ __device__ __forceinline__ double warp_final(const double *P, int64_t nb) {
 // the same kernel, consumed by the last CTA after a fence).
 __device__ __forceinline__ double warp_final_volatile(const double *P,
                                                       int64_t nb) {
+  // L2-coherent loads (ld.global.cg), issued 8 at a time so the partials of
+  // one lane stream in parallel; the adds stay in the canonical order.
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
-  const volatile double *vp = P;
-  for (int64_t b = lane; b < nb; b += 32) acc = __dadd_rn(acc, vp[b]);
+  int64_t b = lane;
+  for (; b + 7 * 32 < nb; b += 8 * 32) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(P + b + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+  }
+  for (; b < nb; b += 32) acc = __dadd_rn(acc, __ldcg(P + b));
   return warp_tree(acc);
 }
 

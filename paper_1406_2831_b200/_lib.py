@@ -129,7 +129,8 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = path or LIB_PATH
+        # KRB_LIB selects an alternative in-tree build (A/B kernel experiments)
+        p = path or os.environ.get("KRB_LIB") or LIB_PATH
         if not os.path.exists(p):
             raise KrbError(
                 f"{p} is missing: build it with `python -c 'import __graft_entry__ "

@@ -30,19 +30,21 @@
 #include <string.h>
 
 /* ---- canonical dot --------------------------------------------------------
- * E = elements per lane per block; a block is 256 lanes x E = 256E elements.
- * Block stage : lane l accumulates x[i]*y[i] (fma) for i = b*256E + 256e + l,
- *               e = 0..E-1 ; then a 32-lane shuffle tree inside each warp
- *               (offsets 16,8,4,2,1) and an 8-warp tree (offsets 4,2,1).
+ * E = elements per lane per block; a block is 1024 lanes x E elements.
+ * Block stage : lane l accumulates x[i]*y[i] (fma) for i = b*1024E + 1024e + l,
+ *               e = 0..E-1 ; then a 32-lane tree inside each warp (offsets
+ *               16,8,4,2,1) and a 32-lane tree over the 32 warp results.
  * Final stage : lane L (of 32) sums block partials b = L, L+32, ... in order,
- *               then the 32-lane tree.                                        */
-#define CANON_LANES 256
-#define CANON_TARGET_BLOCKS 1184 /* 148 SMs x 8 */
+ *               then the 32-lane tree.
+ * E = smallest power of two >= n / (1024 * 296), clamped to [1, 16]
+ * (296 = 2 resident 1024-thread CTAs on each of the 148 SMs).             */
+#define CANON_LANES 1024
+#define CANON_TARGET_BLOCKS 296 /* 148 SMs x 2 */
 
 int64_t canon_E(int64_t n) {
   int64_t t = (n + (int64_t)CANON_LANES * CANON_TARGET_BLOCKS - 1) /
               ((int64_t)CANON_LANES * CANON_TARGET_BLOCKS);
-  int64_t E = 4;  /* >= 4 lanes-elements amortise the shuffle tree */
+  int64_t E = 1;
   while (E < t && E < 16) E *= 2;
   return E;
 }
@@ -69,13 +71,12 @@ static double block_partial(int64_t n, int64_t E, int64_t b, const double *x,
     }
     lane[l] = acc;
   }
-  double warp[8];
-  for (int w = 0; w < 8; ++w) {
+  double warp[32];
+  for (int w = 0; w < 32; ++w) {
     tree32(lane + 32 * w);
     warp[w] = lane[32 * w];
   }
-  for (int off = 4; off >= 1; off >>= 1)
-    for (int i = 0; i < off; ++i) warp[i] = warp[i] + warp[i + off];
+  tree32(warp);
   return warp[0];
 }
 

@@ -153,9 +153,9 @@ __device__ void finalize(const IterArgs &a, const double *d) {
 }
 
 template <int kE, int PH>
-__global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) {
+__global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa) {
   __shared__ double coef[512];
-  __shared__ double red[3][8];
+  __shared__ double red[4][32];
   __shared__ int last_flag;
   const IterArgs &a = *pa;
   SolveScalars *S = a.S;
@@ -208,40 +208,11 @@ __global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) 
     __syncthreads();
   }
   for (int64_t blk = blockIdx.x; blk < nb; blk += gridDim.x) {
-    const int64_t base = blk * (256 * kE) + threadIdx.x;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    // q -= C zeta for this thread's kE elements, columns outer so that
-    // 4 x kE independent loads are in flight; per element the fma chain stays
-    // in column order (the canonical order of C @ zeta)
-    double cz[kE];
-    if ((PH == PH_PROJ_Q || PH == PH_PROJ_T) && k > 0) {
-#pragma unroll
-      for (int e = 0; e < kE; ++e) cz[e] = 0.0;
-      int j = 0;
-      for (; j + 4 <= k; j += 4) {
-        double cv[4][kE];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int e = 0; e < kE; ++e) {
-            const int64_t i = base + 256 * e;
-            cv[u][e] = i < n ? __ldg(Cm + (int64_t)(j + u) * ld + i) : 0.0;
-          }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int e = 0; e < kE; ++e) cz[e] = __fma_rn(cv[u][e], coef[j + u], cz[e]);
-      }
-      for (; j < k; ++j)
-#pragma unroll
-        for (int e = 0; e < kE; ++e) {
-          const int64_t i = base + 256 * e;
-          if (i < n) cz[e] = __fma_rn(__ldg(Cm + (int64_t)j * ld + i), coef[j], cz[e]);
-        }
-    }
+    const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+    double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
-      const int64_t i = base + 256 * e;
+      const int64_t i = base + (int64_t)kLanes * e;
       if (i >= n) continue;
       if (PH == PH_PUPDATE) {
         // p = r + beta * (p - omega * q)          (solvers.py:303)
@@ -251,21 +222,36 @@ __global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) 
         double *v = PH == PH_PROJ_Q ? q : t;
         double vi = v[i];
         if (k > 0) {
-          vi = __dsub_rn(vi, cz[e]);   // q - C @ zeta   (solvers.py:307,329)
+          // C @ zeta for this element: sequential fma over the columns, four
+          // independent column loads in flight per step
+          double cz = 0.0;
+          int j = 0;
+          for (; j + 4 <= k; j += 4) {
+            double c0 = __ldg(Cm + (int64_t)j * ld + i);
+            double c1 = __ldg(Cm + (int64_t)(j + 1) * ld + i);
+            double c2 = __ldg(Cm + (int64_t)(j + 2) * ld + i);
+            double c3 = __ldg(Cm + (int64_t)(j + 3) * ld + i);
+            cz = __fma_rn(c0, coef[j], cz);
+            cz = __fma_rn(c1, coef[j + 1], cz);
+            cz = __fma_rn(c2, coef[j + 2], cz);
+            cz = __fma_rn(c3, coef[j + 3], cz);
+          }
+          for (; j < k; ++j) cz = __fma_rn(__ldg(Cm + (int64_t)j * ld + i), coef[j], cz);
+          vi = __dsub_rn(vi, cz);   // q - C @ zeta   (solvers.py:307,329)
           v[i] = vi;
         }
         if (PH == PH_PROJ_Q) {
-          acc0 = __fma_rn(rt0[i], vi, acc0);   // (rt0, q)
-          acc1 = __fma_rn(vi, vi, acc1);       // (q, q)
+          acc[0] = __fma_rn(rt0[i], vi, acc[0]);   // (rt0, q)
+          acc[1] = __fma_rn(vi, vi, acc[1]);       // (q, q)
         } else {
-          acc0 = __fma_rn(vi, vi, acc0);       // (t, t)
-          acc1 = __fma_rn(vi, s[i], acc1);     // (t, s)
+          acc[0] = __fma_rn(vi, vi, acc[0]);       // (t, t)
+          acc[1] = __fma_rn(vi, s[i], acc[1]);     // (t, s)
         }
       } else if (PH == PH_SUPD) {
         // s = r - alpha * q                       (solvers.py:313)
         double sv = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
         s[i] = sv;
-        acc0 = __fma_rn(sv, sv, acc0);
+        acc[0] = __fma_rn(sv, sv, acc[0]);
       } else if (PH == PH_XR) {
         // x = x + alpha*p + omega*s ; r = s - omega*t   (solvers.py:338,341)
         double sv = s[i];
@@ -273,49 +259,31 @@ __global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) 
                          __dmul_rn(omega, sv));
         double rv = __dsub_rn(sv, __dmul_rn(omega, t[i]));
         r[i] = rv;
-        acc0 = __fma_rn(rv, rv, acc0);
-        acc1 = __fma_rn(rt0[i], rv, acc1);
+        acc[0] = __fma_rn(rv, rv, acc[0]);
+        acc[1] = __fma_rn(rt0[i], rv, acc[1]);
       } else if (PH == PH_BNORM) {
         double bv = bvec[i];
-        acc0 = __fma_rn(bv, bv, acc0);
+        acc[0] = __fma_rn(bv, bv, acc[0]);
       } else if (PH == PH_INIT) {
         double rv = r[i], tv = rt0[i];
-        acc0 = __fma_rn(rv, rv, acc0);
-        acc1 = __fma_rn(tv, rv, acc1);
-        acc2 = __fma_rn(tv, tv, acc2);
+        acc[0] = __fma_rn(rv, rv, acc[0]);
+        acc[1] = __fma_rn(tv, rv, acc[1]);
+        acc[2] = __fma_rn(tv, tv, acc[2]);
       } else if (PH == PH_TRUE) {
         // true residual b - A x_out   (solvers.py:147-153); A x_out in t
         double bv = bvec[i];
         double res = __dsub_rn(bv, t[i]);
-        acc0 = __fma_rn(res, res, acc0);
-        acc1 = __fma_rn(bv, bv, acc1);
+        acc[0] = __fma_rn(res, res, acc[0]);
+        acc[1] = __fma_rn(bv, bv, acc[1]);
       } else if (PH == PH_RINIT) {
         // r = b - A x_init            (recycling.py:200); A x_init in t
         r[i] = __dsub_rn(bvec[i], t[i]);
       }
     }
     if (ND > 0) {
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      double w0 = warp_tree(acc0);
-      double w1 = ND > 1 ? warp_tree(acc1) : 0.0;
-      double w2 = ND > 2 ? warp_tree(acc2) : 0.0;
-      if (lane == 0) {
-        red[0][warp] = w0;
-        if (ND > 1) red[1][warp] = w1;
-        if (ND > 2) red[2][warp] = w2;
-      }
-      __syncthreads();
-      if ((int)threadIdx.x < ND) {
-        double v8[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v8[u] = red[threadIdx.x][u];
-#pragma unroll
-        for (int off = 4; off >= 1; off >>= 1)
-#pragma unroll
-          for (int u = 0; u < off; ++u) v8[u] = __dadd_rn(v8[u], v8[u + off]);
-        part[threadIdx.x * nb + blk] = v8[0];
-      }
-      __syncthreads();
+      double bp = block_tree_multi<ND == 0 ? 1 : ND>(acc, red);
+      const int warp = threadIdx.x >> 5;
+      if (warp < ND && (threadIdx.x & 31) == 0) part[warp * nb + blk] = bp;
     }
   }
   if (ND == 0) return;
@@ -343,7 +311,7 @@ __global__ void __launch_bounds__(256) k_phase(const IterArgs *__restrict__ pa) 
 
 // projection dots inside the iteration: Chat^T v -> zeta / gamma
 template <int kE, bool kGamma>
-__global__ void __launch_bounds__(256) k_proj_dot(const IterArgs *__restrict__ pa) {
+__global__ void __launch_bounds__(1024) k_proj_dot(const IterArgs *__restrict__ pa) {
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
   tdot_body<kE, false>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
@@ -386,7 +354,7 @@ template <int PH>
 static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.nb == 0) return KRB_OK;
   int grid = grid_for(h.nb);
-  KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH><<<grid, 256, 0, st>>>(d)));
+  KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -395,7 +363,7 @@ template <bool kGamma>
 static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.k <= 0 || h.nb == 0) return KRB_OK;
   dim3 grid = tdot_grid(h.nb, h.k);
-  KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma><<<grid, 256, 0, st>>>(d)));
+  KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }

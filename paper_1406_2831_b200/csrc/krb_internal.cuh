@@ -70,14 +70,14 @@ int64_t &launch_counter();
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ------------------------------------------------------- canonical order
-constexpr int kLanes = 256;            // threads per canonical block
-constexpr int kTargetBlocks = 1184;    // 148 SMs x 8
+constexpr int kLanes = 1024;           // lanes (= threads) per canonical block
+constexpr int kTargetBlocks = 296;     // 148 SMs x 2 resident 1024-thread CTAs
 constexpr int kNumSMs = 148;
 
 inline int64_t canon_E(int64_t n) {
   int64_t t = (n + (int64_t)kLanes * kTargetBlocks - 1) /
               ((int64_t)kLanes * kTargetBlocks);
-  int64_t E = 4;  /* >= 4 lanes-elements amortise the shuffle tree */
+  int64_t E = 1;
   while (E < t && E < 16) E *= 2;
   return E;
 }
@@ -99,29 +99,66 @@ __device__ __forceinline__ double warp_tree(double a) {
   return a;
 }
 
-// canonical 8-warp tree over w[0..7] held by lanes 0..7 of one warp
-__device__ __forceinline__ double warp8_tree(double a) {
+// The canonical 32-lane tree for NCP (power of two <= 8) independent columns
+// at once, "transposed": at offsets 16, 8, 4 the two partner lanes split the
+// columns between them (each computes exactly the canonical pair sums, lower
+// lane's value first, for half of the columns), so only NCP-1 + (5 - log2 NCP)
+// shuffles are needed instead of 5 NCP.  On return the lanes whose low
+// (5 - log2 NCP) bits are zero hold column `col` (bit-identical to warp_tree
+// applied per column).
+template <int NCP>
+__device__ __forceinline__ double warp_tree_multi(double (&a)[NCP], int &col) {
+  constexpr int H = NCP == 1 ? 0 : NCP == 2 ? 1 : NCP == 4 ? 2 : 3;
+  const int lane = threadIdx.x & 31;
+  int c = 0;
 #pragma unroll
-  for (int off = 4; off >= 1; off >>= 1)
-    a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, off));
-  return a;
+  for (int lvl = 0; lvl < H; ++lvl) {
+    const int off = 16 >> lvl;
+    const int half = NCP >> (lvl + 1);
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int u = 0; u < half; ++u) {
+      double send = hi ? a[u] : a[half + u];
+      double recv = __shfl_xor_sync(0xffffffffu, send, off);
+      a[u] = hi ? __dadd_rn(recv, a[half + u]) : __dadd_rn(a[u], recv);
+    }
+    if (hi) c += half;
+  }
+  double v = a[0];
+#pragma unroll
+  for (int off = 16 >> H; off >= 1; off >>= 1)
+    v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+  col = c;
+  return v;
 }
 
-// Block stage of the canonical dot: every thread of a 256-thread CTA passes
-// its lane accumulator; returns the block partial on thread 0.  `sm` needs 8
-// doubles.  Contains __syncthreads (call uniformly).
-__device__ __forceinline__ double block_tree(double acc, double *sm) {
+// Block stage for ND <= 4 dots of a 1024-lane canonical block: lane
+// accumulators acc[d] -> per-warp transposed trees -> red[d][warp] ->
+// warp d: canonical 32-lane tree over the 32 warp results.  The block partial
+// of dot d lands on lane 0 of warp d (returned there; `red` needs 4 x 32).
+// Contains __syncthreads (call uniformly).
+template <int ND>
+__device__ __forceinline__ double block_tree_multi(const double *acc,
+                                                   double (*red)[32]) {
+  constexpr int NCP = ND == 1 ? 1 : ND == 2 ? 2 : 4;
+  constexpr int H = NCP == 1 ? 0 : NCP == 2 ? 1 : 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double w = warp_tree(acc);
-  __syncthreads();
-  if (lane == 0) sm[warp] = w;
+  double a[NCP];
+#pragma unroll
+  for (int d = 0; d < NCP; ++d) a[d] = d < ND ? acc[d] : 0.0;
+  int col;
+  double v = warp_tree_multi<NCP>(a, col);
+  if ((lane & ((32 >> H) - 1)) == 0 && col < ND) red[col][warp] = v;
   __syncthreads();
   double r = 0.0;
-  if (warp == 0) {
-    double v = lane < 8 ? sm[lane] : 0.0;
-    r = warp8_tree(v);
-  }
+  if (warp < ND) r = warp_tree(red[warp][lane]);
+  __syncthreads();
   return r;
+}
+
+// Block stage of one canonical dot (1024 threads); block partial on thread 0.
+__device__ __forceinline__ double block_tree(double acc, double (*red)[32]) {
+  return block_tree_multi<1>(&acc, red);
 }
 
 // Final stage over nb block partials (one warp): lane L sums b = L, L+32, ...
@@ -192,7 +229,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
     default: { constexpr int kE = 16; __VA_ARGS__; } break; \
   }
 
-inline int grid_for(int64_t nb, int per_sm = 8) {
+inline int grid_for(int64_t nb, int per_sm = 2) {
   int64_t g = (int64_t)kNumSMs * per_sm;
   if (nb < g) g = nb;
   return (int)(g < 1 ? 1 : g);

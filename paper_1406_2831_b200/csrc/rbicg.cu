@@ -169,9 +169,9 @@ __device__ void bi_finalize(const BiArgs &a, const double *d) {
 }
 
 template <int kE, int PH>
-__global__ void __launch_bounds__(256) k_bphase(const BiArgs *__restrict__ pa) {
+__global__ void __launch_bounds__(1024) k_bphase(const BiArgs *__restrict__ pa) {
   __shared__ double coef[2][512];
-  __shared__ double red[3][8];
+  __shared__ double red[4][32];
   __shared__ int last_flag;
   const BiArgs &a = *pa;
   BiScalars *S = a.S;
@@ -217,11 +217,11 @@ __global__ void __launch_bounds__(256) k_bphase(const BiArgs *__restrict__ pa) {
   const double rn = S->rnorm;
   double *vcol = a.V + S->ncols * a.ring_ld;
   for (int64_t blk = blockIdx.x; blk < nb; blk += gridDim.x) {
-    const int64_t base = blk * (256 * kE) + threadIdx.x;
+    const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
-      const int64_t i = base + 256 * e;
+      const int64_t i = base + (int64_t)kLanes * e;
       if (i >= n) continue;
       if (PH == BP_PUPDATE) {
         // p = r + beta p ; pt = rt + conj(beta) pt     (solvers.py:589-590)
@@ -287,27 +287,10 @@ __global__ void __launch_bounds__(256) k_bphase(const BiArgs *__restrict__ pa) {
       }
     }
     if (ND > 0) {
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      double w0 = warp_tree(acc0);
-      double w1 = ND > 1 ? warp_tree(acc1) : 0.0;
-      double w2 = ND > 2 ? warp_tree(acc2) : 0.0;
-      if (lane == 0) {
-        red[0][warp] = w0;
-        if (ND > 1) red[1][warp] = w1;
-        if (ND > 2) red[2][warp] = w2;
-      }
-      __syncthreads();
-      if ((int)threadIdx.x < ND) {
-        double v8[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v8[u] = red[threadIdx.x][u];
-#pragma unroll
-        for (int off = 4; off >= 1; off >>= 1)
-#pragma unroll
-          for (int u = 0; u < off; ++u) v8[u] = __dadd_rn(v8[u], v8[u + off]);
-        a.part[threadIdx.x * nb + blk] = v8[0];
-      }
-      __syncthreads();
+      double accs[3] = {acc0, acc1, acc2};
+      double bp = block_tree_multi<ND == 0 ? 1 : ND>(accs, red);
+      const int warp = threadIdx.x >> 5;
+      if (warp < ND && (threadIdx.x & 31) == 0) a.part[warp * nb + blk] = bp;
     }
   }
   if (ND == 0) return;
@@ -333,7 +316,7 @@ __global__ void __launch_bounds__(256) k_bphase(const BiArgs *__restrict__ pa) {
 }
 
 template <int kE, bool kDual>
-__global__ void __launch_bounds__(256) k_bproj_dot(const BiArgs *__restrict__ pa) {
+__global__ void __launch_bounds__(1024) k_bproj_dot(const BiArgs *__restrict__ pa) {
   const BiArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
   tdot_body<kE, false>(a.n, a.nb, a.k, kDual ? a.Ccheck : a.Chat, a.ld,
@@ -378,7 +361,7 @@ template <int PH>
 static int bi_launch(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   if (h.nb == 0) return KRB_OK;
   int grid = grid_for(h.nb);
-  KRB_DISPATCH_E(canon_E(h.n), (k_bphase<kE, PH><<<grid, 256, 0, st>>>(d)));
+  KRB_DISPATCH_E(canon_E(h.n), (k_bphase<kE, PH><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -400,7 +383,7 @@ template <bool kDual>
 static int bi_proj_dot(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   if (h.k <= 0 || h.nb == 0) return KRB_OK;
   dim3 grid = tdot_grid(h.nb, h.k);
-  KRB_DISPATCH_E(canon_E(h.n), (k_bproj_dot<kE, kDual><<<grid, 256, 0, st>>>(d)));
+  KRB_DISPATCH_E(canon_E(h.n), (k_bproj_dot<kE, kDual><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }

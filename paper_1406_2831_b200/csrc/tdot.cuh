@@ -6,12 +6,14 @@
 
 namespace krb {
 
-// Projection dots out[j] = (M[:,j], v) (self: ||M[:,j]||), j < k.
-// Grid (gx, ceil(k/kTdotCG)): CTA (bx, cy) owns columns [cy*CG, cy*CG+CG) of
-// canonical blocks b = bx, bx+gx, ...; every (block, column) gets its own
-// canonical block partial part[j*nb + b]; the last CTA to finish runs the
-// canonical final stage for all k columns (one warp per column).
-constexpr int kTdotCG = 4;
+// Projection dots out[j] = (M[:,j], v) (self: ||M[:,j]|| or its square), j < k.
+// Grid (gx, ceil(k/kTdotCG)) of 1024-thread CTAs: CTA (bx, cy) owns columns
+// [cy*CG, cy*CG+CG) of canonical blocks b = bx, bx+gx, ...  Each lane runs
+// the canonical per-lane fma chain for all CG columns, one transposed warp
+// tree reduces the CG columns together (warp_tree_multi), then warp c does the
+// canonical 32-warp tree of column c -> part[j*nb + b].  The last CTA to
+// finish runs the canonical final stage for all k columns.
+constexpr int kTdotCG = 8;
 
 template <int kE, bool kSelf, bool kSqrt = kSelf>
 __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
@@ -21,48 +23,37 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           double *__restrict__ part,
                                           double *__restrict__ out,
                                           unsigned int *counter) {
-  __shared__ double sm[kTdotCG][8];
+  __shared__ double red[kTdotCG][32];
   __shared__ int last_flag;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j0 = blockIdx.y * kTdotCG;
   const int nj = min(kTdotCG, k - j0);
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int64_t base = b * (256 * kE) + threadIdx.x;
-    double vr[kE];
-    if (!kSelf) {
+    const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
+    double acc[kTdotCG];
 #pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        int64_t i = base + 256 * e;
-        vr[e] = i < n ? __ldg(v + i) : 0.0;
+    for (int c = 0; c < kTdotCG; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int e = 0; e < kE; ++e) {
+      const int64_t i = base + (int64_t)kLanes * e;
+      if (i < n) {
+        const double vi = kSelf ? 0.0 : v[i];
+        double m[kTdotCG];
+#pragma unroll
+        for (int c = 0; c < kTdotCG; ++c)
+          m[c] = c < nj ? __ldg(M + (int64_t)(j0 + c) * ldm + i) : 0.0;
+#pragma unroll
+        for (int c = 0; c < kTdotCG; ++c)
+          acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
       }
     }
-#pragma unroll
-    for (int jj = 0; jj < kTdotCG; ++jj) {
-      if (jj < nj) {
-        const double *col = M + (int64_t)(j0 + jj) * ldm;
-        double acc = 0.0;
-#pragma unroll
-        for (int e = 0; e < kE; ++e) {
-          int64_t i = base + 256 * e;
-          if (i < n) {
-            double m = __ldg(col + i);
-            acc = __fma_rn(m, kSelf ? m : vr[e], acc);
-          }
-        }
-        double w = warp_tree(acc);
-        if (lane == 0) sm[jj][warp] = w;
-      }
-    }
+    int col;
+    double w = warp_tree_multi<kTdotCG>(acc, col);
+    if ((lane & 3) == 0) red[col][warp] = w;
     __syncthreads();
-    if (threadIdx.x < nj) {
-      double a[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) a[t] = sm[threadIdx.x][t];
-#pragma unroll
-      for (int off = 4; off >= 1; off >>= 1)
-#pragma unroll
-        for (int t = 0; t < off; ++t) a[t] = __dadd_rn(a[t], a[t + off]);
-      part[(int64_t)(j0 + threadIdx.x) * nb + b] = a[0];
+    if (warp < nj) {
+      double r = warp_tree(red[warp][lane]);
+      if (lane == 0) part[(int64_t)(j0 + warp) * nb + b] = r;
     }
     __syncthreads();
   }

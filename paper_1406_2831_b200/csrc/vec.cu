@@ -14,20 +14,20 @@
 namespace krb {
 
 template <int kE>
-__global__ void __launch_bounds__(256) k_dot_part(int64_t n, int64_t nb,
-                                                  const double *__restrict__ x,
-                                                  const double *__restrict__ y,
-                                                  double *__restrict__ part) {
-  __shared__ double sm[8];
+__global__ void __launch_bounds__(1024) k_dot_part(int64_t n, int64_t nb,
+                                                   const double *__restrict__ x,
+                                                   const double *__restrict__ y,
+                                                   double *__restrict__ part) {
+  __shared__ double red[1][32];
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int64_t base = b * (256 * kE) + threadIdx.x;
+    const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
     double acc = 0.0;
 #pragma unroll
     for (int e = 0; e < kE; ++e) {
-      int64_t i = base + 256 * e;
+      int64_t i = base + (int64_t)kLanes * e;
       if (i < n) acc = __fma_rn(__ldg(x + i), __ldg(y + i), acc);
     }
-    double r = block_tree(acc, sm);
+    double r = block_tree(acc, red);
     if (threadIdx.x == 0) part[b] = r;
   }
 }
@@ -50,7 +50,7 @@ __global__ void k_final_sqrt(int ndots, int64_t nb,
 }
 
 template <int kE, bool kSelf, bool kSqrt>
-__global__ void __launch_bounds__(256) k_tdot(
+__global__ void __launch_bounds__(1024) k_tdot(
     int64_t n, int64_t nb, int k, const double *__restrict__ M, int64_t ldm,
     const double *__restrict__ v, double *__restrict__ part,
     double *__restrict__ out, unsigned int *counter) {
@@ -248,7 +248,7 @@ int launch_dot_partials(int64_t n, const double *x, const double *y,
   int64_t nb = canon_nblocks(n);
   if (nb == 0) return KRB_OK;
   int grid = grid_for(nb);
-  KRB_DISPATCH_E(canon_E(n), (k_dot_part<kE><<<grid, 256, 0, st>>>(n, nb, x, y, part)));
+  KRB_DISPATCH_E(canon_E(n), (k_dot_part<kE><<<grid, 1024, 0, st>>>(n, nb, x, y, part)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -263,7 +263,7 @@ int launch_final(int ndots, int64_t nb, const double *part, double *out,
 
 dim3 tdot_grid(int64_t nb, int64_t k) {
   int64_t gy = (k + kTdotCG - 1) / kTdotCG;
-  int64_t want = (int64_t)kNumSMs * 8;
+  int64_t want = (int64_t)kNumSMs * 2;
   int64_t gx = (want + gy - 1) / gy;
   if (gx > nb) gx = nb;
   if (gx < 1) gx = 1;
@@ -288,14 +288,14 @@ int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
   unsigned int *cnt = ctx->counters + kCounterTdotStandalone;
   if (self) {
     if (self_sqrt) {
-      KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true, true><<<grid, 256, 0, st>>>(
+      KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true, true><<<grid, 1024, 0, st>>>(
                                      n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
     } else {
-      KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true, false><<<grid, 256, 0, st>>>(
+      KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, true, false><<<grid, 1024, 0, st>>>(
                                      n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
     }
   } else {
-    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, false, false><<<grid, 256, 0, st>>>(
+    KRB_DISPATCH_E(canon_E(n), (k_tdot<kE, false, false><<<grid, 1024, 0, st>>>(
                                    n, nb, (int)k, M, ldm, v, ctx->part, out, cnt)));
   }
   KRB_CHECK_LAUNCH();

@@ -180,6 +180,26 @@ def case_bicgstab(out):
         hist_arrays(p, h, out)
         out[p + "resid_8thr"] = np.asarray(hf.resid)
         out[p + "resid_exactdot"] = np.asarray(he.resid)
+        out[p + "resid_variant_reldiff"] = np.asarray(
+            _variant_reldiffs(lambda: K.bicgstab_solve(RA, b, config=cfg), h.resid))
+
+
+def _variant_reldiffs(fn, ref_resid, m=51):
+    """Max relative history difference (first m entries) of the reference
+    rerun with each alternative dot order of _DOT_VARIANTS."""
+    import krecycle.solvers as KS
+    out = []
+    for dotf in _DOT_VARIANTS:
+        KS.np = _numpy_with_dot(dotf)
+        try:
+            with threadpool_limits(1):
+                _, hx = fn()
+        finally:
+            KS.np = np
+        L = min(len(hx.resid), len(ref_resid), m)
+        a, r = np.asarray(hx.resid[:L]), np.asarray(ref_resid[:L])
+        out.append(float(np.max(np.abs(a - r) / r)))
+    return out
 
 
 def case_rbicgstab(out):
@@ -203,6 +223,8 @@ def case_rbicgstab(out):
     hist_arrays(p, h, out)
     out[p + "resid_8thr"] = np.asarray(hf.resid)
     out[p + "resid_exactdot"] = np.asarray(he.resid)
+    out[p + "resid_variant_reldiff"] = np.asarray(_variant_reldiffs(
+        lambda: K.rbicgstab_solve(RA, b, recycle=space, config=cfg), h.resid))
     # x_init path (one counted product)
     x0 = rng.standard_normal(300)
     (x2, h2), _, (_, h2e) = _solver_pair(

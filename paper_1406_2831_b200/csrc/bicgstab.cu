@@ -1,23 +1,27 @@
 // Deflated BiCGSTAB (Algorithm 2 of arXiv 1406.2831) on sm_100a.
 //
 // Restates rbicgstab_solve (reference solvers.py:245-361; bicgstab_solve
-// solvers.py:156-242 is the k = 0 case) as a short chain of fused,
-// HBM-streaming phase kernels.  All scalar logic (alpha, omega, beta, rho,
-// breakdown and convergence predicates, history records) runs on the device
-// in the last CTA of the kernel that produced the reduction it needs, in
-// exactly the reference's order, so an iteration needs no host round trip.
+// solvers.py:156-242 is the k = 0 case) as a chain of fused, HBM-streaming
+// phases.  All scalar logic (alpha, omega, beta, rho, breakdown and
+// convergence predicates, history records) runs on the device, in the
+// reference's order, in the one CTA that finishes a phase's reduction last.
 //
-// The iteration is captured once into a CUDA graph whose WHILE conditional
-// node is re-armed by the device (cudaGraphSetConditional) until the status
-// leaves RUNNING: a whole solve is one graph launch plus one final readback.
-// Kernels read every per-solve pointer (matrix, recycle blocks) from a
-// descriptor in device memory, so one instantiated graph serves every solve of
-// the same shape (n, k, format) — e.g. all systems of a sequence.
+// Two drivers share the phase bodies below:
+//  * persistent (default): ONE cooperative kernel runs the whole solve; the
+//    phases are separated by grid barriers whose last-arriving CTA ("leader")
+//    does the phase's final reduction and scalar logic before releasing the
+//    others -- no kernel launches and no host round trips per iteration;
+//  * graph: each phase is its own kernel, the iteration is captured once into
+//    a CUDA graph whose WHILE conditional node is re-armed by the device
+//    (cudaGraphSetConditional) until the status leaves RUNNING;
+//  * host loop (debug / per-kernel profiling).
+// Every per-solve pointer lives in a device descriptor, so the graph and the
+// persistent kernel serve every solve of the same shape.
 //
 // Per iteration (k > 0; Z vanishes and Q/T skip the update for k = 0):
 //   P  p = r + beta (p - omega q)                      3 read, 1 write
 //   M  q = A p                                         SpMV
-//   Z  zeta = Chat^T q  (column groups + last-CTA final)  n x k + n read
+//   Z  zeta = Chat^T q  (block x column-group units)   n x k + n read
 //   Q  q -= C zeta ; (rt0,q), (q,q) -> den, alpha       n x k + 2 read, 1 write
 //   S  s = r - alpha q ; (s,s) -> half-step exit        2 read, 1 write
 //   M  t = A s ;  Z gamma = Chat^T t
@@ -62,6 +66,11 @@ struct IterArgs {
   uint64_t *hist_t;
 };
 
+struct GridSync {
+  unsigned int count;
+  unsigned int gen;
+};
+
 __device__ __forceinline__ void record(const IterArgs &a, double rn) {
   SolveScalars *S = a.S;
   int64_t h = S->hist_len;
@@ -77,8 +86,8 @@ __host__ __device__ constexpr int ndots_of(int PH) {
        : PH == PH_TRUE ? 2 : 0;
 }
 
-// Scalar logic of each phase, executed by thread 0 of the last CTA once the
-// dot products d[] are final.  Mirrors solvers.py:288-356 line by line.
+// Scalar logic of each phase, executed by thread 0 of the finishing CTA once
+// the dot products d[] are final.  Mirrors solvers.py:288-356 line by line.
 template <int PH>
 __device__ void finalize(const IterArgs &a, const double *d) {
   SolveScalars *S = a.S;
@@ -152,33 +161,24 @@ __device__ void finalize(const IterArgs &a, const double *d) {
   }
 }
 
+struct PhaseScal {
+  double alpha, omega, beta;
+};
+
+__device__ __forceinline__ PhaseScal load_scal(const SolveScalars *S) {
+  return PhaseScal{S->alpha, S->omega, S->beta};
+}
+
+// Elementwise work + canonical block partials of one phase for canonical
+// blocks blk = first, first + step, ...   `coef` (k values of zeta / gamma)
+// must already be in shared memory for the projection phases.
 template <int kE, int PH>
-__global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa) {
-  __shared__ double coef[512];
-  __shared__ double red[4][32];
-  __shared__ int last_flag;
-  const IterArgs &a = *pa;
-  SolveScalars *S = a.S;
+__device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal sc,
+                                             double (*red)[32],
+                                             const double *coef, int64_t first,
+                                             int64_t step) {
   constexpr int ND = ndots_of(PH);
-  constexpr bool kGated = (PH == PH_PUPDATE || PH == PH_PROJ_Q ||
-                           PH == PH_SUPD || PH == PH_PROJ_T || PH == PH_XR);
-  bool half_exit = false;
-  if (PH == PH_XR && blockIdx.x == 0 && threadIdx.x == 0) S->bodies += 1;
-  if (kGated && S->status != KRB_RUNNING) {
-    if (PH == PH_PUPDATE) {
-      // a half-step exit was applied by the previous X phase: mark consumed
-      // (only matters for the host-driven loop, which may overshoot)
-      if (blockIdx.x == 0 && threadIdx.x == 0 && S->early == 1) S->early = 2;
-      return;
-    }
-    if (PH != PH_XR || S->early != 1) {
-      if (PH == PH_XR && a.use_cond && blockIdx.x == 0 && threadIdx.x == 0)
-        cudaGraphSetConditional(a.cond, 0);
-      return;
-    }
-    half_exit = true;   // X phase applies x += alpha p, xc += alpha zeta
-  }
-  const double alpha = S->alpha, omega = S->omega, beta = S->beta;
+  const double alpha = sc.alpha, omega = sc.omega, beta = sc.beta;
   const int k = a.k;
   const int64_t n = a.n, nb = a.nb, ld = a.ld;
   double *__restrict__ x = a.x;
@@ -191,26 +191,10 @@ __global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa)
   const double *__restrict__ bvec = a.b;
   const double *__restrict__ Cm = a.C;
   double *__restrict__ part = a.part;
-  if (half_exit) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));   // solvers.py:316
-    if (blockIdx.x == 0) {
-      for (int j = threadIdx.x; j < k; j += blockDim.x)  // solvers.py:318
-        a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
-      if (threadIdx.x == 0 && a.use_cond) cudaGraphSetConditional(a.cond, 0);
-    }
-    return;
-  }
-  if (PH == PH_PROJ_Q || PH == PH_PROJ_T) {
-    const double *src = PH == PH_PROJ_Q ? a.zeta : a.gamma;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) coef[j] = src[j];
-    __syncthreads();
-  }
-  for (int64_t blk = blockIdx.x; blk < nb; blk += gridDim.x) {
+  for (int64_t blk = first; blk < nb; blk += step) {
     const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
     double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll
+#pragma unroll(kE < 4 ? kE : 4)
     for (int e = 0; e < kE; ++e) {
       const int64_t i = base + (int64_t)kLanes * e;
       if (i >= n) continue;
@@ -286,23 +270,81 @@ __global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa)
       if (warp < ND && (threadIdx.x & 31) == 0) part[warp * nb + blk] = bp;
     }
   }
-  if (ND == 0) return;
-  if (!elect_last_cta(a.counters + PH, &last_flag)) return;
+}
+
+// Final stage + scalar logic of a phase, run by every thread of the one CTA
+// that finished the phase last (all partials visible).
+template <int PH>
+__device__ __forceinline__ void phase_leader(const IterArgs &a, const PhaseScal sc) {
+  constexpr int ND = ndots_of(PH);
   __shared__ double dfin[3];
   const int warp = threadIdx.x >> 5;
   if (warp < ND) {
-    double v = warp_final_volatile(part + warp * nb, nb);
+    double v = warp_final_volatile(a.part + warp * a.nb, a.nb);
     if ((threadIdx.x & 31) == 0) dfin[warp] = v;
   }
   if (PH == PH_XR) {
     // xc = xc + alpha*zeta + omega*gamma     (solvers.py:340)
-    for (int j = threadIdx.x; j < k; j += blockDim.x)
-      a.xc[j] = __dadd_rn(__dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j])),
-                          __dmul_rn(omega, a.gamma[j]));
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x)
+      a.xc[j] = __dadd_rn(__dadd_rn(a.xc[j], __dmul_rn(sc.alpha, a.zeta[j])),
+                          __dmul_rn(sc.omega, a.gamma[j]));
   }
   __syncthreads();
+  if (threadIdx.x == 0) finalize<PH>(a, dfin);
+  __syncthreads();
+}
+
+// half-step exit (solvers.py:315-325): x += alpha p, xc += alpha zeta
+__device__ __forceinline__ void half_exit_update(const IterArgs &a, double alpha,
+                                                 int64_t first, int64_t step) {
+  for (int64_t i = first * blockDim.x + threadIdx.x; i < a.n; i += step * blockDim.x)
+    a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));   // solvers.py:316
+  if (first == 0)
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x)     // solvers.py:318
+      a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
+}
+
+// ---------------------------------------------------------------------------
+// graph / host-loop driver: one kernel per phase, last CTA finalizes
+// ---------------------------------------------------------------------------
+template <int kE, int PH>
+__global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa) {
+  __shared__ double coef[512];
+  __shared__ double red[4][32];
+  __shared__ int last_flag;
+  const IterArgs &a = *pa;
+  SolveScalars *S = a.S;
+  constexpr int ND = ndots_of(PH);
+  constexpr bool kGated = (PH == PH_PUPDATE || PH == PH_PROJ_Q ||
+                           PH == PH_SUPD || PH == PH_PROJ_T || PH == PH_XR);
+  if (PH == PH_XR && blockIdx.x == 0 && threadIdx.x == 0) S->bodies += 1;
+  const PhaseScal sc = load_scal(S);
+  if (kGated && S->status != KRB_RUNNING) {
+    if (PH == PH_PUPDATE) {
+      // a half-step exit was applied by the previous X phase: mark consumed
+      // (only matters for the host-driven loop, which may overshoot)
+      if (blockIdx.x == 0 && threadIdx.x == 0 && S->early == 1) S->early = 2;
+      return;
+    }
+    if (PH == PH_XR && S->early == 1) {
+      half_exit_update(a, sc.alpha, blockIdx.x, gridDim.x);
+      if (blockIdx.x == 0 && threadIdx.x == 0 && a.use_cond) cudaGraphSetConditional(a.cond, 0);
+      return;
+    }
+    if (PH == PH_XR && a.use_cond && blockIdx.x == 0 && threadIdx.x == 0)
+      cudaGraphSetConditional(a.cond, 0);
+    return;
+  }
+  if (PH == PH_PROJ_Q || PH == PH_PROJ_T) {
+    const double *src = PH == PH_PROJ_Q ? a.zeta : a.gamma;
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x) coef[j] = src[j];
+    __syncthreads();
+  }
+  phase_blocks<kE, PH>(a, sc, red, coef, blockIdx.x, gridDim.x);
+  if (ND == 0) return;
+  if (!elect_last_cta(a.counters + PH, &last_flag)) return;
+  phase_leader<PH>(a, sc);
   if (threadIdx.x == 0) {
-    finalize<PH>(a, dfin);
     a.counters[PH] = 0;
     if (PH == PH_XR && a.use_cond)
       cudaGraphSetConditional(a.cond, S->status == KRB_RUNNING ? 1u : 0u);
@@ -328,6 +370,123 @@ __global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ 
   const double *x = kSecond ? a.s : a.p;
   double *y = kSecond ? a.t : a.q;
   y[i] = spmv_row<kSell>(i, a.A, x);
+}
+
+// ---------------------------------------------------------------------------
+// persistent driver: the whole solve in one cooperative kernel
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool gs_arrive(GridSync *g, unsigned int *s_gen,
+                                          int *s_lead) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int ge = *(volatile unsigned int *)&g->gen;
+    __threadfence();
+    unsigned int prev = atomicAdd(&g->count, 1u);
+    *s_lead = (prev == gridDim.x - 1);
+    *s_gen = ge;
+    if (*s_lead) __threadfence();
+  }
+  __syncthreads();
+  return *s_lead != 0;
+}
+
+__device__ __forceinline__ void gs_release(GridSync *g) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g->count = 0;
+    __threadfence();
+    atomicAdd(&g->gen, 1u);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void gs_wait(GridSync *g, unsigned int gen0) {
+  if (threadIdx.x == 0) {
+    while (*(volatile unsigned int *)&g->gen == gen0) __nanosleep(20);
+    __threadfence();   // acquire + L1 invalidate (CCTL.IVALL)
+  }
+  __syncthreads();
+}
+
+template <int kE, bool kSell>
+__global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ pa,
+                                                  GridSync *gs) {
+  __shared__ double coef[512];
+  __shared__ double red[kTdotCG][32];
+  __shared__ unsigned int s_gen;
+  __shared__ int s_lead;
+  const IterArgs &a = *pa;
+  SolveScalars *S = a.S;
+  const int64_t G = gridDim.x, me = blockIdx.x;
+  const int64_t n = a.n, nb = a.nb;
+  const int k = a.k;
+  const int64_t ncg = (k + kTdotCG - 1) / kTdotCG;
+  const krb_matrix A = a.A;
+
+#define KRB_GRID_SYNC(LEADER)                       \
+  do {                                              \
+    if (gs_arrive(gs, &s_gen, &s_lead)) {           \
+      LEADER;                                       \
+      gs_release(gs);                               \
+    } else {                                        \
+      gs_wait(gs, s_gen);                           \
+    }                                               \
+  } while (0)
+
+  for (;;) {
+    if (S->status != KRB_RUNNING) break;
+    PhaseScal sc = load_scal(S);
+    // P
+    phase_blocks<kE, PH_PUPDATE>(a, sc, red, coef, me, G);
+    KRB_GRID_SYNC((void)0);
+    // M: q = A p
+    for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
+      a.q[i] = spmv_row<kSell, false>(i, A, a.p);
+    KRB_GRID_SYNC((void)0);
+    // Z: zeta = Chat^T q
+    if (k > 0) {
+      for (int64_t u = me; u < nb * ncg; u += G)
+        tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.q, a.part, u % nb,
+                             (int)(u / nb) * kTdotCG, red);
+      KRB_GRID_SYNC(tdot_finals<false>(nb, k, a.part, a.zeta));
+      for (int j = threadIdx.x; j < k; j += blockDim.x) coef[j] = a.zeta[j];
+      __syncthreads();
+    }
+    // Q
+    phase_blocks<kE, PH_PROJ_Q>(a, sc, red, coef, me, G);
+    KRB_GRID_SYNC(phase_leader<PH_PROJ_Q>(a, sc));
+    if (S->status != KRB_RUNNING) break;
+    sc = load_scal(S);
+    // S
+    phase_blocks<kE, PH_SUPD>(a, sc, red, coef, me, G);
+    KRB_GRID_SYNC(phase_leader<PH_SUPD>(a, sc));
+    if (S->status != KRB_RUNNING) {
+      if (S->early == 1) half_exit_update(a, sc.alpha, me, G);
+      break;
+    }
+    // M: t = A s
+    for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
+      a.t[i] = spmv_row<kSell, false>(i, A, a.s);
+    KRB_GRID_SYNC((void)0);
+    // Z: gamma = Chat^T t
+    if (k > 0) {
+      for (int64_t u = me; u < nb * ncg; u += G)
+        tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.t, a.part, u % nb,
+                             (int)(u / nb) * kTdotCG, red);
+      KRB_GRID_SYNC(tdot_finals<false>(nb, k, a.part, a.gamma));
+      for (int j = threadIdx.x; j < k; j += blockDim.x) coef[j] = a.gamma[j];
+      __syncthreads();
+    }
+    // T
+    phase_blocks<kE, PH_PROJ_T>(a, sc, red, coef, me, G);
+    KRB_GRID_SYNC(phase_leader<PH_PROJ_T>(a, sc));
+    if (S->status != KRB_RUNNING) break;
+    sc = load_scal(S);
+    // X
+    phase_blocks<kE, PH_XR>(a, sc, red, coef, me, G);
+    KRB_GRID_SYNC(phase_leader<PH_XR>(a, sc));
+  }
+#undef KRB_GRID_SYNC
 }
 
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
@@ -392,6 +551,38 @@ static int launch_iteration(const IterArgs &h, const IterArgs *d, cudaStream_t s
   KRB_TRY(launch_phase<PH_PROJ_T>(h, d, st));
   KRB_TRY(launch_phase<PH_XR>(h, d, st));
   return KRB_OK;
+}
+
+template <int kE, bool kSell>
+static int persist_launch(const IterArgs *d, GridSync *gs, cudaStream_t st) {
+  static int grid = 0;
+  if (grid == 0) {
+    int per_sm = 0;
+    KRB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_persist<kE, kSell>, 1024, 0));
+    int dev = 0, sms = kNumSMs;
+    KRB_CHECK_CUDA(cudaGetDevice(&dev));
+    KRB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  void *args[] = {(void *)&d, (void *)&gs};
+  KRB_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_persist<kE, kSell>,
+                                             dim3(grid), dim3(1024), args, 0, st));
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+static int launch_persistent(const IterArgs &h, const IterArgs *d, GridSync *gs,
+                             cudaStream_t st) {
+  if (h.n == 0) return KRB_OK;
+  const bool sell = h.A.format == 2;
+  switch (canon_E(h.n)) {
+    case 1: return sell ? persist_launch<1, true>(d, gs, st) : persist_launch<1, false>(d, gs, st);
+    case 2: return sell ? persist_launch<2, true>(d, gs, st) : persist_launch<2, false>(d, gs, st);
+    case 4: return sell ? persist_launch<4, true>(d, gs, st) : persist_launch<4, false>(d, gs, st);
+    case 8: return sell ? persist_launch<8, true>(d, gs, st) : persist_launch<8, false>(d, gs, st);
+    default: return sell ? persist_launch<16, true>(d, gs, st) : persist_launch<16, false>(d, gs, st);
+  }
 }
 
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k) {
@@ -511,12 +702,14 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   h.hist_r = hist_r;
   h.hist_m = hist_m;
   h.hist_t = hist_t;
-  const bool graph = cfg->use_graph == 1;
+  const int mode = cfg->use_graph;   // 0 host loop, 1 graph, 2 persistent
+  const bool graph = mode == 1;
   GraphCache &G = ctx->graph;
   const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format;
   h.use_cond = graph ? 1 : 0;
   h.cond = hit ? G.cond : 0;
   IterArgs *d = reinterpret_cast<IterArgs *>(ctx->desc);
+  GridSync *gs = reinterpret_cast<GridSync *>(ctx->counters + kCounterGridSync);
 
   // ---- setup (solvers.py:257-296) -------------------------------------
   if (graph && !hit) {
@@ -567,7 +760,10 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   KRB_TRY(launch_phase<PH_INIT>(h, d, st));
 
   // ---- iterations (solvers.py:298-356) --------------------------------
-  if (graph) {
+  if (mode == 2) {
+    KRB_CHECK_CUDA(cudaMemsetAsync(gs, 0, sizeof(GridSync), st));
+    KRB_TRY(launch_persistent(h, d, gs, st));
+  } else if (graph) {
     KRB_CHECK_CUDA(cudaGraphLaunch(G.exec, st));
     per_body = G.kernels_per_body;
   } else {
@@ -602,7 +798,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   res->rhs_norm = hs.bnorm;
   res->final_true_resid = hs.final_true_resid;
   res->t_start_ns = hs.t_start;
-  res->iterations_run = hs.bodies;
+  res->iterations_run = mode == 2 ? hs.itn : hs.bodies;
   launch_counter() += hs.bodies * per_body;
   res->kernel_launches = launch_counter() - l0;
   return KRB_OK;

@@ -67,6 +67,7 @@ namespace krb {
 constexpr int kNumCounters = 64;
 constexpr int kCounterTdotStandalone = 20;
 constexpr int kCounterTdotGraph = 21;
+constexpr int kCounterGridSync = 48;   // 2 words: persistent-kernel grid barrier
 
 int ctx_reserve_part(krb_context *ctx, size_t doubles);
 int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);

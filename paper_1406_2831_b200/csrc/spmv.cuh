@@ -6,8 +6,16 @@
 
 namespace krb {
 
+template <bool kRO>
+__device__ __forceinline__ double ldx(const double *p) {
+  if (kRO) return __ldg(p);
+  return *p;
+}
+
 // ---- SpMV kernels: one thread per row, CSR order, mul then add ----------
-template <bool kSell>
+// kXro: x is read-only for the whole kernel (ld.global.nc); false inside the
+// persistent solver, where x was written by other CTAs earlier in the kernel.
+template <bool kSell, bool kXro = true>
 __device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
                                           const double *__restrict__ x) {
   double sum = 0.0;
@@ -22,15 +30,15 @@ __device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
       int c2 = __ldg(cp + 32 * (j + 2)), c3 = __ldg(cp + 32 * (j + 3));
       double v0 = __ldg(vp + 32 * j), v1 = __ldg(vp + 32 * (j + 1));
       double v2 = __ldg(vp + 32 * (j + 2)), v3 = __ldg(vp + 32 * (j + 3));
-      double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2),
-             x3 = __ldg(x + c3);
+      double x0 = ldx<kXro>(x + c0), x1 = ldx<kXro>(x + c1), x2 = ldx<kXro>(x + c2),
+             x3 = ldx<kXro>(x + c3);
       sum = __dadd_rn(sum, __dmul_rn(v0, x0));
       sum = __dadd_rn(sum, __dmul_rn(v1, x1));
       sum = __dadd_rn(sum, __dmul_rn(v2, x2));
       sum = __dadd_rn(sum, __dmul_rn(v3, x3));
     }
     for (; j < len; ++j)
-      sum = __dadd_rn(sum, __dmul_rn(__ldg(vp + 32 * j), __ldg(x + __ldg(cp + 32 * j))));
+      sum = __dadd_rn(sum, __dmul_rn(__ldg(vp + 32 * j), ldx<kXro>(x + __ldg(cp + 32 * j))));
   } else {
     int64_t b = __ldg(A.rp + i), e = __ldg(A.rp + i + 1);
     int64_t jj = b;
@@ -39,15 +47,15 @@ __device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
       int c2 = __ldg(A.ci + jj + 2), c3 = __ldg(A.ci + jj + 3);
       double v0 = __ldg(A.val + jj), v1 = __ldg(A.val + jj + 1);
       double v2 = __ldg(A.val + jj + 2), v3 = __ldg(A.val + jj + 3);
-      double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2),
-             x3 = __ldg(x + c3);
+      double x0 = ldx<kXro>(x + c0), x1 = ldx<kXro>(x + c1), x2 = ldx<kXro>(x + c2),
+             x3 = ldx<kXro>(x + c3);
       sum = __dadd_rn(sum, __dmul_rn(v0, x0));
       sum = __dadd_rn(sum, __dmul_rn(v1, x1));
       sum = __dadd_rn(sum, __dmul_rn(v2, x2));
       sum = __dadd_rn(sum, __dmul_rn(v3, x3));
     }
     for (; jj < e; ++jj)
-      sum = __dadd_rn(sum, __dmul_rn(__ldg(A.val + jj), __ldg(x + __ldg(A.ci + jj))));
+      sum = __dadd_rn(sum, __dmul_rn(__ldg(A.val + jj), ldx<kXro>(x + __ldg(A.ci + jj))));
   }
   return sum;
 }

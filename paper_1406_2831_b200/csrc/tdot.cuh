@@ -1,5 +1,5 @@
-// Canonical projection-dot block (shared by the standalone and the graph
-// variants of the kernel).
+// Canonical projection dots (shared by the standalone kernel, the graph
+// kernels and the persistent solver).
 #pragma once
 
 #include "ctx.cuh"
@@ -7,14 +7,64 @@
 namespace krb {
 
 // Projection dots out[j] = (M[:,j], v) (self: ||M[:,j]|| or its square), j < k.
-// Grid (gx, ceil(k/kTdotCG)) of 1024-thread CTAs: CTA (bx, cy) owns columns
-// [cy*CG, cy*CG+CG) of canonical blocks b = bx, bx+gx, ...  Each lane runs
-// the canonical per-lane fma chain for all CG columns, one transposed warp
-// tree reduces the CG columns together (warp_tree_multi), then warp c does the
-// canonical 32-warp tree of column c -> part[j*nb + b].  The last CTA to
-// finish runs the canonical final stage for all k columns.
+// Work unit = (canonical block b, group of kTdotCG columns from j0), done by
+// one 1024-thread CTA: each lane runs the canonical per-lane fma chain for the
+// group's columns, one transposed warp tree reduces all of them together
+// (warp_tree_multi), then warp c runs the canonical 32-warp tree of column c
+// -> part[j*nb + b].
 constexpr int kTdotCG = 8;
 
+template <int kE, bool kSelf>
+__device__ __forceinline__ void tdot_unit(int64_t n, int64_t nb, int k,
+                                          const double *__restrict__ M,
+                                          int64_t ldm,
+                                          const double *__restrict__ v,
+                                          double *__restrict__ part, int64_t b,
+                                          int j0, double (*red)[32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nj = min(kTdotCG, k - j0);
+  const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
+  double acc[kTdotCG];
+#pragma unroll
+  for (int c = 0; c < kTdotCG; ++c) acc[c] = 0.0;
+#pragma unroll(kE < 4 ? kE : 4)
+  for (int e = 0; e < kE; ++e) {
+    const int64_t i = base + (int64_t)kLanes * e;
+    if (i < n) {
+      const double vi = kSelf ? 0.0 : v[i];
+      double m[kTdotCG];
+#pragma unroll
+      for (int c = 0; c < kTdotCG; ++c)
+        m[c] = c < nj ? __ldg(M + (int64_t)(j0 + c) * ldm + i) : 0.0;
+#pragma unroll
+      for (int c = 0; c < kTdotCG; ++c)
+        acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
+    }
+  }
+  int col;
+  double w = warp_tree_multi<kTdotCG>(acc, col);
+  if ((lane & 3) == 0) red[col][warp] = w;
+  __syncthreads();
+  if (warp < nj) {
+    double r = warp_tree(red[warp][lane]);
+    if (lane == 0) part[(int64_t)(j0 + warp) * nb + b] = r;
+  }
+  __syncthreads();
+}
+
+// canonical final stage of k columns (partials part[j*nb + b]) by the warps
+// of one CTA
+template <bool kSqrt>
+__device__ __forceinline__ void tdot_finals(int64_t nb, int k,
+                                            const double *part, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = warp; j < k; j += (blockDim.x >> 5)) {
+    double r = warp_final_volatile(part + (int64_t)j * nb, nb);
+    if (lane == 0) out[j] = kSqrt ? __dsqrt_rn(r) : r;
+  }
+}
+
+// Grid (gx, ceil(k/kTdotCG)); the last CTA to finish runs the final stage.
 template <int kE, bool kSelf, bool kSqrt = kSelf>
 __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           const double *__restrict__ M,
@@ -25,39 +75,9 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           unsigned int *counter) {
   __shared__ double red[kTdotCG][32];
   __shared__ int last_flag;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j0 = blockIdx.y * kTdotCG;
-  const int nj = min(kTdotCG, k - j0);
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
-    double acc[kTdotCG];
-#pragma unroll
-    for (int c = 0; c < kTdotCG; ++c) acc[c] = 0.0;
-#pragma unroll
-    for (int e = 0; e < kE; ++e) {
-      const int64_t i = base + (int64_t)kLanes * e;
-      if (i < n) {
-        const double vi = kSelf ? 0.0 : v[i];
-        double m[kTdotCG];
-#pragma unroll
-        for (int c = 0; c < kTdotCG; ++c)
-          m[c] = c < nj ? __ldg(M + (int64_t)(j0 + c) * ldm + i) : 0.0;
-#pragma unroll
-        for (int c = 0; c < kTdotCG; ++c)
-          acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
-      }
-    }
-    int col;
-    double w = warp_tree_multi<kTdotCG>(acc, col);
-    if ((lane & 3) == 0) red[col][warp] = w;
-    __syncthreads();
-    if (warp < nj) {
-      double r = warp_tree(red[warp][lane]);
-      if (lane == 0) part[(int64_t)(j0 + warp) * nb + b] = r;
-    }
-    __syncthreads();
-  }
-  // last CTA of the whole (gx x gy) grid: canonical final stage per column
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
+    tdot_unit<kE, kSelf>(n, nb, k, M, ldm, v, part, b, j0, red);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -67,10 +87,7 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
   __syncthreads();
   if (!last_flag) return;
   __threadfence();
-  for (int j = warp; j < k; j += (blockDim.x >> 5)) {
-    double r = warp_final_volatile(part + (int64_t)j * nb, nb);
-    if (lane == 0) out[j] = kSqrt ? __dsqrt_rn(r) : r;
-  }
+  tdot_finals<kSqrt>(nb, k, part, out);
   if (threadIdx.x == 0) *counter = 0;
 }
 

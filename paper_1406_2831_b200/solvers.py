@@ -179,12 +179,15 @@ def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
 
 
 def _graph_mode():
-    """KRB_GRAPH_MODE=1 (default): one CUDA graph with a device-driven WHILE
-    node per solve; 0: host-launched iterations with a status poll every 8
-    (identical kernels and results; used for per-kernel ncu profiling, which
-    cannot see inside conditional graph nodes)."""
+    """Iteration driver (bit-identical results in every mode):
+    KRB_GRAPH_MODE=2 (default for RBiCGSTAB): one persistent cooperative kernel
+    per solve, phases separated by grid barriers whose last CTA finalizes;
+    1: one CUDA graph per solve with a device-driven WHILE node (the RBiCG
+    generation solve always uses this, pausing at every harvest cycle);
+    0: host-launched iterations with a status poll every 8 (per-kernel ncu
+    profiling: ncu cannot see inside conditional graph nodes)."""
     import os
-    return int(os.environ.get("KRB_GRAPH_MODE", "1"))
+    return int(os.environ.get("KRB_GRAPH_MODE", "2"))
 
 
 def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
@@ -360,7 +363,7 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
               ctypes.byref(view) if view is not None else None,
               int(cfg.s), int(cfg.max_itn), stream_ptr())
     try:
-        graph = _graph_mode()
+        graph = min(_graph_mode(), 1)
         dual = (ctypes.c_double * 3)()
         n_rmv = 0
         for attempt in range(4):

@@ -155,3 +155,29 @@ def test_graph_and_host_loop_agree(pkg):
     # second graph launch (cached graph) reproduces the first
     x3, h3 = S._device_solve(A, b, None, None, cfg, "bicgstab", time.perf_counter(), use_graph=1)
     assert h3.resid == h1.resid and np.array_equal(x3, x1)
+    # persistent cooperative kernel (default driver)
+    x4, h4 = S._device_solve(A, b, None, None, cfg, "bicgstab", time.perf_counter(), use_graph=2)
+    assert h4.resid == h1.resid and np.array_equal(x4, x1)
+
+
+@pytest.mark.parametrize("cfg,k", [("c1", 10), ("c2", 20), ("c4", 30), ("c5", 30)])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_drivers_bitwise_with_space(pkg, canon, cfg, k, mode):
+    """Host loop, CUDA graph and persistent kernel: identical to the oracle,
+    including half-step exits and breakdown paths exercised by max_itn."""
+    import time
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import solvers as S
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence(cfg, small=True)
+    A = seq.matrix(2)
+    Sp = random_space_arrays(A, k, seed=9, ops=canon)
+    b = seq.rhs(2, 0)
+    for max_itn in (7, 400):
+        cfgp = pkg.SolverConfig(tol=seq.tol, max_itn=max_itn, seed=4)
+        xo, ho = O.rbicgstab(A, b, recycle=Sp, config=O.Config(tol=seq.tol, max_itn=max_itn,
+                                                               seed=4), ops=canon)
+        xg, hg = S._device_solve(pkg.SparseMatrix.from_csr(A), b, None, _space(pkg, Sp), cfgp,
+                                 "rbicgstab", time.perf_counter(), use_graph=mode)
+        assert hg.status == ho.status and hg.resid == ho.resid
+        assert hg.matvecs == ho.matvecs and np.array_equal(xg, xo)

@@ -187,7 +187,22 @@ def _graph_mode():
     0: host-launched iterations with a status poll every 8 (per-kernel ncu
     profiling: ncu cannot see inside conditional graph nodes)."""
     import os
-    return int(os.environ.get("KRB_GRAPH_MODE", "2"))
+    v = os.environ.get("KRB_GRAPH_MODE")
+    return int(v) if v is not None else None
+
+
+# Below this size one persistent cooperative kernel beats per-phase kernels
+# (launch / tail latency dominates); above it the per-phase kernels run at
+# higher occupancy (measured on B200: C1/C2 persistent -10..15 %, C3-C5
+# graph -10..20 %).
+PERSISTENT_MAX_N = 600_000
+
+
+def _auto_mode(n):
+    m = _graph_mode()
+    if m is not None:
+        return m
+    return 2 if n <= PERSISTENT_MAX_N else 1
 
 
 def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
@@ -198,7 +213,7 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     if t0 is None:
         t0 = time.perf_counter()
     if use_graph is None:
-        use_graph = _graph_mode()
+        use_graph = _auto_mode(M.n)
     ctx = Context.get()
     R = None
     if recycle is not None and recycle.k > 0:
@@ -363,7 +378,7 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
               ctypes.byref(view) if view is not None else None,
               int(cfg.s), int(cfg.max_itn), stream_ptr())
     try:
-        graph = min(_graph_mode(), 1)
+        graph = min(_graph_mode() if _graph_mode() is not None else 1, 1)
         dual = (ctypes.c_double * 3)()
         n_rmv = 0
         for attempt in range(4):

@@ -29,6 +29,7 @@
 //   X  x = x + alpha p + omega s ; r = s - omega t ;
 //      (r,r), (rt0,r) -> record, converge, rho, beta    5 read, 2 write
 //      (on a half-step exit instead: x += alpha p, xc += alpha zeta)
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "ctx.cuh"
@@ -36,6 +37,8 @@
 #include "tdot.cuh"
 
 namespace krb {
+
+namespace cg = cooperative_groups;
 
 enum Phase {
   PH_PUPDATE = 0,
@@ -71,12 +74,16 @@ struct GridSync {
   unsigned int gen;
 };
 
-__device__ __forceinline__ void record(const IterArgs &a, double rn) {
-  SolveScalars *S = a.S;
+// S: the scalar block to update (global, or a CTA's shared copy in the
+// persistent kernel); only the writer CTA stores the history entries.
+__device__ __forceinline__ void record(const IterArgs &a, SolveScalars *S,
+                                       double rn, bool writer) {
   int64_t h = S->hist_len;
-  a.hist_r[h] = rn;
-  a.hist_m[h] = S->matvecs;
-  a.hist_t[h] = globaltimer();
+  if (writer) {
+    a.hist_r[h] = rn;
+    a.hist_m[h] = S->matvecs;
+    a.hist_t[h] = globaltimer();
+  }
   S->hist_len = h + 1;
 }
 
@@ -89,14 +96,14 @@ __host__ __device__ constexpr int ndots_of(int PH) {
 // Scalar logic of each phase, executed by thread 0 of the finishing CTA once
 // the dot products d[] are final.  Mirrors solvers.py:288-356 line by line.
 template <int PH>
-__device__ void finalize(const IterArgs &a, const double *d) {
-  SolveScalars *S = a.S;
+__device__ __noinline__ void finalize(const IterArgs &a, SolveScalars *S, const double *d,
+                                     bool writer = true) {
   if (PH == PH_BNORM) {
     S->bnorm = __dsqrt_rn(d[0]);
     S->tol_abs = __dmul_rn(S->tol_abs, S->bnorm);  // tol_abs held tol
   } else if (PH == PH_INIT) {
     double rn = __dsqrt_rn(d[0]);
-    record(a, rn);
+    record(a, S, rn, writer);
     S->rnorm = rn;
     S->rho = d[1];
     S->nrt0 = __dsqrt_rn(d[2]);
@@ -120,7 +127,7 @@ __device__ void finalize(const IterArgs &a, const double *d) {
     double sn = __dsqrt_rn(d[0]);
     S->snorm = sn;
     if (sn <= S->tol_abs) {
-      record(a, sn);
+      record(a, S, sn, writer);
       S->early = 1;
       S->status = KRB_CONVERGED;
     }
@@ -141,7 +148,7 @@ __device__ void finalize(const IterArgs &a, const double *d) {
   } else if (PH == PH_XR) {
     double rn = __dsqrt_rn(d[0]);
     S->rnorm = rn;
-    record(a, rn);
+    record(a, S, rn, writer);
     S->itn += 1;
     if (rn <= S->tol_abs) {
       S->status = KRB_CONVERGED;
@@ -290,7 +297,7 @@ __device__ __forceinline__ void phase_leader(const IterArgs &a, const PhaseScal 
                           __dmul_rn(sc.omega, a.gamma[j]));
   }
   __syncthreads();
-  if (threadIdx.x == 0) finalize<PH>(a, dfin);
+  if (threadIdx.x == 0) finalize<PH>(a, a.S, dfin);
   __syncthreads();
 }
 
@@ -374,119 +381,133 @@ __global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ 
 
 // ---------------------------------------------------------------------------
 // persistent driver: the whole solve in one cooperative kernel
+//
+// Phases are separated by cooperative-groups grid barriers (~1.2 us on B200,
+// one round trip).  After a barrier EVERY CTA runs the canonical final stage
+// of the phase's dots and the scalar logic itself, on its own shared copy of
+// the scalar block: the inputs are the same partials in the same order, so
+// every copy is bit-identical and no second barrier is needed to broadcast
+// the scalars.  CTA 0 alone writes the history and, at the end, the scalar
+// block and xc back to global memory.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool gs_arrive(GridSync *g, unsigned int *s_gen,
-                                          int *s_lead) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int ge = *(volatile unsigned int *)&g->gen;
-    __threadfence();
-    unsigned int prev = atomicAdd(&g->count, 1u);
-    *s_lead = (prev == gridDim.x - 1);
-    *s_gen = ge;
-    if (*s_lead) __threadfence();
-  }
-  __syncthreads();
-  return *s_lead != 0;
-}
-
-__device__ __forceinline__ void gs_release(GridSync *g) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    g->count = 0;
-    __threadfence();
-    atomicAdd(&g->gen, 1u);
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void gs_wait(GridSync *g, unsigned int gen0) {
-  if (threadIdx.x == 0) {
-    while (*(volatile unsigned int *)&g->gen == gen0) __nanosleep(20);
-    __threadfence();   // acquire + L1 invalidate (CCTL.IVALL)
+template <int ND>
+__device__ __forceinline__ void local_finals(const IterArgs &a, double *dfin) {
+  const int warp = threadIdx.x >> 5;
+  if (warp < ND) {
+    double v = warp_final_volatile(a.part + warp * a.nb, a.nb);
+    if ((threadIdx.x & 31) == 0) dfin[warp] = v;
   }
   __syncthreads();
 }
 
 template <int kE, bool kSell>
-__global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ pa,
-                                                  GridSync *gs) {
-  __shared__ double coef[512];
+__global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ pa) {
+  __shared__ double zeta[512], gamma[512], xc[512];
   __shared__ double red[kTdotCG][32];
-  __shared__ unsigned int s_gen;
-  __shared__ int s_lead;
+  __shared__ double dfin[3];
+  __shared__ SolveScalars L;
+  cg::grid_group grid = cg::this_grid();
   const IterArgs &a = *pa;
-  SolveScalars *S = a.S;
   const int64_t G = gridDim.x, me = blockIdx.x;
   const int64_t n = a.n, nb = a.nb;
   const int k = a.k;
   const int64_t ncg = (k + kTdotCG - 1) / kTdotCG;
+  const bool writer = me == 0;
   const krb_matrix A = a.A;
-
-#define KRB_GRID_SYNC(LEADER)                       \
-  do {                                              \
-    if (gs_arrive(gs, &s_gen, &s_lead)) {           \
-      LEADER;                                       \
-      gs_release(gs);                               \
-    } else {                                        \
-      gs_wait(gs, s_gen);                           \
-    }                                               \
-  } while (0)
+  if (threadIdx.x == 0) L = *a.S;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) xc[j] = a.xc[j];
+  __syncthreads();
 
   for (;;) {
-    if (S->status != KRB_RUNNING) break;
-    PhaseScal sc = load_scal(S);
-    // P
-    phase_blocks<kE, PH_PUPDATE>(a, sc, red, coef, me, G);
-    KRB_GRID_SYNC((void)0);
+    if (L.status != KRB_RUNNING) break;
+    PhaseScal sc{L.alpha, L.omega, L.beta};
+    // P: p = r + beta (p - omega q)
+    phase_blocks<kE, PH_PUPDATE>(a, sc, red, zeta, me, G);
+    grid.sync();
     // M: q = A p
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
       a.q[i] = spmv_row<kSell, false>(i, A, a.p);
-    KRB_GRID_SYNC((void)0);
-    // Z: zeta = Chat^T q
+    grid.sync();
+    // Z: zeta = Chat^T q   (every CTA computes the k finals into smem)
     if (k > 0) {
       for (int64_t u = me; u < nb * ncg; u += G)
         tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.q, a.part, u % nb,
                              (int)(u / nb) * kTdotCG, red);
-      KRB_GRID_SYNC(tdot_finals<false>(nb, k, a.part, a.zeta));
-      for (int j = threadIdx.x; j < k; j += blockDim.x) coef[j] = a.zeta[j];
+      grid.sync();
+      tdot_finals<false>(nb, k, a.part, zeta);
       __syncthreads();
+      grid.sync();   // partial buffer is reused by the next phase
     }
-    // Q
-    phase_blocks<kE, PH_PROJ_Q>(a, sc, red, coef, me, G);
-    KRB_GRID_SYNC(phase_leader<PH_PROJ_Q>(a, sc));
-    if (S->status != KRB_RUNNING) break;
-    sc = load_scal(S);
-    // S
-    phase_blocks<kE, PH_SUPD>(a, sc, red, coef, me, G);
-    KRB_GRID_SYNC(phase_leader<PH_SUPD>(a, sc));
-    if (S->status != KRB_RUNNING) {
-      if (S->early == 1) half_exit_update(a, sc.alpha, me, G);
+    // Q: q -= C zeta ; den, ||q|| -> alpha
+    phase_blocks<kE, PH_PROJ_Q>(a, sc, red, zeta, me, G);
+    grid.sync();
+    local_finals<2>(a, dfin);
+    if (threadIdx.x == 0) finalize<PH_PROJ_Q>(a, &L, dfin, writer);
+    __syncthreads();
+    if (L.status != KRB_RUNNING) break;
+    grid.sync();
+    sc.alpha = L.alpha;
+    // S: s = r - alpha q ; ||s|| -> half-step exit
+    phase_blocks<kE, PH_SUPD>(a, sc, red, zeta, me, G);
+    grid.sync();
+    local_finals<1>(a, dfin);
+    if (threadIdx.x == 0) finalize<PH_SUPD>(a, &L, dfin, writer);
+    __syncthreads();
+    if (L.status != KRB_RUNNING) {
+      // solvers.py:315-325: x += alpha p, xc += alpha zeta
+      for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
+        a.x[i] = __dadd_rn(a.x[i], __dmul_rn(sc.alpha, a.p[i]));
+      for (int j = threadIdx.x; j < k; j += blockDim.x)
+        xc[j] = __dadd_rn(xc[j], __dmul_rn(sc.alpha, zeta[j]));
+      __syncthreads();
       break;
     }
+    grid.sync();
     // M: t = A s
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
       a.t[i] = spmv_row<kSell, false>(i, A, a.s);
-    KRB_GRID_SYNC((void)0);
+    grid.sync();
     // Z: gamma = Chat^T t
     if (k > 0) {
       for (int64_t u = me; u < nb * ncg; u += G)
         tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.t, a.part, u % nb,
                              (int)(u / nb) * kTdotCG, red);
-      KRB_GRID_SYNC(tdot_finals<false>(nb, k, a.part, a.gamma));
-      for (int j = threadIdx.x; j < k; j += blockDim.x) coef[j] = a.gamma[j];
+      grid.sync();
+      tdot_finals<false>(nb, k, a.part, gamma);
       __syncthreads();
+      grid.sync();
     }
-    // T
-    phase_blocks<kE, PH_PROJ_T>(a, sc, red, coef, me, G);
-    KRB_GRID_SYNC(phase_leader<PH_PROJ_T>(a, sc));
-    if (S->status != KRB_RUNNING) break;
-    sc = load_scal(S);
-    // X
-    phase_blocks<kE, PH_XR>(a, sc, red, coef, me, G);
-    KRB_GRID_SYNC(phase_leader<PH_XR>(a, sc));
+    // T: t -= C gamma ; (t,t), (t,s) -> omega
+    phase_blocks<kE, PH_PROJ_T>(a, sc, red, gamma, me, G);
+    grid.sync();
+    local_finals<2>(a, dfin);
+    if (threadIdx.x == 0) finalize<PH_PROJ_T>(a, &L, dfin, writer);
+    __syncthreads();
+    if (L.status != KRB_RUNNING) break;
+    grid.sync();
+    sc.omega = L.omega;
+    // X: x, r ; ||r||, (rt0, r) -> record, convergence, rho, beta
+    phase_blocks<kE, PH_XR>(a, sc, red, zeta, me, G);
+    for (int j = threadIdx.x; j < k; j += blockDim.x)   // solvers.py:340
+      xc[j] = __dadd_rn(__dadd_rn(xc[j], __dmul_rn(sc.alpha, zeta[j])),
+                        __dmul_rn(sc.omega, gamma[j]));
+    grid.sync();
+    local_finals<2>(a, dfin);
+    if (threadIdx.x == 0) finalize<PH_XR>(a, &L, dfin, writer);
+    __syncthreads();
+    grid.sync();
   }
-#undef KRB_GRID_SYNC
+  if (writer) {
+    if (threadIdx.x == 0) {
+      L.bodies = L.itn;
+      *a.S = L;
+    }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      a.xc[j] = xc[j];
+      a.zeta[j] = zeta[j];
+      a.gamma[j] = gamma[j];
+    }
+  }
 }
 
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
@@ -554,7 +575,7 @@ static int launch_iteration(const IterArgs &h, const IterArgs *d, cudaStream_t s
 }
 
 template <int kE, bool kSell>
-static int persist_launch(const IterArgs *d, GridSync *gs, cudaStream_t st) {
+static int persist_launch(const IterArgs *d, cudaStream_t st) {
   static int grid = 0;
   if (grid == 0) {
     int per_sm = 0;
@@ -565,23 +586,23 @@ static int persist_launch(const IterArgs *d, GridSync *gs, cudaStream_t st) {
     KRB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     grid = (per_sm > 0 ? per_sm : 1) * sms;
   }
-  void *args[] = {(void *)&d, (void *)&gs};
+  void *args[] = {(void *)&d};
   KRB_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_persist<kE, kSell>,
                                              dim3(grid), dim3(1024), args, 0, st));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
 
-static int launch_persistent(const IterArgs &h, const IterArgs *d, GridSync *gs,
-                             cudaStream_t st) {
+static int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.n == 0) return KRB_OK;
   const bool sell = h.A.format == 2;
+  // small systems only (E <= 2, n <= 606208): larger ones run the graph
   switch (canon_E(h.n)) {
-    case 1: return sell ? persist_launch<1, true>(d, gs, st) : persist_launch<1, false>(d, gs, st);
-    case 2: return sell ? persist_launch<2, true>(d, gs, st) : persist_launch<2, false>(d, gs, st);
-    case 4: return sell ? persist_launch<4, true>(d, gs, st) : persist_launch<4, false>(d, gs, st);
-    case 8: return sell ? persist_launch<8, true>(d, gs, st) : persist_launch<8, false>(d, gs, st);
-    default: return sell ? persist_launch<16, true>(d, gs, st) : persist_launch<16, false>(d, gs, st);
+    case 1: return sell ? persist_launch<1, true>(d, st) : persist_launch<1, false>(d, st);
+    case 2: return sell ? persist_launch<2, true>(d, st) : persist_launch<2, false>(d, st);
+    default:
+      set_error("persistent driver supports n <= %d (canon_E <= 2)", 2 * kLanes * kTargetBlocks);
+      return KRB_EINVAL;
   }
 }
 
@@ -709,7 +730,6 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   h.use_cond = graph ? 1 : 0;
   h.cond = hit ? G.cond : 0;
   IterArgs *d = reinterpret_cast<IterArgs *>(ctx->desc);
-  GridSync *gs = reinterpret_cast<GridSync *>(ctx->counters + kCounterGridSync);
 
   // ---- setup (solvers.py:257-296) -------------------------------------
   if (graph && !hit) {
@@ -761,8 +781,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
 
   // ---- iterations (solvers.py:298-356) --------------------------------
   if (mode == 2) {
-    KRB_CHECK_CUDA(cudaMemsetAsync(gs, 0, sizeof(GridSync), st));
-    KRB_TRY(launch_persistent(h, d, gs, st));
+    KRB_TRY(launch_persistent(h, d, st));
   } else if (graph) {
     KRB_CHECK_CUDA(cudaGraphLaunch(G.exec, st));
     per_body = G.kernels_per_body;

@@ -33,7 +33,8 @@ def num(v):
     val, unit = v
     x = float(val.replace(",", ""))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-             "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(unit, 1)
+             "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3,
+             "second": 1, "s": 1}.get(unit, 1)
     return x * scale
 
 

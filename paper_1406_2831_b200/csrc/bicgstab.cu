@@ -61,7 +61,7 @@ struct IterArgs {
   const double *C, *Chat, *U;
   double *x, *r, *p, *q, *s, *t, *rt0, *b;
   double *zeta, *gamma, *xc;
-  double *part;
+  double *part, *part2;   // part2: second partial buffer (persistent kernel)
   unsigned int *counters;
   SolveScalars *S;
   double *hist_r;
@@ -183,7 +183,7 @@ template <int kE, int PH>
 __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal sc,
                                              double (*red)[32],
                                              const double *coef, int64_t first,
-                                             int64_t step) {
+                                             int64_t step, double *part_buf) {
   constexpr int ND = ndots_of(PH);
   const double alpha = sc.alpha, omega = sc.omega, beta = sc.beta;
   const int k = a.k;
@@ -197,7 +197,7 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
   const double *__restrict__ rt0 = a.rt0;
   const double *__restrict__ bvec = a.b;
   const double *__restrict__ Cm = a.C;
-  double *__restrict__ part = a.part;
+  double *__restrict__ part = part_buf;
   for (int64_t blk = first; blk < nb; blk += step) {
     const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
     double acc[3] = {0.0, 0.0, 0.0};
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa)
     for (int j = threadIdx.x; j < a.k; j += blockDim.x) coef[j] = src[j];
     __syncthreads();
   }
-  phase_blocks<kE, PH>(a, sc, red, coef, blockIdx.x, gridDim.x);
+  phase_blocks<kE, PH>(a, sc, red, coef, blockIdx.x, gridDim.x, a.part);
   if (ND == 0) return;
   if (!elect_last_cta(a.counters + PH, &last_flag)) return;
   phase_leader<PH>(a, sc);
@@ -391,10 +391,11 @@ __global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ 
 // block and xc back to global memory.
 // ---------------------------------------------------------------------------
 template <int ND>
-__device__ __forceinline__ void local_finals(const IterArgs &a, double *dfin) {
+__device__ __forceinline__ void local_finals(const IterArgs &a, const double *pb,
+                                             double *dfin) {
   const int warp = threadIdx.x >> 5;
   if (warp < ND) {
-    double v = warp_final_volatile(a.part + warp * a.nb, a.nb);
+    double v = warp_final_volatile(pb + warp * a.nb, a.nb);
     if ((threadIdx.x & 31) == 0) dfin[warp] = v;
   }
   __syncthreads();
@@ -418,11 +419,16 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
   for (int j = threadIdx.x; j < k; j += blockDim.x) xc[j] = a.xc[j];
   __syncthreads();
 
+  // Partials alternate between two buffers: a phase writes one while the
+  // previous phase's partials (still being read by slower CTAs after their
+  // barrier) stay intact in the other -- one barrier per phase.
+  double *pb[2] = {a.part, a.part2};
+  int cur = 0;
   for (;;) {
     if (L.status != KRB_RUNNING) break;
     PhaseScal sc{L.alpha, L.omega, L.beta};
     // P: p = r + beta (p - omega q)
-    phase_blocks<kE, PH_PUPDATE>(a, sc, red, zeta, me, G);
+    phase_blocks<kE, PH_PUPDATE>(a, sc, red, zeta, me, G, pb[cur]);
     grid.sync();
     // M: q = A p
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
@@ -431,26 +437,27 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     // Z: zeta = Chat^T q   (every CTA computes the k finals into smem)
     if (k > 0) {
       for (int64_t u = me; u < nb * ncg; u += G)
-        tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.q, a.part, u % nb,
+        tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.q, pb[cur], u % nb,
                              (int)(u / nb) * kTdotCG, red);
       grid.sync();
-      tdot_finals<false>(nb, k, a.part, zeta);
+      tdot_finals<false>(nb, k, pb[cur], zeta);
       __syncthreads();
-      grid.sync();   // partial buffer is reused by the next phase
+      cur ^= 1;
     }
     // Q: q -= C zeta ; den, ||q|| -> alpha
-    phase_blocks<kE, PH_PROJ_Q>(a, sc, red, zeta, me, G);
+    phase_blocks<kE, PH_PROJ_Q>(a, sc, red, zeta, me, G, pb[cur]);
     grid.sync();
-    local_finals<2>(a, dfin);
+    local_finals<2>(a, pb[cur], dfin);
+    cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_PROJ_Q>(a, &L, dfin, writer);
     __syncthreads();
     if (L.status != KRB_RUNNING) break;
-    grid.sync();
     sc.alpha = L.alpha;
     // S: s = r - alpha q ; ||s|| -> half-step exit
-    phase_blocks<kE, PH_SUPD>(a, sc, red, zeta, me, G);
+    phase_blocks<kE, PH_SUPD>(a, sc, red, zeta, me, G, pb[cur]);
     grid.sync();
-    local_finals<1>(a, dfin);
+    local_finals<1>(a, pb[cur], dfin);
+    cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_SUPD>(a, &L, dfin, writer);
     __syncthreads();
     if (L.status != KRB_RUNNING) {
@@ -462,7 +469,6 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
       __syncthreads();
       break;
     }
-    grid.sync();
     // M: t = A s
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
       a.t[i] = spmv_row<kSell, false>(i, A, a.s);
@@ -470,32 +476,32 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     // Z: gamma = Chat^T t
     if (k > 0) {
       for (int64_t u = me; u < nb * ncg; u += G)
-        tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.t, a.part, u % nb,
+        tdot_unit<kE, false>(n, nb, k, a.Chat, a.ld, a.t, pb[cur], u % nb,
                              (int)(u / nb) * kTdotCG, red);
       grid.sync();
-      tdot_finals<false>(nb, k, a.part, gamma);
+      tdot_finals<false>(nb, k, pb[cur], gamma);
       __syncthreads();
-      grid.sync();
+      cur ^= 1;
     }
     // T: t -= C gamma ; (t,t), (t,s) -> omega
-    phase_blocks<kE, PH_PROJ_T>(a, sc, red, gamma, me, G);
+    phase_blocks<kE, PH_PROJ_T>(a, sc, red, gamma, me, G, pb[cur]);
     grid.sync();
-    local_finals<2>(a, dfin);
+    local_finals<2>(a, pb[cur], dfin);
+    cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_PROJ_T>(a, &L, dfin, writer);
     __syncthreads();
     if (L.status != KRB_RUNNING) break;
-    grid.sync();
     sc.omega = L.omega;
     // X: x, r ; ||r||, (rt0, r) -> record, convergence, rho, beta
-    phase_blocks<kE, PH_XR>(a, sc, red, zeta, me, G);
+    phase_blocks<kE, PH_XR>(a, sc, red, zeta, me, G, pb[cur]);
     for (int j = threadIdx.x; j < k; j += blockDim.x)   // solvers.py:340
       xc[j] = __dadd_rn(__dadd_rn(xc[j], __dmul_rn(sc.alpha, zeta[j])),
                         __dmul_rn(sc.omega, gamma[j]));
     grid.sync();
-    local_finals<2>(a, dfin);
+    local_finals<2>(a, pb[cur], dfin);
+    cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_XR>(a, &L, dfin, writer);
     __syncthreads();
-    grid.sync();
   }
   if (writer) {
     if (threadIdx.x == 0) {
@@ -700,7 +706,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   const int64_t l0 = launch_counter();
   int64_t per_body = 0;
   const int64_t nb = canon_nblocks(n);
-  KRB_TRY(ctx_reserve_part(ctx, (size_t)(3 * nb > k * nb ? 3 * nb : k * nb) + 64));
+  const size_t part_one = (size_t)(3 * nb > k * nb ? 3 * nb : k * nb) + 64;
+  KRB_TRY(ctx_reserve_part(ctx, 2 * part_one));
   IterArgs h = {};
   h.A = *A;
   h.A.T = nullptr;
@@ -718,6 +725,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   h.xc = ctx->kbuf + 2 * ctx->vec_k;
   double *ybuf = ctx->kbuf + 3 * ctx->vec_k;
   h.part = ctx->part;
+  h.part2 = ctx->part + part_one;
   h.counters = ctx->counters;
   h.S = ctx->S;
   h.hist_r = hist_r;

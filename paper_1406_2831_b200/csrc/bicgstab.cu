@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ 
   if (i >= a.A.n) return;
   const double *x = kSecond ? a.s : a.p;
   double *y = kSecond ? a.t : a.q;
-  y[i] = spmv_row<kSell>(i, a.A, x);
+  y[(kSell && a.A.perm) ? a.A.perm[i] : i] = spmv_row<kSell>(i, a.A, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     grid.sync();
     // M: q = A p
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
-      a.q[i] = spmv_row<kSell, false>(i, A, a.p);
+      a.q[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell, false>(i, A, a.p);
     grid.sync();
     // Z: zeta = Chat^T q   (every CTA computes the k finals into smem)
     if (k > 0) {
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     }
     // M: t = A s
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
-      a.t[i] = spmv_row<kSell, false>(i, A, a.s);
+      a.t[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell, false>(i, A, a.s);
     grid.sync();
     // Z: gamma = Chat^T t
     if (k > 0) {

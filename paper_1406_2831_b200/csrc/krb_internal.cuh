@@ -27,6 +27,7 @@ struct krb_matrix {
   int32_t *rlen = nullptr;
   int32_t *s_col = nullptr;
   double *s_val = nullptr;
+  int32_t *perm = nullptr;  // SELL-C-sigma: slice position -> row (NULL: identity)
   krb_matrix *T = nullptr;  // lazily built transpose
   int64_t bytes = 0;
 };

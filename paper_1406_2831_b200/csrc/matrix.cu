@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
   if (status && *status) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
-  y[i] = spmv_row<kSell>(i, A, x);
+  y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
 }
 
 int spmv_launch(const krb_matrix *A, const double *x, double *y,
@@ -98,42 +98,127 @@ __global__ void k_i64_to_i32(int64_t m, const int64_t *src, int32_t *dst) {
   if (i < m) dst[i] = (int32_t)src[i];
 }
 
-static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
+__global__ void k_iota(int64_t m, int32_t *p) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) p[i] = (int32_t)i;
+}
+
+__global__ void k_sell_fill_perm(int64_t n, const int64_t *__restrict__ rp,
+                                 const int32_t *__restrict__ ci,
+                                 const double *__restrict__ val,
+                                 const int64_t *__restrict__ sl_ptr,
+                                 const int32_t *__restrict__ perm,
+                                 int32_t *__restrict__ s_col,
+                                 double *__restrict__ s_val) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t row = perm[p];
+  int64_t base = sl_ptr[p >> 5] + (p & 31);
+  int64_t b = rp[row], e = rp[row + 1];
+  for (int64_t jj = b; jj < e; ++jj) {
+    s_col[base + 32 * (jj - b)] = ci[jj];
+    s_val[base + 32 * (jj - b)] = val[jj];
+  }
+}
+
+__global__ void k_window_offsets(int64_t nseg, int64_t n, int64_t sigma, int *off) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= nseg) off[i] = (int)(i * sigma < n ? i * sigma : n);
+}
+
+// slice widths + exclusive scan -> sl_ptr; returns the padded element count
+static int sell_layout(krb_matrix *A, const int32_t *rlen_pos, int64_t *total,
+                       cudaStream_t st) {
   const int64_t n = A->n;
-  A->nslices = (n + 31) / 32;
   int64_t *width = nullptr;
-  KRB_CHECK_CUDA(cudaMalloc(&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1)));
   KRB_CHECK_CUDA(cudaMalloc(&width, sizeof(int64_t) * (A->nslices + 1)));
-  KRB_CHECK_CUDA(cudaMalloc(&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1)));
-  unsigned blocks = (unsigned)((n + 255) / 256);
   if (n > 0) {
-    k_row_len<<<blocks, 256, 0, st>>>(n, A->rp, A->rlen);
-    KRB_CHECK_LAUNCH();
     unsigned wblocks = (unsigned)((A->nslices * 32 + 255) / 256);
-    k_slice_width<<<wblocks, 256, 0, st>>>(n, A->rlen, width);
+    k_slice_width<<<wblocks, 256, 0, st>>>(n, rlen_pos, width);
     KRB_CHECK_LAUNCH();
   }
   KRB_CHECK_CUDA(cudaMemsetAsync(width + A->nslices, 0, sizeof(int64_t), st));
   void *tmp = nullptr;
   size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr,
-                                A->nslices + 1, st);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr, A->nslices + 1, st);
   KRB_CHECK_CUDA(cudaMalloc(&tmp, tmp_bytes));
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr,
-                                A->nslices + 1, st);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr, A->nslices + 1, st);
   KRB_CHECK_CUDA(cudaGetLastError());
-  int64_t total = 0;
-  KRB_CHECK_CUDA(cudaMemcpyAsync(&total, A->sl_ptr + A->nslices,
-                                 sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaMemcpyAsync(total, A->sl_ptr + A->nslices, sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));
   cudaFree(tmp);
   cudaFree(width);
+  return KRB_OK;
+}
+
+// SELL-C-sigma: sort rows by length (descending, stable) inside windows of
+// kSigma rows so every 32-row slice holds rows of similar length; the
+// permutation only moves whole rows, each row is still summed in CSR order.
+constexpr int64_t kSigma = 4096;
+
+static int sigma_sort(krb_matrix *A, cudaStream_t st) {
+  const int64_t n = A->n;
+  const int64_t nseg = (n + kSigma - 1) / kSigma;
+  int32_t *keys_out = nullptr, *iota = nullptr;
+  int *off = nullptr;
+  KRB_CHECK_CUDA(cudaMalloc(&keys_out, sizeof(int32_t) * n));
+  KRB_CHECK_CUDA(cudaMalloc(&iota, sizeof(int32_t) * n));
+  KRB_CHECK_CUDA(cudaMalloc(&A->perm, sizeof(int32_t) * n));
+  KRB_CHECK_CUDA(cudaMalloc(&off, sizeof(int) * (nseg + 1)));
+  k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, iota);
+  KRB_CHECK_LAUNCH();
+  k_window_offsets<<<(unsigned)((nseg + 256) / 256), 256, 0, st>>>(nseg, n, kSigma, off);
+  KRB_CHECK_LAUNCH();
+  void *tmp = nullptr;
+  size_t tb = 0;
+  cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, A->rlen, keys_out, iota,
+                                                     A->perm, (int)n, (int)nseg, off, off + 1,
+                                                     0, 32, st);
+  KRB_CHECK_CUDA(cudaMalloc(&tmp, tb));
+  cub::DeviceSegmentedRadixSort::SortPairsDescending(tmp, tb, A->rlen, keys_out, iota,
+                                                     A->perm, (int)n, (int)nseg, off, off + 1,
+                                                     0, 32, st);
+  KRB_CHECK_CUDA(cudaGetLastError());
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  cudaFree(off);
+  cudaFree(iota);
+  cudaFree(A->rlen);
+  A->rlen = keys_out;   // lengths now indexed by slice position
+  return KRB_OK;
+}
+
+static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
+  const int64_t n = A->n;
+  A->nslices = (n + 31) / 32;
+  KRB_CHECK_CUDA(cudaMalloc(&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1)));
+  KRB_CHECK_CUDA(cudaMalloc(&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1)));
+  unsigned blocks = (unsigned)((n + 255) / 256);
+  if (n > 0) {
+    k_row_len<<<blocks, 256, 0, st>>>(n, A->rp, A->rlen);
+    KRB_CHECK_LAUNCH();
+  }
+  int64_t total = 0;
+  int rc = sell_layout(A, A->rlen, &total, st);
+  if (rc) return rc;
+  const int64_t budget = A->nnz + A->nnz / 5;   // <= 20 % padding
+  bool use_sell = format == 2 || (format == 0 && total <= budget);
+  if (!use_sell && (format == 0 || format == 3) && n > 0) {
+    rc = sigma_sort(A, st);
+    if (rc) return rc;
+    rc = sell_layout(A, A->rlen, &total, st);
+    if (rc) return rc;
+    use_sell = format == 3 || total <= budget;
+    if (!use_sell) {
+      cudaFree(A->perm);
+      A->perm = nullptr;
+    }
+  }
   A->sell_elems = total;
-  bool use_sell = format == 2 || (format == 0 && total <= A->nnz + A->nnz / 5);
   if (!use_sell) {
     cudaFree(A->sl_ptr);
     A->sl_ptr = nullptr;
-    // keep rlen (4 B/row) - unused by CSR kernels, free it
     cudaFree(A->rlen);
     A->rlen = nullptr;
     A->format = 1;
@@ -146,14 +231,16 @@ static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
     KRB_CHECK_LAUNCH();
   }
   if (n > 0) {
-    k_sell_fill<<<blocks, 256, 0, st>>>(n, A->rp, A->ci, A->val, A->sl_ptr,
-                                        A->s_col, A->s_val);
+    if (A->perm)
+      k_sell_fill_perm<<<blocks, 256, 0, st>>>(n, A->rp, A->ci, A->val, A->sl_ptr, A->perm,
+                                               A->s_col, A->s_val);
+    else
+      k_sell_fill<<<blocks, 256, 0, st>>>(n, A->rp, A->ci, A->val, A->sl_ptr,
+                                          A->s_col, A->s_val);
     KRB_CHECK_LAUNCH();
   }
   A->format = 2;
-  // the CSR copy is still needed to build the transpose; drop values/cols
-  // once the transpose exists (see ensure_transpose).
-  A->bytes += total * 12 + (A->nslices + 1) * 8 + n * 4;
+  A->bytes += total * 12 + (A->nslices + 1) * 8 + n * 4 + (A->perm ? n * 4 : 0);
   return KRB_OK;
 }
 
@@ -207,10 +294,6 @@ __global__ void k_entry_rows(int64_t n, const int64_t *__restrict__ rp,
   for (int64_t jj = rp[i]; jj < rp[i + 1]; ++jj) rows[jj] = (int32_t)i;
 }
 
-__global__ void k_iota(int64_t m, int32_t *p) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) p[i] = (int32_t)i;
-}
 
 __global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ ci,
                             int64_t *__restrict__ cnt) {
@@ -302,6 +385,7 @@ void matrix_free(krb_matrix *A) {
   cudaFree(A->rlen);
   cudaFree(A->s_col);
   cudaFree(A->s_val);
+  cudaFree(A->perm);
   delete A;
 }
 
@@ -341,7 +425,7 @@ int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz, int *format,
   KRB_REQUIRE(A != nullptr, "krb_matrix_info: NULL matrix");
   if (n) *n = A->n;
   if (nnz) *nnz = A->nnz;
-  if (format) *format = A->format;
+  if (format) *format = (A->format == 2 && A->perm) ? 3 : A->format;
   if (bytes) *bytes = A->bytes + (A->T ? A->T->bytes : 0);
   return KRB_OK;
 }

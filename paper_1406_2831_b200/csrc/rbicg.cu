@@ -332,9 +332,9 @@ __global__ void __launch_bounds__(256) k_bspmv(const BiArgs *__restrict__ pa) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   if (kTrans)
-    a.qt[i] = spmv_row<kSell>(i, a.AT, a.pt);
+    a.qt[(kSell && a.AT.perm) ? a.AT.perm[i] : i] = spmv_row<kSell>(i, a.AT, a.pt);
   else
-    a.q[i] = spmv_row<kSell>(i, a.A, a.p);
+    a.q[(kSell && a.A.perm) ? a.A.perm[i] : i] = spmv_row<kSell>(i, a.A, a.p);
 }
 
 __global__ void k_bi_init_scalars(BiScalars *S, double tol, double btol,

@@ -43,7 +43,7 @@ def test_spmv_bitwise_vs_reference_golden(dev, golden, name):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
-@pytest.mark.parametrize("fmt", [0, 1, 2])
+@pytest.mark.parametrize("fmt", [0, 1, 2, 3])
 def test_spmv_formats_bitwise(dev, canon, cfg, fmt):
     from oracle.ops import CsrOperand
     from paper_1406_2831_b200.workloads import make_sequence
@@ -55,6 +55,15 @@ def test_spmv_formats_bitwise(dev, canon, cfg, fmt):
     assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(),
                           canon.rmatvec(op, x))
     assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), op._csr @ x)
+
+
+def test_sell_sigma_chosen_for_power_law(dev):
+    from paper_1406_2831_b200.workloads import c4_sequence
+    A = c4_sequence(n=50_000, num=1).matrix(0)
+    M = dev.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+    assert M.format == "sell32-sigma"
+    x = np.random.default_rng(1).standard_normal(A.n)
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), A.to_scipy() @ x)
 
 
 def test_spmv_empty_rows_and_tiny(dev):

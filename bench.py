@@ -365,6 +365,13 @@ def synthetic_pass(wl, dmats, drhs):
     share = {k: v[1] for k, v in kern.items()}
     dom = max(share, key=share.get)
     b, t = kern[dom]
+    from paper_1406_2831_b200.solvers import _auto_mode
+    if _auto_mode(wl.n) == 2:
+        # the persistent driver runs each whole solve as ONE kernel (k_persist):
+        # it is the dominant (only) kernel of the step; per launch = one solve
+        dom = "k_persist (one RBiCGSTAB solve per launch)"
+        b = B_it * its / max(len(ks), 1)
+        t = t_solve / max(len(ks), 1)
     ach = b / t / 1e9
     return {
         "synthetic": {"iterations": its, "seconds": t_solve, "k_per_system": ks,

@@ -373,6 +373,15 @@ def synthetic_pass(wl, dmats, drhs):
         b = B_it * its / max(len(ks), 1)
         t = t_solve / max(len(ks), 1)
     ach = b / t / 1e9
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp)).get(wl.name)
+        if tj and dom.startswith(tj["kernel"]):
+            if "bytes_per_iteration" in tj:
+                traffic = int(tj["bytes_per_iteration"] * its / max(len(ks), 1))
+            else:
+                traffic = int(tj["bytes_per_launch"])
     return {
         "synthetic": {"iterations": its, "seconds": t_solve, "k_per_system": ks,
                       "iters_per_s": its / t_solve,
@@ -382,7 +391,7 @@ def synthetic_pass(wl, dmats, drhs):
                                "peak": peak, "frac": round(it_ach / peak, 4)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1),
                      "peak": peak, "peak_source": src, "unit": "GB/s",
-                     "frac": round(ach / peak, 4), "traffic": None,
+                     "frac": round(ach / peak, 4), "traffic": traffic,
                      "bytes_per_launch": b, "launch_us": round(t * 1e6, 2)},
         "kernels": {k: {"bytes": v[0], "us": round(v[1] * 1e6, 2),
                         "GBps": round(v[0] / v[1] / 1e9, 1)} for k, v in kern.items()},

@@ -149,7 +149,12 @@ typedef struct krb_solve_config {
    * device from these PCG64 words (numpy default_rng(seed) state)          */
   const double *d_shadow;
   uint64_t pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo;
-  int use_graph;         /* 1: CUDA graph with device-side while loop      */
+  int use_graph;         /* 0 host loop, 1 CUDA graph with a device WHILE
+                            node, 2 persistent cooperative kernel           */
+  /* optional (persistent driver): %globaltimer stamp after each of the 10
+   * phase boundaries of iteration i at d_phase_stamps[16 i + slot]        */
+  uint64_t *d_phase_stamps;
+  int64_t phase_stamps_cap;  /* iterations covered                        */
 } krb_solve_config;
 
 typedef struct krb_solve_result {

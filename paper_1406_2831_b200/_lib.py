@@ -46,7 +46,8 @@ class SolveConfig(ctypes.Structure):
                 ("d_shadow", c_vp),
                 ("pcg_state_hi", c_u64), ("pcg_state_lo", c_u64),
                 ("pcg_inc_hi", c_u64), ("pcg_inc_lo", c_u64),
-                ("use_graph", c_int)]
+                ("use_graph", c_int), ("d_phase_stamps", c_vp),
+                ("phase_stamps_cap", c_i64)]
 
 
 class SolveResult(ctypes.Structure):

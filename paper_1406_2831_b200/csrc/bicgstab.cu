@@ -62,6 +62,8 @@ struct IterArgs {
   double *x, *r, *p, *q, *s, *t, *rt0, *b;
   double *zeta, *gamma, *xc;
   double *part, *part2;   // part2: second partial buffer (persistent kernel)
+  uint64_t *prof;         // optional per-phase %globaltimer stamps (16/iter)
+  int64_t prof_cap;
   unsigned int *counters;
   SolveScalars *S;
   double *hist_r;
@@ -424,16 +426,24 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
   // barrier) stay intact in the other -- one barrier per phase.
   double *pb[2] = {a.part, a.part2};
   int cur = 0;
+  uint64_t *prof = (writer && threadIdx.x == 0) ? a.prof : nullptr;
+#define KRB_STAMP(slot)                                              \
+  do {                                                               \
+    if (prof && L.itn < a.prof_cap) prof[L.itn * 16 + (slot)] = globaltimer(); \
+  } while (0)
   for (;;) {
     if (L.status != KRB_RUNNING) break;
     PhaseScal sc{L.alpha, L.omega, L.beta};
+    KRB_STAMP(0);
     // P: p = r + beta (p - omega q)
     phase_blocks<kE, PH_PUPDATE>(a, sc, red, zeta, me, G, pb[cur]);
     grid.sync();
+    KRB_STAMP(1);
     // M: q = A p
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
       a.q[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell, false>(i, A, a.p);
     grid.sync();
+    KRB_STAMP(2);
     // Z: zeta = Chat^T q   (every CTA computes the k finals into smem)
     if (k > 0) {
       for (int64_t u = me; u < nb * ncg; u += G)
@@ -444,6 +454,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
       __syncthreads();
       cur ^= 1;
     }
+    KRB_STAMP(3);
     // Q: q -= C zeta ; den, ||q|| -> alpha
     phase_blocks<kE, PH_PROJ_Q>(a, sc, red, zeta, me, G, pb[cur]);
     grid.sync();
@@ -451,6 +462,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_PROJ_Q>(a, &L, dfin, writer);
     __syncthreads();
+    KRB_STAMP(4);
     if (L.status != KRB_RUNNING) break;
     sc.alpha = L.alpha;
     // S: s = r - alpha q ; ||s|| -> half-step exit
@@ -460,6 +472,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_SUPD>(a, &L, dfin, writer);
     __syncthreads();
+    KRB_STAMP(5);
     if (L.status != KRB_RUNNING) {
       // solvers.py:315-325: x += alpha p, xc += alpha zeta
       for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
@@ -473,6 +486,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
       a.t[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell, false>(i, A, a.s);
     grid.sync();
+    KRB_STAMP(6);
     // Z: gamma = Chat^T t
     if (k > 0) {
       for (int64_t u = me; u < nb * ncg; u += G)
@@ -483,6 +497,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
       __syncthreads();
       cur ^= 1;
     }
+    KRB_STAMP(7);
     // T: t -= C gamma ; (t,t), (t,s) -> omega
     phase_blocks<kE, PH_PROJ_T>(a, sc, red, gamma, me, G, pb[cur]);
     grid.sync();
@@ -490,6 +505,7 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_PROJ_T>(a, &L, dfin, writer);
     __syncthreads();
+    KRB_STAMP(8);
     if (L.status != KRB_RUNNING) break;
     sc.omega = L.omega;
     // X: x, r ; ||r||, (rt0, r) -> record, convergence, rho, beta
@@ -500,9 +516,11 @@ __global__ void __launch_bounds__(1024) k_persist(const IterArgs *__restrict__ p
     grid.sync();
     local_finals<2>(a, pb[cur], dfin);
     cur ^= 1;
+    KRB_STAMP(9);
     if (threadIdx.x == 0) finalize<PH_XR>(a, &L, dfin, writer);
     __syncthreads();
   }
+#undef KRB_STAMP
   if (writer) {
     if (threadIdx.x == 0) {
       L.bodies = L.itn;
@@ -731,6 +749,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   h.hist_r = hist_r;
   h.hist_m = hist_m;
   h.hist_t = hist_t;
+  h.prof = cfg->d_phase_stamps;
+  h.prof_cap = cfg->d_phase_stamps ? cfg->phase_stamps_cap : 0;
   const int mode = cfg->use_graph;   // 0 host loop, 1 graph, 2 persistent
   const bool graph = mode == 1;
   GraphCache &G = ctx->graph;

@@ -92,6 +92,66 @@ int spmv_launch(const krb_matrix *A, const double *x, double *y,
   return KRB_OK;
 }
 
+
+// ---- SpMM: Y[:,c] = A X[:,c] for a group of kNC columns per pass --------
+// Each thread owns one row and walks it ONCE in CSR order, keeping kNC
+// independent sequential sums (multiply then add, from 0.0) -- so every
+// column is bit-identical to its own SpMV, while the matrix is read once per
+// group of kNC columns instead of once per column.
+template <bool kSell, int kNC>
+__global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
+                                              const double *__restrict__ X,
+                                              int64_t ldx, double *__restrict__ Y,
+                                              int64_t ldy) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  const int c0 = blockIdx.y * kNC;
+  const int nc = min(kNC, ncols - c0);
+  const double *Xc = X + (int64_t)c0 * ldx;
+  double sum[kNC];
+#pragma unroll
+  for (int c = 0; c < kNC; ++c) sum[c] = 0.0;
+  int64_t row = i;
+  if (kSell) {
+    if (A.perm) row = A.perm[i];
+    const int len = __ldg(A.rlen + i);
+    const int64_t base = __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
+    for (int j = 0; j < len; ++j) {
+      const int col = __ldg(A.s_col + base + 32 * j);
+      const double v = __ldg(A.s_val + base + 32 * j);
+#pragma unroll
+      for (int c = 0; c < kNC; ++c)
+        if (c < nc) sum[c] = __dadd_rn(sum[c], __dmul_rn(v, __ldg(Xc + (int64_t)c * ldx + col)));
+    }
+  } else {
+    const int64_t b = __ldg(A.rp + i), e = __ldg(A.rp + i + 1);
+    for (int64_t jj = b; jj < e; ++jj) {
+      const int col = __ldg(A.ci + jj);
+      const double v = __ldg(A.val + jj);
+#pragma unroll
+      for (int c = 0; c < kNC; ++c)
+        if (c < nc) sum[c] = __dadd_rn(sum[c], __dmul_rn(v, __ldg(Xc + (int64_t)c * ldx + col)));
+    }
+  }
+  double *Yc = Y + (int64_t)c0 * ldy;
+#pragma unroll
+  for (int c = 0; c < kNC; ++c)
+    if (c < nc) Yc[(int64_t)c * ldy + row] = sum[c];
+}
+
+int spmm_launch(const krb_matrix *M, int64_t ncols, const double *X, int64_t ldx,
+                double *Y, int64_t ldy, cudaStream_t st) {
+  constexpr int kNC = 8;
+  if (M->n == 0 || ncols == 0) return KRB_OK;
+  dim3 grid((unsigned)((M->n + 255) / 256), (unsigned)((ncols + kNC - 1) / kNC));
+  if (M->format == 2)
+    k_spmm<true, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
+  else
+    k_spmm<false, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
 // ---- build ---------------------------------------------------------------
 __global__ void k_i64_to_i32(int64_t m, const int64_t *src, int32_t *dst) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -454,11 +514,7 @@ int krb_spmm(krb_matrix *A, int transpose, int64_t ncols, const double *d_X,
     if (rc) return rc;
     M = A->T;
   }
-  for (int64_t c = 0; c < ncols; ++c) {
-    int rc = spmv_launch(M, d_X + c * ldx, d_Y + c * ldy, nullptr, st);
-    if (rc) return rc;
-  }
-  return KRB_OK;
+  return spmm_launch(M, ncols, d_X, ldx, d_Y, ldy, st);
 }
 
 }  // extern "C"

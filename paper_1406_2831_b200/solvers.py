@@ -167,6 +167,8 @@ _STATUS = {1: CONVERGED, 2: MAX_ITN, 3: BREAKDOWN_SERIOUS, 4: BREAKDOWN_OMEGA,
 
 
 LAST_SOLVE = {}   # launch accounting of the most recent solve (bench / tests)
+import os as _os
+_PHASE_PROF = _os.environ.get("KRB_PHASE_PROF") == "1"   # per-phase device stamps
 
 
 def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
@@ -229,6 +231,11 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     c.d_shadow = None
     c.pcg_state_hi, c.pcg_state_lo, c.pcg_inc_hi, c.pcg_inc_lo = pcg64_words(cfg.seed)
     c.use_graph = int(use_graph)
+    prof = None
+    if _PHASE_PROF and use_graph == 2:
+        prof = t.zeros((cfg.max_itn + 1) * 16, dtype=t.int64, device="cuda")
+        c.d_phase_stamps = prof.data_ptr()
+        c.phase_stamps_cap = cfg.max_itn + 1
     res = _lib.SolveResult()
     view = R.view() if R is not None else None
     t_launch = time.perf_counter()
@@ -251,6 +258,8 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     LAST_SOLVE.clear()
     LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
                       kernel_launches=int(res.kernel_launches))
+    if prof is not None:
+        LAST_SOLVE["phase_stamps"] = prof.view(-1, 16)[:hist.iterations].cpu().numpy()
     return xo, hist
 
 

@@ -46,13 +46,40 @@ def run(name, k=None, reps=3, max_itn=None):
             "GBps_alg": round(B * its / best / 1e9, 1)}
 
 
+def phase_breakdown(name, k=None):
+    """Per-phase device time inside the persistent kernel (KRB_PHASE_PROF=1):
+    median us per phase over the iterations of one solve."""
+    import paper_1406_2831_b200 as P
+    from paper_1406_2831_b200 import device as D, solvers as S, workloads as W
+    seq = W.make_sequence(name)
+    A = seq.matrix(0)
+    k = seq.k if k is None else k
+    M = D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+    r = np.random.default_rng(12345)
+    space = P.biorthonormalize(r.standard_normal((A.n, k)), r.standard_normal((A.n, k)), M) if k else None
+    b = D.to_device(seq.rhs(0, 0))
+    S.solve_device(M, b, None, space, P.SolverConfig(tol=seq.tol, seed=0), use_graph=2)
+    st = S.LAST_SOLVE["phase_stamps"].astype(np.int64)
+    names = ["P", "M1", "Z1", "Q", "S", "M2", "Z2", "T", "X"]
+    d = np.diff(st[:-1, :10], axis=1) / 1e3
+    full = (st[1:, 0] - st[:-1, 0]) / 1e3
+    return {"config": name, "k": k, "us_per_iteration": float(np.median(full)),
+            **{nm: round(float(np.median(d[:, i])), 2) for i, nm in enumerate(names)}}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", nargs="+", default=["c2"])
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--max-itn", type=int, default=None)
     ap.add_argument("--both", action="store_true", help="also k = 0")
+    ap.add_argument("--phases", action="store_true",
+                    help="per-phase breakdown of the persistent kernel")
     a = ap.parse_args()
+    if a.phases:
+        for c in a.config:
+            print(json.dumps(phase_breakdown(c, a.k)), flush=True)
+        sys.exit(0)
     for c in a.config:
         print(json.dumps(run(c, a.k, max_itn=a.max_itn)), flush=True)
         if a.both:

@@ -47,7 +47,7 @@ int krb_context_destroy(krb_context *ctx) {
   if (!ctx) return KRB_OK;
   ctx->graph.reset();
   double *bufs[] = {ctx->part, ctx->x, ctx->r, ctx->p, ctx->q, ctx->s,
-                    ctx->t, ctx->rt0, ctx->b, ctx->w, ctx->kbuf};
+                    ctx->t, ctx->rt0, ctx->b, ctx->w, ctx->p2, ctx->q2, ctx->kbuf};
   for (double *b : bufs)
     if (b) cudaFree(b);
   if (ctx->S) cudaFree(ctx->S);

@@ -58,6 +58,7 @@ struct krb_context {
   int64_t vec_n = 0, vec_k = 0;
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *s = nullptr,
          *t = nullptr, *rt0 = nullptr, *b = nullptr, *w = nullptr;
+  double *p2 = nullptr, *q2 = nullptr;   // double buffers (persistent v2)
   double *kbuf = nullptr;  // zeta, gamma, xc, y  (4 x k)
   krb::GraphCache graph;
 };

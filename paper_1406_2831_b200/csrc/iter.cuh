@@ -1,0 +1,286 @@
+// Shared pieces of the BiCGSTAB drivers (graph kernels and persistent
+// kernels): the solve descriptor, the per-phase scalar logic and the
+// fused elementwise + canonical-partial phase bodies.
+#pragma once
+
+#include "ctx.cuh"
+
+namespace krb {
+
+enum Phase {
+  PH_PUPDATE = 0,
+  PH_PROJ_Q,
+  PH_SUPD,
+  PH_PROJ_T,
+  PH_XR,
+  PH_BNORM,
+  PH_INIT,
+  PH_TRUE,
+  PH_RINIT,
+};
+
+struct IterArgs {
+  krb_matrix A;  // copy of the matrix handle (device pointers)
+  int64_t n, nb, ld;
+  int k;
+  int use_cond;
+  int l2keep;   // keep C / Chat resident in L2 (evict_last loads)
+  cudaGraphConditionalHandle cond;
+  const double *C, *Chat, *U;
+  double *x, *r, *p, *q, *s, *t, *rt0, *b;
+  double *p2, *q2;        // second p / q buffers (fused persistent kernel)
+  double *zeta, *gamma, *xc;
+  double *part, *part2;   // part2: second partial buffer (persistent kernel)
+  uint64_t *prof;         // optional per-phase %globaltimer stamps (16/iter)
+  int64_t prof_cap;
+  unsigned int *counters;
+  SolveScalars *S;
+  double *hist_r;
+  int64_t *hist_m;
+  uint64_t *hist_t;
+};
+
+struct GridSync {
+  unsigned int count;
+  unsigned int gen;
+};
+
+// S: the scalar block to update (global, or a CTA's shared copy in the
+// persistent kernel); only the writer CTA stores the history entries.
+__device__ __forceinline__ void record(const IterArgs &a, SolveScalars *S,
+                                       double rn, bool writer) {
+  int64_t h = S->hist_len;
+  if (writer) {
+    a.hist_r[h] = rn;
+    a.hist_m[h] = S->matvecs;
+    a.hist_t[h] = globaltimer();
+  }
+  S->hist_len = h + 1;
+}
+
+__host__ __device__ constexpr int ndots_of(int PH) {
+  return PH == PH_PROJ_Q ? 2 : PH == PH_SUPD ? 1 : PH == PH_PROJ_T ? 2
+       : PH == PH_XR ? 2 : PH == PH_BNORM ? 1 : PH == PH_INIT ? 3
+       : PH == PH_TRUE ? 2 : 0;
+}
+
+// Scalar logic of each phase, executed by thread 0 of the finishing CTA once
+// the dot products d[] are final.  Mirrors solvers.py:288-356 line by line.
+template <int PH>
+__device__ __noinline__ void finalize(const IterArgs &a, SolveScalars *S, const double *d,
+                                     bool writer = true) {
+  if (PH == PH_BNORM) {
+    S->bnorm = __dsqrt_rn(d[0]);
+    S->tol_abs = __dmul_rn(S->tol_abs, S->bnorm);  // tol_abs held tol
+  } else if (PH == PH_INIT) {
+    double rn = __dsqrt_rn(d[0]);
+    record(a, S, rn, writer);
+    S->rnorm = rn;
+    S->rho = d[1];
+    S->nrt0 = __dsqrt_rn(d[2]);
+    S->beta = 0.0;
+    S->omega = 0.0;
+    if (rn <= S->tol_abs)
+      S->status = KRB_CONVERGED;
+    else if (S->max_itn <= 0)
+      S->status = KRB_MAX_ITN;
+  } else if (PH == PH_PROJ_Q) {
+    S->matvecs += 1;
+    double den = d[0];
+    double nq = __dsqrt_rn(d[1]);
+    S->den = den;
+    S->qnorm = nq;
+    if (fabs(den) <= __dmul_rn(__dmul_rn(S->breakdown_tol, S->nrt0), nq))
+      S->status = KRB_BREAKDOWN_SERIOUS;
+    else
+      S->alpha = __ddiv_rn(S->rho, den);
+  } else if (PH == PH_SUPD) {
+    double sn = __dsqrt_rn(d[0]);
+    S->snorm = sn;
+    if (sn <= S->tol_abs) {
+      record(a, S, sn, writer);
+      S->early = 1;
+      S->status = KRB_CONVERGED;
+    }
+  } else if (PH == PH_PROJ_T) {
+    S->matvecs += 1;
+    double tt = d[0];
+    S->tt = tt;
+    S->ts = d[1];
+    if (tt == 0.0) {
+      S->status = KRB_BREAKDOWN_OMEGA;
+    } else {
+      double om = __ddiv_rn(d[1], tt);
+      if (om == 0.0)
+        S->status = KRB_BREAKDOWN_OMEGA;
+      else
+        S->omega = om;
+    }
+  } else if (PH == PH_XR) {
+    double rn = __dsqrt_rn(d[0]);
+    S->rnorm = rn;
+    record(a, S, rn, writer);
+    S->itn += 1;
+    if (rn <= S->tol_abs) {
+      S->status = KRB_CONVERGED;
+    } else {
+      double rho_new = d[1];
+      if (fabs(rho_new) <= __dmul_rn(__dmul_rn(S->breakdown_tol, S->nrt0), rn)) {
+        S->status = KRB_BREAKDOWN_SERIOUS;
+      } else {
+        S->beta = __dmul_rn(__ddiv_rn(rho_new, S->rho), __ddiv_rn(S->alpha, S->omega));
+        S->rho = rho_new;
+      }
+    }
+    if (S->status == KRB_RUNNING && S->itn >= S->max_itn) S->status = KRB_MAX_ITN;
+  } else if (PH == PH_TRUE) {
+    double bn = __dsqrt_rn(d[1]);
+    S->final_true_resid = __ddiv_rn(__dsqrt_rn(d[0]), bn > 0.0 ? bn : 1.0);
+  }
+}
+
+struct PhaseScal {
+  double alpha, omega, beta;
+};
+
+__device__ __forceinline__ PhaseScal load_scal(const SolveScalars *S) {
+  return PhaseScal{S->alpha, S->omega, S->beta};
+}
+
+// Elementwise work + canonical block partials of one phase for canonical
+// blocks blk = first, first + step, ...   `coef` (k values of zeta / gamma)
+// must already be in shared memory for the projection phases.
+template <int kE, int PH>
+__device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal sc,
+                                             double (*red)[32],
+                                             const double *coef, int64_t first,
+                                             int64_t step, double *part_buf) {
+  constexpr int ND = ndots_of(PH);
+  const double alpha = sc.alpha, omega = sc.omega, beta = sc.beta;
+  const int k = a.k;
+  const int64_t n = a.n, nb = a.nb, ld = a.ld;
+  double *__restrict__ x = a.x;
+  double *__restrict__ r = a.r;
+  double *__restrict__ p = a.p;
+  double *__restrict__ q = a.q;
+  double *__restrict__ s = a.s;
+  double *__restrict__ t = a.t;
+  const double *__restrict__ rt0 = a.rt0;
+  const double *__restrict__ bvec = a.b;
+  const double *__restrict__ Cm = a.C;
+  double *__restrict__ part = part_buf;
+  const uint64_t pol = l2_policy(a.l2keep);
+  for (int64_t blk = first; blk < nb; blk += step) {
+    const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll(kE < 4 ? kE : 4)
+    for (int e = 0; e < kE; ++e) {
+      const int64_t i = base + (int64_t)kLanes * e;
+      if (i >= n) continue;
+      if (PH == PH_PUPDATE) {
+        // p = r + beta * (p - omega * q)          (solvers.py:303)
+        double pv = __dsub_rn(p[i], __dmul_rn(omega, q[i]));
+        p[i] = __dadd_rn(r[i], __dmul_rn(beta, pv));
+      } else if (PH == PH_PROJ_Q || PH == PH_PROJ_T) {
+        double *v = PH == PH_PROJ_Q ? q : t;
+        double vi = v[i];
+        if (k > 0) {
+          // C @ zeta for this element: sequential fma over the columns, four
+          // independent column loads in flight per step
+          double cz = 0.0;
+          int j = 0;
+          for (; j + 4 <= k; j += 4) {
+            double c0 = ldg_pol(Cm + (int64_t)j * ld + i, pol);
+            double c1 = ldg_pol(Cm + (int64_t)(j + 1) * ld + i, pol);
+            double c2 = ldg_pol(Cm + (int64_t)(j + 2) * ld + i, pol);
+            double c3 = ldg_pol(Cm + (int64_t)(j + 3) * ld + i, pol);
+            cz = __fma_rn(c0, coef[j], cz);
+            cz = __fma_rn(c1, coef[j + 1], cz);
+            cz = __fma_rn(c2, coef[j + 2], cz);
+            cz = __fma_rn(c3, coef[j + 3], cz);
+          }
+          for (; j < k; ++j) cz = __fma_rn(ldg_pol(Cm + (int64_t)j * ld + i, pol), coef[j], cz);
+          vi = __dsub_rn(vi, cz);   // q - C @ zeta   (solvers.py:307,329)
+          v[i] = vi;
+        }
+        if (PH == PH_PROJ_Q) {
+          acc[0] = __fma_rn(rt0[i], vi, acc[0]);   // (rt0, q)
+          acc[1] = __fma_rn(vi, vi, acc[1]);       // (q, q)
+        } else {
+          acc[0] = __fma_rn(vi, vi, acc[0]);       // (t, t)
+          acc[1] = __fma_rn(vi, s[i], acc[1]);     // (t, s)
+        }
+      } else if (PH == PH_SUPD) {
+        // s = r - alpha * q                       (solvers.py:313)
+        double sv = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+        s[i] = sv;
+        acc[0] = __fma_rn(sv, sv, acc[0]);
+      } else if (PH == PH_XR) {
+        // x = x + alpha*p + omega*s ; r = s - omega*t   (solvers.py:338,341)
+        double sv = s[i];
+        x[i] = __dadd_rn(__dadd_rn(x[i], __dmul_rn(alpha, p[i])),
+                         __dmul_rn(omega, sv));
+        double rv = __dsub_rn(sv, __dmul_rn(omega, t[i]));
+        r[i] = rv;
+        acc[0] = __fma_rn(rv, rv, acc[0]);
+        acc[1] = __fma_rn(rt0[i], rv, acc[1]);
+      } else if (PH == PH_BNORM) {
+        double bv = bvec[i];
+        acc[0] = __fma_rn(bv, bv, acc[0]);
+      } else if (PH == PH_INIT) {
+        double rv = r[i], tv = rt0[i];
+        acc[0] = __fma_rn(rv, rv, acc[0]);
+        acc[1] = __fma_rn(tv, rv, acc[1]);
+        acc[2] = __fma_rn(tv, tv, acc[2]);
+      } else if (PH == PH_TRUE) {
+        // true residual b - A x_out   (solvers.py:147-153); A x_out in t
+        double bv = bvec[i];
+        double res = __dsub_rn(bv, t[i]);
+        acc[0] = __fma_rn(res, res, acc[0]);
+        acc[1] = __fma_rn(bv, bv, acc[1]);
+      } else if (PH == PH_RINIT) {
+        // r = b - A x_init            (recycling.py:200); A x_init in t
+        r[i] = __dsub_rn(bvec[i], t[i]);
+      }
+    }
+    if (ND > 0) {
+      double bp = block_tree_multi<ND == 0 ? 1 : ND>(acc, red);
+      const int warp = threadIdx.x >> 5;
+      if (warp < ND && (threadIdx.x & 31) == 0) part[warp * nb + blk] = bp;
+    }
+  }
+}
+
+// Final stage + scalar logic of a phase, run by every thread of the one CTA
+// that finished the phase last (all partials visible).
+template <int PH>
+__device__ __forceinline__ void phase_leader(const IterArgs &a, const PhaseScal sc) {
+  constexpr int ND = ndots_of(PH);
+  __shared__ double dfin[3];
+  const int warp = threadIdx.x >> 5;
+  if (warp < ND) {
+    double v = warp_final_volatile(a.part + warp * a.nb, a.nb);
+    if ((threadIdx.x & 31) == 0) dfin[warp] = v;
+  }
+  if (PH == PH_XR) {
+    // xc = xc + alpha*zeta + omega*gamma     (solvers.py:340)
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x)
+      a.xc[j] = __dadd_rn(__dadd_rn(a.xc[j], __dmul_rn(sc.alpha, a.zeta[j])),
+                          __dmul_rn(sc.omega, a.gamma[j]));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) finalize<PH>(a, a.S, dfin);
+  __syncthreads();
+}
+
+// half-step exit (solvers.py:315-325): x += alpha p, xc += alpha zeta
+__device__ __forceinline__ void half_exit_update(const IterArgs &a, double alpha,
+                                                 int64_t first, int64_t step) {
+  for (int64_t i = first * blockDim.x + threadIdx.x; i < a.n; i += step * blockDim.x)
+    a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));   // solvers.py:316
+  if (first == 0)
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x)     // solvers.py:318
+      a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
+}
+
+}  // namespace krb

@@ -215,6 +215,49 @@ __device__ __forceinline__ bool elect_last_cta(unsigned int *counter,
   return last;
 }
 
+// L2 eviction-priority policy (createpolicy) for loads of blocks that should
+// stay resident across iterations (the recycle blocks of small systems).
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// read-only global load carrying an L2 cache policy
+__device__ __forceinline__ double ldg_pol(const double *ptr, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+
+// Ampere-style per-thread async copies (LDGSTS): each thread stages the
+// elements it will consume itself, so no CTA barrier is needed between the
+// copy and its use -- the copies just add memory-level parallelism without
+// registers.  valid == false zero-fills (src-size 0).
+// pol == 0: no per-instruction L2 policy (an access-policy window applies)
+__device__ __forceinline__ void cp_async8(double *smem, const double *g, bool valid,
+                                          uint64_t pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (pol == 0)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(s),
+                 "l"(g), "r"(valid ? 8 : 0), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

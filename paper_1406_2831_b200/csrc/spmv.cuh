@@ -15,50 +15,55 @@ __device__ __forceinline__ double ldx(const double *p) {
 // ---- SpMV kernels: one thread per row, CSR order, mul then add ----------
 // kXro: x is read-only for the whole kernel (ld.global.nc); false inside the
 // persistent solver, where x was written by other CTAs earlier in the kernel.
-template <bool kSell, bool kXro = true>
-__device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
-                                          const double *__restrict__ x) {
+// xf(c) supplies x[c] (a plain load, or a value recomputed on the fly from
+// other vectors by the fused persistent phases).  Entries go in batches of
+// kB with predicated tails, so a row of up to kB entries costs two dependent
+// memory round trips (indices, then gathers); the sum stays sequential in
+// CSR order.
+template <bool kSell, int kB = 4, class XF>
+__device__ __forceinline__ double spmv_row_f(int64_t i, const krb_matrix &A, XF xf) {
   double sum = 0.0;
+  const int32_t *__restrict__ cp;
+  const double *__restrict__ vp;
+  int len, stride;
   if (kSell) {
-    const int len = __ldg(A.rlen + i);
+    len = __ldg(A.rlen + i);
     const int64_t base = __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
-    const int32_t *__restrict__ cp = A.s_col + base;
-    const double *__restrict__ vp = A.s_val + base;
-    int j = 0;
-    for (; j + 4 <= len; j += 4) {
-      int c0 = __ldg(cp + 32 * j), c1 = __ldg(cp + 32 * (j + 1));
-      int c2 = __ldg(cp + 32 * (j + 2)), c3 = __ldg(cp + 32 * (j + 3));
-      double v0 = __ldg(vp + 32 * j), v1 = __ldg(vp + 32 * (j + 1));
-      double v2 = __ldg(vp + 32 * (j + 2)), v3 = __ldg(vp + 32 * (j + 3));
-      double x0 = ldx<kXro>(x + c0), x1 = ldx<kXro>(x + c1), x2 = ldx<kXro>(x + c2),
-             x3 = ldx<kXro>(x + c3);
-      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
-      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
-      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
-      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
-    }
-    for (; j < len; ++j)
-      sum = __dadd_rn(sum, __dmul_rn(__ldg(vp + 32 * j), ldx<kXro>(x + __ldg(cp + 32 * j))));
+    cp = A.s_col + base;
+    vp = A.s_val + base;
+    stride = 32;
   } else {
-    int64_t b = __ldg(A.rp + i), e = __ldg(A.rp + i + 1);
-    int64_t jj = b;
-    for (; jj + 4 <= e; jj += 4) {
-      int c0 = __ldg(A.ci + jj), c1 = __ldg(A.ci + jj + 1);
-      int c2 = __ldg(A.ci + jj + 2), c3 = __ldg(A.ci + jj + 3);
-      double v0 = __ldg(A.val + jj), v1 = __ldg(A.val + jj + 1);
-      double v2 = __ldg(A.val + jj + 2), v3 = __ldg(A.val + jj + 3);
-      double x0 = ldx<kXro>(x + c0), x1 = ldx<kXro>(x + c1), x2 = ldx<kXro>(x + c2),
-             x3 = ldx<kXro>(x + c3);
-      sum = __dadd_rn(sum, __dmul_rn(v0, x0));
-      sum = __dadd_rn(sum, __dmul_rn(v1, x1));
-      sum = __dadd_rn(sum, __dmul_rn(v2, x2));
-      sum = __dadd_rn(sum, __dmul_rn(v3, x3));
+    const int64_t b = __ldg(A.rp + i);
+    len = (int)(__ldg(A.rp + i + 1) - b);
+    cp = A.ci + b;
+    vp = A.val + b;
+    stride = 1;
+  }
+  for (int j = 0; j < len; j += kB) {
+    int c[kB];
+    double v[kB], xv[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const bool ok = j + u < len;
+      c[u] = ok ? __ldg(cp + (int64_t)stride * (j + u)) : 0;
+      v[u] = ok ? __ldg(vp + (int64_t)stride * (j + u)) : 0.0;
     }
-    for (; jj < e; ++jj)
-      sum = __dadd_rn(sum, __dmul_rn(__ldg(A.val + jj), ldx<kXro>(x + __ldg(A.ci + jj))));
+#pragma unroll
+    for (int u = 0; u < kB; ++u) xv[u] = j + u < len ? xf(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (j + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
   }
   return sum;
 }
 
+// ---- SpMV row: one thread per row, CSR order, mul then add --------------
+// kXro: x is read-only for the whole kernel (ld.global.nc); false inside the
+// persistent solver, where x was written by other CTAs earlier in the kernel.
+template <bool kSell, bool kXro = true>
+__device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
+                                          const double *__restrict__ x) {
+  return spmv_row_f<kSell>(i, A, [x](int c) { return ldx<kXro>(x + c); });
+}
 
 }  // namespace krb

@@ -20,7 +20,9 @@ __device__ __forceinline__ void tdot_unit(int64_t n, int64_t nb, int k,
                                           int64_t ldm,
                                           const double *__restrict__ v,
                                           double *__restrict__ part, int64_t b,
-                                          int j0, double (*red)[32]) {
+                                          int j0, double (*red)[32],
+                                          bool keep = false) {
+  const uint64_t pol = l2_policy(keep);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nj = min(kTdotCG, k - j0);
   const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
@@ -35,7 +37,7 @@ __device__ __forceinline__ void tdot_unit(int64_t n, int64_t nb, int k,
       double m[kTdotCG];
 #pragma unroll
       for (int c = 0; c < kTdotCG; ++c)
-        m[c] = c < nj ? __ldg(M + (int64_t)(j0 + c) * ldm + i) : 0.0;
+        m[c] = c < nj ? ldg_pol(M + (int64_t)(j0 + c) * ldm + i, pol) : 0.0;
 #pragma unroll
       for (int c = 0; c < kTdotCG; ++c)
         acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
@@ -72,12 +74,13 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           const double *__restrict__ v,
                                           double *__restrict__ part,
                                           double *__restrict__ out,
-                                          unsigned int *counter) {
+                                          unsigned int *counter,
+                                          bool keep = false) {
   __shared__ double red[kTdotCG][32];
   __shared__ int last_flag;
   const int j0 = blockIdx.y * kTdotCG;
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
-    tdot_unit<kE, kSelf>(n, nb, k, M, ldm, v, part, b, j0, red);
+    tdot_unit<kE, kSelf>(n, nb, k, M, ldm, v, part, b, j0, red, keep);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

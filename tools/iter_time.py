@@ -60,11 +60,20 @@ def phase_breakdown(name, k=None):
     b = D.to_device(seq.rhs(0, 0))
     S.solve_device(M, b, None, space, P.SolverConfig(tol=seq.tol, seed=0), use_graph=2)
     st = S.LAST_SOLVE["phase_stamps"].astype(np.int64)
-    names = ["P", "M1", "Z1", "Q", "S", "M2", "Z2", "T", "X"]
-    d = np.diff(st[:-1, :10], axis=1) / 1e3
+    used = 6 if st[0, 12] != 0 else 10   # fused v2 stamps slots 12, 13
+    names = (["P", "M1", "Z1", "Q", "S", "M2", "Z2", "T", "X"] if used >= 10 else
+             ["A:P+MZ1", "B:Q", "C:S+MZ2", "D:T", "E:X"])   # v1 / fused v2
+    d = np.diff(st[:-1, :len(names) + 1], axis=1) / 1e3
     full = (st[1:, 0] - st[:-1, 0]) / 1e3
-    return {"config": name, "k": k, "us_per_iteration": float(np.median(full)),
-            **{nm: round(float(np.median(d[:, i])), 2) for i, nm in enumerate(names)}}
+    out = {"config": name, "k": k, "us_per_iteration": float(np.median(full)),
+           **{nm: round(float(np.median(d[:, i])), 2) for i, nm in enumerate(names)}}
+    if used < 10:   # fused v2 sub-stamps (slots 6..13, see persist.cu)
+        rel = lambda j, i: round(float(np.median((st[:-1, j] - st[:-1, i]) / 1e3)), 2)
+        out.update({"A.spmv": rel(6, 0), "A.proj": rel(7, 6), "A.sync": rel(8, 7),
+                    "A.finals": rel(1, 8), "B.work": rel(12, 1), "B.sync": rel(13, 12),
+                    "B.finals": rel(2, 13), "C.spmv": rel(9, 2), "C.proj": rel(10, 9),
+                    "C.sync": rel(11, 10), "C.finals": rel(3, 11)})
+    return out
 
 
 if __name__ == "__main__":

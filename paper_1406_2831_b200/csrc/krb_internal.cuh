@@ -237,18 +237,12 @@ __device__ __forceinline__ double ldg_pol(const double *ptr, uint64_t pol) {
 // elements it will consume itself, so no CTA barrier is needed between the
 // copy and its use -- the copies just add memory-level parallelism without
 // registers.  valid == false zero-fills (src-size 0).
-// pol == 0: no per-instruction L2 policy (an access-policy window applies)
 __device__ __forceinline__ void cp_async8(double *smem, const double *g, bool valid,
                                           uint64_t pol) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  if (pol == 0)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g),
-                 "r"(valid ? 8 : 0)
-                 : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(s),
-                 "l"(g), "r"(valid ? 8 : 0), "l"(pol)
-                 : "memory");
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(s),
+               "l"(g), "r"(valid ? 8 : 0), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");

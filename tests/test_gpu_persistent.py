@@ -1,0 +1,106 @@
+"""The persistent drivers (persist.cu) over the shapes that change their work
+split, bit-identical to the canonical oracle (oracle/krylov.py + CanonOps):
+
+* fused v2 (k <= 32, unpermuted rows): one CTA per SM owning canonical blocks
+  me and me + G -- a single partial block (n < 1024), ragged last blocks,
+  CTAs owning one and two blocks, E = 2 (n > 303104) up to the largest
+  persistent size (606208), k = 0, k in the last column group, k = 32;
+* v1 (k = 33 and sigma-permuted rows) on the same matrices;
+* SELL-32 and CSR storage.
+Matrices are random non-symmetric, diagonally dominant, with ragged rows
+(1..9 entries) so the SpMV's predicated batches see every tail length.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import gpu, random_space_arrays
+
+pytestmark = gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_1406_2831_b200 as P
+    return P
+
+
+def ragged_matrix(n, seed):
+    """Random sparse A = D + N: rows with 0..8 off-diagonals at random
+    columns, |D| ~ 3, sorted columns (canonical CSR)."""
+    from paper_1406_2831_b200.workloads import CSR
+    r = np.random.default_rng(seed)
+    cnt = r.integers(0, 9, size=n)
+    rows = np.repeat(np.arange(n), cnt)
+    cols = r.integers(0, n, size=rows.size)
+    vals = r.uniform(-1.0, 1.0, size=rows.size)
+    rows = np.concatenate([rows, np.arange(n)])
+    cols = np.concatenate([cols, np.arange(n)])
+    vals = np.concatenate([vals, 2.5 + r.uniform(0.0, 1.0, size=n)])
+    import scipy.sparse as sp
+    S = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    S.sum_duplicates()
+    S.sort_indices()
+    return CSR(n, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data.copy())
+
+
+def _space(P, S):
+    return P.RecycleSpace(U=S.U, Ut=S.Ut, C=S.C, Ct=S.Ct, Dc=S.Dc, Chat=S.Chat,
+                          Ccheck=S.Ccheck)
+
+
+CASES = [
+    # n, k, fmt (2 = SELL-32, 1 = CSR)
+    (1000, 0, 2),
+    (1000, 5, 2),
+    (16389, 10, 2),
+    (16389, 10, 1),
+    (200_000, 20, 2),
+    (200_000, 32, 2),
+    (200_000, 33, 2),      # k > 32: v1 kernel
+    (400_000, 8, 2),       # E = 2
+    (606_208, 3, 1),       # largest persistent size, CSR
+]
+
+
+@pytest.mark.parametrize("n,k,fmt", CASES)
+def test_persistent_bitwise_vs_oracle(pkg, canon, n, k, fmt):
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import solvers as S
+    from paper_1406_2831_b200.device import DeviceMatrix, to_device
+    A = ragged_matrix(n, seed=n + k)
+    b = np.random.default_rng(n).standard_normal(n)
+    Sp = random_space_arrays(A, k, seed=11, ops=canon) if k else None
+    M = DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=fmt)
+    assert M.format == {1: "csr", 2: "sell32"}[fmt]
+    for tol, max_itn in ((1e-14, 7), (1e-9, 400)):
+        cfg = pkg.SolverConfig(tol=tol, max_itn=max_itn, seed=5)
+        xo, ho = O.rbicgstab(A, b, recycle=Sp, config=O.Config(tol=tol, max_itn=max_itn, seed=5),
+                             ops=canon)
+        xg, hg = S.solve_device(M, to_device(b), None, _space(pkg, Sp) if k else None, cfg,
+                                use_graph=2)
+        assert hg.status == ho.status
+        assert hg.resid == ho.resid
+        assert hg.matvecs == ho.matvecs
+        assert np.array_equal(xg.cpu().numpy(), xo)
+
+
+def test_persistent_sigma_rows_use_v1(pkg, canon):
+    """sigma-permuted SELL rows run the v1 persistent kernel: still bitwise."""
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import solvers as S
+    from paper_1406_2831_b200.device import DeviceMatrix, to_device
+    A = ragged_matrix(70_000, seed=3)
+    b = np.random.default_rng(1).standard_normal(A.n)
+    Sp = random_space_arrays(A, 6, seed=2, ops=canon)
+    M = DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=3)
+    assert M.format == "sell32-sigma"
+    cfg = pkg.SolverConfig(tol=1e-9, max_itn=60, seed=2)
+    xo, ho = O.rbicgstab(A, b, recycle=Sp, config=O.Config(tol=1e-9, max_itn=60, seed=2),
+                         ops=canon)
+    xg, hg = S.solve_device(M, to_device(b), None, _space(pkg, Sp), cfg, use_graph=2)
+    assert (hg.status, hg.resid, hg.matvecs) == (ho.status, ho.resid, ho.matvecs)
+    assert np.array_equal(xg.cpu().numpy(), xo)

@@ -126,6 +126,11 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first_sample(self, timeout=10.0):
+        t0 = time.time()
+        while self.proc is not None and len(self.lines) < 2 and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
@@ -211,6 +216,9 @@ def gpu_arm(args, wl, rank, world):
 
     clocks = Clocks(torch.cuda.current_device())
     clocks.start()
+    # let nvidia-smi finish initialising (its start-up RM calls stall CUDA API
+    # calls of this host-synchronising workload); it keeps sampling throughout
+    clocks.wait_first_sample()
     times, its, last = [], 0, None
     l0 = _lib.launch_count()
     for _ in range(args.steps):
@@ -238,6 +246,7 @@ def gpu_arm(args, wl, rank, world):
         t_total, its_all = float(mx[0]), float(tt[1])
 
     out = {"t_total": t_total, "iters": its, "iters_all": its_all,
+           "step_ms": [round(1e3 * t, 3) for t in times],
            "launches": launches, "clocks": clk,
            "space_dims": last.space_dims,
            "rec_matvecs": last.recycling.total_matvecs,
@@ -367,9 +376,10 @@ def synthetic_pass(wl, dmats, drhs):
     b, t = kern[dom]
     from paper_1406_2831_b200.solvers import _auto_mode
     if _auto_mode(wl.n) == 2:
-        # the persistent driver runs each whole solve as ONE kernel (k_persist):
-        # it is the dominant (only) kernel of the step; per launch = one solve
-        dom = "k_persist (one RBiCGSTAB solve per launch)"
+        # the persistent driver runs each whole solve as ONE kernel (fused
+        # k_persist2, persist.cu): the dominant kernel of the step; per
+        # launch = one solve
+        dom = "k_persist2 (fused persistent RBiCGSTAB, one solve per launch)"
         b = B_it * its / max(len(ks), 1)
         t = t_solve / max(len(ks), 1)
     ach = b / t / 1e9
@@ -496,6 +506,7 @@ def main():
                 "recycling_matvecs": res["rec_matvecs"],
                 "recycling_aux_matvecs": res["rec_aux_matvecs"],
                 "baseline": res["baseline"],
+                "step_ms": res["step_ms"],
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "e2e": res["e2e"]}
         for key in ("roofline", "iteration_roofline", "kernels", "synthetic"):

@@ -73,6 +73,10 @@ int krb_matrix_create_i64(krb_matrix **out, int64_t n, int64_t nnz,
                           const int64_t *d_row_ptr, const int64_t *d_col_idx,
                           const double *d_values, int format, void *stream);
 int krb_matrix_destroy(krb_matrix *A);
+/* Stream-ordered destroy: storage returns to the device memory pool after
+ * the work already queued on `stream`; no device-wide synchronisation.  No
+ * other stream may still use the matrix. */
+int krb_matrix_destroy_async(krb_matrix *A, void *stream);
 /* n, nnz, chosen format, device bytes held (incl. transpose when built) */
 int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz,
                     int *format, int64_t *bytes);

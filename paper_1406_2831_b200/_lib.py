@@ -69,6 +69,7 @@ SIGNATURES = {
     "krb_matrix_create_i64": (c_int, [ctypes.POINTER(c_vp), c_i64, c_i64,
                                       c_vp, c_vp, c_vp, c_int, c_vp]),
     "krb_matrix_destroy": (c_int, [c_vp]),
+    "krb_matrix_destroy_async": (c_int, [c_vp, c_vp]),
     "krb_matrix_info": (c_int, [c_vp, ctypes.POINTER(c_i64),
                                 ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
                                 ctypes.POINTER(c_i64)]),

@@ -191,7 +191,7 @@ static int sell_layout(krb_matrix *A, const int32_t *rlen_pos, int64_t *total,
                        cudaStream_t st) {
   const int64_t n = A->n;
   int64_t *width = nullptr;
-  KRB_CHECK_CUDA(cudaMalloc(&width, sizeof(int64_t) * (A->nslices + 1)));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&width, sizeof(int64_t) * (A->nslices + 1), st));
   if (n > 0) {
     unsigned wblocks = (unsigned)((A->nslices * 32 + 255) / 256);
     k_slice_width<<<wblocks, 256, 0, st>>>(n, rlen_pos, width);
@@ -201,14 +201,14 @@ static int sell_layout(krb_matrix *A, const int32_t *rlen_pos, int64_t *total,
   void *tmp = nullptr;
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr, A->nslices + 1, st);
-  KRB_CHECK_CUDA(cudaMalloc(&tmp, tmp_bytes));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tmp, tmp_bytes, st));
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr, A->nslices + 1, st);
   KRB_CHECK_CUDA(cudaGetLastError());
   KRB_CHECK_CUDA(cudaMemcpyAsync(total, A->sl_ptr + A->nslices, sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(tmp);
-  cudaFree(width);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(width, st);
   return KRB_OK;
 }
 
@@ -222,10 +222,10 @@ static int sigma_sort(krb_matrix *A, cudaStream_t st) {
   const int64_t nseg = (n + kSigma - 1) / kSigma;
   int32_t *keys_out = nullptr, *iota = nullptr;
   int *off = nullptr;
-  KRB_CHECK_CUDA(cudaMalloc(&keys_out, sizeof(int32_t) * n));
-  KRB_CHECK_CUDA(cudaMalloc(&iota, sizeof(int32_t) * n));
-  KRB_CHECK_CUDA(cudaMalloc(&A->perm, sizeof(int32_t) * n));
-  KRB_CHECK_CUDA(cudaMalloc(&off, sizeof(int) * (nseg + 1)));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&keys_out, sizeof(int32_t) * n, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&iota, sizeof(int32_t) * n, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->perm, sizeof(int32_t) * n, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&off, sizeof(int) * (nseg + 1), st));
   k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, iota);
   KRB_CHECK_LAUNCH();
   k_window_offsets<<<(unsigned)((nseg + 256) / 256), 256, 0, st>>>(nseg, n, kSigma, off);
@@ -235,16 +235,15 @@ static int sigma_sort(krb_matrix *A, cudaStream_t st) {
   cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, A->rlen, keys_out, iota,
                                                      A->perm, (int)n, (int)nseg, off, off + 1,
                                                      0, 32, st);
-  KRB_CHECK_CUDA(cudaMalloc(&tmp, tb));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tmp, tb, st));
   cub::DeviceSegmentedRadixSort::SortPairsDescending(tmp, tb, A->rlen, keys_out, iota,
                                                      A->perm, (int)n, (int)nseg, off, off + 1,
                                                      0, 32, st);
   KRB_CHECK_CUDA(cudaGetLastError());
-  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(tmp);
-  cudaFree(off);
-  cudaFree(iota);
-  cudaFree(A->rlen);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(off, st);
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(A->rlen, st);
   A->rlen = keys_out;   // lengths now indexed by slice position
   return KRB_OK;
 }
@@ -252,8 +251,8 @@ static int sigma_sort(krb_matrix *A, cudaStream_t st) {
 static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
   const int64_t n = A->n;
   A->nslices = (n + 31) / 32;
-  KRB_CHECK_CUDA(cudaMalloc(&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1)));
-  KRB_CHECK_CUDA(cudaMalloc(&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1)));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1), st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1), st));
   unsigned blocks = (unsigned)((n + 255) / 256);
   if (n > 0) {
     k_row_len<<<blocks, 256, 0, st>>>(n, A->rp, A->rlen);
@@ -271,21 +270,21 @@ static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
     if (rc) return rc;
     use_sell = format == 3 || total <= budget;
     if (!use_sell) {
-      cudaFree(A->perm);
+      cudaFreeAsync(A->perm, st);
       A->perm = nullptr;
     }
   }
   A->sell_elems = total;
   if (!use_sell) {
-    cudaFree(A->sl_ptr);
+    cudaFreeAsync(A->sl_ptr, st);
     A->sl_ptr = nullptr;
-    cudaFree(A->rlen);
+    cudaFreeAsync(A->rlen, st);
     A->rlen = nullptr;
     A->format = 1;
     return KRB_OK;
   }
-  KRB_CHECK_CUDA(cudaMalloc(&A->s_col, sizeof(int32_t) * (total > 0 ? total : 1)));
-  KRB_CHECK_CUDA(cudaMalloc(&A->s_val, sizeof(double) * (total > 0 ? total : 1)));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->s_col, sizeof(int32_t) * (total > 0 ? total : 1), st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->s_val, sizeof(double) * (total > 0 ? total : 1), st));
   if (total > A->nnz) {
     k_pad_fill<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(total, A->s_col, A->s_val);
     KRB_CHECK_LAUNCH();
@@ -312,15 +311,28 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   KRB_REQUIRE(n >= 0 && nnz >= 0, "krb_matrix_create: negative size");
   KRB_REQUIRE(nnz < ((int64_t)1 << 31), "krb_matrix_create: nnz >= 2^31");
   KRB_REQUIRE(n < ((int64_t)1 << 31), "krb_matrix_create: n >= 2^31");
+  static bool pool_ready = false;
+  if (!pool_ready) {
+    // keep freed blocks in the default pool: re-creating a sequence's
+    // matrices every step must not pay cudaMalloc / implicit syncs again
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_ready = true;
+  }
   krb_matrix *A = new krb_matrix();
   A->n = n;
   A->nnz = nnz;
-  cudaError_t e = cudaMalloc(&A->rp, sizeof(int64_t) * (n + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&A->ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
-  if (e == cudaSuccess) e = cudaMalloc(&A->val, sizeof(double) * (nnz > 0 ? nnz : 1));
+  cudaError_t e = cudaMallocAsync((void **)&A->rp, sizeof(int64_t) * (n + 1), st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&A->ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&A->val, sizeof(double) * (nnz > 0 ? nnz : 1), st);
   if (e != cudaSuccess) {
     set_error("krb_matrix_create: %s", cudaGetErrorString(e));
-    cudaFree(A->rp); cudaFree(A->ci); cudaFree(A->val);
+    cudaFreeAsync(A->rp, st); cudaFreeAsync(A->ci, st); cudaFreeAsync(A->val, st);
     delete A;
     return KRB_ENOMEM;
   }
@@ -380,12 +392,12 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   int64_t *cnt = nullptr, *trp = nullptr;
   double *tval = nullptr;
   size_t m = nnz > 0 ? nnz : 1;
-  KRB_CHECK_CUDA(cudaMalloc(&rows, sizeof(int32_t) * m));
-  KRB_CHECK_CUDA(cudaMalloc(&keys_out, sizeof(int32_t) * m));
-  KRB_CHECK_CUDA(cudaMalloc(&perm_in, sizeof(int32_t) * m));
-  KRB_CHECK_CUDA(cudaMalloc(&perm_out, sizeof(int32_t) * m));
-  KRB_CHECK_CUDA(cudaMalloc(&cnt, sizeof(int64_t) * (n + 1)));
-  KRB_CHECK_CUDA(cudaMalloc(&trp, sizeof(int64_t) * (n + 1)));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&rows, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&keys_out, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&perm_in, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&perm_out, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&cnt, sizeof(int64_t) * (n + 1), st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&trp, sizeof(int64_t) * (n + 1), st));
   KRB_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n + 1), st));
   unsigned nb = (unsigned)((nnz + 255) / 256), rb = (unsigned)((n + 255) / 256);
   if (n > 0) {
@@ -405,47 +417,49 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   cub::DeviceRadixSort::SortPairs(nullptr, tb1, A->ci, keys_out, perm_in,
                                   perm_out, (int)nnz, 0, end_bit, st);
   cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, trp, n + 1, st);
-  KRB_CHECK_CUDA(cudaMalloc(&tmp, tb1 > tb2 ? tb1 : tb2));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tmp, tb1 > tb2 ? tb1 : tb2, st));
   if (nnz > 0)
     cub::DeviceRadixSort::SortPairs(tmp, tb1, A->ci, keys_out, perm_in,
                                     perm_out, (int)nnz, 0, end_bit, st);
   cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, trp, n + 1, st);
   KRB_CHECK_CUDA(cudaGetLastError());
-  KRB_CHECK_CUDA(cudaMalloc(&tci, sizeof(int32_t) * m));
-  KRB_CHECK_CUDA(cudaMalloc(&tval, sizeof(double) * m));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tci, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tval, sizeof(double) * m, st));
   if (nnz > 0) {
     k_gather_t<<<nb, 256, 0, st>>>(nnz, perm_out, rows, A->val, tci, tval);
     KRB_CHECK_LAUNCH();
   }
-  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(tmp);
-  cudaFree(rows);
-  cudaFree(keys_out);
-  cudaFree(perm_in);
-  cudaFree(perm_out);
-  cudaFree(cnt);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(rows, st);
+  cudaFreeAsync(keys_out, st);
+  cudaFreeAsync(perm_in, st);
+  cudaFreeAsync(perm_out, st);
+  cudaFreeAsync(cnt, st);
   krb_matrix *T = nullptr;
   int rc = matrix_create(&T, n, nnz, trp, tci, nullptr, tval, 0, st);
-  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(trp);
-  cudaFree(tci);
-  cudaFree(tval);
+  cudaFreeAsync(trp, st);
+  cudaFreeAsync(tci, st);
+  cudaFreeAsync(tval, st);
   if (rc != KRB_OK) return rc;
   A->T = T;
   return KRB_OK;
 }
 
-void matrix_free(krb_matrix *A) {
+// async: free stream-ordered on `st` (no device-wide synchronisation; the
+// arrays return to the memory pool once the work queued on `st` before the
+// call is done -- the caller guarantees no other stream still reads them);
+// otherwise cudaFree (synchronises the device).
+void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
   if (!A) return;
-  matrix_free(A->T);
-  cudaFree(A->rp);
-  cudaFree(A->ci);
-  cudaFree(A->val);
-  cudaFree(A->sl_ptr);
-  cudaFree(A->rlen);
-  cudaFree(A->s_col);
-  cudaFree(A->s_val);
-  cudaFree(A->perm);
+  matrix_free(A->T, async, st);
+  void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm};
+  for (void *p : arrays)
+    if (p) {
+      if (async)
+        cudaFreeAsync(p, st);
+      else
+        cudaFree(p);
+    }
   delete A;
 }
 
@@ -476,7 +490,12 @@ int krb_matrix_create_i64(krb_matrix **out, int64_t n, int64_t nnz,
 }
 
 int krb_matrix_destroy(krb_matrix *A) {
-  matrix_free(A);
+  matrix_free(A, false, nullptr);
+  return KRB_OK;
+}
+
+int krb_matrix_destroy_async(krb_matrix *A, void *stream) {
+  matrix_free(A, true, as_stream(stream));
   return KRB_OK;
 }
 

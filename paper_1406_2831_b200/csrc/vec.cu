@@ -152,8 +152,115 @@ __global__ void __launch_bounds__(256) k_gram_part(
   }
 }
 
-// out[i + c*ldo] = sum_j X[i + j*ldx] Z[j*nc + c]  (sequential fma, j order)
+// Register-tiled Gram chunk partials (same order as k_gram_part): each thread
+// owns a 4 x 4 tile of entries and runs their 16 sequential fma chains over
+// the chunk's rows, so a row costs 8 shared loads for 16 fma instead of 2
+// per fma.  Sub-tiles of kGT rows are staged column-major (padded stride)
+// with coalesced loads.  Requires ceil(na/4) * ceil(nc/4) <= 256.
 constexpr int kGemmCT = 8;
+constexpr int kGT = 64;
+constexpr int kGS = kGT + 1;   // padded column stride in shared memory
+__global__ void __launch_bounds__(256) k_gram_tiled(
+    int64_t n, int64_t R, int64_t nch, int na, int nc,
+    const double *__restrict__ X, int64_t ldx, const double *__restrict__ Y,
+    int64_t ldy, double *__restrict__ part) {
+  extern __shared__ double sm[];
+  const int na4 = (na + 3) & ~3, nc4 = (nc + 3) & ~3;
+  double *xs = sm;                  // [na4][kGS]
+  double *ys = sm + na4 * kGS;      // [nc4][kGS]
+  const int ntc = nc4 >> 2, ntile = (na4 >> 2) * ntc;
+  const int tid = threadIdx.x;
+  const int a0 = (tid / ntc) * 4, c0 = (tid % ntc) * 4;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const int64_t r0 = ch * R;
+    const int64_t r1 = min(n, r0 + R);
+    for (int64_t t0 = r0; t0 < r1; t0 += kGT) {
+      const int rows = (int)min((int64_t)kGT, r1 - t0);
+      __syncthreads();
+      for (int idx = tid; idx < na4 * kGT; idx += blockDim.x) {
+        const int a = idx / kGT, rr = idx - a * kGT;
+        xs[a * kGS + rr] = (a < na && rr < rows) ? __ldg(X + (int64_t)a * ldx + t0 + rr) : 0.0;
+      }
+      for (int idx = tid; idx < nc4 * kGT; idx += blockDim.x) {
+        const int c = idx / kGT, rr = idx - c * kGT;
+        ys[c * kGS + rr] = (c < nc && rr < rows) ? __ldg(Y + (int64_t)c * ldy + t0 + rr) : 0.0;
+      }
+      __syncthreads();
+      if (tid < ntile) {
+        for (int rr = 0; rr < rows; ++rr) {
+          double xv[4], yv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) xv[i] = xs[(a0 + i) * kGS + rr];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) yv[j] = ys[(c0 + j) * kGS + rr];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(xv[i], yv[j], acc[i][j]);
+        }
+      }
+    }
+    if (tid < ntile) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (a0 + i < na && c0 + j < nc)
+            part[(int64_t)((a0 + i) * nc + c0 + j) * nch + ch] = acc[i][j];
+    }
+  }
+}
+
+// out = X Z with X's rows staged in shared memory by per-thread async
+// copies (each thread copies and consumes its own row: no CTA barrier), so
+// X is read from HBM once for all nc columns (k_gemm re-reads it per group
+// of kGemmCT columns).  Sequential fma over j per output, as k_gemm.
+constexpr int kGemmRows = 128;
+__global__ void __launch_bounds__(kGemmRows) k_gemm_staged(int64_t n, int m, int nc,
+                                                         const double *__restrict__ X,
+                                                         int64_t ldx,
+                                                         const double *__restrict__ Z,
+                                                         double *__restrict__ out,
+                                                         int64_t ldo) {
+  extern __shared__ double sm[];
+  double *zs = sm;                          // [m][nc]
+  double *xs = sm + ((m * nc + 1) & ~1);    // [m][kGemmRows]
+  for (int idx = threadIdx.x; idx < m * nc; idx += blockDim.x) zs[idx] = Z[idx];
+  const uint64_t pol = l2_policy(false);
+  for (int64_t i0 = (int64_t)blockIdx.x * kGemmRows; i0 < n;
+       i0 += (int64_t)gridDim.x * kGemmRows) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    for (int j = 0; j < m; ++j)
+      cp_async8(xs + j * kGemmRows + threadIdx.x, X + (int64_t)j * ldx + (ok ? i : 0), ok, pol);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();   // zs (first pass) and nothing else: xs rows are private
+    if (ok) {
+      for (int c0 = 0; c0 < nc; c0 += kGemmCT) {
+        double acc[kGemmCT];
+#pragma unroll
+        for (int t = 0; t < kGemmCT; ++t) acc[t] = 0.0;
+        for (int j = 0; j < m; ++j) {
+          const double xv = xs[j * kGemmRows + threadIdx.x];
+#pragma unroll
+          for (int t = 0; t < kGemmCT; ++t)
+            if (c0 + t < nc) acc[t] = __fma_rn(xv, zs[j * nc + c0 + t], acc[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < kGemmCT; ++t)
+          if (c0 + t < nc) out[(int64_t)(c0 + t) * ldo + i] = acc[t];
+      }
+    }
+  }
+}
+
+// out[i + c*ldo] = sum_j X[i + j*ldx] Z[j*nc + c]  (sequential fma, j order)
 __global__ void __launch_bounds__(256) k_gemm(int64_t n, int m, int nc,
                                               const double *__restrict__ X,
                                               int64_t ldx,
@@ -416,13 +523,24 @@ int krb_gram(krb_context *ctx, int64_t n, int64_t na, int64_t nc,
   }
   int rc = ctx_reserve_part(ctx, (size_t)(ne * nch));
   if (rc) return rc;
-  size_t smem = sizeof(double) * kGramTile * (na + nc);
-  KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_part,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-  int grid = (int)(nch < kNumSMs * 4 ? nch : kNumSMs * 4);
-  k_gram_part<<<grid, 256, smem, st>>>(n, R, nch, (int)na, (int)nc, d_X, ldx,
-                                       d_Y, ldy, ctx->part);
+  const int64_t na4 = (na + 3) & ~3, nc4 = (nc + 3) & ~3;
+  if ((na4 / 4) * (nc4 / 4) <= 256) {
+    size_t smem = sizeof(double) * kGS * (na4 + nc4);
+    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_tiled,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    int grid = (int)(nch < kNumSMs * 4 ? nch : kNumSMs * 4);
+    k_gram_tiled<<<grid, 256, smem, st>>>(n, R, nch, (int)na, (int)nc, d_X, ldx, d_Y, ldy,
+                                          ctx->part);
+  } else {
+    size_t smem = sizeof(double) * kGramTile * (na + nc);
+    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_part,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    int grid = (int)(nch < kNumSMs * 4 ? nch : kNumSMs * 4);
+    k_gram_part<<<grid, 256, smem, st>>>(n, R, nch, (int)na, (int)nc, d_X, ldx,
+                                         d_Y, ldy, ctx->part);
+  }
   KRB_CHECK_LAUNCH();
   return launch_final((int)ne, nch, ctx->part, d_G, st);
 }
@@ -433,6 +551,18 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
   KRB_REQUIRE(m * nc <= 8192, "krb_gemm: m*nc > 8192");
   cudaStream_t st = as_stream(stream);
   if (n == 0 || nc == 0) return KRB_OK;
+  const size_t staged = sizeof(double) * (((m * nc + 1) & ~1) + (size_t)m * kGemmRows);
+  if (m > 0 && staged <= 160 * 1024) {
+    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gemm_staged,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)staged));
+    int64_t blocks = (n + kGemmRows - 1) / kGemmRows;
+    int grid = (int)(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16);
+    k_gemm_staged<<<grid, kGemmRows, staged, st>>>(n, (int)m, (int)nc, d_X, ldx, d_Z, d_out,
+                                                   ldo);
+    KRB_CHECK_LAUNCH();
+    return KRB_OK;
+  }
   size_t smem = sizeof(double) * (m * nc > 0 ? m * nc : 1);
   KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gemm,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,

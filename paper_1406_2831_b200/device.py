@@ -184,8 +184,9 @@ class DeviceMatrix:
 
 
 def _destroy_matrix(h):
+    # stream-ordered on the (single) stream the matrix is used on
     try:
-        _lib.load().krb_matrix_destroy(ctypes.c_void_p(h))
+        _lib.load().krb_matrix_destroy_async(ctypes.c_void_p(h), stream_ptr())
     except Exception:
         pass
 

@@ -110,7 +110,8 @@ def test_projection_primitives_bitwise(dev, canon, n, k):
     assert np.array_equal(R.colnorms(Md).cpu().numpy(), canon.colnorms(M))
 
 
-@pytest.mark.parametrize("n,na,nc", [(500, 3, 4), (70_000, 20, 20), (1_000_000, 47, 47)])
+@pytest.mark.parametrize("n,na,nc", [(500, 3, 4), (70_000, 20, 20), (1_000_000, 47, 47),
+                                     (262_144, 40, 40), (5_000, 130, 30), (3_001, 1, 64)])
 def test_gram_gemm_bitwise(dev, canon, n, na, nc):
     from paper_1406_2831_b200 import recycling as R
     r = np.random.default_rng(na)
@@ -135,3 +136,15 @@ def test_pcg64_matches_numpy(dev, seed, n):
               ctypes.c_void_p(out.data_ptr()), dev.stream_ptr())
     ref = np.random.default_rng(seed).uniform(-1.0, 1.0, size=n)
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n,m,nc", [(1_000, 3, 1), (262_144, 40, 40), (5_003, 64, 64),
+                                    (70_001, 200, 30)])
+def test_gemm_shapes_bitwise(dev, canon, n, m, nc):
+    """staged (X rows in shared memory) and fallback gemm paths"""
+    from paper_1406_2831_b200 import recycling as R
+    r = np.random.default_rng(m + nc)
+    X = r.standard_normal((n, m))
+    Z = r.standard_normal((m, nc))
+    out = R.gemm(_cols(X), Z).cpu().numpy().T
+    assert np.array_equal(out, canon.gemm(X, Z))

@@ -216,50 +216,6 @@ __global__ void __launch_bounds__(256) k_gram_tiled(
   }
 }
 
-// out = X Z with X's rows staged in shared memory by per-thread async
-// copies (each thread copies and consumes its own row: no CTA barrier), so
-// X is read from HBM once for all nc columns (k_gemm re-reads it per group
-// of kGemmCT columns).  Sequential fma over j per output, as k_gemm.
-constexpr int kGemmRows = 128;
-__global__ void __launch_bounds__(kGemmRows) k_gemm_staged(int64_t n, int m, int nc,
-                                                         const double *__restrict__ X,
-                                                         int64_t ldx,
-                                                         const double *__restrict__ Z,
-                                                         double *__restrict__ out,
-                                                         int64_t ldo) {
-  extern __shared__ double sm[];
-  double *zs = sm;                          // [m][nc]
-  double *xs = sm + ((m * nc + 1) & ~1);    // [m][kGemmRows]
-  for (int idx = threadIdx.x; idx < m * nc; idx += blockDim.x) zs[idx] = Z[idx];
-  const uint64_t pol = l2_policy(false);
-  for (int64_t i0 = (int64_t)blockIdx.x * kGemmRows; i0 < n;
-       i0 += (int64_t)gridDim.x * kGemmRows) {
-    const int64_t i = i0 + threadIdx.x;
-    const bool ok = i < n;
-    for (int j = 0; j < m; ++j)
-      cp_async8(xs + j * kGemmRows + threadIdx.x, X + (int64_t)j * ldx + (ok ? i : 0), ok, pol);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();   // zs (first pass) and nothing else: xs rows are private
-    if (ok) {
-      for (int c0 = 0; c0 < nc; c0 += kGemmCT) {
-        double acc[kGemmCT];
-#pragma unroll
-        for (int t = 0; t < kGemmCT; ++t) acc[t] = 0.0;
-        for (int j = 0; j < m; ++j) {
-          const double xv = xs[j * kGemmRows + threadIdx.x];
-#pragma unroll
-          for (int t = 0; t < kGemmCT; ++t)
-            if (c0 + t < nc) acc[t] = __fma_rn(xv, zs[j * nc + c0 + t], acc[t]);
-        }
-#pragma unroll
-        for (int t = 0; t < kGemmCT; ++t)
-          if (c0 + t < nc) out[(int64_t)(c0 + t) * ldo + i] = acc[t];
-      }
-    }
-  }
-}
-
 // out[i + c*ldo] = sum_j X[i + j*ldx] Z[j*nc + c]  (sequential fma, j order)
 __global__ void __launch_bounds__(256) k_gemm(int64_t n, int m, int nc,
                                               const double *__restrict__ X,
@@ -551,18 +507,6 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
   KRB_REQUIRE(m * nc <= 8192, "krb_gemm: m*nc > 8192");
   cudaStream_t st = as_stream(stream);
   if (n == 0 || nc == 0) return KRB_OK;
-  const size_t staged = sizeof(double) * (((m * nc + 1) & ~1) + (size_t)m * kGemmRows);
-  if (m > 0 && staged <= 160 * 1024) {
-    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gemm_staged,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)staged));
-    int64_t blocks = (n + kGemmRows - 1) / kGemmRows;
-    int grid = (int)(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16);
-    k_gemm_staged<<<grid, kGemmRows, staged, st>>>(n, (int)m, (int)nc, d_X, ldx, d_Z, d_out,
-                                                   ldo);
-    KRB_CHECK_LAUNCH();
-    return KRB_OK;
-  }
   size_t smem = sizeof(double) * (m * nc > 0 ? m * nc : 1);
   KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gemm,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -99,6 +99,30 @@ class _Staging:
 
 
 _STAGING = _Staging()
+_POOL = None
+_PAR_BYTES = 8 << 20     # host copies above this size are split across threads
+
+
+def _host_copy(dst: np.ndarray, src: np.ndarray):
+    """dst[:] = src (flat uint8 views), split across threads for large
+    arrays: numpy releases the GIL inside the copy loop, so the memcpy into
+    pinned staging runs at several times single-thread bandwidth."""
+    global _POOL
+    n = src.nbytes
+    if n < _PAR_BYTES:
+        np.copyto(dst, src)
+        return
+    if _POOL is None:
+        import concurrent.futures as cf
+        import os
+        _POOL = cf.ThreadPoolExecutor(max_workers=max(2, min(8, (os.cpu_count() or 2))))
+    parts = _POOL._max_workers
+    step = -(-n // parts)
+    step = (step + 4095) & ~4095
+    futs = [_POOL.submit(np.copyto, dst[o:o + step], src[o:o + step])
+            for o in range(0, n, step)]
+    for f in futs:
+        f.result()
 _TDT = {np.dtype(np.float64): "float64", np.dtype(np.int64): "int64",
         np.dtype(np.int32): "int32"}
 
@@ -111,7 +135,7 @@ def to_device(a: np.ndarray, dtype=np.float64):
         return t.from_numpy(a).to("cuda")
     i, buf = _STAGING.get(a.nbytes)
     host = buf[:a.nbytes].numpy()
-    np.copyto(host, a.reshape(-1).view(np.uint8))
+    _host_copy(host, a.reshape(-1).view(np.uint8))
     out = t.empty(a.shape, dtype=getattr(t, _TDT[a.dtype]), device="cuda")
     out.view(-1).view(t.uint8).copy_(buf[:a.nbytes], non_blocking=True)
     _STAGING.mark(i)

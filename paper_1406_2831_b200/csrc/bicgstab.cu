@@ -240,6 +240,8 @@ static int build_graph(krb_context *ctx, const IterArgs &h, const IterArgs *d,
   G.graph = g;
   G.exec = exec;
   G.cond = hc;
+  KRB_CHECK_CUDA(cudaGraphUpload(exec, capture));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(capture));
   return KRB_OK;
 }
 

@@ -47,6 +47,8 @@ struct GraphCache {
 
 }  // namespace krb
 
+struct krb_rbicg;
+
 struct krb_context {
   // generic partial buffer for canonical reductions
   double *part = nullptr;
@@ -61,6 +63,10 @@ struct krb_context {
   double *p2 = nullptr, *q2 = nullptr;   // double buffers (persistent v2)
   double *kbuf = nullptr;  // zeta, gamma, xc, y  (4 x k)
   krb::GraphCache graph;
+  // buffers + instantiated graph of the last destroyed RBiCG handle, reused
+  // by the next krb_rbicg_create of the same shape (no cudaMalloc / graph
+  // instantiation / device-synchronising cudaFree per generation solve)
+  krb_rbicg *bi_cache = nullptr;
 };
 
 namespace krb {
@@ -74,6 +80,7 @@ int ctx_reserve_part(krb_context *ctx, size_t doubles);
 int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);
 dim3 tdot_grid(int64_t nb, int64_t k);
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k);
+void rbicg_cache_free(krb_context *ctx);
 
 // canonical primitives used across translation units (stream-ordered)
 int launch_dot_partials(int64_t n, const double *x, const double *y,

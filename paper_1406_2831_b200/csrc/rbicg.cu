@@ -428,6 +428,7 @@ struct krb_rbicg {
   int64_t per_body = 0;
   int64_t l0 = 0;
   int use_graph = 1;
+  int fmt = -1, fmt_t = -1;   // storage formats the graph was captured for
 };
 
 namespace krb {
@@ -491,6 +492,9 @@ static int bi_build_graph(krb_rbicg *H) {
   H->graph = g;
   H->h.cond = hc;
   H->h.use_cond = 1;
+  // upload once so every resume after a harvest pause is a plain launch
+  KRB_CHECK_CUDA(cudaGraphUpload(H->exec, cs));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(cs));
   return KRB_OK;
 }
 
@@ -508,26 +512,33 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   cudaStream_t st = as_stream(stream);
   int rc = ensure_transpose(A, st);
   if (rc) return rc;
-  krb_rbicg *H = new krb_rbicg();
+  const int64_t n = A->n;
+  const int64_t k = (R && R->k > 0) ? R->k : 0;
+  if (k > 0 && (R->n != n || R->ld < n)) {
+    set_error("recycle space dimension does not match the operator");
+    return KRB_EINVAL;
+  }
+  // reuse the cached handle of the same shape (buffers, descriptors and the
+  // instantiated graph, whose kernels read everything per solve from H->d)
+  krb_rbicg *H = ctx->bi_cache;
+  const bool reuse = H && H->h.n == n && H->k == k && H->s == s && H->max_itn == max_itn &&
+                     H->fmt == A->format && H->fmt_t == A->T->format;
+  if (H && !reuse) bi_free(H);
+  ctx->bi_cache = nullptr;
+  if (!reuse) H = new krb_rbicg();
   H->ctx = ctx;
   H->A = A;
   H->s = s;
   H->max_itn = max_itn;
-  const int64_t n = A->n;
-  const int64_t k = (R && R->k > 0) ? R->k : 0;
-  if (k > 0) {
-    if (R->n != n || R->ld < n) {
-      delete H;
-      set_error("recycle space dimension does not match the operator");
-      return KRB_EINVAL;
-    }
-    H->R = *R;
-    H->has_R = true;
-  }
+  H->has_R = k > 0;
+  if (k > 0) H->R = *R;
   H->k = k;
+  H->fmt = A->format;
+  H->fmt_t = A->T->format;
   const int64_t nb = canon_nblocks(n);
   const int64_t ring_cols = (s > 0 ? s : 0) + 3;
   cudaError_t e = cudaSuccess;
+  if (reuse) goto fill;
   e = cudaMalloc(&H->d, sizeof(BiArgs));
   if (e == cudaSuccess) e = cudaMalloc(&H->d_nc, sizeof(BiArgs));
   if (e == cudaSuccess) e = cudaMalloc(&H->bufs, sizeof(double) * 10 * (n > 0 ? n : 1));
@@ -543,6 +554,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
     bi_free(H);
     return KRB_ENOMEM;
   }
+fill:
   rc = ctx_reserve_part(ctx, (size_t)((k > 3 ? 2 * k : 3) * nb) + 64);
   if (!rc) rc = ctx_reserve_counters(ctx, st);
   if (rc) {
@@ -584,9 +596,29 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
 }
 
 int krb_rbicg_destroy(krb_rbicg *H) {
+  if (!H) return KRB_OK;
+  // keep the resources for the next generation solve of the same shape
+  if (H->ctx) {
+    if (H->ctx->bi_cache && H->ctx->bi_cache != H) bi_free(H->ctx->bi_cache);
+    H->ctx->bi_cache = H;
+    return KRB_OK;
+  }
   bi_free(H);
   return KRB_OK;
 }
+
+}  // extern "C"
+
+namespace krb {
+void rbicg_cache_free(krb_context *ctx) {
+  if (ctx && ctx->bi_cache) {
+    bi_free(ctx->bi_cache);
+    ctx->bi_cache = nullptr;
+  }
+}
+}  // namespace krb
+
+extern "C" {
 
 /* Setup: b, b_dual, x_init, x_init_dual (device, NULLable except b, bt).
  * Runs project_initial / project_initial_dual and the dual-start test; the

@@ -485,6 +485,26 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
       prologue<kE, false>(stage, Cm, ld, n, k, ncg, me, G, Tt, pol);
       __syncthreads();
       cta_stage(wred, nown, k, 0, 0, me, G, nb, pb[cur]);
+    } else {
+      // k = 0: nothing to project, so B's (rt0, q), (q, q) come straight from
+      // the registers holding q -- phase B and its barrier disappear
+#pragma unroll
+      for (int bi = 0; bi < kMaxOwn; ++bi) {
+        if (bi >= nown) break;
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int64_t i = owned_elem<kE>(me + bi * G, e);
+          if (i < n) {
+            const double vi = qreg[bi][e];
+            acc[0] = __fma_rn(rt0[i], vi, acc[0]);   // (rt0, q)
+            acc[1] = __fma_rn(vi, vi, acc[1]);       // (q, q)
+          }
+        }
+        warp_stage<2>(acc, wred, bi, kV2MaxK - 1);
+      }
+      __syncthreads();
+      cta_stage(wred, nown, 2, kV2MaxK - 1, 0, me, G, nb, pb[cur]);
     }
     KRB_STAMP(7);
     grid.sync();
@@ -493,17 +513,17 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
       tdot_finals<false>(nb, k, pb[cur], zeta);
       __syncthreads();
       cur ^= 1;
+      KRB_STAMP(1);
+      // ---- B: q' -= C zeta; (rt0, q'), (q', q') -> alpha
+      correct_warps<kE, false>(stage, Cm, ld, n, k, ncg, me, G, nown, qreg, sreg, zeta, qn,
+                               rt0, wred, pol);
+      prologue<kE, true>(stage, Chat, ld, n, k, ncg, me, G, Tt, pol);
+      __syncthreads();
+      cta_stage(wred, nown, 2, kV2MaxK - 1, 0, me, G, nb, pb[cur]);
+      KRB_STAMP(12);
+      grid.sync();
+      KRB_STAMP(13);
     }
-    KRB_STAMP(1);
-    // ---- B: q' -= C zeta; (rt0, q'), (q', q') -> alpha
-    correct_warps<kE, false>(stage, Cm, ld, n, k, ncg, me, G, nown, qreg, sreg, zeta, qn,
-                             rt0, wred, pol);
-    if (k > 0) prologue<kE, true>(stage, Chat, ld, n, k, ncg, me, G, Tt, pol);
-    __syncthreads();
-    cta_stage(wred, nown, 2, kV2MaxK - 1, 0, me, G, nb, pb[cur]);
-    KRB_STAMP(12);
-    grid.sync();
-    KRB_STAMP(13);
     local_finals<2>(a, pb[cur], dfin);
     cur ^= 1;
     if (threadIdx.x == 0) finalize<PH_PROJ_Q>(a, &L, dfin, writer);
@@ -519,7 +539,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
 #pragma unroll
       for (int bi = 0; bi < kMaxOwn; ++bi) {
         if (bi >= nown) break;
-        double acc[2] = {0.0, 0.0};
+        double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
 #pragma unroll
         for (int e = 0; e < kE; ++e) {
           sreg[bi][e] = treg[bi][e] = 0.0;
@@ -532,9 +552,14 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
             const double tv = spmv_row_f<kSell>(i, A, sf);
             tv_[i] = tv;
             treg[bi][e] = tv;
+            if (k == 0) {   // D's dots, straight from registers
+              acc2[0] = __fma_rn(tv, tv, acc2[0]);   // (t, t)
+              acc2[1] = __fma_rn(tv, sv, acc2[1]);   // (t, s)
+            }
           }
         }
         warp_stage<1>(acc, wred, bi, kV2MaxK);
+        if (k == 0) warp_stage<2>(acc2, wred, bi, 0);
         if (k > 0) proj_block<kE>(stage, Chat, ld, n, k, ncg, me, G, nown, bi, treg, wred, pol);
       }
     }
@@ -543,6 +568,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
     __syncthreads();
     cta_stage(wred, nown, 1, kV2MaxK, k, me, G, nb, pb[cur]);   // (s, s) -> row k
     if (k > 0) cta_stage(wred, nown, k, 0, 0, me, G, nb, pb[cur]);
+    else cta_stage(wred, nown, 2, 0, 1, me, G, nb, pb[cur]);      // (t,t), (t,s) -> rows 1, 2
     KRB_STAMP(10);
     grid.sync();
     KRB_STAMP(11);
@@ -553,6 +579,10 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
       if (warp < k) {
         double v = warp_final_volatile(pb[cur] + (int64_t)warp * nb, nb);
         if (lane == 0) gamma[warp] = v;
+      }
+      if (k == 0 && warp < 2) {
+        double v = warp_final_volatile(pb[cur] + (int64_t)(1 + warp) * nb, nb);
+        if (lane == 0) dfin[1 + warp] = v;
       }
       if (warp == 31) {
         double v = warp_final_volatile(pb[cur] + (int64_t)k * nb, nb);
@@ -578,16 +608,20 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
       __syncthreads();
       break;
     }
-    // ---- D: t -= C gamma; (t, t), (t, s) -> omega
-    correct_warps<kE, true>(stage, Cm, ld, n, k, ncg, me, G, nown, treg, sreg, gamma, tv_,
-                            rt0, wred, pol);
-    if (k > 0) prologue<kE, true>(stage, Chat, ld, n, k, ncg, me, G, Tt, pol);  // next A
-    __syncthreads();
-    cta_stage(wred, nown, 2, kV2MaxK - 1, 0, me, G, nb, pb[cur]);
-    grid.sync();
-    local_finals<2>(a, pb[cur], dfin);
-    cur ^= 1;
-    if (threadIdx.x == 0) finalize<PH_PROJ_T>(a, &L, dfin, writer);
+    // ---- D: t -= C gamma; (t, t), (t, s) -> omega   (k = 0: dots done in C)
+    if (k > 0) {
+      correct_warps<kE, true>(stage, Cm, ld, n, k, ncg, me, G, nown, treg, sreg, gamma, tv_,
+                              rt0, wred, pol);
+      prologue<kE, true>(stage, Chat, ld, n, k, ncg, me, G, Tt, pol);  // next A
+      __syncthreads();
+      cta_stage(wred, nown, 2, kV2MaxK - 1, 0, me, G, nb, pb[cur]);
+      grid.sync();
+      local_finals<2>(a, pb[cur], dfin);
+      cur ^= 1;
+      if (threadIdx.x == 0) finalize<PH_PROJ_T>(a, &L, dfin, writer);
+    } else if (threadIdx.x == 0) {
+      finalize<PH_PROJ_T>(a, &L, dfin + 1, writer);
+    }
     __syncthreads();
     KRB_STAMP(4);
     if (L.status != KRB_RUNNING) break;

@@ -698,9 +698,12 @@ static int persist2_launch(const IterArgs *d, int64_t nb, cudaStream_t st) {
     set_error("fused persistent kernel: %lld blocks > %d x %d CTAs", (long long)nb, kMaxOwn, grid);
     return KRB_EINVAL;
   }
+  // small systems: one CTA per canonical block (fewer CTAs make every grid
+  // barrier and final-stage read cheaper; idle CTAs would only add arrivals)
+  const int g = nb < grid ? (int)(nb > 0 ? nb : 1) : grid;
   void *args[] = {(void *)&d};
   KRB_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_persist2<kE, kSell>,
-                                             dim3(grid), dim3(1024), args, kStageBytes, st));
+                                             dim3(g), dim3(1024), args, kStageBytes, st));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }

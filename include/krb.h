@@ -191,6 +191,20 @@ int krb_rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
  * begin -> run (returns at every completed cycle of s iterations, so the
  * recycle-space update can run, or when the solve stops) -> rotate after an
  * emitted cycle -> finish. */
+/* Multi-right-hand-side RBiCGSTAB: nrhs <= 4
+ * independent solves with the same matrix and recycle space (k <= 128) in
+ * lockstep -- each iteration reads A, C and Chat once for all of them.  Every
+ * per-rhs argument is a host array of nrhs device pointers (d_x_init may be
+ * NULL, or hold NULL entries); cfgs and h_results are host arrays of nrhs.
+ * Results are bit-identical to nrhs separate krb_rbicgstab calls.
+ * use_graph (cfgs[0]): 0 host loop, otherwise CUDA graph. */
+int krb_rbicgstab_batch(krb_context *ctx, const krb_matrix *A, int64_t nrhs,
+                        const double *const *d_b, const double *const *d_x_init,
+                        const krb_space_view *R, const krb_solve_config *cfgs,
+                        double *const *d_x_out, double *const *d_hist_resid,
+                        int64_t *const *d_hist_matvecs, uint64_t *const *d_hist_stamp,
+                        krb_solve_result *h_results, void *stream);
+
 typedef struct krb_rbicg krb_rbicg;
 int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
                      const krb_space_view *R, int64_t s, int64_t max_itn,

@@ -13,7 +13,8 @@ from .recycling import (CapturedCycle, RecycleSpace, biorthonormalize,
 from .solvers import (BREAKDOWN_OMEGA, BREAKDOWN_SECOND_KIND,
                       BREAKDOWN_SERIOUS, CONVERGED, MAX_ITN,
                       ConvergenceHistory, SolverConfig, bicgstab_solve,
-                      rbicg_solve, rbicgstab_solve)
+                      bicgstab_solve_batch, rbicg_solve, rbicgstab_solve,
+                      rbicgstab_solve_batch)
 from .update import update_recycle_space
 from .sparse import SparseMatrix
 
@@ -25,6 +26,7 @@ __all__ = [
     "refresh_images",
     "ConvergenceHistory", "SolverConfig", "bicgstab_solve", "rbicgstab_solve",
     "rbicg_solve", "update_recycle_space",
+    "rbicgstab_solve_batch", "bicgstab_solve_batch",
     "CONVERGED", "MAX_ITN", "BREAKDOWN_SERIOUS", "BREAKDOWN_OMEGA",
     "BREAKDOWN_SECOND_KIND",
     "SparseMatrix",

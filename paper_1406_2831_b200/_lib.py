@@ -92,6 +92,10 @@ SIGNATURES = {
                               ctypes.POINTER(SolveConfig), c_vp, c_vp, c_vp,
                               c_vp, ctypes.POINTER(SolveResult), c_vp]),
     "krb_last_scalars": (c_int, [c_vp, ctypes.POINTER(c_dbl)]),
+    "krb_rbicgstab_batch": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp,
+                                    ctypes.POINTER(SpaceView),
+                                    ctypes.POINTER(SolveConfig), c_vp, c_vp, c_vp,
+                                    c_vp, ctypes.POINTER(SolveResult), c_vp]),
     "krb_memcpy_d2d": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "krb_colsq": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "krb_ritz_combine": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,

@@ -47,6 +47,7 @@ int krb_context_destroy(krb_context *ctx) {
   if (!ctx) return KRB_OK;
   ctx->graph.reset();
   krb::rbicg_cache_free(ctx);
+  krb::batch_pool_free(ctx);
   double *bufs[] = {ctx->part, ctx->x, ctx->r, ctx->p, ctx->q, ctx->s,
                     ctx->t, ctx->rt0, ctx->b, ctx->w, ctx->p2, ctx->q2, ctx->kbuf};
   for (double *b : bufs)

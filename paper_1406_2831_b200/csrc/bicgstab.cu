@@ -123,11 +123,6 @@ __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
   }
 }
 
-#define KRB_TRY(x)          \
-  do {                      \
-    int rc_ = (x);          \
-    if (rc_) return rc_;    \
-  } while (0)
 
 template <int PH>
 static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
@@ -245,6 +240,71 @@ static int build_graph(krb_context *ctx, const IterArgs &h, const IterArgs *d,
   return KRB_OK;
 }
 
+// Per-solve setup (solvers.py:257-296) for the solve described by h / d (the
+// device descriptor must already hold h): scalars, ||b||, shadow residual,
+// x0 / r0 (project_initial), rt0 projection, INIT.  w: n-vector scratch for
+// the shadow residual, ybuf: k-vector scratch.  Stream-ordered, no sync.
+int solve_setup(krb_context *ctx, const krb_matrix *A, const double *d_b,
+                const double *d_x_init, const krb_space_view *R,
+                const krb_solve_config *cfg, const IterArgs &h, const IterArgs *d,
+                double *w, double *ybuf, cudaStream_t st) {
+  const int64_t n = h.n, k = h.k;
+  KRB_CHECK_CUDA(cudaMemcpyAsync(h.b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  k_init_scalars<<<1, 1, 0, st>>>(h.S, cfg->tol, cfg->breakdown_tol, cfg->max_itn,
+                                  (int)k, d_x_init ? 1 : 0);
+  KRB_CHECK_LAUNCH();
+  KRB_TRY(launch_phase<PH_BNORM>(h, d, st));
+  // shadow residual rt_{-1} (solvers.py:268-269)
+  if (cfg->d_shadow)
+    KRB_CHECK_CUDA(cudaMemcpyAsync(w, cfg->d_shadow, sizeof(double) * n,
+                                   cudaMemcpyDeviceToDevice, st));
+  else
+    KRB_TRY(krb_uniform_pcg64(n, cfg->pcg_state_hi, cfg->pcg_state_lo, cfg->pcg_inc_hi,
+                              cfg->pcg_inc_lo, -1.0, 1.0, w, st));
+  // x0, r0 (project_initial, recycling.py:189-206)
+  if (d_x_init) {
+    KRB_CHECK_CUDA(cudaMemcpyAsync(h.x, d_x_init, sizeof(double) * n,
+                                   cudaMemcpyDeviceToDevice, st));
+    KRB_TRY(spmv_launch(A, h.x, h.t, nullptr, st));
+    KRB_TRY(launch_phase<PH_RINIT>(h, d, st));
+  } else {
+    KRB_CHECK_CUDA(cudaMemsetAsync(h.x, 0, sizeof(double) * n, st));
+    KRB_CHECK_CUDA(cudaMemcpyAsync(h.r, h.b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  }
+  if (k > 0) {
+    KRB_TRY(launch_tdot(ctx, n, k, R->Chat, R->ld, h.r, false, ybuf, nullptr, st));
+    KRB_TRY(launch_gemv(n, k, R->U, R->ld, ybuf, h.x, +1, h.x, st));
+    KRB_TRY(launch_gemv(n, k, R->C, R->ld, ybuf, h.r, -1, h.r, st));
+    // rt0 = rt_{-1} - Ct (Ccheck^H rt_{-1})   (solvers.py:273)
+    KRB_TRY(launch_tdot(ctx, n, k, R->Ccheck, R->ld, w, false, ybuf, nullptr, st));
+    KRB_TRY(launch_gemv(n, k, R->Ct, R->ld, ybuf, w, -1, h.rt0, st));
+    KRB_CHECK_CUDA(cudaMemsetAsync(h.xc, 0, sizeof(double) * k, st));
+  } else {
+    KRB_CHECK_CUDA(cudaMemcpyAsync(h.rt0, w, sizeof(double) * n,
+                                   cudaMemcpyDeviceToDevice, st));
+  }
+  KRB_CHECK_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * n, st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(h.q, 0, sizeof(double) * n, st));
+  KRB_TRY(launch_phase<PH_INIT>(h, d, st));
+
+  return KRB_OK;
+}
+
+// x_out = x - U xc (solvers.py:359) and the final true residual (:360);
+// stream-ordered, no sync.
+int solve_tail(const krb_matrix *A, const krb_space_view *R, const IterArgs &h,
+               const IterArgs *d, double *d_x_out, cudaStream_t st) {
+  const int64_t n = h.n, k = h.k;
+  if (k > 0)
+    KRB_TRY(launch_gemv(n, k, R->U, R->ld, h.xc, h.x, -1, d_x_out, st));
+  else
+    KRB_CHECK_CUDA(cudaMemcpyAsync(d_x_out, h.x, sizeof(double) * n,
+                                   cudaMemcpyDeviceToDevice, st));
+  KRB_TRY(spmv_launch(A, d_x_out, h.t, nullptr, st));
+  KRB_TRY(launch_phase<PH_TRUE>(h, d, st));
+  return KRB_OK;
+}
+
 static cudaStream_t capture_stream() {
   static thread_local cudaStream_t s = nullptr;
   if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
@@ -324,43 +384,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   // the descriptor is written in stream order (the previous solve on this
   // stream has finished reading it)
   KRB_CHECK_CUDA(cudaMemcpyAsync(d, &h, sizeof(IterArgs), cudaMemcpyHostToDevice, st));
-  KRB_CHECK_CUDA(cudaMemcpyAsync(h.b, d_b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-  k_init_scalars<<<1, 1, 0, st>>>(h.S, cfg->tol, cfg->breakdown_tol, cfg->max_itn,
-                                  (int)k, d_x_init ? 1 : 0);
-  KRB_CHECK_LAUNCH();
-  KRB_TRY(launch_phase<PH_BNORM>(h, d, st));
-  // shadow residual rt_{-1} (solvers.py:268-269)
-  if (cfg->d_shadow)
-    KRB_CHECK_CUDA(cudaMemcpyAsync(ctx->w, cfg->d_shadow, sizeof(double) * n,
-                                   cudaMemcpyDeviceToDevice, st));
-  else
-    KRB_TRY(krb_uniform_pcg64(n, cfg->pcg_state_hi, cfg->pcg_state_lo, cfg->pcg_inc_hi,
-                              cfg->pcg_inc_lo, -1.0, 1.0, ctx->w, st));
-  // x0, r0 (project_initial, recycling.py:189-206)
-  if (d_x_init) {
-    KRB_CHECK_CUDA(cudaMemcpyAsync(h.x, d_x_init, sizeof(double) * n,
-                                   cudaMemcpyDeviceToDevice, st));
-    KRB_TRY(spmv_launch(A, h.x, h.t, nullptr, st));
-    KRB_TRY(launch_phase<PH_RINIT>(h, d, st));
-  } else {
-    KRB_CHECK_CUDA(cudaMemsetAsync(h.x, 0, sizeof(double) * n, st));
-    KRB_CHECK_CUDA(cudaMemcpyAsync(h.r, h.b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-  }
-  if (k > 0) {
-    KRB_TRY(launch_tdot(ctx, n, k, R->Chat, R->ld, h.r, false, ybuf, nullptr, st));
-    KRB_TRY(launch_gemv(n, k, R->U, R->ld, ybuf, h.x, +1, h.x, st));
-    KRB_TRY(launch_gemv(n, k, R->C, R->ld, ybuf, h.r, -1, h.r, st));
-    // rt0 = rt_{-1} - Ct (Ccheck^H rt_{-1})   (solvers.py:273)
-    KRB_TRY(launch_tdot(ctx, n, k, R->Ccheck, R->ld, ctx->w, false, ybuf, nullptr, st));
-    KRB_TRY(launch_gemv(n, k, R->Ct, R->ld, ybuf, ctx->w, -1, h.rt0, st));
-    KRB_CHECK_CUDA(cudaMemsetAsync(h.xc, 0, sizeof(double) * k, st));
-  } else {
-    KRB_CHECK_CUDA(cudaMemcpyAsync(h.rt0, ctx->w, sizeof(double) * n,
-                                   cudaMemcpyDeviceToDevice, st));
-  }
-  KRB_CHECK_CUDA(cudaMemsetAsync(h.p, 0, sizeof(double) * n, st));
-  KRB_CHECK_CUDA(cudaMemsetAsync(h.q, 0, sizeof(double) * n, st));
-  KRB_TRY(launch_phase<PH_INIT>(h, d, st));
+  KRB_TRY(solve_setup(ctx, A, d_b, d_x_init, R, cfg, h, d, ctx->w, ybuf, st));
 
   // ---- iterations (solvers.py:298-356) --------------------------------
   if (mode == 2) {
@@ -383,14 +407,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     }
   }
 
-  // ---- x_out = x - U xc (solvers.py:359), true residual (:360) ----------
-  if (k > 0)
-    KRB_TRY(launch_gemv(n, k, R->U, R->ld, h.xc, h.x, -1, d_x_out, st));
-  else
-    KRB_CHECK_CUDA(cudaMemcpyAsync(d_x_out, h.x, sizeof(double) * n,
-                                   cudaMemcpyDeviceToDevice, st));
-  KRB_TRY(spmv_launch(A, d_x_out, h.t, nullptr, st));
-  KRB_TRY(launch_phase<PH_TRUE>(h, d, st));
+  KRB_TRY(solve_tail(A, R, h, d, d_x_out, st));
   SolveScalars hs;
   KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, h.S, sizeof(SolveScalars), cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));

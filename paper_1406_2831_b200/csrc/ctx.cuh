@@ -67,6 +67,7 @@ struct krb_context {
   // by the next krb_rbicg_create of the same shape (no cudaMalloc / graph
   // instantiation / device-synchronising cudaFree per generation solve)
   krb_rbicg *bi_cache = nullptr;
+  void *batch = nullptr;   // multi-rhs pool (batch.cu)
 };
 
 namespace krb {
@@ -81,6 +82,7 @@ int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);
 dim3 tdot_grid(int64_t nb, int64_t k);
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k);
 void rbicg_cache_free(krb_context *ctx);
+void batch_pool_free(krb_context *ctx);
 
 // canonical primitives used across translation units (stream-ordered)
 int launch_dot_partials(int64_t n, const double *x, const double *y,

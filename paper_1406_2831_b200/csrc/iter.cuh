@@ -283,4 +283,13 @@ __device__ __forceinline__ void half_exit_update(const IterArgs &a, double alpha
       a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
 }
 
+// per-solve setup / tail shared by the single and batched drivers
+// (bicgstab.cu)
+int solve_setup(krb_context *ctx, const krb_matrix *A, const double *d_b,
+                const double *d_x_init, const krb_space_view *R,
+                const krb_solve_config *cfg, const IterArgs &h, const IterArgs *d,
+                double *w, double *ybuf, cudaStream_t st);
+int solve_tail(const krb_matrix *A, const krb_space_view *R, const IterArgs &h,
+               const IterArgs *d, double *d_x_out, cudaStream_t st);
+
 }  // namespace krb

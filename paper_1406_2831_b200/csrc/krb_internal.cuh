@@ -258,6 +258,12 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+#define KRB_TRY(x)          \
+  do {                      \
+    int rc_ = (x);          \
+    if (rc_) return rc_;    \
+  } while (0)
+
 #define KRB_DISPATCH_E(E, ...)                 \
   switch (E) {                                 \
     case 1: { constexpr int kE = 1; __VA_ARGS__; } break;   \

@@ -351,11 +351,6 @@ __global__ void k_bi_init_scalars(BiScalars *S, double tol, double btol,
   }
 }
 
-#define KRB_TRY(x)          \
-  do {                      \
-    int rc_ = (x);          \
-    if (rc_) return rc_;    \
-  } while (0)
 
 template <int PH>
 static int bi_launch(const BiArgs &h, const BiArgs *d, cudaStream_t st) {

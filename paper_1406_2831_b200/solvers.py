@@ -263,6 +263,115 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     return xo, hist
 
 
+BATCH_MAX = 4   # right-hand sides per batched launch (batch.cu kMaxB)
+
+
+def solve_device_batch(M, bds, xds, recycle, cfgs, label="rbicgstab", t0=None,
+                       use_graph=None):
+    """Device-resident multi-right-hand-side entry: up to BATCH_MAX solves
+    with the same DeviceMatrix and recycle space advanced in lockstep
+    (krb_rbicgstab_batch, batch.cu).  Returns [(x device tensor, history)]."""
+    t = torch()
+    if t0 is None:
+        t0 = time.perf_counter()
+    nr = len(bds)
+    if not 1 <= nr <= BATCH_MAX:
+        raise ValueError(f"1 <= number of right-hand sides <= {BATCH_MAX}")
+    if use_graph is None:
+        use_graph = 0 if _graph_mode() == 0 else 1
+    ctx = Context.get()
+    R = None
+    if recycle is not None and recycle.k > 0:
+        R = RecycleSpace.of(recycle)
+        if R.n != M.n:
+            raise ValueError("recycle space dimension does not match the operator")
+    xos, hrs, hms, hts = [], [], [], []
+    cs = (_lib.SolveConfig * nr)()
+    for j, cfg in enumerate(cfgs):
+        L = int(cfg.max_itn) + 2
+        xos.append(t.empty(M.n, dtype=t.float64, device="cuda"))
+        hrs.append(t.empty(L, dtype=t.float64, device="cuda"))
+        hms.append(t.empty(L, dtype=t.int64, device="cuda"))
+        hts.append(t.empty(L, dtype=t.int64, device="cuda"))
+        c = cs[j]
+        c.tol = float(cfg.tol)
+        c.breakdown_tol = float(cfg.breakdown_tol)
+        c.max_itn = int(cfg.max_itn)
+        c.d_shadow = None
+        c.pcg_state_hi, c.pcg_state_lo, c.pcg_inc_hi, c.pcg_inc_lo = pcg64_words(cfg.seed)
+        c.use_graph = int(use_graph)
+
+    def parr(ts):
+        return (ctypes.c_void_p * nr)(*[x.data_ptr() if x is not None else None for x in ts])
+
+    res = (_lib.SolveResult * nr)()
+    view = R.view() if R is not None else None
+    t_launch = time.perf_counter()
+    _lib.call("krb_rbicgstab_batch", ctx.h, M.h, nr, parr(bds),
+              parr(xds) if xds is not None and any(x is not None for x in xds) else None,
+              ctypes.byref(view) if view is not None else None, cs, parr(xos), parr(hrs),
+              parr(hms), parr(hts), res, stream_ptr())
+    out = []
+    total_mv = 0
+    for j in range(nr):
+        L = int(res[j].hist_len)
+        stamps = hts[j][:L].cpu().numpy().astype(np.int64)
+        hist = ConvergenceHistory(solver=label, rhs_norm=float(res[j].rhs_norm))
+        st0 = int(res[j].t_start_ns)
+        hist.resid = [float(v) for v in hrs[j][:L].cpu().numpy()]
+        hist.matvecs = [int(v) for v in hms[j][:L].cpu().numpy()]
+        hist.seconds = [(t_launch - t0) + (int(s) - st0) * 1e-9 for s in stamps]
+        hist.status = _STATUS.get(int(res[j].status), f"unknown:{res[j].status}")
+        hist.final_true_resid = float(res[j].final_true_resid)
+        total_mv += int(res[j].matvecs)
+        out.append((xos[j], hist))
+    LAST_SOLVE.clear()
+    LAST_SOLVE.update(matvecs=total_mv, bodies=max(int(r.iterations_run) for r in res),
+                      kernel_launches=int(res[nr - 1].kernel_launches))
+    return out
+
+
+def _batch_solve(A, bs, x_inits, recycle, configs, label):
+    t0 = time.perf_counter()
+    bs = list(bs)
+    if not bs:
+        return []
+    configs = list(configs) if configs is not None else [SolverConfig()] * len(bs)
+    if len(configs) != len(bs):
+        raise ValueError("one SolverConfig per right-hand side")
+    x_inits = list(x_inits) if x_inits is not None else [None] * len(bs)
+    M, _ = _check_common(A, bs[0], None, configs[0])
+    on_device = _is_device(bs[0])
+    out = []
+    for c0 in range(0, len(bs), BATCH_MAX):
+        chunk = range(c0, min(c0 + BATCH_MAX, len(bs)))
+        bds = [_dev_vec(_check_common(A, bs[j], None, configs[j])[1]) for j in chunk]
+        xds = [_dev_vec(x_inits[j]) for j in chunk]
+        res = solve_device_batch(M, bds, xds, recycle, [configs[j] for j in chunk], label, t0)
+        _count(A, nm=LAST_SOLVE["matvecs"])
+        out += [(x if on_device else x.cpu().numpy(), h) for x, h in res]
+    return out
+
+
+def rbicgstab_solve_batch(A, bs, x_inits=None, recycle=None, configs=None, precond=None):
+    """Multi-right-hand-side extension (not in the
+    reference API): ``len(bs)`` independent rbicgstab_solve calls with the same
+    operator and recycle space, advanced together on the device (up to 4 per
+    launch) so the matrix and the n x k blocks are read once per iteration
+    for all of them.  Bit-identical to the separate calls; returns a list of
+    (x, ConvergenceHistory) in order."""
+    if precond is not None:
+        raise NotImplementedError("preconditioning is out of scope on the device path")
+    return _batch_solve(A, bs, x_inits, recycle, configs, "rbicgstab")
+
+
+def bicgstab_solve_batch(A, bs, x_inits=None, configs=None, precond=None):
+    """Batched bicgstab_solve (the k = 0 case of rbicgstab_solve_batch)."""
+    if precond is not None:
+        raise NotImplementedError("preconditioning is out of scope on the device path")
+    return _batch_solve(A, bs, x_inits, None, configs, "bicgstab")
+
+
 def bicgstab_solve(A, b, x_init=None, precond=None, config=None):
     """solvers.py:156-242 — stabilized BiCG, shadow residual from the seeded
     uniform(-1, 1) stream (drawn on the device, bit-identical to numpy)."""

@@ -200,6 +200,22 @@ __global__ void __launch_bounds__(1024, 1) vp(Mats M, int copies, int R, int64_t
         if (t + 3 < T) issue(t + 3);
         commit();
       }
+    } else if (kMode == 2) {   // grid-stride double2 over the whole block
+      const double2 *A2 = (const double2 *)A;
+      const int64_t n2 = n * k / 2;
+      for (int64_t i = blockIdx.x * 1024 + threadIdx.x; i < n2; i += (int64_t)gridDim.x * 1024) {
+        double2 v = __ldg(A2 + i);
+        tot += v.x + v.y;
+      }
+    } else if (kMode == 3) {   // owned blocks, column loop, double2 (512 threads/row pair)
+      for (int bi = 0; bi < nown; ++bi) {
+        const int64_t b = blockIdx.x + (int64_t)bi * gridDim.x;
+#pragma unroll 4
+        for (int c = 0; c < k; ++c) {
+          const double2 *col = (const double2 *)(A + c * n + b * 1024);
+          if (threadIdx.x < 512) { double2 v = __ldg(col + threadIdx.x); tot += v.x + v.y; }
+        }
+      }
     } else {            // plain loads, all 20 columns of both blocks at once
       double m[2][20];
 #pragma unroll
@@ -280,7 +296,7 @@ int main(int argc, char **argv) {
   CK(cudaFuncSetAttribute(vp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 8 * 1024 * 8));
   Mats mats;
   for (int c = 0; c < copies; ++c) mats.m[c] = M[c];
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     for (int R : {1, 50}) {
       int cp = copies;
       float best = 1e9;
@@ -307,7 +323,9 @@ int main(int argc, char **argv) {
           cfg.numAttrs = 2;
         }
         cudaEventRecord(e0);
-        if (mode) CK(cudaLaunchKernelEx(&cfg, vp<1>, mats, cp, R, n, k, nb, out));
+        if (mode == 1) CK(cudaLaunchKernelEx(&cfg, vp<1>, mats, cp, R, n, k, nb, out));
+        else if (mode == 2) CK(cudaLaunchKernelEx(&cfg, vp<2>, mats, cp, R, n, k, nb, out));
+        else if (mode == 3) CK(cudaLaunchKernelEx(&cfg, vp<3>, mats, cp, R, n, k, nb, out));
         else CK(cudaLaunchKernelEx(&cfg, vp<0>, mats, cp, R, n, k, nb, out));
         cudaEventRecord(e1);
         CK(cudaEventSynchronize(e1));

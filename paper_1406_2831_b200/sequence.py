@@ -82,15 +82,20 @@ def default_api():
 
 def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                  policy="first", baseline=True, api=None, systems=None,
-                 max_seconds=None):
+                 max_seconds=None, batch=True):
     """Run the recycling policy (and the baseline) over ``seq``
     (a workloads.SequenceSpec).  ``max_seconds`` stops after the first system
-    that ends past the budget (bounded CPU samples).  Returns a
-    SequenceResult."""
+    that ends past the budget (bounded CPU samples).  ``batch``: when the api
+    has the multi-right-hand-side solvers, the right-hand sides of one matrix
+    that share the recycle space (kappa > 0 under "verbatim"; every kappa of
+    the baseline track) are solved together -- bit-identical to the
+    one-by-one schedule, the matrix and the n x k blocks read once per
+    iteration for all of them.  Returns a SequenceResult."""
     api = api or default_api()
     k = seq.k if k is None else k
     tol = seq.tol if tol is None else tol
     max_itn = seq.max_itn if max_itn is None else max_itn
+    use_batch = batch and hasattr(api, "rbicgstab_solve_batch") and seq.rhs_per_matrix > 1
     rec = RunReport("recycling")
     base = RunReport("baseline") if baseline else None
     rebuild_points, rebuild_matvecs, space_dims = [], [], []
@@ -107,9 +112,9 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
         op_rec = api.CountingOperator(A)
         op_base = api.CountingOperator(A)
         dual_rhs = np.ones(A.nrows if hasattr(A, "nrows") else seq.n)
-        for kappa in range(seq.rhs_per_matrix):
-            if gidx >= total:
-                break
+        nk = min(seq.rhs_per_matrix, total - gidx)
+        pre_rec, pre_base = {}, {}   # kappa -> (history, seconds) of batched solves
+        for kappa in range(nk):
             b = seq.rhs(i, kappa)
             cfg = api.SolverConfig(tol=tol, max_itn=max_itn, k=k, s=s, seed=seed + gidx)
             t0 = time.perf_counter()
@@ -138,8 +143,28 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
             else:
                 if kappa == 0 and space is not None and i > 0:
                     space = api.refresh_images(space, op_rec)
-                if space is not None and space.k > 0:
-                    attempt = replace(cfg, max_itn=min(max_itn, max(block_itn, 50)))
+                recycled = space is not None and space.k > 0
+                cap = min(max_itn, max(block_itn, 50))
+                if use_batch and kappa not in pre_rec and kappa + 1 < nk:
+                    # every remaining rhs of this matrix shares the space
+                    ks = list(range(kappa, nk))
+                    cfgs = [api.SolverConfig(tol=tol, max_itn=cap if recycled else max_itn,
+                                             k=k, s=s, seed=seed + gidx + (kk - kappa))
+                            for kk in ks]
+                    tb = time.perf_counter()
+                    out = api.rbicgstab_solve_batch(op_rec, [seq.rhs(i, kk) for kk in ks],
+                                                    recycle=space if recycled else None,
+                                                    configs=cfgs)
+                    share = (time.perf_counter() - tb) / len(ks)
+                    for kk, (_, h) in zip(ks, out):
+                        pre_rec[kk] = (h, share)
+                if kappa in pre_rec:
+                    hist, _ = pre_rec[kappa]
+                    if recycled and hist.status != "converged":
+                        _, hist = api.rbicgstab_solve(op_rec, b, recycle=None,
+                                                      config=_reseed(cfg))
+                elif recycled:
+                    attempt = replace(cfg, max_itn=cap)
                     _, hist = api.rbicgstab_solve(op_rec, b, recycle=space,
                                                   config=attempt)
                     if hist.status != "converged":
@@ -147,14 +172,28 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                                                       config=_reseed(cfg))
                 else:
                     _, hist = api.rbicgstab_solve(op_rec, b, recycle=None, config=cfg)
-            rec.seconds += time.perf_counter() - t0
+            rec.seconds += time.perf_counter() - t0 + (pre_rec[kappa][1] if kappa in pre_rec else 0.0)
             rec.histories.append(hist)
             if base is not None:
                 t0 = time.perf_counter()
-                _, bh = api.bicgstab_solve(op_base, b, config=cfg)
+                if use_batch and kappa == 0 and nk > 1:
+                    cfgs = [api.SolverConfig(tol=tol, max_itn=max_itn, k=k, s=s,
+                                             seed=seed + gidx + kk) for kk in range(nk)]
+                    tb = time.perf_counter()
+                    out = api.bicgstab_solve_batch(op_base, [seq.rhs(i, kk) for kk in range(nk)],
+                                                   configs=cfgs)
+                    share = (time.perf_counter() - tb) / nk
+                    for kk, (_, h) in enumerate(out):
+                        pre_base[kk] = (h, share)
+                    t0 = time.perf_counter()
+                if kappa in pre_base:
+                    bh, extra = pre_base[kappa]
+                else:
+                    _, bh = api.bicgstab_solve(op_base, b, config=cfg)
+                    extra = 0.0
                 if bh.status != "converged":
                     _, bh = api.bicgstab_solve(op_base, b, config=_reseed(cfg))
-                base.seconds += time.perf_counter() - t0
+                base.seconds += time.perf_counter() - t0 + extra
                 base.histories.append(bh)
             gidx += 1
             if max_seconds is not None and time.perf_counter() - t_start > max_seconds:

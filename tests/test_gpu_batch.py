@@ -87,3 +87,20 @@ def test_batch_counts_matvecs(pkg):
     for j in range(3):
         pkg.bicgstab_solve(op2, bs[j], config=cfgs[j])
     assert op1.n_matvec == op2.n_matvec > 0
+
+
+@pytest.mark.parametrize("policy", ["verbatim", "first"])
+def test_sequence_batched_schedule_identical(pkg, policy):
+    """run_sequence(batch=True) == the one-by-one schedule on C3 (4 rhs per
+    matrix): every recycling and baseline history, statuses and meters."""
+    from paper_1406_2831_b200.sequence import run_sequence
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence("c3", small=True)
+    r1 = run_sequence(seq, policy=policy, systems=8, batch=True)
+    r2 = run_sequence(seq, policy=policy, systems=8, batch=False)
+    for a, b in ((r1.recycling, r2.recycling), (r1.baseline, r2.baseline)):
+        assert [h.resid for h in a.histories] == [h.resid for h in b.histories]
+        assert [h.matvecs for h in a.histories] == [h.matvecs for h in b.histories]
+        assert [h.status for h in a.histories] == [h.status for h in b.histories]
+        assert a.total_matvecs == b.total_matvecs
+    assert r1.space_dims == r2.space_dims

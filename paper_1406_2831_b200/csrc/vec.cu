@@ -152,106 +152,138 @@ __global__ void __launch_bounds__(256) k_gram_part(
   }
 }
 
-// Register-tiled Gram chunk partials (same order as k_gram_part): each thread
-// owns a 4 x 4 tile of entries and runs their 16 sequential fma chains over
-// the chunk's rows, so a row costs 8 shared loads for 16 fma instead of 2
-// per fma.  Sub-tiles of kGT rows are staged column-major (padded stride)
-// with coalesced loads.  Requires ceil(na/4) * ceil(nc/4) <= 256.
+// Register-tiled Gram chunk partials (same order as k_gram_part): a 16 x 16
+// thread grid, thread (ty, tx) owning the T x T entries (ty + 16 i, tx + 16 j)
+// and running their sequential fma chains over the chunk's rows.  Row
+// sub-tiles of kGT rows are staged column-major in shared memory with an odd
+// stride (conflict-free: the 16 distinct columns a warp reads hit distinct
+// banks) by per-thread cp.async, double-buffered so the next sub-tile loads
+// while this one is consumed.  FP64-FMA bound (m x m x n fma per Gram).
 constexpr int kGemmCT = 8;
 constexpr int kGT = 64;
-constexpr int kGS = kGT + 1;   // padded column stride in shared memory
-__global__ void __launch_bounds__(256) k_gram_tiled(
-    int64_t n, int64_t R, int64_t nch, int na, int nc,
-    const double *__restrict__ X, int64_t ldx, const double *__restrict__ Y,
-    int64_t ldy, double *__restrict__ part) {
+constexpr int kGS = kGT + 1;   // odd column stride in shared memory
+template <int T>
+__global__ void __launch_bounds__(256) k_gram_rt(int64_t n, int64_t R, int64_t nch, int na,
+                                                 int nc, const double *__restrict__ X,
+                                                 int64_t ldx, const double *__restrict__ Y,
+                                                 int64_t ldy, double *__restrict__ part) {
   extern __shared__ double sm[];
-  const int na4 = (na + 3) & ~3, nc4 = (nc + 3) & ~3;
-  double *xs = sm;                  // [na4][kGS]
-  double *ys = sm + na4 * kGS;      // [nc4][kGS]
-  const int ntc = nc4 >> 2, ntile = (na4 >> 2) * ntc;
-  const int tid = threadIdx.x;
-  const int a0 = (tid / ntc) * 4, c0 = (tid % ntc) * 4;
+  constexpr int W = 16 * T;                 // staged columns of X and of Y
+  constexpr int kBuf = 2 * W * kGS;         // doubles per buffer (X then Y)
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const uint64_t pol = l2_policy(false);
   for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
     const int64_t r0 = ch * R;
     const int64_t r1 = min(n, r0 + R);
-    for (int64_t t0 = r0; t0 < r1; t0 += kGT) {
+    const int nsub = (int)((r1 - r0 + kGT - 1) / kGT);
+    auto stage = [&](int sub, int buf) {
+      const int64_t t0 = r0 + (int64_t)sub * kGT;
       const int rows = (int)min((int64_t)kGT, r1 - t0);
+      double *xs = sm + buf * kBuf, *ys = xs + W * kGS;
+      for (int idx = tid; idx < W * kGT; idx += 256) {
+        const int a = idx >> 6, rr = idx & (kGT - 1);
+        const bool okx = a < na && rr < rows, oky = a < nc && rr < rows;
+        cp_async8(xs + a * kGS + rr, X + (okx ? (int64_t)a * ldx + t0 + rr : 0), okx, pol);
+        cp_async8(ys + a * kGS + rr, Y + (oky ? (int64_t)a * ldy + t0 + rr : 0), oky, pol);
+      }
+      cp_async_commit();
+    };
+    double acc[T][T];
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+      for (int j = 0; j < T; ++j) acc[i][j] = 0.0;
+    __syncthreads();   // previous chunk's readers are done with both buffers
+    stage(0, 0);
+    for (int sub = 0; sub < nsub; ++sub) {
+      if (sub + 1 < nsub) {
+        stage(sub + 1, (sub + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
       __syncthreads();
-      for (int idx = tid; idx < na4 * kGT; idx += blockDim.x) {
-        const int a = idx / kGT, rr = idx - a * kGT;
-        xs[a * kGS + rr] = (a < na && rr < rows) ? __ldg(X + (int64_t)a * ldx + t0 + rr) : 0.0;
+      const double *xs = sm + (sub & 1) * kBuf, *ys = xs + W * kGS;
+      const int rows = (int)min((int64_t)kGT, r1 - (r0 + (int64_t)sub * kGT));
+      for (int rr = 0; rr < rows; ++rr) {
+        double xv[T], yv[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i) xv[i] = xs[(ty + 16 * i) * kGS + rr];
+#pragma unroll
+        for (int j = 0; j < T; ++j) yv[j] = ys[(tx + 16 * j) * kGS + rr];
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+#pragma unroll
+          for (int j = 0; j < T; ++j) acc[i][j] = __fma_rn(xv[i], yv[j], acc[i][j]);
       }
-      for (int idx = tid; idx < nc4 * kGT; idx += blockDim.x) {
-        const int c = idx / kGT, rr = idx - c * kGT;
-        ys[c * kGS + rr] = (c < nc && rr < rows) ? __ldg(Y + (int64_t)c * ldy + t0 + rr) : 0.0;
-      }
-      __syncthreads();
-      if (tid < ntile) {
-        for (int rr = 0; rr < rows; ++rr) {
-          double xv[4], yv[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) xv[i] = xs[(a0 + i) * kGS + rr];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) yv[j] = ys[(c0 + j) * kGS + rr];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = __fma_rn(xv[i], yv[j], acc[i][j]);
-        }
-      }
+      __syncthreads();   // buffer (sub & 1) is refilled two sub-tiles later
     }
-    if (tid < ntile) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < T; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (a0 + i < na && c0 + j < nc)
-            part[(int64_t)((a0 + i) * nc + c0 + j) * nch + ch] = acc[i][j];
-    }
+      for (int j = 0; j < T; ++j) {
+        const int a = ty + 16 * i, c = tx + 16 * j;
+        if (a < na && c < nc) part[(int64_t)(a * nc + c) * nch + ch] = acc[i][j];
+      }
   }
 }
 
 // out[i + c*ldo] = sum_j X[i + j*ldx] Z[j*nc + c]  (sequential fma, j order)
-__global__ void __launch_bounds__(256) k_gemm(int64_t n, int m, int nc,
-                                              const double *__restrict__ X,
-                                              int64_t ldx,
-                                              const double *__restrict__ Z,
-                                              double *__restrict__ out,
-                                              int64_t ldo) {
-  extern __shared__ double zs[];
-  for (int idx = threadIdx.x; idx < m * nc; idx += blockDim.x) zs[idx] = Z[idx];
+// One thread per row, kCT output columns per pass (X is re-read once per
+// pass: ceil(nc / kCT) passes), Z in shared memory with an even row stride
+// so a row's kCT coefficients are kCT / 2 broadcast 16-byte loads.
+constexpr int kGemmCT2 = 24;
+__global__ void __launch_bounds__(256, 2) k_gemm(int64_t n, int m, int nc,
+                                                 const double *__restrict__ X,
+                                                 int64_t ldx,
+                                                 const double *__restrict__ Z,
+                                                 double *__restrict__ out,
+                                                 int64_t ldo) {
+  extern __shared__ double2 zs2[];
+  double *zs = reinterpret_cast<double *>(zs2);
+  const int ncp = ((nc + kGemmCT2 - 1) / kGemmCT2) * kGemmCT2;   // padded stride
+  for (int idx = threadIdx.x; idx < m * ncp; idx += blockDim.x) {
+    const int j = idx / ncp, c = idx - j * ncp;
+    zs[idx] = c < nc ? Z[j * nc + c] : 0.0;
+  }
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    for (int c0 = 0; c0 < nc; c0 += kGemmCT) {
-      double acc[kGemmCT];
+    for (int c0 = 0; c0 < nc; c0 += kGemmCT2) {
+      double acc[kGemmCT2];
 #pragma unroll
-      for (int t = 0; t < kGemmCT; ++t) acc[t] = 0.0;
+      for (int t = 0; t < kGemmCT2; ++t) acc[t] = 0.0;
+      const double *xp = X + i;
+      const double2 *zrow = zs2 + (c0 >> 1);
+#pragma unroll 2
       for (int j = 0; j < m; ++j) {
-        double xv = __ldg(X + (int64_t)j * ldx + i);
+        const double xv = __ldg(xp + (int64_t)j * ldx);
+        const double2 *zr = zrow + j * (ncp >> 1);
 #pragma unroll
-        for (int t = 0; t < kGemmCT; ++t)
-          if (c0 + t < nc) acc[t] = __fma_rn(xv, zs[j * nc + c0 + t], acc[t]);
+        for (int t = 0; t < kGemmCT2 / 2; ++t) {
+          const double2 z = zr[t];
+          acc[2 * t] = __fma_rn(xv, z.x, acc[2 * t]);
+          acc[2 * t + 1] = __fma_rn(xv, z.y, acc[2 * t + 1]);
+        }
       }
 #pragma unroll
-      for (int t = 0; t < kGemmCT; ++t)
+      for (int t = 0; t < kGemmCT2; ++t)
         if (c0 + t < nc) out[(int64_t)(c0 + t) * ldo + i] = acc[t];
     }
   }
 }
 
-__global__ void k_colscale_div(int64_t n, int k, double *X, int64_t ldx,
-                               const double *__restrict__ s) {
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-       idx < n * k; idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t j = idx / n, i = idx % n;
-    X[j * ldx + i] = __ddiv_rn(X[j * ldx + i], s[j]);
-  }
+// X[:, j] /= s[j]: column j on blockIdx.y (no per-element index division),
+// two elements per thread
+__global__ void __launch_bounds__(256) k_colscale_div(int64_t n, int k, double *X,
+                                                      int64_t ldx,
+                                                      const double *__restrict__ s) {
+  const int j = blockIdx.y;
+  double *col = X + (int64_t)j * ldx;
+  const double d = __ldg(s + j);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    col[i] = __ddiv_rn(col[i], d);
 }
 
 // ---- PCG64 (numpy default_rng) -----------------------------------------
@@ -479,15 +511,25 @@ int krb_gram(krb_context *ctx, int64_t n, int64_t na, int64_t nc,
   }
   int rc = ctx_reserve_part(ctx, (size_t)(ne * nch));
   if (rc) return rc;
-  const int64_t na4 = (na + 3) & ~3, nc4 = (nc + 3) & ~3;
-  if ((na4 / 4) * (nc4 / 4) <= 256) {
-    size_t smem = sizeof(double) * kGS * (na4 + nc4);
-    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_tiled,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-    int grid = (int)(nch < kNumSMs * 4 ? nch : kNumSMs * 4);
-    k_gram_tiled<<<grid, 256, smem, st>>>(n, R, nch, (int)na, (int)nc, d_X, ldx, d_Y, ldy,
-                                          ctx->part);
+  const int64_t T = ((na > nc ? na : nc) + 15) / 16;
+  if (T <= 4) {
+    const size_t smem = sizeof(double) * 2 * 2 * 16 * T * kGS;
+    int grid = (int)(nch < kNumSMs * 2 ? nch : kNumSMs * 2);
+#define KRB_GRAM_RT(TT)                                                                  \
+  do {                                                                                   \
+    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_rt<TT>,                                   \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                        (int)smem));                                     \
+    k_gram_rt<TT><<<grid, 256, smem, st>>>(n, R, nch, (int)na, (int)nc, d_X, ldx, d_Y, ldy, \
+                                           ctx->part);                                   \
+  } while (0)
+    switch (T) {
+      case 1: KRB_GRAM_RT(1); break;
+      case 2: KRB_GRAM_RT(2); break;
+      case 3: KRB_GRAM_RT(3); break;
+      default: KRB_GRAM_RT(4); break;
+    }
+#undef KRB_GRAM_RT
   } else {
     size_t smem = sizeof(double) * kGramTile * (na + nc);
     KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_part,
@@ -507,12 +549,14 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
   KRB_REQUIRE(m * nc <= 8192, "krb_gemm: m*nc > 8192");
   cudaStream_t st = as_stream(stream);
   if (n == 0 || nc == 0) return KRB_OK;
-  size_t smem = sizeof(double) * (m * nc > 0 ? m * nc : 1);
+  const int64_t ncp = ((nc + kGemmCT2 - 1) / kGemmCT2) * kGemmCT2;
+  size_t smem = sizeof(double) * (m * ncp > 0 ? m * ncp : 2);
+  KRB_REQUIRE(smem <= 200 * 1024, "krb_gemm: Z too large for shared memory");
   KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gemm,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   int64_t blocks = (n + 255) / 256;
-  int grid = (int)(blocks < kNumSMs * 8 ? blocks : kNumSMs * 8);
+  int grid = (int)(blocks < kNumSMs * 2 ? blocks : kNumSMs * 2);
   k_gemm<<<grid, 256, smem, st>>>(n, (int)m, (int)nc, d_X, ldx, d_Z, d_out, ldo);
   KRB_CHECK_LAUNCH();
   return KRB_OK;
@@ -522,8 +566,10 @@ int krb_colscale_div(int64_t n, int64_t k, double *d_X, int64_t ldx,
                      const double *d_s, void *stream) {
   KRB_REQUIRE(ldx >= n, "krb_colscale_div: ldx < n");
   if (n * k == 0) return KRB_OK;
-  int64_t blocks = (n * k + 255) / 256;
-  int grid = (int)(blocks < kNumSMs * 16 ? blocks : kNumSMs * 16);
+  int64_t blocks = (n + 255) / 256;
+  int64_t per_col = (int64_t)kNumSMs * 8 / k;
+  if (per_col < 1) per_col = 1;
+  dim3 grid((unsigned)(blocks < per_col ? blocks : per_col), (unsigned)k);
   k_colscale_div<<<grid, 256, 0, as_stream(stream)>>>(n, (int)k, d_X, ldx, d_s);
   KRB_CHECK_LAUNCH();
   return KRB_OK;

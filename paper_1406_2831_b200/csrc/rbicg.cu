@@ -10,6 +10,7 @@
 // the host) only when a cycle of s iterations is complete, so the host-side
 // recycle-space update (a tiny generalized eigenproblem) can run, or when the
 // solve ends.  Scalar logic follows solvers.py:584-631 in order.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "ctx.cuh"
@@ -17,6 +18,8 @@
 #include "tdot.cuh"
 
 namespace krb {
+
+namespace cg = cooperative_groups;
 
 enum BiPhase {
   BP_PUPDATE = 0,
@@ -65,7 +68,7 @@ struct BiArgs {
   double *zeta, *zetat, *zc, *ztc;
   double *V, *Vt;          // capture rings (ring_ld stride per column)
   double *rhos, *alphas, *betas;
-  double *part;
+  double *part, *part2;   // part2: ping-pong buffer of the persistent kernel
   unsigned int *counters;
   BiScalars *S;
   double *hist_r, *hist_rt;
@@ -73,13 +76,16 @@ struct BiArgs {
   uint64_t *hist_t;
 };
 
-__device__ __forceinline__ void bi_record(const BiArgs &a) {
-  BiScalars *S = a.S;
+// S: the scalar block to update (global, or a CTA's shared copy in the
+// persistent kernel); only the writer CTA stores history / scalar arrays.
+__device__ __forceinline__ void bi_record(const BiArgs &a, BiScalars *S, bool writer) {
   int64_t h = S->hist_len;
-  a.hist_r[h] = S->rnorm;
-  a.hist_rt[h] = S->rtnorm;
-  a.hist_m[h] = S->n_matvec + S->n_rmatvec;
-  a.hist_t[h] = globaltimer();
+  if (writer) {
+    a.hist_r[h] = S->rnorm;
+    a.hist_rt[h] = S->rtnorm;
+    a.hist_m[h] = S->n_matvec + S->n_rmatvec;
+    a.hist_t[h] = globaltimer();
+  }
   S->hist_len = h + 1;
 }
 
@@ -90,8 +96,8 @@ __host__ __device__ constexpr int bi_ndots(int PH) {
 }
 
 template <int PH>
-__device__ void bi_finalize(const BiArgs &a, const double *d) {
-  BiScalars *S = a.S;
+__device__ __noinline__ void bi_finalize(const BiArgs &a, BiScalars *S, const double *d,
+                                         bool writer = true) {
   const double btol = S->breakdown_tol;
   if (PH == BP_BNORM) {
     S->bnorm = __dsqrt_rn(d[0]);
@@ -104,7 +110,7 @@ __device__ void bi_finalize(const BiArgs &a, const double *d) {
     // record entry 0 and decide the initial status (solvers.py:508-579)
     S->rnorm = __dsqrt_rn(d[0]);
     S->rtnorm = __dsqrt_rn(d[1]);
-    bi_record(a);
+    bi_record(a, S, writer);
     S->rho = S->dual_rho;
     S->beta = 0.0;
     bool conv = S->rnorm <= __dmul_rn(S->tol, S->bnorm) &&
@@ -125,7 +131,7 @@ __device__ void bi_finalize(const BiArgs &a, const double *d) {
     S->rnorm = __dsqrt_rn(d[0]);
     S->rtnorm = __dsqrt_rn(d[1]);
     S->rho_new = d[2];
-    bi_record(a);
+    bi_record(a, S, writer);
     S->itn += 1;
     S->xr_done = 1;
     // capture block (solvers.py:617-622): record alpha/beta, push attempt
@@ -133,8 +139,10 @@ __device__ void bi_finalize(const BiArgs &a, const double *d) {
     S->push_ok = 0;
     S->cap_now = 0;
     if (S->capture) {
-      a.alphas[S->nalpha] = S->alpha;
-      a.betas[S->nalpha] = S->beta;
+      if (writer) {
+        a.alphas[S->nalpha] = S->alpha;
+        a.betas[S->nalpha] = S->beta;
+      }
       S->nalpha += 1;
       if (S->rnorm == 0.0) S->capture = 0;
       else S->cap_now = 1;
@@ -158,7 +166,7 @@ __device__ void bi_finalize(const BiArgs &a, const double *d) {
     if (fabs(sigma) <= __dmul_rn(btol, S->rtnorm)) {
       S->capture = 0;
     } else {
-      a.rhos[S->npush] = S->rnorm;
+      if (writer) a.rhos[S->npush] = S->rnorm;
       S->npush += 1;
       S->push_ok = 1;
     }
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(1024) k_bphase(const BiArgs *__restrict__ pa) 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    bi_finalize<PH>(a, dfin);
+    bi_finalize<PH>(a, a.S, dfin);
     a.counters[32 + PH] = 0;
   }
 }
@@ -381,6 +389,230 @@ static int bi_proj_dot(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   KRB_DISPATCH_E(canon_E(h.n), (k_bproj_dot<kE, kDual><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// persistent driver for n <= 606208 (the graph's conditional-node loop costs
+// ~16 us per iteration at this size): one cooperative kernel runs iterations
+// until a cycle is complete (emit) or the solve stops; phases separated by
+// grid barriers, every CTA runs the canonical final stages and the scalar
+// logic on its own shared copy of the scalar block (identical inputs, order
+// -> identical scalars), CTA 0 writes history, rings' scalars and the block.
+// ---------------------------------------------------------------------------
+template <int ND>
+__device__ __forceinline__ void bi_local_finals(const double *pb, int64_t nb, double *dfin) {
+  const int warp = threadIdx.x >> 5;
+  if (warp < ND) {
+    double v = warp_final_volatile(pb + warp * nb, nb);
+    if ((threadIdx.x & 31) == 0) dfin[warp] = v;
+  }
+  __syncthreads();
+}
+
+template <int ND>
+__device__ __forceinline__ void bi_block_partials(double *acc, double (*red)[32],
+                                                  double *pb, int64_t nb, int64_t blk) {
+  double bp = block_tree_multi<ND>(acc, red);
+  const int warp = threadIdx.x >> 5;
+  if (warp < ND && (threadIdx.x & 31) == 0) pb[warp * nb + blk] = bp;
+}
+
+template <bool kSell>
+__device__ __forceinline__ double bi_row(int64_t i, const krb_matrix &M, const double *x) {
+  return spmv_row<kSell, false>(i, M, x);
+}
+
+template <int kE, bool kSell>
+__global__ void __launch_bounds__(1024) k_bpersist(const BiArgs *__restrict__ pa) {
+  __shared__ double zeta[512], zetat[512];
+  __shared__ double red[kTdotCG][32];
+  __shared__ double dfin[3];
+  __shared__ BiScalars L;
+  cg::grid_group grid = cg::this_grid();
+  const BiArgs &a = *pa;
+  const int64_t G = gridDim.x, me = blockIdx.x;
+  const int64_t n = a.n, nb = a.nb, ld = a.ld;
+  const int k = a.k;
+  const int64_t ncg = (k + kTdotCG - 1) / kTdotCG;
+  const bool writer = me == 0;
+  const krb_matrix A = a.A, AT = a.AT;
+  const bool tsell = AT.format == 2;
+  if (threadIdx.x == 0) L = *a.S;
+  __syncthreads();
+  double *pb[2] = {a.part, a.part2};
+  int cur = 0;
+  for (;;) {
+    if (L.status != KRB_RUNNING) break;
+    // ---- P: p = r + beta p ; pt = rt + conj(beta) pt   (solvers.py:589-590)
+    if (threadIdx.x == 0) {
+      L.bodies += 1;
+      L.xr_done = 0;
+    }
+    const double beta = L.beta;
+    for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x) {
+      a.p[i] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[i]));
+      a.pt[i] = __dadd_rn(a.rt[i], __dmul_rn(beta, a.pt[i]));
+    }
+    grid.sync();
+    // ---- M: q = A p, qt = A^T pt
+    for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x) {
+      a.q[(kSell && A.perm) ? A.perm[i] : i] = bi_row<kSell>(i, A, a.p);
+      const double qt = tsell ? bi_row<true>(i, AT, a.pt) : bi_row<false>(i, AT, a.pt);
+      a.qt[(tsell && AT.perm) ? AT.perm[i] : i] = qt;
+    }
+    grid.sync();
+    // ---- Z: zeta = Chat^T q, zetat = Ccheck^T qt
+    if (k > 0) {
+      for (int64_t u = me; u < 2 * nb * ncg; u += G) {
+        const bool dual = u >= nb * ncg;
+        const int64_t v = dual ? u - nb * ncg : u;
+        tdot_unit<kE, false>(n, nb, k, dual ? a.Ccheck : a.Chat, ld, dual ? a.qt : a.q,
+                             pb[cur] + (dual ? (int64_t)k * nb : 0), v % nb,
+                             (int)(v / nb) * kTdotCG, red);
+      }
+      grid.sync();
+      tdot_finals<false>(nb, k, pb[cur], zeta);
+      tdot_finals<false>(nb, k, pb[cur] + (int64_t)k * nb, zetat);
+      __syncthreads();
+      cur ^= 1;
+    }
+    // ---- Q: q -= C zeta, qt -= Ct zetat ; (pt,q), (pt,pt), (q,q)
+    for (int64_t blk = me; blk < nb; blk += G) {
+      const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+      double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < kE; ++e) {
+        const int64_t i = base + (int64_t)kLanes * e;
+        if (i >= n) continue;
+        double qi = a.q[i], qti = a.qt[i];
+        if (k > 0) {
+          double c1 = 0.0, c2 = 0.0;
+          for (int j = 0; j < k; ++j) {
+            c1 = __fma_rn(__ldg(a.C + (int64_t)j * ld + i), zeta[j], c1);
+            c2 = __fma_rn(__ldg(a.Ct + (int64_t)j * ld + i), zetat[j], c2);
+          }
+          qi = __dsub_rn(qi, c1);     // solvers.py:595
+          qti = __dsub_rn(qti, c2);   // solvers.py:597
+          a.q[i] = qi;
+          a.qt[i] = qti;
+        }
+        const double pti = a.pt[i];
+        acc[0] = __fma_rn(pti, qi, acc[0]);
+        acc[1] = __fma_rn(pti, pti, acc[1]);
+        acc[2] = __fma_rn(qi, qi, acc[2]);
+      }
+      bi_block_partials<3>(acc, red, pb[cur], nb, blk);
+    }
+    grid.sync();
+    bi_local_finals<3>(pb[cur], nb, dfin);
+    cur ^= 1;
+    if (threadIdx.x == 0) bi_finalize<BP_PROJ>(a, &L, dfin, writer);
+    __syncthreads();
+    if (L.status == KRB_RUNNING) {
+      // ---- X: x, xt, r, rt ; (r,r), (rt,rt), (rt,r)   (solvers.py:603-609)
+      const double alpha = L.alpha;
+      for (int64_t blk = me; blk < nb; blk += G) {
+        const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int64_t i = base + (int64_t)kLanes * e;
+          if (i >= n) continue;
+          a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));
+          a.xt[i] = __dadd_rn(a.xt[i], __dmul_rn(alpha, a.pt[i]));
+          const double ri = __dsub_rn(a.r[i], __dmul_rn(alpha, a.q[i]));
+          const double rti = __dsub_rn(a.rt[i], __dmul_rn(alpha, a.qt[i]));
+          a.r[i] = ri;
+          a.rt[i] = rti;
+          acc[0] = __fma_rn(ri, ri, acc[0]);
+          acc[1] = __fma_rn(rti, rti, acc[1]);
+          acc[2] = __fma_rn(rti, ri, acc[2]);
+        }
+        bi_block_partials<3>(acc, red, pb[cur], nb, blk);
+      }
+      if (writer)   // zc += alpha zeta ; ztc += conj(alpha) zetat   (:605-607)
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+          a.zc[j] = __dadd_rn(a.zc[j], __dmul_rn(alpha, zeta[j]));
+          a.ztc[j] = __dadd_rn(a.ztc[j], __dmul_rn(alpha, zetat[j]));
+        }
+      grid.sync();
+      bi_local_finals<3>(pb[cur], nb, dfin);
+      cur ^= 1;
+      if (threadIdx.x == 0) bi_finalize<BP_XR>(a, &L, dfin, writer);
+      __syncthreads();
+      // ---- capture: v = r / ||r|| into the ring ; sigma = (v, rt)   (:568-569)
+      if (L.cap_now) {
+        const double rn = L.rnorm;
+        double *vcol = a.V + L.ncols * a.ring_ld;
+        for (int64_t blk = me; blk < nb; blk += G) {
+          const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+          double acc[1] = {0.0};
+#pragma unroll
+          for (int e = 0; e < kE; ++e) {
+            const int64_t i = base + (int64_t)kLanes * e;
+            if (i >= n) continue;
+            const double v = __ddiv_rn(a.r[i], rn);
+            vcol[i] = v;
+            acc[0] = __fma_rn(v, a.rt[i], acc[0]);
+          }
+          bi_block_partials<1>(acc, red, pb[cur], nb, blk);
+        }
+        grid.sync();
+        bi_local_finals<1>(pb[cur], nb, dfin);
+        cur ^= 1;
+        if (threadIdx.x == 0) bi_finalize<BP_CAP1>(a, &L, dfin, writer);
+        __syncthreads();
+      }
+      if (L.push_ok) {   // vt = rt / sigma
+        const double sg = L.sigma;
+        double *vt = a.Vt + L.ncols * a.ring_ld;
+        for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x)
+          vt[i] = __ddiv_rn(a.rt[i], sg);
+      }
+    }
+    // loop control (the graph's CAP2 bookkeeping)
+    if (threadIdx.x == 0) {
+      if (L.push_ok) L.ncols += 1;
+      L.push_ok = 0;
+      L.cap_now = 0;
+      if (!L.xr_done) L.emit = 0;
+    }
+    __syncthreads();
+    if (L.status != KRB_RUNNING || L.emit) break;
+  }
+  if (writer && threadIdx.x == 0) *a.S = L;
+}
+
+template <int kE, bool kSell>
+static int bpersist_launch(const BiArgs *d, cudaStream_t st) {
+  static int grid = 0;
+  if (grid == 0) {
+    int per_sm = 0;
+    KRB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_bpersist<kE, kSell>, 1024, 0));
+    int dev = 0, sms = kNumSMs;
+    KRB_CHECK_CUDA(cudaGetDevice(&dev));
+    KRB_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  void *args[] = {(void *)&d};
+  KRB_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_bpersist<kE, kSell>,
+                                             dim3(grid), dim3(1024), args, 0, st));
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+static int bi_persistent(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
+  if (h.n == 0) return KRB_OK;
+  const bool sell = h.A.format == 2;
+  switch (canon_E(h.n)) {
+    case 1: return sell ? bpersist_launch<1, true>(d, st) : bpersist_launch<1, false>(d, st);
+    case 2: return sell ? bpersist_launch<2, true>(d, st) : bpersist_launch<2, false>(d, st);
+    default:
+      set_error("persistent rbicg driver supports n <= %d", 2 * kLanes * kTargetBlocks);
+      return KRB_EINVAL;
+  }
 }
 
 static int bi_iteration(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
@@ -550,7 +782,8 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
     return KRB_ENOMEM;
   }
 fill:
-  rc = ctx_reserve_part(ctx, (size_t)((k > 3 ? 2 * k : 3) * nb) + 64);
+  const size_t part_one = (size_t)((2 * k + 3) * nb) + 64;
+  rc = ctx_reserve_part(ctx, 2 * part_one);
   if (!rc) rc = ctx_reserve_counters(ctx, st);
   if (rc) {
     bi_free(H);
@@ -580,6 +813,7 @@ fill:
   h.alphas = H->scal + (max_itn + ring_cols + 2);
   h.betas = H->scal + 2 * (max_itn + ring_cols + 2);
   h.part = ctx->part;
+  h.part2 = ctx->part + part_one;
   h.counters = ctx->counters;
   h.S = H->S;
   h.hist_r = H->hist;
@@ -750,6 +984,8 @@ int krb_rbicg_run(krb_rbicg *H, int64_t *h_state, void *stream) {
                                    cudaMemcpyHostToDevice, st));
     if (H->use_graph == 1) {
       KRB_CHECK_CUDA(cudaGraphLaunch(H->exec, st));
+    } else if (H->use_graph == 2) {
+      KRB_TRY(bi_persistent(H->h, H->d_nc, st));
     } else {
       for (int64_t it = 0; it <= H->max_itn; ++it) {
         KRB_TRY(bi_iteration(H->h, H->d_nc, st));

@@ -496,7 +496,8 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
               ctypes.byref(view) if view is not None else None,
               int(cfg.s), int(cfg.max_itn), stream_ptr())
     try:
-        graph = min(_graph_mode() if _graph_mode() is not None else 1, 1)
+        # 2: persistent kernel per cycle (small n), 1: graph, 0: host loop
+        graph = max(0, min(_auto_mode(n), 2))
         dual = (ctypes.c_double * 3)()
         n_rmv = 0
         for attempt in range(4):

@@ -210,3 +210,32 @@ def test_sequence_policy_matches_oracle(P, canon, cfg, policy):
     assert r_g.recycling.aux_matvecs == r_o.recycling.aux_matvecs
     assert r_g.baseline.total_matvecs == r_o.baseline.total_matvecs
     assert abs(r_g.savings - r_o.savings) < 1e-12
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_rbicg_drivers_bitwise(P, canon, cfg, monkeypatch):
+    """persistent kernel (per cycle), CUDA graph and host loop give the same
+    bits: histories, cycles (ring columns) and solutions, with a space."""
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence(cfg, small=True)
+    A = seq.matrix(1)
+    S = random_space_arrays(A, 6, seed=3, ops=canon)
+    Sg = P.RecycleSpace(**{f: getattr(S, f) for f in FIELDS})
+    b = seq.rhs(1, 0)
+    cfg_ = P.SolverConfig(tol=1e-9, max_itn=300, s=10, seed=5)
+    out = {}
+    for mode in ("2", "1", "0"):
+        monkeypatch.setenv("KRB_GRAPH_MODE", mode)
+        out[mode] = P.rbicg_solve(P.SparseMatrix.from_csr(A), b, b_dual=np.ones(A.n),
+                                  recycle=Sg, config=cfg_)
+    ref = out["2"]
+    assert len(ref[3]) >= 2
+    for mode in ("1", "0"):
+        x, xt, h, cyc = out[mode]
+        assert h.resid == ref[2].resid and h.resid_dual == ref[2].resid_dual
+        assert h.matvecs == ref[2].matvecs and h.status == ref[2].status
+        assert np.array_equal(x, ref[0]) and np.array_equal(xt, ref[1])
+        assert len(cyc) == len(ref[3])
+        for c1, c2 in zip(cyc, ref[3]):
+            assert c1.first_index == c2.first_index
+            assert np.array_equal(c1.V, c2.V) and np.array_equal(c1.Vt, c2.Vt)

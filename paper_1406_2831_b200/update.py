@@ -36,29 +36,39 @@ def colsq(X_dev):
 
 def select_pencil_columns(theta, VR, VL, k, real_pencil, eligible=None):
     """k smallest-|theta| eigenvectors with conjugate pairs split into real
-    and imaginary parts (recycling.py:231-273); host-side on m x m data."""
+    and imaginary parts (recycling.py:231-273); host-side on m x m data.
+    Same selection as the reference's loop (oracle/krylov.py restates it
+    verbatim): the conjugate mate is the first available eigenvalue, in
+    ranked order, at the smallest |theta_j - conj(theta)| -- found here with
+    one vectorised pass, then re-decided exactly (Python abs, strict <, in
+    ranked order) among the candidates within 1e-9 of that minimum."""
     ok = np.isfinite(theta)
     if eligible is not None:
         ok = ok & eligible
-    ranked = [i for i in np.argsort(np.abs(np.where(ok, theta, np.inf))) if ok[i]]
-    taken = set()
+    ranked = np.array([i for i in np.argsort(np.abs(np.where(ok, theta, np.inf))) if ok[i]],
+                      dtype=np.int64)
+    avail = np.ones(ranked.size, dtype=bool)
     right, left = [], []
-    for idx in ranked:
-        if idx in taken:
+    for p in range(ranked.size):
+        if not avail[p]:
             continue
-        taken.add(idx)
+        avail[p] = False
+        idx = ranked[p]
         th = theta[idx]
         zr, zl = VR[:, idx], VL[:, idx]
         if real_pencil and abs(th.imag) > 1e-12 * (1.0 + abs(th)):
-            mate, gap = None, np.inf
-            for j in ranked:
-                if j in taken:
-                    continue
-                d = abs(theta[j] - np.conj(th))
-                if d < gap:
-                    mate, gap = j, d
-            if mate is not None:
-                taken.add(mate)
+            cand = np.nonzero(avail)[0]
+            if cand.size:
+                ct = np.conj(th)
+                dn = np.abs(theta[ranked[cand]] - ct)
+                close = cand[dn <= dn.min() * (1.0 + 1e-9)]
+                mate, gap = None, np.inf
+                for q in close:
+                    d = abs(theta[ranked[q]] - ct)
+                    if d < gap:
+                        mate, gap = q, d
+                if mate is not None:
+                    avail[mate] = False
             right += [zr.real, zr.imag]
             left += [zl.real, zl.imag]
         else:

@@ -71,3 +71,35 @@ def test_policy_canon_close_to_reference(golden, canon, tag, name, policy):
         assert h.status == str(golden[p + f"rec{j}_status"])
         assert h.final_true_resid <= 1.1 * make_sequence(name, small=True).tol or \
             h.status != "converged"
+
+
+def test_select_pencil_columns_matches_reference_loop():
+    """the vectorised mate search picks exactly what the reference's loop
+    (restated in oracle/krylov.py) picks, on random spectra with conjugate
+    pairs, ties and near-ties"""
+    import numpy as np
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import update as U
+    r = np.random.default_rng(0)
+    for trial in range(300):
+        m = int(r.integers(1, 60))
+        re = r.standard_normal(m)
+        im = r.standard_normal(m) * (r.random(m) < 0.5)
+        if trial % 3 == 0:          # exact conjugate pairs and duplicates
+            h = m // 2
+            re[h:2 * h], im[h:2 * h] = re[:h], -im[:h]
+        if trial % 5 == 0:
+            re = np.round(re, 1)
+            im = np.round(im, 1)
+        theta = re + 1j * im
+        if trial % 7 == 0:
+            theta[r.integers(0, m)] = np.inf
+        VR = r.standard_normal((m, m)) + 1j * r.standard_normal((m, m))
+        VL = r.standard_normal((m, m)) + 1j * r.standard_normal((m, m))
+        elig = (r.random(m) < 0.8) if trial % 2 else None
+        k = int(r.integers(1, m + 1))
+        a = U.select_pencil_columns(theta, VR, VL, k, True, elig)
+        b = O.select_pencil_columns(theta, VR, VL, k, True, elig)
+        assert (a[0] is None) == (b[0] is None)
+        if a[0] is not None:
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])

@@ -100,7 +100,8 @@ class _Staging:
 
 _STAGING = _Staging()
 _POOL = None
-_PAR_BYTES = 8 << 20     # host copies above this size are split across threads
+_PAR_BYTES = 1 << 20     # host copies above this size are split across threads
+_CHUNK = 8 << 20         # H2D pipeline chunk (two pinned buffers alternate)
 
 
 def _host_copy(dst: np.ndarray, src: np.ndarray):
@@ -128,17 +129,38 @@ _TDT = {np.dtype(np.float64): "float64", np.dtype(np.int64): "int64",
 
 
 def to_device(a: np.ndarray, dtype=np.float64):
-    """Host numpy -> device tensor through reusable pinned staging."""
+    """Host numpy -> device tensor through reusable pinned staging, in
+    chunks: the (multi-threaded) host copy of chunk i+1 into one pinned
+    buffer overlaps the DMA of chunk i out of the other."""
     t = torch()
     a = np.ascontiguousarray(a, dtype=dtype)
     if a.nbytes < (1 << 16):
         return t.from_numpy(a).to("cuda")
-    i, buf = _STAGING.get(a.nbytes)
-    host = buf[:a.nbytes].numpy()
-    _host_copy(host, a.reshape(-1).view(np.uint8))
+    ht = t.from_numpy(a)
+    if ht.is_pinned():
+        # caller-owned page-locked memory: one DMA, no staging copy
+        return ht.to("cuda", non_blocking=True)
     out = t.empty(a.shape, dtype=getattr(t, _TDT[a.dtype]), device="cuda")
-    out.view(-1).view(t.uint8).copy_(buf[:a.nbytes], non_blocking=True)
-    _STAGING.mark(i)
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(t.uint8)
+    n = a.nbytes
+    for o in range(0, n, _CHUNK):
+        m = min(_CHUNK, n - o)
+        i, buf = _STAGING.get(m)          # waits for this buffer's previous DMA
+        _host_copy(buf[:m].numpy(), src[o:o + m])
+        dst[o:o + m].copy_(buf[:m], non_blocking=True)
+        _STAGING.mark(i)
+    return out
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """A page-locked host copy of ``a`` (numpy view of a pinned torch
+    buffer): inputs kept in pinned memory upload by DMA alone."""
+    t = torch()
+    a = np.ascontiguousarray(a)
+    buf = t.empty(max(a.nbytes, 1), dtype=t.uint8, pin_memory=True)
+    out = buf.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+    out[...] = a
     return out
 
 

@@ -712,9 +712,18 @@ static bool persist2_eligible(const IterArgs &h) {
   return h.A.perm == nullptr && h.k <= kV2MaxK;
 }
 
+bool cluster_eligible(const IterArgs &h);
+int cluster_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
+
 int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.n == 0) return KRB_OK;
   const bool sell = h.A.format == 2;
+  // tiny systems: one thread-block cluster, everything on chip (cluster.cu);
+  // KRB_EINVAL = clusters of this size unavailable -> grid-wide kernel
+  if (cluster_eligible(h)) {
+    const int rc = cluster_launch(h, d, st);
+    if (rc != KRB_EINVAL) return rc;
+  }
   // fused v2 unless the rows are sigma-permuted (KRB_PERSIST=1 forces v1)
   const char *ev = getenv("KRB_PERSIST");
   const bool v2 = persist2_eligible(h) && !(ev && atoi(ev) == 1);

@@ -55,6 +55,7 @@ struct BiScalars {
   int32_t push_ok;
   int32_t emit;         // pause requested: cycle complete
   int32_t xr_done;
+  int32_t pbuf;         // persistent k = 0 path: p / pt live in (p2, pt2) when 1
 };
 
 struct BiArgs {
@@ -65,6 +66,7 @@ struct BiArgs {
   cudaGraphConditionalHandle cond;
   const double *C, *Chat, *Ct, *Ccheck;
   double *x, *xt, *r, *rt, *p, *pt, *q, *qt, *b, *bt;
+  double *p2, *pt2;        // double buffers of the fused persistent k = 0 path
   double *zeta, *zetat, *zc, *ztc;
   double *V, *Vt;          // capture rings (ring_ld stride per column)
   double *rhos, *alphas, *betas;
@@ -438,6 +440,9 @@ __global__ void __launch_bounds__(1024) k_bpersist(const BiArgs *__restrict__ pa
   const bool writer = me == 0;
   const krb_matrix A = a.A, AT = a.AT;
   const bool tsell = AT.format == 2;
+  // owner-computes fusion needs unpermuted rows of A, k = 0 and every
+  // canonical block owned by one CTA (E <= 2, nb <= 2 G)
+  const bool fused = k == 0 && A.perm == nullptr && nb <= 2 * G;
   if (threadIdx.x == 0) L = *a.S;
   __syncthreads();
   double *pb[2] = {a.part, a.part2};
@@ -450,64 +455,103 @@ __global__ void __launch_bounds__(1024) k_bpersist(const BiArgs *__restrict__ pa
       L.xr_done = 0;
     }
     const double beta = L.beta;
-    for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x) {
-      a.p[i] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[i]));
-      a.pt[i] = __dadd_rn(a.rt[i], __dmul_rn(beta, a.pt[i]));
-    }
-    grid.sync();
-    // ---- M: q = A p, qt = A^T pt
-    for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x) {
-      a.q[(kSell && A.perm) ? A.perm[i] : i] = bi_row<kSell>(i, A, a.p);
-      const double qt = tsell ? bi_row<true>(i, AT, a.pt) : bi_row<false>(i, AT, a.pt);
-      a.qt[(tsell && AT.perm) ? AT.perm[i] : i] = qt;
-    }
-    grid.sync();
-    // ---- Z: zeta = Chat^T q, zetat = Ccheck^T qt
-    if (k > 0) {
-      for (int64_t u = me; u < 2 * nb * ncg; u += G) {
-        const bool dual = u >= nb * ncg;
-        const int64_t v = dual ? u - nb * ncg : u;
-        tdot_unit<kE, false>(n, nb, k, dual ? a.Ccheck : a.Chat, ld, dual ? a.qt : a.q,
-                             pb[cur] + (dual ? (int64_t)k * nb : 0), v % nb,
-                             (int)(v / nb) * kTdotCG, red);
+    double *pcur = a.p, *ptcur = a.pt;
+    if (fused) {
+      // k = 0, unpermuted rows: p, pt recomputed on the fly for every
+      // gathered column (owners write the new ones into the other buffer),
+      // both SpMVs and Q's dots from registers -- P, M and Q in one phase
+      const double *po = L.pbuf ? a.p2 : a.p, *pto = L.pbuf ? a.pt2 : a.pt;
+      double *pn = L.pbuf ? a.p : a.p2, *ptn = L.pbuf ? a.pt : a.pt2;
+      pcur = pn;
+      ptcur = ptn;
+      const double *__restrict__ r_ = a.r;
+      const double *__restrict__ rt_ = a.rt;
+      auto pf = [=](int c) { return __dadd_rn(r_[c], __dmul_rn(beta, po[c])); };
+      auto ptf = [=](int c) { return __dadd_rn(rt_[c], __dmul_rn(beta, pto[c])); };
+      for (int64_t blk = me; blk < nb; blk += G) {
+        const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int64_t i = base + (int64_t)kLanes * e;
+          if (i >= n) continue;
+          const double pv = pf((int)i), ptv = ptf((int)i);
+          pn[i] = pv;
+          ptn[i] = ptv;
+          const double qi = spmv_row_f<kSell>(i, A, pf);
+          a.q[i] = qi;
+          const double qt = tsell ? spmv_row_f<true>(i, AT, ptf) : spmv_row_f<false>(i, AT, ptf);
+          a.qt[(tsell && AT.perm) ? AT.perm[i] : i] = qt;
+          acc[0] = __fma_rn(ptv, qi, acc[0]);
+          acc[1] = __fma_rn(ptv, ptv, acc[1]);
+          acc[2] = __fma_rn(qi, qi, acc[2]);
+        }
+        bi_block_partials<3>(acc, red, pb[cur], nb, blk);
       }
       grid.sync();
-      tdot_finals<false>(nb, k, pb[cur], zeta);
-      tdot_finals<false>(nb, k, pb[cur] + (int64_t)k * nb, zetat);
-      __syncthreads();
-      cur ^= 1;
-    }
-    // ---- Q: q -= C zeta, qt -= Ct zetat ; (pt,q), (pt,pt), (q,q)
-    for (int64_t blk = me; blk < nb; blk += G) {
-      const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
-      double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int e = 0; e < kE; ++e) {
-        const int64_t i = base + (int64_t)kLanes * e;
-        if (i >= n) continue;
-        double qi = a.q[i], qti = a.qt[i];
-        if (k > 0) {
-          double c1 = 0.0, c2 = 0.0;
-          for (int j = 0; j < k; ++j) {
-            c1 = __fma_rn(__ldg(a.C + (int64_t)j * ld + i), zeta[j], c1);
-            c2 = __fma_rn(__ldg(a.Ct + (int64_t)j * ld + i), zetat[j], c2);
-          }
-          qi = __dsub_rn(qi, c1);     // solvers.py:595
-          qti = __dsub_rn(qti, c2);   // solvers.py:597
-          a.q[i] = qi;
-          a.qt[i] = qti;
-        }
-        const double pti = a.pt[i];
-        acc[0] = __fma_rn(pti, qi, acc[0]);
-        acc[1] = __fma_rn(pti, pti, acc[1]);
-        acc[2] = __fma_rn(qi, qi, acc[2]);
+    } else {
+      for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x) {
+        a.p[i] = __dadd_rn(a.r[i], __dmul_rn(beta, a.p[i]));
+        a.pt[i] = __dadd_rn(a.rt[i], __dmul_rn(beta, a.pt[i]));
       }
-      bi_block_partials<3>(acc, red, pb[cur], nb, blk);
+      grid.sync();
+      // ---- M: q = A p, qt = A^T pt
+      for (int64_t i = me * blockDim.x + threadIdx.x; i < n; i += G * blockDim.x) {
+        a.q[(kSell && A.perm) ? A.perm[i] : i] = bi_row<kSell>(i, A, a.p);
+        const double qt = tsell ? bi_row<true>(i, AT, a.pt) : bi_row<false>(i, AT, a.pt);
+        a.qt[(tsell && AT.perm) ? AT.perm[i] : i] = qt;
+      }
+      grid.sync();
+      // ---- Z: zeta = Chat^T q, zetat = Ccheck^T qt
+      if (k > 0) {
+        for (int64_t u = me; u < 2 * nb * ncg; u += G) {
+          const bool dual = u >= nb * ncg;
+          const int64_t v = dual ? u - nb * ncg : u;
+          tdot_unit<kE, false>(n, nb, k, dual ? a.Ccheck : a.Chat, ld, dual ? a.qt : a.q,
+                               pb[cur] + (dual ? (int64_t)k * nb : 0), v % nb,
+                               (int)(v / nb) * kTdotCG, red);
+        }
+        grid.sync();
+        tdot_finals<false>(nb, k, pb[cur], zeta);
+        tdot_finals<false>(nb, k, pb[cur] + (int64_t)k * nb, zetat);
+        __syncthreads();
+        cur ^= 1;
+      }
+      // ---- Q: q -= C zeta, qt -= Ct zetat ; (pt,q), (pt,pt), (q,q)
+      for (int64_t blk = me; blk < nb; blk += G) {
+        const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+          const int64_t i = base + (int64_t)kLanes * e;
+          if (i >= n) continue;
+          double qi = a.q[i], qti = a.qt[i];
+          if (k > 0) {
+            double c1 = 0.0, c2 = 0.0;
+            for (int j = 0; j < k; ++j) {
+              c1 = __fma_rn(__ldg(a.C + (int64_t)j * ld + i), zeta[j], c1);
+              c2 = __fma_rn(__ldg(a.Ct + (int64_t)j * ld + i), zetat[j], c2);
+            }
+            qi = __dsub_rn(qi, c1);     // solvers.py:595
+            qti = __dsub_rn(qti, c2);   // solvers.py:597
+            a.q[i] = qi;
+            a.qt[i] = qti;
+          }
+          const double pti = a.pt[i];
+          acc[0] = __fma_rn(pti, qi, acc[0]);
+          acc[1] = __fma_rn(pti, pti, acc[1]);
+          acc[2] = __fma_rn(qi, qi, acc[2]);
+        }
+        bi_block_partials<3>(acc, red, pb[cur], nb, blk);
+      }
+      grid.sync();
     }
-    grid.sync();
     bi_local_finals<3>(pb[cur], nb, dfin);
     cur ^= 1;
-    if (threadIdx.x == 0) bi_finalize<BP_PROJ>(a, &L, dfin, writer);
+    if (threadIdx.x == 0) {
+      bi_finalize<BP_PROJ>(a, &L, dfin, writer);
+      if (fused) L.pbuf ^= 1;
+    }
     __syncthreads();
     if (L.status == KRB_RUNNING) {
       // ---- X: x, xt, r, rt ; (r,r), (rt,rt), (rt,r)   (solvers.py:603-609)
@@ -519,8 +563,8 @@ __global__ void __launch_bounds__(1024) k_bpersist(const BiArgs *__restrict__ pa
         for (int e = 0; e < kE; ++e) {
           const int64_t i = base + (int64_t)kLanes * e;
           if (i >= n) continue;
-          a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));
-          a.xt[i] = __dadd_rn(a.xt[i], __dmul_rn(alpha, a.pt[i]));
+          a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, pcur[i]));
+          a.xt[i] = __dadd_rn(a.xt[i], __dmul_rn(alpha, ptcur[i]));
           const double ri = __dsub_rn(a.r[i], __dmul_rn(alpha, a.q[i]));
           const double rti = __dsub_rn(a.rt[i], __dmul_rn(alpha, a.qt[i]));
           a.r[i] = ri;
@@ -768,7 +812,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   if (reuse) goto fill;
   e = cudaMalloc(&H->d, sizeof(BiArgs));
   if (e == cudaSuccess) e = cudaMalloc(&H->d_nc, sizeof(BiArgs));
-  if (e == cudaSuccess) e = cudaMalloc(&H->bufs, sizeof(double) * 10 * (n > 0 ? n : 1));
+  if (e == cudaSuccess) e = cudaMalloc(&H->bufs, sizeof(double) * 12 * (n > 0 ? n : 1));
   if (e == cudaSuccess) e = cudaMalloc(&H->kb, sizeof(double) * 5 * (k > 0 ? k : 1));
   if (e == cudaSuccess) e = cudaMalloc(&H->scal, sizeof(double) * (3 * (max_itn + ring_cols + 2)));
   if (e == cudaSuccess) e = cudaMalloc(&H->ring, sizeof(double) * 2 * ring_cols * (n > 0 ? n : 1));
@@ -806,6 +850,7 @@ fill:
   double *B = H->bufs;
   h.x = B; h.xt = B + n; h.r = B + 2 * n; h.rt = B + 3 * n; h.p = B + 4 * n;
   h.pt = B + 5 * n; h.q = B + 6 * n; h.qt = B + 7 * n; h.b = B + 8 * n; h.bt = B + 9 * n;
+  h.p2 = B + 10 * n; h.pt2 = B + 11 * n;
   h.zeta = H->kb; h.zetat = H->kb + k; h.zc = H->kb + 2 * k; h.ztc = H->kb + 3 * k;
   h.V = H->ring;
   h.Vt = H->ring + ring_cols * n;

@@ -212,15 +212,18 @@ def test_sequence_policy_matches_oracle(P, canon, cfg, policy):
     assert abs(r_g.savings - r_o.savings) < 1e-12
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2"])
-def test_rbicg_drivers_bitwise(P, canon, cfg, monkeypatch):
-    """persistent kernel (per cycle), CUDA graph and host loop give the same
-    bits: histories, cycles (ring columns) and solutions, with a space."""
+@pytest.mark.parametrize("cfg,k", [("c1", 6), ("c2", 6), ("c2", 0), ("c4", 0)])
+def test_rbicg_drivers_bitwise(P, canon, cfg, k, monkeypatch):
+    """persistent kernel (per cycle; k = 0 takes the fused P+M+Q phase),
+    CUDA graph and host loop give the same bits: histories, cycles (ring
+    columns) and solutions."""
     from paper_1406_2831_b200.workloads import make_sequence
     seq = make_sequence(cfg, small=True)
     A = seq.matrix(1)
-    S = random_space_arrays(A, 6, seed=3, ops=canon)
-    Sg = P.RecycleSpace(**{f: getattr(S, f) for f in FIELDS})
+    Sg = None
+    if k:
+        S = random_space_arrays(A, k, seed=3, ops=canon)
+        Sg = P.RecycleSpace(**{f: getattr(S, f) for f in FIELDS})
     b = seq.rhs(1, 0)
     cfg_ = P.SolverConfig(tol=1e-9, max_itn=300, s=10, seed=5)
     out = {}

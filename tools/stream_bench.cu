@@ -181,7 +181,28 @@ __global__ void __launch_bounds__(1024, 1) vp(Mats M, int copies, int R, int64_t
   const int nown = blockIdx.x < nb ? (int)((nb - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   for (int rep = 0; rep < R; ++rep) {
     const double *A = M.m[rep % copies];
-    if (kMode == 0) {   // cp.async 3-stage
+    if (kMode == 4) {   // cp.async 3-stage, next pass's prologue issued before the barrier
+      const int T = nown * ncg;
+      const double *An = M.m[(rep + 1) % copies];
+      auto issue = [&](const double *Src, int t) {
+        int bi = t / ncg, g = t % ncg;
+        int64_t i = (blockIdx.x + (int64_t)bi * gridDim.x) * 1024 + threadIdx.x;
+        double *d = st + (size_t)(t % 3) * 8 * 1024 + threadIdx.x;
+        for (int c = 0; c < 8; ++c)
+          if (g * 8 + c < k) cp_async8(d + c * 1024, Src + (g * 8 + c) * n + i);
+      };
+      if (rep == 0) { for (int t = 0; t < 3; ++t) { if (t < T) issue(A, t); commit(); } }
+      for (int t = 0; t < T; ++t) {
+        wait_g<2>();
+        const double *s = st + (size_t)(t % 3) * 8 * 1024 + threadIdx.x;
+        int g = t % ncg;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) if (g * 8 + c < k) tot += s[c * 1024];
+        if (t + 3 < T) issue(A, t + 3);
+        commit();
+      }
+      for (int t = 0; t < 3; ++t) { if (t < T) issue(An, t); commit(); }
+    } else if (kMode == 0) {   // cp.async 3-stage
       const int T = nown * ncg;
       auto issue = [&](int t) {
         int bi = t / ncg, g = t % ncg;
@@ -296,7 +317,8 @@ int main(int argc, char **argv) {
   CK(cudaFuncSetAttribute(vp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 8 * 1024 * 8));
   Mats mats;
   for (int c = 0; c < copies; ++c) mats.m[c] = M[c];
-  for (int mode = 0; mode < 4; ++mode) {
+  CK(cudaFuncSetAttribute(vp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 8 * 1024 * 8));
+  for (int mode = 0; mode < 5; ++mode) {
     for (int R : {1, 50}) {
       int cp = copies;
       float best = 1e9;
@@ -304,7 +326,7 @@ int main(int argc, char **argv) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(sms);
         cfg.blockDim = dim3(1024);
-        cfg.dynamicSmemBytes = mode ? 0 : 3 * 8 * 1024 * 8;
+        cfg.dynamicSmemBytes = (mode == 0 || mode == 4) ? 3 * 8 * 1024 * 8 : 0;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeCooperative;
         at[0].val.cooperative = 1;
@@ -326,6 +348,7 @@ int main(int argc, char **argv) {
         if (mode == 1) CK(cudaLaunchKernelEx(&cfg, vp<1>, mats, cp, R, n, k, nb, out));
         else if (mode == 2) CK(cudaLaunchKernelEx(&cfg, vp<2>, mats, cp, R, n, k, nb, out));
         else if (mode == 3) CK(cudaLaunchKernelEx(&cfg, vp<3>, mats, cp, R, n, k, nb, out));
+        else if (mode == 4) CK(cudaLaunchKernelEx(&cfg, vp<4>, mats, cp, R, n, k, nb, out));
         else CK(cudaLaunchKernelEx(&cfg, vp<0>, mats, cp, R, n, k, nb, out));
         cudaEventRecord(e1);
         CK(cudaEventSynchronize(e1));

@@ -369,7 +369,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     // evict_last for the recycle blocks when C and Chat fit in about half of
     // the L2 (KRB_L2KEEP=0/1 overrides)
     const char *e = getenv("KRB_L2KEEP");
-    h.l2keep = e ? atoi(e) : (2.0 * 8.0 * (double)n * (double)k <= 64e6 ? 1 : 0);
+    h.l2keep = e ? atoi(e) : (2.0 * 8.0 * (double)n * (double)k <= 100e6 ? 1 : 0);
   }
   h.cond = hit ? G.cond : 0;
   IterArgs *d = reinterpret_cast<IterArgs *>(ctx->desc);

@@ -423,6 +423,8 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
   const bool writer = me == 0;
   const krb_matrix A = a.A;
   const uint64_t pol = l2_policy(a.l2keep);
+  // matrix entries: evict_first when the recycle blocks are kept (l2keep)
+  const uint64_t polm = a.l2keep ? l2_policy_first() : l2_policy(false);
   const double *__restrict__ Chat = a.Chat;
   const double *__restrict__ Cm = a.C;
   double *__restrict__ x = a.x;
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
             const double pv = pf((int)i);   // solvers.py:303
             pn[i] = pv;
             preg[bi][e] = pv;
-            const double qv = spmv_row_f<kSell>(i, A, pf);
+            const double qv = spmv_row_f<kSell, 4, true>(i, A, pf, polm);
             qn[i] = qv;
             qreg[bi][e] = qv;
           }
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
             s[i] = sv;
             sreg[bi][e] = sv;
             acc[0] = __fma_rn(sv, sv, acc[0]);
-            const double tv = spmv_row_f<kSell>(i, A, sf);
+            const double tv = spmv_row_f<kSell, 4, true>(i, A, sf, polm);
             tv_[i] = tv;
             treg[bi][e] = tv;
             if (k == 0) {   // D's dots, straight from registers

@@ -20,8 +20,9 @@ __device__ __forceinline__ double ldx(const double *p) {
 // kB with predicated tails, so a row of up to kB entries costs two dependent
 // memory round trips (indices, then gathers); the sum stays sequential in
 // CSR order.
-template <bool kSell, int kB = 4, class XF>
-__device__ __forceinline__ double spmv_row_f(int64_t i, const krb_matrix &A, XF xf) {
+template <bool kSell, int kB = 4, bool kHint = false, class XF>
+__device__ __forceinline__ double spmv_row_f(int64_t i, const krb_matrix &A, XF xf,
+                                            uint64_t pol = 0) {
   double sum = 0.0;
   const int32_t *__restrict__ cp;
   const double *__restrict__ vp;
@@ -45,8 +46,13 @@ __device__ __forceinline__ double spmv_row_f(int64_t i, const krb_matrix &A, XF 
 #pragma unroll
     for (int u = 0; u < kB; ++u) {
       const bool ok = j + u < len;
-      c[u] = ok ? __ldg(cp + (int64_t)stride * (j + u)) : 0;
-      v[u] = ok ? __ldg(vp + (int64_t)stride * (j + u)) : 0.0;
+      if (kHint) {   // matrix entries with an L2 policy (evict_first: streamed)
+        c[u] = ok ? ldg_pol_i32(cp + (int64_t)stride * (j + u), pol) : 0;
+        v[u] = ok ? ldg_pol(vp + (int64_t)stride * (j + u), pol) : 0.0;
+      } else {
+        c[u] = ok ? __ldg(cp + (int64_t)stride * (j + u)) : 0;
+        v[u] = ok ? __ldg(vp + (int64_t)stride * (j + u)) : 0.0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kB; ++u) xv[u] = j + u < len ? xf(c[u]) : 0.0;

@@ -366,8 +366,9 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format;
   h.use_cond = graph ? 1 : 0;
   {
-    // evict_last for the recycle blocks when C and Chat fit in about half of
-    // the L2 (KRB_L2KEEP=0/1 overrides)
+    // evict_last for the recycle blocks (and evict_first for the matrix
+    // entries in the fused kernel) when C and Chat fit in about 3/4 of the
+    // L2 (KRB_L2KEEP=0/1 overrides)
     const char *e = getenv("KRB_L2KEEP");
     h.l2keep = e ? atoi(e) : (2.0 * 8.0 * (double)n * (double)k <= 100e6 ? 1 : 0);
   }

@@ -170,7 +170,16 @@ typedef struct krb_solve_result {
   uint64_t t_start_ns;   /* device %globaltimer at setup                   */
   int64_t iterations_run;   /* loop-body executions (incl. no-op tail)     */
   int64_t kernel_launches;  /* libkrb kernels executed by this solve       */
+  int32_t driver;        /* loop driver that ran: KRB_DRIVER_*              */
 } krb_solve_result;
+
+/* krb_solve_result.driver */
+#define KRB_DRIVER_HOST_LOOP 0
+#define KRB_DRIVER_GRAPH 1
+#define KRB_DRIVER_PERSISTENT 2     /* grid-wide persistent, nine barriers   */
+#define KRB_DRIVER_FUSED 3          /* fused persistent (k_persist2)        */
+#define KRB_DRIVER_CLUSTER 4        /* single thread-block cluster          */
+#define KRB_DRIVER_BATCH_GRAPH 5    /* multi-rhs graph                      */
 
 /* rbicgstab_solve (solvers.py:245-361), bicgstab_solve when R == NULL or
  * R->k == 0 (solvers.py:156-242, identical arithmetic).  Synchronous: returns

@@ -54,7 +54,12 @@ class SolveResult(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("hist_len", c_i64),
                 ("matvecs", c_i64), ("rhs_norm", c_dbl),
                 ("final_true_resid", c_dbl), ("t_start_ns", c_u64),
-                ("iterations_run", c_i64), ("kernel_launches", c_i64)]
+                ("iterations_run", c_i64), ("kernel_launches", c_i64),
+                ("driver", ctypes.c_int32)]
+
+
+DRIVERS = {0: "host_loop", 1: "graph", 2: "persistent", 3: "fused", 4: "cluster",
+           5: "batch_graph"}
 
 
 # name -> (restype, argtypes); every symbol declared in include/krb.h

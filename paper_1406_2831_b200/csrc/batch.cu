@@ -671,6 +671,7 @@ int rbicgstab_batch(krb_context *ctx, const krb_matrix *A, int64_t nrhs,
     res[b].t_start_ns = hs[b].t_start;
     res[b].iterations_run = hs[b].bodies;
     res[b].kernel_launches = launch_counter() - l0;
+    res[b].driver = mode == 1 ? KRB_DRIVER_BATCH_GRAPH : KRB_DRIVER_HOST_LOOP;
   }
   return KRB_OK;
 }

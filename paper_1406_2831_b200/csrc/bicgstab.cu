@@ -168,7 +168,7 @@ static int launch_iteration(const IterArgs &h, const IterArgs *d, cudaStream_t s
   return KRB_OK;
 }
 
-int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st);
+int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int *driver);
 
 
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k) {
@@ -388,8 +388,9 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   KRB_TRY(solve_setup(ctx, A, d_b, d_x_init, R, cfg, h, d, ctx->w, ybuf, st));
 
   // ---- iterations (solvers.py:298-356) --------------------------------
+  int driver = mode == 1 ? KRB_DRIVER_GRAPH : KRB_DRIVER_HOST_LOOP;
   if (mode == 2) {
-    KRB_TRY(launch_persistent(h, d, st));
+    KRB_TRY(launch_persistent(h, d, st, &driver));
   } else if (graph) {
     KRB_CHECK_CUDA(cudaGraphLaunch(G.exec, st));
     per_body = G.kernels_per_body;
@@ -421,6 +422,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   res->iterations_run = mode == 2 ? hs.itn : hs.bodies;
   launch_counter() += hs.bodies * per_body;
   res->kernel_launches = launch_counter() - l0;
+  res->driver = driver;
   return KRB_OK;
 }
 

@@ -717,24 +717,30 @@ static bool persist2_eligible(const IterArgs &h) {
 bool cluster_eligible(const IterArgs &h);
 int cluster_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
 
-int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
+int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int *driver) {
+  *driver = KRB_DRIVER_PERSISTENT;
   if (h.n == 0) return KRB_OK;
   const bool sell = h.A.format == 2;
   // tiny systems: one thread-block cluster, everything on chip (cluster.cu);
   // KRB_EINVAL = clusters of this size unavailable -> grid-wide kernel
   if (cluster_eligible(h)) {
     const int rc = cluster_launch(h, d, st);
-    if (rc != KRB_EINVAL) return rc;
+    if (rc != KRB_EINVAL) {
+      *driver = KRB_DRIVER_CLUSTER;
+      return rc;
+    }
   }
   // fused v2 unless the rows are sigma-permuted (KRB_PERSIST=1 forces v1)
   const char *ev = getenv("KRB_PERSIST");
   const bool v2 = persist2_eligible(h) && !(ev && atoi(ev) == 1);
   if (v2) {
+    *driver = KRB_DRIVER_FUSED;
     switch (canon_E(h.n)) {
       case 1: return sell ? persist2_launch<1, true>(d, h.nb, st) : persist2_launch<1, false>(d, h.nb, st);
       case 2: return sell ? persist2_launch<2, true>(d, h.nb, st) : persist2_launch<2, false>(d, h.nb, st);
       default: break;
     }
+    *driver = KRB_DRIVER_PERSISTENT;
   }
   // small systems only (E <= 2, n <= 606208): larger ones run the graph
   switch (canon_E(h.n)) {

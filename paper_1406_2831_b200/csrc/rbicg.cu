@@ -1129,6 +1129,8 @@ int krb_rbicg_finish(krb_rbicg *H, double *d_x_out, double *d_xt_out,
   res->iterations_run = hs.bodies;
   if (H->use_graph == 1) launch_counter() += hs.bodies * H->per_body;
   res->kernel_launches = launch_counter() - H->l0;
+  res->driver = H->use_graph == 2 ? KRB_DRIVER_PERSISTENT
+                : (H->use_graph == 1 ? KRB_DRIVER_GRAPH : KRB_DRIVER_HOST_LOOP);
   h_counts[0] = hs.n_matvec;
   h_counts[1] = hs.n_rmatvec;
   *h_btnorm = hs.btnorm;

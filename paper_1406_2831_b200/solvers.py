@@ -257,7 +257,8 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     hist.final_true_resid = float(res.final_true_resid)
     LAST_SOLVE.clear()
     LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
-                      kernel_launches=int(res.kernel_launches))
+                      kernel_launches=int(res.kernel_launches),
+                      driver=_lib.DRIVERS.get(int(res.driver), str(res.driver)))
     if prof is not None:
         LAST_SOLVE["phase_stamps"] = prof.view(-1, 16)[:hist.iterations].cpu().numpy()
     return xo, hist

@@ -82,6 +82,13 @@ def test_persistent_bitwise_vs_oracle(pkg, canon, n, k, fmt):
                              ops=canon)
         xg, hg = S.solve_device(M, to_device(b), None, _space(pkg, Sp) if k else None, cfg,
                                 use_graph=2)
+        # the driver that actually ran: single cluster for tiny systems,
+        # the fused kernel up to k = 32, the nine-barrier kernel above
+        # (a 16-CTA cluster needs a GPC with 16 free SMs; without one the
+        # fused kernel runs instead)
+        want = {"cluster", "fused"} if (A.n <= 16384 and k <= 10) else \
+            ({"fused"} if k <= 32 else {"persistent"})
+        assert S.LAST_SOLVE["driver"] in want, (S.LAST_SOLVE["driver"], want)
         assert hg.status == ho.status
         assert hg.resid == ho.resid
         assert hg.matvecs == ho.matvecs
@@ -102,5 +109,6 @@ def test_persistent_sigma_rows_use_v1(pkg, canon):
     xo, ho = O.rbicgstab(A, b, recycle=Sp, config=O.Config(tol=1e-9, max_itn=60, seed=2),
                          ops=canon)
     xg, hg = S.solve_device(M, to_device(b), None, _space(pkg, Sp), cfg, use_graph=2)
+    assert S.LAST_SOLVE["driver"] == "persistent"
     assert (hg.status, hg.resid, hg.matvecs) == (ho.status, ho.resid, ho.matvecs)
     assert np.array_equal(xg.cpu().numpy(), xo)

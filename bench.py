@@ -414,6 +414,7 @@ def synthetic_pass(wl, dmats, drhs):
                 traffic = int(tj["bytes_per_launch"])
     return {
         "synthetic": {"iterations": its, "seconds": t_solve, "k_per_system": ks,
+                      "driver": S.LAST_SOLVE.get("driver"),
                       "iters_per_s": its / t_solve,
                       "us_per_iteration": round(1e6 * t_solve / max(its, 1), 2)},
         "iteration_roofline": {"bytes_per_iteration": B_it, "k": kmean,

@@ -95,8 +95,11 @@ def near_null_eligibility(theta, VR, W, AW, res_tol):
     thi = to_device(np.ascontiguousarray(th.imag))
     _lib.call("krb_ritz_combine", n, VR.shape[1], ptr(Yre), ptr(Yim), ptr(Are),
               ptr(Aim), n, ptr(thr), ptr(thi), stream_ptr())
-    rn = np.sqrt(colsq(Are).cpu().numpy() + colsq(Aim).cpu().numpy())
-    yn = np.sqrt(colsq(Yre).cpu().numpy() + colsq(Yim).cpu().numpy())
+    t = torch()
+    sq = t.cat([colsq(Are), colsq(Aim), colsq(Yre), colsq(Yim)]).cpu().numpy()  # one read
+    c = VR.shape[1]
+    rn = np.sqrt(sq[:c] + sq[c:2 * c])
+    yn = np.sqrt(sq[2 * c:3 * c] + sq[3 * c:])
     res = rn / np.maximum(yn, 1e-300)
     ab = np.abs(th)
     top = ab.max() if ab.size else 0.0
@@ -148,17 +151,17 @@ def update_recycle_space(A, cycles, previous, k: int, rank_tol: float = 1e-12,
     W, Wt = t.cat(bu, 0), t.cat(but, 0)
     AW, AhWt = t.cat(bc, 0), t.cat(bct, 0)
     # column scaling (recycling.py:333-340)
-    sw = colnorms(W).cpu().numpy()
+    nrm = t.cat([colnorms(W), colnorms(Wt)]).cpu().numpy()   # one read
+    sw, st = nrm[:W.shape[0]].copy(), nrm[W.shape[0]:].copy()
     sw[sw == 0] = 1.0
-    st = colnorms(Wt).cpu().numpy()
     st[st == 0] = 1.0
     swd, std_ = to_device(sw), to_device(st)
     colscale_div(W, swd)
     colscale_div(AW, swd)
     colscale_div(Wt, std_)
     colscale_div(AhWt, std_)
-    GA = gram(Wt, AW).cpu().numpy()
-    GI = gram(Wt, W).cpu().numpy()
+    G2 = t.stack([gram(Wt, AW), gram(Wt, W)]).cpu().numpy()   # one read
+    GA, GI = G2[0].copy(), G2[1].copy()
     import scipy.linalg as la
     theta, VL, VR = la.eig(GA, GI, left=True, right=True)
     eligible = None

@@ -716,6 +716,8 @@ static bool persist2_eligible(const IterArgs &h) {
 
 bool cluster_eligible(const IterArgs &h);
 int cluster_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
+bool persist3_eligible(const IterArgs &h);
+int persist3_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
 
 int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int *driver) {
   *driver = KRB_DRIVER_PERSISTENT;
@@ -729,6 +731,12 @@ int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int
       *driver = KRB_DRIVER_CLUSTER;
       return rc;
     }
+  }
+  // large n (canon_E >= 4): the fused kernel with block-owned global round
+  // trips (persist3.cu)
+  if (persist3_eligible(h)) {
+    *driver = KRB_DRIVER_FUSED;
+    return persist3_launch(h, d, st);
   }
   // fused v2 unless the rows are sigma-permuted (KRB_PERSIST=1 forces v1)
   const char *ev = getenv("KRB_PERSIST");

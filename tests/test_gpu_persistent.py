@@ -62,7 +62,10 @@ CASES = [
     (200_000, 32, 2),
     (200_000, 33, 2),      # k > 32: v1 kernel
     (400_000, 8, 2),       # E = 2
-    (606_208, 3, 1),       # largest persistent size, CSR
+    (606_208, 3, 1),       # largest E = 2 size, CSR
+    (700_001, 6, 2),       # E = 4: large-n fused kernel (persist3.cu)
+    (1_300_000, 0, 2),     # E = 8, k = 0
+    (1_300_000, 9, 1),     # E = 8, CSR
 ]
 
 

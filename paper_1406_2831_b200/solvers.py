@@ -244,9 +244,11 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
               ctypes.byref(c), ptr(xo), ptr(hr), ptr(hm), ptr(ht),
               ctypes.byref(res), stream_ptr())
     L = int(res.hist_len)
-    resid = hr[:L].cpu().numpy()
-    mvs = hm[:L].cpu().numpy()
-    stamps = ht[:L].cpu().numpy().astype(np.int64)
+    # one device->host read for the three history arrays (bit views)
+    t3 = torch().stack([hr[:L].view(torch().int64), hm[:L], ht[:L]]).cpu().numpy()
+    resid = t3[0].view(np.float64)
+    mvs = t3[1]
+    stamps = t3[2]
     hist = ConvergenceHistory(solver=label, rhs_norm=float(res.rhs_norm))
     base = (t_launch - t0)
     st0 = int(res.t_start_ns)

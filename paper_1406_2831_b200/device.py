@@ -135,7 +135,10 @@ def to_device(a: np.ndarray, dtype=np.float64):
     t = torch()
     a = np.ascontiguousarray(a, dtype=dtype)
     if a.nbytes < (1 << 16):
-        return t.from_numpy(a).to("cuda")
+        # small operands (Ritz coefficients, column scales): a pinned copy
+        # from torch's caching host allocator makes the upload asynchronous
+        # (a pageable copy would stall the host until the GPU queue drains)
+        return t.from_numpy(a).pin_memory().to("cuda", non_blocking=True)
     ht = t.from_numpy(a)
     if ht.is_pinned():
         # caller-owned page-locked memory: one DMA, no staging copy

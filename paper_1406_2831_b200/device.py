@@ -31,7 +31,10 @@ def require_cuda():
 
 
 def stream_ptr():
-    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+    """The current CUDA stream of the current device (raw handle; the direct
+    torch._C queries avoid ~20 us of Python per call)."""
+    C = torch()._C
+    return ctypes.c_void_p(C._cuda_getCurrentRawStream(C._cuda_getDevice()))
 
 
 def ptr(tensor):

@@ -333,7 +333,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   int64_t per_body = 0;
   const int64_t nb = canon_nblocks(n);
   const size_t part_one = (size_t)((k + 3) * nb) + 64;
-  KRB_TRY(ctx_reserve_part(ctx, 2 * part_one));
+  KRB_TRY(ctx_reserve_part(ctx, 2 * part_one + 16 * 160));   // + per-CTA flags (<= 160 CTAs)
   IterArgs h = {};
   h.A = *A;
   h.A.T = nullptr;
@@ -353,6 +353,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   double *ybuf = ctx->kbuf + 3 * ctx->vec_k;
   h.part = ctx->part;
   h.part2 = ctx->part + part_one;
+  h.flags = reinterpret_cast<unsigned int *>(ctx->part + 2 * part_one);
   h.counters = ctx->counters;
   h.S = ctx->S;
   h.hist_r = hist_r;

@@ -34,6 +34,7 @@ struct IterArgs {
   uint64_t *prof;         // optional per-phase %globaltimer stamps (16/iter)
   int64_t prof_cap;
   unsigned int *counters;
+  unsigned int *flags;    // per-CTA phase epochs, 128 B apart (persist0.cu)
   SolveScalars *S;
   double *hist_r;
   int64_t *hist_m;

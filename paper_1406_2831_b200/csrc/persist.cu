@@ -718,6 +718,8 @@ bool cluster_eligible(const IterArgs &h);
 int cluster_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
 bool persist3_eligible(const IterArgs &h);
 int persist3_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
+bool persist0_eligible(const IterArgs &h);
+int persist0_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
 
 int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int *driver) {
   *driver = KRB_DRIVER_PERSISTENT;
@@ -731,6 +733,12 @@ int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int
       *driver = KRB_DRIVER_CLUSTER;
       return rc;
     }
+  }
+  // k = 0, canon_E == 1: the fused kernel with the operator on chip
+  // (persist0.cu; KRB_PERSIST0=0 disables)
+  if (persist0_eligible(h)) {
+    *driver = KRB_DRIVER_FUSED;
+    return persist0_launch(h, d, st);
   }
   // large n (canon_E >= 4): the fused kernel with block-owned global round
   // trips (persist3.cu)

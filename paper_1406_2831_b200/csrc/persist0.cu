@@ -52,6 +52,10 @@ constexpr int kLoc = kOwn * kLanes;        // xs slots of the owned rows
 constexpr int kDynBytes = 220 * 1024;      // dynamic shared memory per CTA
 constexpr int kMaxXs = 65535;              // operand index is 16-bit
 constexpr int kRows = 3;                   // wred rows per owned block
+#ifndef KRB_P0_HU
+#define KRB_P0_HU 5
+#endif
+constexpr int kHU = KRB_P0_HU;             // halo elements in flight per thread
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -131,8 +135,21 @@ __device__ __forceinline__ void await_finals(const double *part, int nb, double 
   }
   __syncthreads();   // warp 0's acquire orders every warp's later reads
   if (warp < ND) {
-    const double v = warp_final_volatile(part + warp * nb, nb);
-    if (lane == 0) dfin[warp] = v;
+    // warp_final_volatile's order (lane L: 0.0 + P[L] + P[L + 32] + ...),
+    // all <= 10 loads per lane in flight, 32-bit indices (nb <= 320)
+    const double *P = part + warp * nb;
+    double v[10];
+#pragma unroll
+    for (int u = 0; u < 10; ++u) {
+      const int b = lane + 32 * u;
+      v[u] = b < nb ? __ldcg(P + b) : 0.0;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 10; ++u)
+      if (lane + 32 * u < nb) acc = __dadd_rn(acc, v[u]);
+    acc = warp_tree(acc);
+    if (lane == 0) dfin[warp] = acc;
   }
   __syncthreads();
 }
@@ -386,29 +403,32 @@ __global__ void __launch_bounds__(1024, 1)
       pp[bi] = __dadd_rn(rv, __dmul_rn(beta, wv));  // :303
     }
     if (on_chip) {
+      for (int h0 = 0; h0 < nh; h0 += kHU * kLanes) {
+        int c[kHU];
+        double rv[kHU], wv[kHU];
 #pragma unroll
-      for (int bi = 0; bi < kOwn; ++bi)
-        if (bi < nown) xs[bi * kLanes + tid] = pp[bi];
-      for (int h0 = 0; h0 < nh; h0 += 4 * kLanes) {
-        int c[4];
-        double rv[4], wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kHU; ++u) {
           const int hh = h0 + u * kLanes + tid;
           c[u] = hh < nh ? halo[hh] : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kHU; ++u) {
           rv[u] = c[u] >= 0 ? __ldcg(r + c[u]) : 0.0;
           wv[u] = c[u] >= 0 ? __ldcg(w + c[u]) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kHU; ++u)
           if (c[u] >= 0) xs[kLoc + h0 + u * kLanes + tid] = __dadd_rn(rv[u], __dmul_rn(beta, wv[u]));
       }
+      // own rows last: their loads share the halo's round trip
+#pragma unroll
+      for (int bi = 0; bi < kOwn; ++bi)
+        if (bi < nown) xs[bi * kLanes + tid] = pp[bi];
       __syncthreads();
+      KRB_STAMP(13);
 #pragma unroll
       for (int bi = 0; bi < kOwn; ++bi) qq[bi] = ok[bi] ? row_on_chip(rb[bi], len[bi]) : 0.0;
+      KRB_STAMP(14);
     } else {
 #pragma unroll
       for (int bi = 0; bi < kOwn; ++bi)
@@ -446,26 +466,26 @@ __global__ void __launch_bounds__(1024, 1)
       ss[bi] = __dsub_rn(rv, __dmul_rn(alpha, qq[bi]));  // :313
     }
     if (on_chip) {
+      for (int h0 = 0; h0 < nh; h0 += kHU * kLanes) {
+        int c[kHU];
+        double rv[kHU], qv[kHU];
 #pragma unroll
-      for (int bi = 0; bi < kOwn; ++bi)
-        if (bi < nown) xs[bi * kLanes + tid] = ss[bi];
-      for (int h0 = 0; h0 < nh; h0 += 4 * kLanes) {
-        int c[4];
-        double rv[4], qv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kHU; ++u) {
           const int hh = h0 + u * kLanes + tid;
           c[u] = hh < nh ? halo[hh] : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kHU; ++u) {
           rv[u] = c[u] >= 0 ? __ldcg(r + c[u]) : 0.0;
           qv[u] = c[u] >= 0 ? __ldcg(q + c[u]) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kHU; ++u)
           if (c[u] >= 0) xs[kLoc + h0 + u * kLanes + tid] = __dsub_rn(rv[u], __dmul_rn(alpha, qv[u]));
       }
+#pragma unroll
+      for (int bi = 0; bi < kOwn; ++bi)
+        if (bi < nown) xs[bi * kLanes + tid] = ss[bi];
       __syncthreads();
 #pragma unroll
       for (int bi = 0; bi < kOwn; ++bi) tt[bi] = ok[bi] ? row_on_chip(rb[bi], len[bi]) : 0.0;

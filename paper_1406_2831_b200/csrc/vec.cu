@@ -273,6 +273,168 @@ __global__ void __launch_bounds__(256, 2) k_gemm(int64_t n, int m, int nc,
   }
 }
 
+// Tiled variant (same sums, same order): a CTA streams tiles of T rows of
+// X (all m columns) into shared memory with TMA bulk copies (one 8T-byte
+// copy per column, one elected thread, completion on an mbarrier), double
+// buffered, so the next tile is in flight while the current one is
+// consumed; thread (row r, column group g) accumulates its kCT outputs from
+// the staged tile (conflict-free rows) and the broadcast Z.  X is read from
+// HBM exactly once.  Needs 16-byte aligned columns (X, ldx even); the
+// partial last tile goes through plain loads.
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_1d(double *dst, const double *src, unsigned bytes,
+                                       uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <int kCT>
+__device__ __forceinline__ void gemm_tile_rows(const double *xs, int T, int r, int g, int m,
+                                               int nc, int ncp, const double2 *dsm2,
+                                               double *out, int64_t ldo, int64_t i) {
+  const int c0 = g * kCT;
+  double acc[kCT];
+#pragma unroll
+  for (int t = 0; t < kCT; ++t) acc[t] = 0.0;
+  const double2 *zrow = dsm2 + (c0 >> 1);
+#pragma unroll 2
+  for (int j = 0; j < m; ++j) {
+    const double xv = xs[j * T + r];
+    const double2 *zr = zrow + j * (ncp >> 1);
+#pragma unroll
+    for (int t = 0; t < kCT / 2; ++t) {
+      const double2 z = zr[t];
+      acc[2 * t] = __fma_rn(xv, z.x, acc[2 * t]);
+      acc[2 * t + 1] = __fma_rn(xv, z.y, acc[2 * t + 1]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kCT; ++t)
+    if (c0 + t < nc) out[(int64_t)(c0 + t) * ldo + i] = acc[t];
+}
+
+template <int kCT>
+__global__ void __launch_bounds__(256, 2) k_gemm_t(int64_t n, int m, int nc, int lgT,
+                                                   const double *__restrict__ X, int64_t ldx,
+                                                   const double *__restrict__ Z,
+                                                   double *__restrict__ out, int64_t ldo) {
+  extern __shared__ double2 dsm2[];
+  __shared__ uint64_t bar[2];
+  double *dsm = reinterpret_cast<double *>(dsm2);
+  const int T = 1 << lgT;
+  const int ncp = ((nc + kCT - 1) / kCT) * kCT;
+  double *zs = dsm;                                   // m x ncp (16-byte multiple)
+  double *stage = dsm + (size_t)m * ncp;              // 2 x m x T
+  for (int idx = threadIdx.x; idx < m * ncp; idx += blockDim.x) {
+    const int j = idx / ncp, c = idx - j * ncp;
+    zs[idx] = c < nc ? Z[j * nc + c] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nfull = n >> lgT;
+  const int r = threadIdx.x & (T - 1), g = threadIdx.x >> lgT;   // row in tile, column group
+  const int ngroups = ncp / kCT;
+  const int per = m << lgT;
+  const unsigned tile_bytes = (unsigned)per * 8u;
+  auto issue = [&](int64_t t, int b) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[b], tile_bytes);
+    const double *src = X + (t << lgT);
+    double *dst = stage + (size_t)b * per;
+    for (int j = 0; j < m; ++j) tma_1d(dst + (j << lgT), src + (int64_t)j * ldx, (unsigned)T * 8u, &bar[b]);
+  };
+  int64_t tile = blockIdx.x;
+  unsigned ph = 0u;   // bit b: parity of buffer b's next completion
+  if (threadIdx.x == 0 && tile < nfull) issue(tile, 0);
+  int buf = 0;
+  for (; tile < nfull; tile += gridDim.x, buf ^= 1) {
+    if (threadIdx.x == 0 && tile + gridDim.x < nfull) issue(tile + gridDim.x, buf ^ 1);
+    mbar_wait(&bar[buf], (ph >> buf) & 1u);
+    ph ^= 1u << buf;
+    if (g < ngroups)
+      gemm_tile_rows<kCT>(stage + (size_t)buf * per, T, r, g, m, nc, ncp, dsm2, out, ldo,
+                          (tile << lgT) + r);
+    __syncthreads();   // every thread done with `buf` before it is refilled
+  }
+  // partial last tile: plain loads, by the CTA the tile loop would give it to
+  const int64_t rem = n - (nfull << lgT);
+  if (rem > 0 && blockIdx.x == (unsigned)(nfull % gridDim.x)) {
+    double *xs = stage;
+    for (int e = threadIdx.x; e < per; e += blockDim.x) {
+      const int j = e >> lgT, rr = e & (T - 1);
+      xs[e] = rr < rem ? X[(int64_t)j * ldx + (nfull << lgT) + rr] : 0.0;
+    }
+    __syncthreads();
+    if (g < ngroups && r < rem)
+      gemm_tile_rows<kCT>(xs, T, r, g, m, nc, ncp, dsm2, out, ldo, (nfull << lgT) + r);
+  }
+}
+
+template <int kCT>
+static bool gemm_tiled(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
+                       const double *d_Z, double *d_out, int64_t ldo, cudaStream_t st,
+                       int *rc) {
+  const int64_t ncp = ((nc + kCT - 1) / kCT) * kCT;
+  const int64_t groups = ncp / kCT;
+  int lgT = 0;
+  while ((groups << (lgT + 1)) <= 256) ++lgT;
+  if (lgT < 5) return false;   // T >= 32 rows (idle threads when groups does not divide 256)
+  if ((ldx & 1) || (reinterpret_cast<uintptr_t>(d_X) & 15)) return false;   // TMA alignment
+  const size_t smem = sizeof(double) * (size_t)(m * ncp + 2 * (m << lgT));
+  if (smem > 200 * 1024) return false;
+  *rc = KRB_OK;
+  static size_t attr_smem = 0;   // largest dynamic smem opted in so far
+  if (smem > attr_smem) {
+    if (cudaFuncSetAttribute(k_gemm_t<kCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024) != cudaSuccess) {
+      set_error("krb_gemm: cudaFuncSetAttribute failed");
+      *rc = KRB_ECUDA;
+      return true;
+    }
+    attr_smem = 200 * 1024;
+  }
+  // resident CTAs per SM: shared memory (227 KB) and registers (2 x 256 threads)
+  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  const int64_t ntiles = (n + (1 << lgT) - 1) >> lgT;
+  const int64_t cap = (int64_t)kNumSMs * per_sm;
+  const int grid = (int)(ntiles < cap ? ntiles : cap);
+  k_gemm_t<kCT><<<grid, 256, smem, st>>>(n, (int)m, (int)nc, lgT, d_X, ldx, d_Z, d_out, ldo);
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("krb_gemm: launch failed");
+    *rc = KRB_ECUDA;
+  }
+  return true;
+}
+
 // X[:, j] /= s[j]: column j on blockIdx.y (no per-element index division),
 // two elements per thread
 __global__ void __launch_bounds__(256) k_colscale_div(int64_t n, int k, double *X,
@@ -550,6 +712,15 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
   cudaStream_t st = as_stream(stream);
   if (n == 0 || nc == 0) return KRB_OK;
   const int64_t ncp = ((nc + kGemmCT2 - 1) / kGemmCT2) * kGemmCT2;
+  {
+    // tiled kernels (KRB_GEMM_TILED = 0 off, 8 / 12 / 24: columns per thread)
+    const char *e = getenv("KRB_GEMM_TILED");
+    const int mode = e ? atoi(e) : 12;
+    int rc = KRB_OK;
+    if (m > 0 && mode == 8 && gemm_tiled<8>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
+    if (m > 0 && mode == 12 && gemm_tiled<12>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
+    if (m > 0 && mode == 24 && gemm_tiled<24>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
+  }
   size_t smem = sizeof(double) * (m * ncp > 0 ? m * ncp : 2);
   KRB_REQUIRE(smem <= 200 * 1024, "krb_gemm: Z too large for shared memory");
   KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gemm,

@@ -435,17 +435,28 @@ static bool gemm_tiled(int64_t n, int64_t m, int64_t nc, const double *d_X, int6
   return true;
 }
 
-// X[:, j] /= s[j]: column j on blockIdx.y (no per-element index division),
-// two elements per thread
+// X[:, j] /= s[j]: column j on blockIdx.y (no per-element index division);
+// each thread divides four elements 256 apart, loads issued together
 __global__ void __launch_bounds__(256) k_colscale_div(int64_t n, int k, double *X,
                                                       int64_t ldx,
                                                       const double *__restrict__ s) {
   const int j = blockIdx.y;
   double *col = X + (int64_t)j * ldx;
   const double d = __ldg(s + j);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    col[i] = __ddiv_rn(col[i], d);
+  for (int64_t i0 = (int64_t)blockIdx.x * 1024 + threadIdx.x; i0 < n;
+       i0 += (int64_t)gridDim.x * 1024) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + 256 * q;
+      v[q] = i < n ? col[i] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + 256 * q;
+      if (i < n) col[i] = __ddiv_rn(v[q], d);
+    }
+  }
 }
 
 // ---- PCG64 (numpy default_rng) -----------------------------------------
@@ -737,10 +748,10 @@ int krb_colscale_div(int64_t n, int64_t k, double *d_X, int64_t ldx,
                      const double *d_s, void *stream) {
   KRB_REQUIRE(ldx >= n, "krb_colscale_div: ldx < n");
   if (n * k == 0) return KRB_OK;
-  int64_t blocks = (n + 255) / 256;
-  int64_t per_col = (int64_t)kNumSMs * 8 / k;
-  if (per_col < 1) per_col = 1;
-  dim3 grid((unsigned)(blocks < per_col ? blocks : per_col), (unsigned)k);
+  // one pass: every element has its thread (grid.y <= 65535 columns)
+  KRB_REQUIRE(k <= 65535, "krb_colscale_div: more than 65535 columns");
+  const int64_t blocks = (n + 1023) / 1024;
+  dim3 grid((unsigned)(blocks < 65535 ? blocks : 65535), (unsigned)k);
   k_colscale_div<<<grid, 256, 0, as_stream(stream)>>>(n, (int)k, d_X, ldx, d_s);
   KRB_CHECK_LAUNCH();
   return KRB_OK;

@@ -153,3 +153,16 @@ def test_gemm_shapes_bitwise(dev, canon, monkeypatch, mode, n, m, nc):
     Z = r.standard_normal((m, nc))
     out = R.gemm(_cols(X), Z).cpu().numpy().T
     assert np.array_equal(out, canon.gemm(X, Z))
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (1_000, 3), (262_144, 47), (70_001, 20), (5_000_003, 2)])
+def test_colscale_div_bitwise(dev, n, k):
+    """X[:, j] / s[j] (recycling.py:307-308, 333-340): numpy's correctly
+    rounded division, element for element"""
+    from paper_1406_2831_b200 import recycling as R
+    r = np.random.default_rng(n + k)
+    X = r.standard_normal((n, k))
+    sv = r.uniform(0.1, 10.0, size=k)
+    Xd = _cols(X)
+    R.colscale_div(Xd, _tensor(sv))
+    assert np.array_equal(Xd.cpu().numpy().T, X / sv)

@@ -329,27 +329,30 @@ def gpu_arm(args, wl, rank, world):
         out["e2e"] = None
 
     if not args.no_synthetic:
-        out.update(synthetic_pass(wl, dmats, drhs))
+        out.update(synthetic_pass(wl, dmats, drhs,
+                                   max(last.space_dims) if last.space_dims else 0))
     return out
 
 
-def synthetic_pass(wl, dmats, drhs):
-    """Fixed seeded k-space RBiCGSTAB over the sequence + live kernel timing."""
+def _solve_pass(wl, dmats, drhs, fixed_space):
+    """Every system of the sequence solved once more (best of two) with either
+    no recycle space (k = 0: the shape the policy's solves take when the
+    harvest collapses) or a fixed seeded k-space refreshed per
+    matrix.  Returns (iterations, seconds, k per system, driver)."""
     import torch
     import paper_1406_2831_b200 as P
-    from paper_1406_2831_b200 import recycling as R, solvers as S
-    peak, src = peaks()
-    r = np.random.default_rng(12345)
-    U = r.standard_normal((wl.n, wl.k))
-    Ut = r.standard_normal((wl.n, wl.k))
+    from paper_1406_2831_b200 import solvers as S
     space = None
-    its = 0
-    t_solve = 0.0
-    ks = []
+    if fixed_space:
+        r = np.random.default_rng(12345)
+        U = r.standard_normal((wl.n, wl.k))
+        Ut = r.standard_normal((wl.n, wl.k))
+    its, t_solve, ks = 0, 0.0, []
     for idx, key in enumerate(sorted(drhs)):
         M = dmats[key[0]]
-        space = P.biorthonormalize(U, Ut, M) if space is None else P.refresh_images(space, M)
-        ks.append(space.k)
+        if fixed_space:
+            space = P.biorthonormalize(U, Ut, M) if space is None else P.refresh_images(space, M)
+        ks.append(space.k if space is not None else 0)
         best = None
         for _rep in range(2):   # best of two (the first also warms this shape)
             torch.cuda.synchronize()
@@ -364,9 +367,69 @@ def synthetic_pass(wl, dmats, drhs):
             best = dt if best is None else min(best, dt)
         t_solve += best
         its += h.iterations
-    kmean = float(np.mean(ks)) if ks else 0.0
-    B_it = W.bytes_per_iteration(wl.n, wl.nnz, int(round(kmean)))
-    it_ach = B_it * its / t_solve / 1e9
+    return its, t_solve, ks, S.LAST_SOLVE.get("driver"), space
+
+
+def _traffic(wl, kernel, its, nsolves):
+    tp = os.path.join(REPO, "profiles", "traffic.json")
+    if not os.path.exists(tp):
+        return None
+    for tj in json.load(open(tp)).get(wl.name, []):
+        if kernel.startswith(tj["kernel"]):
+            if "bytes_per_iteration" in tj:
+                return int(tj["bytes_per_iteration"] * its / max(nsolves, 1))
+            return int(tj["bytes_per_launch"])
+    return None
+
+
+def synthetic_pass(wl, dmats, drhs, step_k):
+    """Roofline of the dominant kernel of the measured step plus a fixed
+    k-space pass (the reference's harvest collapses to k = 0 on C2, so the
+    fixed space is what exercises the projections) and live kernel timing.
+
+    With n <= PERSISTENT_MAX_N every solve is ONE persistent kernel launch
+    (k = 0: k_persist0, persist0.cu; k > 0: k_persist2, persist.cu), so the
+    kernel's algorithmic bytes per launch = B_it(k) x iterations per solve and
+    its launch duration = the solve's CUDA-event time (setup kernels
+    included, so the fraction is conservative)."""
+    import torch
+    from paper_1406_2831_b200 import recycling as R
+    from paper_1406_2831_b200.solvers import _auto_mode
+    peak, src = peaks()
+    persistent = _auto_mode(wl.n) == 2
+
+    def roofline_of(its, t_solve, ks, k):
+        B_it = W.bytes_per_iteration(wl.n, wl.nnz, k)
+        ach = B_it * its / t_solve / 1e9
+        if k == 0:
+            kern = "k_persist0 (fused persistent BiCGSTAB, k = 0, one solve per launch)"
+        else:
+            kern = "k_persist2 (fused persistent RBiCGSTAB, one solve per launch)"
+        return B_it, {"bound": "hbm", "kernel": kern, "k": k,
+                      "achieved": round(ach, 1), "peak": peak, "peak_source": src,
+                      "unit": "GB/s", "frac": round(ach / peak, 4),
+                      "traffic": _traffic(wl, kern, its, len(ks)),
+                      "bytes_per_launch": B_it * its / max(len(ks), 1),
+                      "launch_us": round(1e6 * t_solve / max(len(ks), 1), 2),
+                      "iterations": its, "seconds": t_solve,
+                      "us_per_iteration": round(1e6 * t_solve / max(its, 1), 2)}
+
+    out = {}
+    its0, t0, ks0, drv0, _ = _solve_pass(wl, dmats, drhs, fixed_space=False)
+    B0, rf0 = roofline_of(its0, t0, ks0, 0)
+    itsk, tk, ksk, drvk, space = _solve_pass(wl, dmats, drhs, fixed_space=True)
+    kmean = int(round(float(np.mean(ksk)))) if ksk else 0
+    Bk, rfk = roofline_of(itsk, tk, ksk, kmean)
+    out["synthetic"] = {"iterations": itsk, "seconds": tk, "k_per_system": ksk,
+                        "driver": drvk, "iters_per_s": itsk / tk,
+                        "us_per_iteration": round(1e6 * tk / max(itsk, 1), 2)}
+    out["iteration_roofline"] = {"bytes_per_iteration": Bk, "k": kmean,
+                                 "achieved": rfk["achieved"], "unit": "GB/s",
+                                 "peak": peak, "frac": rfk["frac"]}
+    out["iteration_roofline_k0"] = {"bytes_per_iteration": B0, "k": 0, "driver": drv0,
+                                    "achieved": rf0["achieved"], "unit": "GB/s",
+                                    "peak": peak, "frac": rf0["frac"],
+                                    "us_per_iteration": rf0["us_per_iteration"]}
 
     M = dmats[0]
     x = torch.randn(wl.n, dtype=torch.float64, device="cuda")
@@ -391,42 +454,24 @@ def synthetic_pass(wl, dmats, drhs):
         kern["proj_dot"] = (8 * wl.n * kk + 8 * wl.n, timeit(lambda: R.tdot(Cb, x, zeta)))
         kern["proj_update"] = (8 * wl.n * kk + 16 * wl.n,
                                timeit(lambda: R.gemv(Cb, zeta, base=x, sign=-1, out=y)))
-    share = {k: v[1] for k, v in kern.items()}
-    dom = max(share, key=share.get)
-    b, t = kern[dom]
-    from paper_1406_2831_b200.solvers import _auto_mode
-    if _auto_mode(wl.n) == 2:
-        # the persistent driver runs each whole solve as ONE kernel (fused
-        # k_persist2, persist.cu): the dominant kernel of the step; per
-        # launch = one solve
-        dom = "k_persist2 (fused persistent RBiCGSTAB, one solve per launch)"
-        b = B_it * its / max(len(ks), 1)
-        t = t_solve / max(len(ks), 1)
-    ach = b / t / 1e9
-    traffic = None
-    tp = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        tj = json.load(open(tp)).get(wl.name)
-        if tj and dom.startswith(tj["kernel"]):
-            if "bytes_per_iteration" in tj:
-                traffic = int(tj["bytes_per_iteration"] * its / max(len(ks), 1))
-            else:
-                traffic = int(tj["bytes_per_launch"])
-    return {
-        "synthetic": {"iterations": its, "seconds": t_solve, "k_per_system": ks,
-                      "driver": S.LAST_SOLVE.get("driver"),
-                      "iters_per_s": its / t_solve,
-                      "us_per_iteration": round(1e6 * t_solve / max(its, 1), 2)},
-        "iteration_roofline": {"bytes_per_iteration": B_it, "k": kmean,
-                               "achieved": round(it_ach, 1), "unit": "GB/s",
-                               "peak": peak, "frac": round(it_ach / peak, 4)},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1),
-                     "peak": peak, "peak_source": src, "unit": "GB/s",
-                     "frac": round(ach / peak, 4), "traffic": traffic,
-                     "bytes_per_launch": b, "launch_us": round(t * 1e6, 2)},
-        "kernels": {k: {"bytes": v[0], "us": round(v[1] * 1e6, 2),
-                        "GBps": round(v[0] / v[1] / 1e9, 1)} for k, v in kern.items()},
-    }
+    out["kernels"] = {k: {"bytes": v[0], "us": round(v[1] * 1e6, 2),
+                          "GBps": round(v[0] / v[1] / 1e9, 1)} for k, v in kern.items()}
+    if persistent:
+        # the step's own shape: its solves run at k = step_k
+        main, other = (rf0, rfk) if step_k == 0 else (rfk, rf0)
+        out["roofline"] = main
+        out["roofline_secondary"] = other
+    else:
+        share = {k: v[1] for k, v in kern.items()}
+        dom = max(share, key=share.get)
+        b, t = kern[dom]
+        ach = b / t / 1e9
+        out["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1),
+                           "peak": peak, "peak_source": src, "unit": "GB/s",
+                           "frac": round(ach / peak, 4),
+                           "traffic": _traffic(wl, dom, 1, 1),
+                           "bytes_per_launch": b, "launch_us": round(t * 1e6, 2)}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -531,7 +576,8 @@ def main():
                 "step_ms": res["step_ms"],
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "e2e": res["e2e"]}
-        for key in ("roofline", "iteration_roofline", "kernels", "synthetic"):
+        for key in ("roofline", "roofline_secondary", "iteration_roofline",
+                    "iteration_roofline_k0", "kernels", "synthetic"):
             if key in res:
                 line[key] = res[key]
         line["cpu_baseline"] = cpu

@@ -228,6 +228,12 @@ int krb_rbicg_set_counts(krb_rbicg *H, int64_t n_matvec, int64_t n_rmatvec,
 int krb_rbicg_begin(krb_rbicg *H, int32_t *h_status, void *stream);
 /* h_state[7] = status, emit, ncols, itn, nalpha, capture, npush */
 int krb_rbicg_run(krb_rbicg *H, int64_t *h_state, void *stream);
+/* krb_rbicg_run split in two (the loop of solvers.py:593-634 up to the next
+ * `itn % s == 0` emit): launch without waiting, so the harvest of the
+ * previous cycle (the cycle_callback's device work and host eigenproblem)
+ * overlaps the next cycle's iterations; then wait and read the state. */
+int krb_rbicg_launch(krb_rbicg *H, int32_t *launched, void *stream);
+int krb_rbicg_wait(krb_rbicg *H, int64_t *h_state, void *stream);
 int krb_rbicg_views(krb_rbicg *H, double **V, double **Vt, double **rhos,
                     double **alphas, double **betas);
 int krb_rbicg_rotate(krb_rbicg *H, int64_t keep, void *stream);

@@ -113,6 +113,8 @@ SIGNATURES = {
     "krb_rbicg_set_counts": (c_int, [c_vp, c_i64, c_i64, c_vp]),
     "krb_rbicg_begin": (c_int, [c_vp, ctypes.POINTER(ctypes.c_int32), c_vp]),
     "krb_rbicg_run": (c_int, [c_vp, ctypes.POINTER(c_i64), c_vp]),
+    "krb_rbicg_launch": (c_int, [c_vp, ctypes.POINTER(ctypes.c_int32), c_vp]),
+    "krb_rbicg_wait": (c_int, [c_vp, ctypes.POINTER(c_i64), c_vp]),
     "krb_rbicg_views": (c_int, [c_vp] + [ctypes.POINTER(c_vp)] * 5),
     "krb_rbicg_rotate": (c_int, [c_vp, c_i64, c_vp]),
     "krb_rbicg_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
@@ -193,3 +195,26 @@ def fetch_f64(src_addr: int, count: int):
     out = torch.empty(count, dtype=torch.float64, device="cuda")
     copy_d2d(out, src_addr, count)
     return out.cpu().numpy()
+
+
+def fetch_f64_many(parts):
+    """Several (device address, count) ranges of doubles to host numpy arrays
+    with ONE device->host read (one synchronisation)."""
+    import numpy as np
+    import torch
+    total = sum(max(c, 0) for _, c in parts)
+    if total == 0:
+        return [np.zeros(0) for _ in parts]
+    buf = torch.empty(total, dtype=torch.float64, device="cuda")
+    off = 0
+    for addr, c in parts:
+        if c > 0:
+            copy_d2d(buf[off:], addr, c)
+            off += c
+    host = buf.cpu().numpy()
+    out, off = [], 0
+    for _, c in parts:
+        c = max(c, 0)
+        out.append(host[off:off + c])
+        off += c
+    return out

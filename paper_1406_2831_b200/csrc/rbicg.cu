@@ -700,6 +700,11 @@ struct krb_rbicg {
   int64_t l0 = 0;
   int use_graph = 1;
   int fmt = -1, fmt_t = -1;   // storage formats the graph was captured for
+  // host copy of the scalar block as of the last begin / run (the device
+  // block only changes inside those calls and in rotate, which keeps this
+  // copy current): run and rotate need no extra read-back + synchronisation
+  krb::BiScalars hs = {};
+  bool hs_valid = false;
 };
 
 namespace krb {
@@ -902,6 +907,7 @@ int krb_rbicg_start(krb_rbicg *H, const double *d_b, const double *d_bt,
                     const double *d_x0, const double *d_xt0, double tol,
                     double breakdown_tol, int use_graph, double *h_dual,
                     void *stream) {
+  if (H) H->hs_valid = false;
   KRB_REQUIRE(H && d_b && d_bt && h_dual, "krb_rbicg_start: NULL argument");
   cudaStream_t st = as_stream(stream);
   BiArgs &h = H->h;
@@ -969,6 +975,7 @@ int krb_rbicg_start(krb_rbicg *H, const double *d_b, const double *d_bt,
 int krb_rbicg_set_counts(krb_rbicg *H, int64_t n_matvec, int64_t n_rmatvec,
                          void *stream) {
   KRB_REQUIRE(H, "krb_rbicg_set_counts: NULL handle");
+  H->hs_valid = false;
   cudaStream_t st = as_stream(stream);
   KRB_CHECK_CUDA(cudaMemcpyAsync(&H->S->n_matvec, &n_matvec, sizeof(int64_t),
                                  cudaMemcpyHostToDevice, st));
@@ -1012,35 +1019,60 @@ int krb_rbicg_begin(krb_rbicg *H, int32_t *h_status, void *stream) {
   KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));
   *h_status = hs.status;
+  H->hs = hs;
+  H->hs_valid = true;
   return KRB_OK;
 }
 
-/* Run iterations until the solve stops or a cycle completes.
- * h_state[0..6] = status, emit, ncols, itn, nalpha, capture, npush. */
-int krb_rbicg_run(krb_rbicg *H, int64_t *h_state, void *stream) {
-  KRB_REQUIRE(H && h_state, "krb_rbicg_run: NULL argument");
+/* Launch the iterations up to the next completed cycle (or the end of the
+ * solve) WITHOUT waiting: graph / persistent drivers only (the host loop
+ * needs a read-back per iteration, so there it runs to the pause here).
+ * The caller may queue more work on the stream (the harvest of the previous
+ * cycle) and then collects the state with krb_rbicg_wait.  *launched = 0
+ * when the solve had already stopped (nothing queued). */
+int krb_rbicg_launch(krb_rbicg *H, int32_t *launched, void *stream) {
+  KRB_REQUIRE(H && launched, "krb_rbicg_launch: NULL argument");
   cudaStream_t st = as_stream(stream);
+  *launched = 0;
   BiScalars hs;
-  KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (hs.status == KRB_RUNNING) {
-    int32_t zero = 0;
-    KRB_CHECK_CUDA(cudaMemcpyAsync(&H->h.S->emit, &zero, sizeof(int32_t),
-                                   cudaMemcpyHostToDevice, st));
-    if (H->use_graph == 1) {
-      KRB_CHECK_CUDA(cudaGraphLaunch(H->exec, st));
-    } else if (H->use_graph == 2) {
-      KRB_TRY(bi_persistent(H->h, H->d_nc, st));
-    } else {
-      for (int64_t it = 0; it <= H->max_itn; ++it) {
-        KRB_TRY(bi_iteration(H->h, H->d_nc, st));
-        KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
-        KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-        if (hs.status != KRB_RUNNING || hs.emit) break;
-      }
-    }
+  if (H->hs_valid) {
+    hs = H->hs;
+  } else {
     KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
     KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
+  if (hs.status != KRB_RUNNING) return KRB_OK;
+  KRB_CHECK_CUDA(cudaMemsetAsync(&H->h.S->emit, 0, sizeof(int32_t), st));
+  if (H->use_graph == 1) {
+    KRB_CHECK_CUDA(cudaGraphLaunch(H->exec, st));
+  } else if (H->use_graph == 2) {
+    KRB_TRY(bi_persistent(H->h, H->d_nc, st));
+  } else {
+    for (int64_t it = 0; it <= H->max_itn; ++it) {
+      KRB_TRY(bi_iteration(H->h, H->d_nc, st));
+      KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+      if (hs.status != KRB_RUNNING || hs.emit) break;
+    }
+  }
+  H->hs_valid = false;   // the device block moves on; krb_rbicg_wait re-reads it
+  *launched = 1;
+  return KRB_OK;
+}
+
+/* Wait for the stream and read the scalar state.
+ * h_state[0..6] = status, emit, ncols, itn, nalpha, capture, npush. */
+int krb_rbicg_wait(krb_rbicg *H, int64_t *h_state, void *stream) {
+  KRB_REQUIRE(H && h_state, "krb_rbicg_wait: NULL argument");
+  cudaStream_t st = as_stream(stream);
+  BiScalars hs;
+  if (H->hs_valid) {
+    hs = H->hs;
+  } else {
+    KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+    H->hs = hs;
+    H->hs_valid = true;
   }
   h_state[0] = hs.status;
   h_state[1] = hs.emit;
@@ -1050,6 +1082,15 @@ int krb_rbicg_run(krb_rbicg *H, int64_t *h_state, void *stream) {
   h_state[5] = hs.capture;
   h_state[6] = hs.npush;
   return KRB_OK;
+}
+
+/* Run iterations until the solve stops or a cycle completes (launch + wait).
+ * h_state[0..6] = status, emit, ncols, itn, nalpha, capture, npush. */
+int krb_rbicg_run(krb_rbicg *H, int64_t *h_state, void *stream) {
+  KRB_REQUIRE(H && h_state, "krb_rbicg_run: NULL argument");
+  int32_t launched = 0;
+  KRB_TRY(krb_rbicg_launch(H, &launched, stream));
+  return krb_rbicg_wait(H, h_state, stream);
 }
 
 /* Device pointers of the capture rings and coefficient arrays (read-only
@@ -1071,10 +1112,15 @@ int krb_rbicg_rotate(krb_rbicg *H, int64_t keep, void *stream) {
   KRB_REQUIRE(H, "krb_rbicg_rotate: NULL handle");
   cudaStream_t st = as_stream(stream);
   BiScalars hs;
-  KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (H->hs_valid) {
+    hs = H->hs;
+  } else {
+    KRB_CHECK_CUDA(cudaMemcpyAsync(&hs, H->h.S, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
   const int64_t n = H->h.n, nc = hs.ncols;
-  KRB_REQUIRE(keep <= nc, "krb_rbicg_rotate: keep > ncols");
+  KRB_REQUIRE(keep >= 0 && keep <= nc, "krb_rbicg_rotate: keep > ncols");
+  KRB_REQUIRE(keep < 256, "krb_rbicg_rotate: keep >= 256");
   for (int64_t c = 0; c < keep; ++c) {
     int64_t src = nc - keep + c;
     if (src == c) continue;
@@ -1083,9 +1129,11 @@ int krb_rbicg_rotate(krb_rbicg *H, int64_t keep, void *stream) {
     KRB_CHECK_CUDA(cudaMemcpyAsync(H->h.Vt + c * n, H->h.Vt + src * n, sizeof(double) * n,
                                    cudaMemcpyDeviceToDevice, st));
   }
-  KRB_CHECK_CUDA(cudaMemcpyAsync(&H->h.S->ncols, &keep, sizeof(int64_t),
-                                 cudaMemcpyHostToDevice, st));
-  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  // ncols = keep without a pageable host->device copy (which may
+  // synchronise): zero the int64, then its low byte (little-endian)
+  KRB_CHECK_CUDA(cudaMemsetAsync(&H->h.S->ncols, 0, sizeof(int64_t), st));
+  if (keep) KRB_CHECK_CUDA(cudaMemsetAsync(&H->h.S->ncols, (int)keep, 1, st));
+  if (H->hs_valid) H->hs.ncols = keep;
   return KRB_OK;
 }
 

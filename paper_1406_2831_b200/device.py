@@ -37,6 +37,27 @@ def stream_ptr():
     return ctypes.c_void_p(C._cuda_getCurrentRawStream(C._cuda_getDevice()))
 
 
+# Deferred device launches: a producer (rbicg_solve's next harvest cycle)
+# registers its launch before handing a cycle to the cycle_callback; a
+# consumer about to run long host-only work (update_recycle_space's
+# eigenproblem) calls flush_pending() so the launch overlaps that host work.
+# The producer flushes again after the callback returns (a no-op if done).
+_PENDING = []
+
+
+def defer_launch(fn):
+    _PENDING.append(fn)
+
+
+def flush_pending():
+    while _PENDING:
+        _PENDING.pop(0)()
+
+
+def drop_pending():
+    _PENDING.clear()
+
+
 def ptr(tensor):
     return ctypes.c_void_p(tensor.data_ptr()) if tensor is not None else None
 

@@ -297,18 +297,20 @@ def biorthonormalize(U_raw, Ut_raw, A, C_raw=None, Ct_raw=None,
         warnings.warn("recycle basis pair is numerically rank deficient; "
                       "returning an empty space", stacklevel=2)
         return RecycleSpace.empty(n)
-    Y = np.ascontiguousarray(Yh.conj().T[:, :r])
-    X = np.ascontiguousarray(X[:, :r])
+    Y = to_device(np.ascontiguousarray(Yh.conj().T[:, :r]))   # uploaded once, used twice
+    X = to_device(np.ascontiguousarray(X[:, :r]))
     U = gemm(U0, Y)
     C = gemm(C_raw, Y)
     Ut = gemm(Ut0, X)
     Ct = gemm(Ct_raw, X)
     nu = colnorms(C)
+    ctn = colnorms(Ct)
     colscale_div(U, nu)
     colscale_div(C, nu)
-    nu_h = nu.cpu().numpy()
+    nh = t.cat([nu, ctn]).cpu().numpy()    # one read
+    nu_h, ctn_h = nh[:r], nh[r:]
     Dc = sig[:r] / nu_h
-    amp = colnorms(Ct).cpu().numpy() / Dc
+    amp = ctn_h / Dc
     keep = amp <= amp_tol
     if not np.all(keep):
         if not np.any(keep):

@@ -111,7 +111,6 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
         A = api.SparseMatrix.from_csr(seq.matrix(i))
         op_rec = api.CountingOperator(A)
         op_base = api.CountingOperator(A)
-        dual_rhs = np.ones(A.nrows if hasattr(A, "nrows") else seq.n)
         nk = min(seq.rhs_per_matrix, total - gidx)
         pre_rec, pre_base = {}, {}   # kappa -> (history, seconds) of batched solves
         for kappa in range(nk):
@@ -128,6 +127,7 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                     _state["space"] = api.update_recycle_space(
                         _op, [cycle], _state["space"], k, res_tol=4.0)
 
+                dual_rhs = np.ones(A.nrows if hasattr(A, "nrows") else seq.n)
                 _, _, hist, _ = api.rbicg_solve(op_rec, b, b_dual=dual_rhs,
                                                 recycle=space, config=cfg,
                                                 cycle_callback=harvest)

@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .device import Context, device_matrix, ptr, stream_ptr, to_device, torch
+from .device import (Context, defer_launch, device_matrix, drop_pending, flush_pending,
+                     ptr, stream_ptr, to_device, torch)
 from .recycling import RecycleSpace
 
 CONVERGED = "converged"
@@ -437,10 +438,12 @@ class _CycleHarvest:
                   ctypes.byref(rh), ctypes.byref(al), ctypes.byref(be))
         self.ptrs = (V.value, Vt.value, rh.value, al.value, be.value)
 
-    def emit(self, state, final=False):
+    def emit(self, state, final=False, launch_next=None):
         ncols, nalpha, npush = int(state[2]), int(state[4]), int(state[6])
         last = self.start + ncols - 1
         if ncols == 0 or last <= self.emitted:
+            if launch_next is not None:
+                launch_next()
             return
         t = torch()
         n = self.n
@@ -448,20 +451,35 @@ class _CycleHarvest:
         Vtd = t.empty((ncols, n), dtype=t.float64, device="cuda")
         _lib.copy_d2d(Vd, self.ptrs[0], ncols * n)
         _lib.copy_d2d(Vtd, self.ptrs[1], ncols * n)
-        rhos = _lib.fetch_f64(self.ptrs[2], npush)
-        alphas = _lib.fetch_f64(self.ptrs[3], nalpha)
-        betas = _lib.fetch_f64(self.ptrs[4], nalpha)
+        rhos, alphas, betas = _lib.fetch_f64_many(
+            [(self.ptrs[2], npush), (self.ptrs[3], nalpha), (self.ptrs[4], nalpha)])
         cyc = self.CapturedCycle(V_dev=Vd, Vt_dev=Vtd,
                                  tri=_tri_block(self.start, ncols, alphas, betas, rhos),
                                  first_index=self.start)
         self.cycles.append(cyc)
         self.emitted = last
-        if self.callback is not None:
-            self.callback(cyc)
         if not final and ncols > 2:
+            # the copies above are queued first on the same stream, so the
+            # ring may be rotated and refilled before the callback runs
             _lib.call("krb_rbicg_rotate", self.H, 2, stream_ptr())
             self.start = last - 1
             state[2] = 2          # the ring now holds the two overlap columns
+        if launch_next is None:
+            if self.callback is not None:
+                self.callback(cyc)
+            return
+        if self.callback is None:
+            launch_next()
+            return
+        # the next cycle's iterations are launched when the callback starts
+        # host-only work (device.flush_pending), else right after it
+        defer_launch(launch_next)
+        try:
+            self.callback(cyc)
+        except BaseException:
+            drop_pending()
+            raise
+        flush_pending()
 
 
 def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
@@ -524,11 +542,21 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
         _lib.call("krb_rbicg_begin", H, ctypes.byref(status), stream_ptr())
         harvest = _CycleHarvest(H, n, cycle_callback)
         state = (ctypes.c_int64 * 7)()
+        launched = ctypes.c_int32()
+
+        def launch_next():
+            _lib.call("krb_rbicg_launch", H, ctypes.byref(launched), stream_ptr())
+
+        launch_next()
         while True:
-            _lib.call("krb_rbicg_run", H, state, stream_ptr())
+            _lib.call("krb_rbicg_wait", H, state, stream_ptr())
+            running = state[0] == 0
             if state[1]:
-                harvest.emit(state, final=False)
-            if state[0] != 0:
+                harvest.emit(state, final=False,
+                             launch_next=launch_next if running else None)
+            elif running:
+                launch_next()
+            if not running:
                 break
         harvest.emit(state, final=True)
         xo = t.empty(n, dtype=t.float64, device="cuda")
@@ -549,10 +577,13 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     Lh = int(res.hist_len)
     hist = ConvergenceHistory(solver="rbicg", rhs_norm=float(res.rhs_norm),
                               rhs_norm_dual=float(btn.value))
-    stamps = ht[:Lh].cpu().numpy().astype(np.int64)
-    hist.resid = [float(v) for v in hr[:Lh].cpu().numpy()]
-    hist.resid_dual = [float(v) for v in hrt[:Lh].cpu().numpy()]
-    hist.matvecs = [int(v) for v in hm[:Lh].cpu().numpy()]
+    # one device->host read for the four history arrays (bit views)
+    h4 = t.stack([hr[:Lh].view(t.int64), hrt[:Lh].view(t.int64), hm[:Lh],
+                  ht[:Lh]]).cpu().numpy()
+    stamps = h4[3]
+    hist.resid = [float(v) for v in h4[0].view(np.float64)]
+    hist.resid_dual = [float(v) for v in h4[1].view(np.float64)]
+    hist.matvecs = [int(v) for v in h4[2]]
     st0 = int(res.t_start_ns)
     base = time.perf_counter() - t0 - (int(stamps[-1]) - st0) * 1e-9 if Lh else 0.0
     hist.seconds = [base + (int(s) - st0) * 1e-9 for s in stamps]

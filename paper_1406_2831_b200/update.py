@@ -16,7 +16,7 @@ import warnings
 import numpy as np
 
 from . import _lib
-from .device import device_matrix, ptr, stream_ptr, to_device, torch
+from .device import device_matrix, flush_pending, ptr, stream_ptr, to_device, torch
 from .recycling import (RecycleSpace, _as_block, _ctx, _ld, _meter,
                         biorthonormalize, colnorms, colscale_div, gemm, gram)
 
@@ -86,8 +86,8 @@ def near_null_eligibility(theta, VR, W, AW, res_tol):
     Y = W VR, R = AW VR - Y theta, res = ||R_c|| / max(||Y_c||, 1e-300)."""
     finite = np.isfinite(theta)
     th = np.where(finite, theta, 0.0)
-    VRr = np.ascontiguousarray(VR.real)
-    VRi = np.ascontiguousarray(VR.imag)
+    VRr = to_device(np.ascontiguousarray(VR.real))   # uploaded once, used twice
+    VRi = to_device(np.ascontiguousarray(VR.imag))
     m, n = W.shape
     Yre, Yim = gemm(W, VRr), gemm(W, VRi)
     Are, Aim = gemm(AW, VRr), gemm(AW, VRi)
@@ -151,11 +151,10 @@ def update_recycle_space(A, cycles, previous, k: int, rank_tol: float = 1e-12,
     W, Wt = t.cat(bu, 0), t.cat(but, 0)
     AW, AhWt = t.cat(bc, 0), t.cat(bct, 0)
     # column scaling (recycling.py:333-340)
-    nrm = t.cat([colnorms(W), colnorms(Wt)]).cpu().numpy()   # one read
-    sw, st = nrm[:W.shape[0]].copy(), nrm[W.shape[0]:].copy()
-    sw[sw == 0] = 1.0
-    st[st == 0] = 1.0
-    swd, std_ = to_device(sw), to_device(st)
+    # scales stay on the device (a zero norm divides by 1, as the reference)
+    swd, std_ = colnorms(W), colnorms(Wt)
+    swd.masked_fill_(swd == 0, 1.0)
+    std_.masked_fill_(std_ == 0, 1.0)
     colscale_div(W, swd)
     colscale_div(AW, swd)
     colscale_div(Wt, std_)
@@ -163,6 +162,7 @@ def update_recycle_space(A, cycles, previous, k: int, rank_tol: float = 1e-12,
     G2 = t.stack([gram(Wt, AW), gram(Wt, W)]).cpu().numpy()   # one read
     GA, GI = G2[0].copy(), G2[1].copy()
     import scipy.linalg as la
+    flush_pending()   # a deferred generation cycle runs on the device meanwhile
     theta, VL, VR = la.eig(GA, GI, left=True, right=True)
     eligible = None
     if res_tol > 0.0:
@@ -172,8 +172,8 @@ def update_recycle_space(A, cycles, previous, k: int, rank_tol: float = 1e-12,
         warnings.warn("recycle-space pencil produced no finite eigenvalues; "
                       "keeping previous space", stacklevel=2)
         return prev if prev is not None else RecycleSpace.empty(n)
-    Zr = np.ascontiguousarray(Zr)
-    Zl = np.ascontiguousarray(Zl)
+    Zr = to_device(np.ascontiguousarray(Zr))   # uploaded once, used twice
+    Zl = to_device(np.ascontiguousarray(Zl))
     return biorthonormalize(gemm(W, Zr), gemm(Wt, Zl), M,
                             C_raw=gemm(AW, Zr), Ct_raw=gemm(AhWt, Zl),
                             rank_tol=rank_tol)

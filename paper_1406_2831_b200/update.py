@@ -83,28 +83,39 @@ def select_pencil_columns(theta, VR, VL, k, real_pencil, eligible=None):
 
 def near_null_eligibility(theta, VR, W, AW, res_tol):
     """recycling.py:348-358 with the complex products as real ones:
-    Y = W VR, R = AW VR - Y theta, res = ||R_c|| / max(||Y_c||, 1e-300)."""
+    Y = W VR, R = AW VR - Y theta, res = ||R_c|| / max(||Y_c||, 1e-300).
+    Only the near-null columns (|theta| < NEAR_NULL_FRAC max|theta|, finite)
+    read their residual, so only those columns are computed: every column of
+    the products, the Ritz combination and the column norms is independent
+    of the others, so the subset gives the same bits per column."""
     finite = np.isfinite(theta)
     th = np.where(finite, theta, 0.0)
-    VRr = to_device(np.ascontiguousarray(VR.real))   # uploaded once, used twice
-    VRi = to_device(np.ascontiguousarray(VR.imag))
-    m, n = W.shape
-    Yre, Yim = gemm(W, VRr), gemm(W, VRi)
-    Are, Aim = gemm(AW, VRr), gemm(AW, VRi)
-    thr = to_device(np.ascontiguousarray(th.real))
-    thi = to_device(np.ascontiguousarray(th.imag))
-    _lib.call("krb_ritz_combine", n, VR.shape[1], ptr(Yre), ptr(Yim), ptr(Are),
-              ptr(Aim), n, ptr(thr), ptr(thi), stream_ptr())
-    t = torch()
-    sq = t.cat([colsq(Are), colsq(Aim), colsq(Yre), colsq(Yim)]).cpu().numpy()  # one read
-    c = VR.shape[1]
-    rn = np.sqrt(sq[:c] + sq[c:2 * c])
-    yn = np.sqrt(sq[2 * c:3 * c] + sq[3 * c:])
-    res = rn / np.maximum(yn, 1e-300)
     ab = np.abs(th)
     top = ab.max() if ab.size else 0.0
     near = ab < NEAR_NULL_FRAC * top
-    return finite & (~near | (res <= res_tol * ab))
+    sel = np.flatnonzero(finite & near)
+    eligible = finite & ~near
+    if sel.size == 0:
+        return eligible
+    VRs = VR[:, sel]
+    ths = th[sel]
+    VRr = to_device(np.ascontiguousarray(VRs.real))   # uploaded once, used twice
+    VRi = to_device(np.ascontiguousarray(VRs.imag))
+    m, n = W.shape
+    Yre, Yim = gemm(W, VRr), gemm(W, VRi)
+    Are, Aim = gemm(AW, VRr), gemm(AW, VRi)
+    thr = to_device(np.ascontiguousarray(ths.real))
+    thi = to_device(np.ascontiguousarray(ths.imag))
+    c = sel.size
+    _lib.call("krb_ritz_combine", n, c, ptr(Yre), ptr(Yim), ptr(Are),
+              ptr(Aim), n, ptr(thr), ptr(thi), stream_ptr())
+    t = torch()
+    sq = t.cat([colsq(Are), colsq(Aim), colsq(Yre), colsq(Yim)]).cpu().numpy()  # one read
+    rn = np.sqrt(sq[:c] + sq[c:2 * c])
+    yn = np.sqrt(sq[2 * c:3 * c] + sq[3 * c:])
+    res = rn / np.maximum(yn, 1e-300)
+    eligible[sel] = res <= res_tol * ab[sel]
+    return eligible
 
 
 def _cycle_blocks(cyc, n):

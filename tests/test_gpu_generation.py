@@ -242,3 +242,28 @@ def test_rbicg_drivers_bitwise(P, canon, cfg, k, monkeypatch):
         for c1, c2 in zip(cyc, ref[3]):
             assert c1.first_index == c2.first_index
             assert np.array_equal(c1.V, c2.V) and np.array_equal(c1.Vt, c2.Vt)
+
+
+@pytest.mark.parametrize("near", [0, 1, 3, 40])
+def test_near_null_eligibility_subset_bitwise(P, canon, near):
+    """The device eigen-residual filter computes only the near-null columns;
+    the decision must equal the oracle's full computation (recycling.py:348-358)
+    whether none, some or all of the Ritz values are near-null, with complex
+    pairs and a non-finite value among them."""
+    import torch
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import update as UP
+    rs = np.random.default_rng(7 + near)
+    n, m = 5000, 47
+    W = rs.standard_normal((n, m))
+    AW = rs.standard_normal((n, m))
+    VR = rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m))
+    theta = (rs.uniform(1.0, 2.0, m) + 1j * rs.uniform(-1.0, 1.0, m)).astype(np.complex128)
+    theta[rs.permutation(m)[:near]] *= 1e-5          # near-null
+    theta[0] = np.inf
+    Wd = torch.as_tensor(np.ascontiguousarray(W.T), device="cuda")
+    AWd = torch.as_tensor(np.ascontiguousarray(AW.T), device="cuda")
+    for res_tol in (0.0, 4.0, 1e9):
+        got = UP.near_null_eligibility(theta, VR, Wd, AWd, res_tol)
+        want = O.near_null_eligibility(theta, VR, W, AW, res_tol, canon)
+        assert np.array_equal(got, want), (near, res_tol)

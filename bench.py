@@ -301,7 +301,8 @@ def gpu_arm(args, wl, rank, world):
             return run_sequence(pview, policy=wl.policy, baseline=False, api=host_api,
                                 systems=wl.nsys)
 
-        host_step()
+        for _ in range(max(args.warmup, 1)):
+            host_step()
         torch.cuda.synchronize()
         e_times, e_its = [], 0
         for _ in range(args.steps):

@@ -7,6 +7,7 @@ C ABI in include/krb.h).  Everything else in the reference (CLI, ILUTP,
 Matrix Market I/O, problem generators, bi-Lanczos harness) is out of scope.
 """
 
+from .device import prefetch_matrix
 from .operators import CountingOperator, as_operator
 from .recycling import (CapturedCycle, RecycleSpace, biorthonormalize,
                         project_initial, refresh_images)
@@ -29,5 +30,5 @@ __all__ = [
     "rbicgstab_solve_batch", "bicgstab_solve_batch",
     "CONVERGED", "MAX_ITN", "BREAKDOWN_SERIOUS", "BREAKDOWN_OMEGA",
     "BREAKDOWN_SECOND_KIND",
-    "SparseMatrix",
+    "SparseMatrix", "prefetch_matrix",
 ]

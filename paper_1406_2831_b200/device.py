@@ -110,9 +110,15 @@ class _Staging:
             self.events[i].synchronize()
         buf = self.bufs[i]
         if buf is None or buf.numel() < nbytes:
+            # both buffers at once (a page-locked allocation costs milliseconds:
+            # pay it once, not again on the first use of the other buffer)
             cap = max(nbytes, 1 << 24)
-            buf = t.empty(cap, dtype=t.uint8, pin_memory=True)
-            self.bufs[i] = buf
+            for j in (0, 1):
+                if self.events[j] is not None:
+                    self.events[j].synchronize()
+                if self.bufs[j] is None or self.bufs[j].numel() < cap:
+                    self.bufs[j] = t.empty(cap, dtype=t.uint8, pin_memory=True)
+            buf = self.bufs[i]
         return i, buf
 
     def mark(self, i):
@@ -192,13 +198,78 @@ def pinned_copy(a: np.ndarray) -> np.ndarray:
 
 
 def to_host(tensor) -> np.ndarray:
-    return tensor.detach().to("cpu").numpy()
+    """Device tensor -> host numpy through a page-locked buffer from torch's
+    caching host allocator: the device->host copy is plain DMA (a copy into
+    pageable memory is staged by the driver at a fraction of the link rate).
+    The returned array keeps the pinned buffer alive; freeing it returns the
+    buffer to the cache."""
+    t = torch()
+    src = tensor.detach()
+    if not src.is_cuda:
+        return src.numpy()
+    out = t.empty(src.shape, dtype=src.dtype, pin_memory=True)
+    out.copy_(src)   # synchronous: the data is on the host on return
+    return out.numpy()
+
+
+def _is_pinned(a) -> bool:
+    try:
+        return torch().from_numpy(np.ascontiguousarray(a)).is_pinned()
+    except Exception:
+        return False
+
+
+class _Prefetch:
+    """Host->device copies of a matrix's CSR arrays issued ahead of use on a
+    side copy stream (run_sequence prefetches matrix i+1 while system i
+    solves: the DMA overlaps the kernels).  Only page-locked inputs are
+    prefetched (their copies are pure DMA; pageable ones would stall the
+    host in the staging copy)."""
+
+    def __init__(self):
+        self.items = {}
+        self.stream = None
+
+    def issue(self, A) -> bool:
+        if getattr(A, "_device", None) is not None or not hasattr(A, "row_ptr"):
+            return False
+        if id(A) in self.items or MATRICES.items.get(id(A), (None,))[0] is A:
+            return False
+        arrs = (np.asarray(A.row_ptr), np.asarray(A.col_idx), np.asarray(A.values))
+        if np.iscomplexobj(arrs[2]) or not all(_is_pinned(a) for a in arrs):
+            return False
+        t = torch()
+        require_cuda()
+        if self.stream is None:
+            self.stream = t.cuda.Stream()
+        with t.cuda.stream(self.stream):
+            d_rp = to_device(arrs[0], np.int64)
+            d_ci = to_device(arrs[1], np.int32 if arrs[1].dtype == np.int32 else np.int64)
+            d_val = to_device(arrs[2], np.float64)
+            ev = t.cuda.Event()
+            ev.record(self.stream)
+        self.items[id(A)] = (A, (d_rp, d_ci, d_val), ev)
+        return True
+
+    def take(self, A):
+        hit = self.items.pop(id(A), None)
+        if hit is None or hit[0] is not A:
+            return None
+        t = torch()
+        cur = t.cuda.current_stream()
+        cur.wait_event(hit[2])
+        for d in hit[1]:
+            d.record_stream(cur)   # freed after this stream's use, not the copy stream's
+        return hit[1]
+
+    def clear(self):
+        self.items.clear()
 
 
 class DeviceMatrix:
     """A krb_matrix handle (device CSR / SELL-32 + lazily built transpose)."""
 
-    def __init__(self, n, row_ptr, col_idx, values, fmt: int = 0):
+    def __init__(self, n, row_ptr, col_idx, values, fmt: int = 0, uploaded=None):
         require_cuda()
         t = torch()
         self.n = int(n)
@@ -209,16 +280,15 @@ class DeviceMatrix:
         if np.iscomplexobj(values):
             raise NotImplementedError("complex matrices are out of scope on the "
                                       "device path (fp64 real only)")
-        d_rp = to_device(row_ptr, np.int64)
-        d_val = to_device(values, np.float64)
         h = ctypes.c_void_p()
         s = stream_ptr()
-        if col_idx.dtype == np.int32:
-            d_ci = to_device(col_idx, np.int32)
-            fn = "krb_matrix_create"
+        if uploaded is not None:
+            d_rp, d_ci, d_val = uploaded
         else:
-            d_ci = to_device(col_idx, np.int64)
-            fn = "krb_matrix_create_i64"
+            d_rp = to_device(row_ptr, np.int64)
+            d_val = to_device(values, np.float64)
+            d_ci = to_device(col_idx, np.int32 if col_idx.dtype == np.int32 else np.int64)
+        fn = "krb_matrix_create" if col_idx.dtype == np.int32 else "krb_matrix_create_i64"
         _lib.call(fn, ctypes.byref(h), self.n, self.nnz, ptr(d_rp), ptr(d_ci),
                   ptr(d_val), int(fmt), s)
         del d_rp, d_ci, d_val
@@ -291,6 +361,13 @@ class _MatrixCache:
 
 
 MATRICES = _MatrixCache()
+PREFETCH = _Prefetch()
+
+
+def prefetch_matrix(A) -> bool:
+    """Start the upload of A's CSR arrays ahead of its first solve (pinned
+    host inputs only); returns whether copies were issued."""
+    return PREFETCH.issue(A)
 
 
 def device_matrix(A) -> DeviceMatrix:
@@ -309,7 +386,7 @@ def device_matrix(A) -> DeviceMatrix:
         if n != ncols:
             raise ValueError("solver requires a square operator")
         return MATRICES.get(A, lambda: DeviceMatrix(n, A.row_ptr, A.col_idx,
-                                                    A.values))
+                                                    A.values, uploaded=PREFETCH.take(A)))
     if isinstance(A, np.ndarray):
         if A.ndim != 2 or A.shape[0] != A.shape[1]:
             raise ValueError("solver requires a square operator")

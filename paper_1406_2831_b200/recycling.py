@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .device import Context, device_matrix, ptr, stream_ptr, to_device, torch
+from .device import Context, device_matrix, ptr, stream_ptr, to_device, to_host, torch
 
 _BLOCKS = ("U", "Ut", "C", "Ct", "Chat", "Ccheck")
 
@@ -350,8 +350,8 @@ def project_initial(A, b, x_minus1, recycle):
         _meter(A, nm=1)
     R = RecycleSpace.of(recycle)
     if R is None or R.k == 0:
-        return x.cpu().numpy(), r.cpu().numpy()
+        return to_host(x), to_host(r)
     y = tdot(R.device("Chat"), r)
     x0 = gemv(R.device("U"), y, base=x, sign=+1)
     r0 = gemv(R.device("C"), y, base=r, sign=-1)
-    return x0.cpu().numpy(), r0.cpu().numpy()
+    return to_host(x0), to_host(r0)

@@ -105,10 +105,18 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
     gidx = 0
     total = seq.num_systems if systems is None else min(systems, seq.num_systems)
     t_start = time.perf_counter()
+    prefetch = getattr(api, "prefetch_matrix", None)
+    A_next = None
     for i in range(seq.num_matrices):
         if gidx >= total:
             break
-        A = api.SparseMatrix.from_csr(seq.matrix(i))
+        A = A_next if A_next is not None else api.SparseMatrix.from_csr(seq.matrix(i))
+        A_next = None
+        if prefetch is not None and i + 1 < seq.num_matrices and \
+                gidx + min(seq.rhs_per_matrix, total - gidx) < total:
+            # the next matrix's upload overlaps this matrix's solves
+            A_next = api.SparseMatrix.from_csr(seq.matrix(i + 1))
+            prefetch(A_next)
         op_rec = api.CountingOperator(A)
         op_base = api.CountingOperator(A)
         nk = min(seq.rhs_per_matrix, total - gidx)

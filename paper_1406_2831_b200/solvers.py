@@ -12,6 +12,7 @@ fallback): split preconditioning (``precond``), complex data, and
 from __future__ import annotations
 
 import ctypes
+import functools
 import time
 from dataclasses import dataclass, field
 
@@ -19,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .device import (Context, defer_launch, device_matrix, drop_pending, flush_pending,
-                     ptr, stream_ptr, to_device, torch)
+                     ptr, stream_ptr, to_device, to_host, torch)
 from .recycling import RecycleSpace
 
 CONVERGED = "converged"
@@ -99,6 +100,7 @@ def _pcg_advance(state: int, inc: int, steps: int) -> int:
     return (am * state + ap) & _M128
 
 
+@functools.lru_cache(maxsize=256)
 def pcg64_words(seed: int, skip: int = 0):
     """128-bit PCG64 (state, inc) numpy's default_rng(seed) is at after `skip`
     doubles were drawn; the device draw continues that exact stream
@@ -178,7 +180,7 @@ def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
     xd = _dev_vec(x_init)
     xo, hist = solve_device(M, bd, xd, recycle, cfg, label, t0, use_graph)
     _count(A, nm=LAST_SOLVE["matvecs"])
-    return (xo if _is_device(b) else xo.cpu().numpy()), hist
+    return (xo if _is_device(b) else to_host(xo)), hist
 
 
 def _graph_mode():
@@ -353,7 +355,7 @@ def _batch_solve(A, bs, x_inits, recycle, configs, label):
         xds = [_dev_vec(x_inits[j]) for j in chunk]
         res = solve_device_batch(M, bds, xds, recycle, [configs[j] for j in chunk], label, t0)
         _count(A, nm=LAST_SOLVE["matvecs"])
-        out += [(x if on_device else x.cpu().numpy(), h) for x, h in res]
+        out += [(x if on_device else to_host(x), h) for x, h in res]
     return out
 
 
@@ -595,4 +597,4 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     _count(A, nm=int(counts[0]), nr=int(counts[1]))
     if on_device:
         return xo, xto, hist, harvest.cycles
-    return xo.cpu().numpy(), xto.cpu().numpy(), hist, harvest.cycles
+    return to_host(xo), to_host(xto), hist, harvest.cycles

@@ -267,3 +267,32 @@ def test_near_null_eligibility_subset_bitwise(P, canon, near):
         got = UP.near_null_eligibility(theta, VR, Wd, AWd, res_tol)
         want = O.near_null_eligibility(theta, VR, W, AW, res_tol, canon)
         assert np.array_equal(got, want), (near, res_tol)
+
+
+def test_sequence_with_pinned_inputs_prefetches_and_matches(P):
+    """Page-locked host matrices are uploaded one system ahead on a side copy
+    stream (device.prefetch_matrix); the results equal the pageable run's."""
+    from paper_1406_2831_b200 import device as D
+    from paper_1406_2831_b200.sequence import run_sequence
+    from paper_1406_2831_b200.workloads import CSR, SequenceSpec, make_sequence
+    seq = make_sequence("c2", small=True)
+    nm = seq.num_matrices
+    mats = {i: seq.matrix(i) for i in range(nm)}
+    pm = {i: CSR(A.n, D.pinned_copy(A.row_ptr), D.pinned_copy(A.col_idx),
+                 D.pinned_copy(A.values)) for i, A in mats.items()}
+    pseq = SequenceSpec(seq.name, seq.n, seq.k, seq.tol, nm, seq.rhs_per_matrix,
+                        lambda i: pm[i], seq.rhs, s=seq.s, max_itn=seq.max_itn,
+                        meta=seq.meta)
+    issued = []
+    orig = D.PREFETCH.issue
+    D.PREFETCH.issue = lambda A: issued.append(orig(A)) or issued[-1]
+    try:
+        r_p = run_sequence(pseq, baseline=False)
+    finally:
+        D.PREFETCH.issue = orig
+    assert issued and all(issued), issued
+    assert not D.PREFETCH.items
+    r_g = run_sequence(seq, baseline=False)
+    assert len(r_p.recycling.histories) == len(r_g.recycling.histories) == nm
+    for hp, hg in zip(r_p.recycling.histories, r_g.recycling.histories):
+        assert hp.status == hg.status and hp.resid == hg.resid and hp.matvecs == hg.matvecs

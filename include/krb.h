@@ -129,6 +129,12 @@ int krb_ritz_combine(int64_t n, int64_t m, const double *d_Yre,
 /* X[:, j] *= 1/s[j] done as a division X[i,j] / s[j] (recycling.py:156,337) */
 int krb_colscale_div(int64_t n, int64_t k, double *d_X, int64_t ldx,
                      const double *d_s, void *stream);
+/* Y[:, j] = X[:, j] / s[j], out of place: the column scaling of
+ * recycling.py:156,337 fused with the assembly of W = [U_prev, V] (the
+ * hstacks of recycling.py:326-329) or with the Chat / Ccheck copies
+ * (recycling.py:168-169) -- one read and one write per element */
+int krb_colscale_div_to(int64_t n, int64_t k, const double *d_X, int64_t ldx,
+                        const double *d_s, double *d_Y, int64_t ldy, void *stream);
 /* numpy default_rng(seed).uniform(lo, hi, n), bit-identical: PCG64
  * (XSL-RR) from the 128-bit (state, inc) that numpy seeds
  * (solvers.py:111-113, 268-269). */

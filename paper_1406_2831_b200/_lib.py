@@ -91,6 +91,7 @@ SIGNATURES = {
                          c_vp]),
     "krb_colnorms": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "krb_colscale_div": (c_int, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "krb_colscale_div_to": (c_int, [c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "krb_uniform_pcg64": (c_int, [c_i64, c_u64, c_u64, c_u64, c_u64, c_dbl,
                                   c_dbl, c_vp, c_vp]),
     "krb_rbicgstab": (c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(SpaceView),

@@ -437,11 +437,14 @@ static bool gemm_tiled(int64_t n, int64_t m, int64_t nc, const double *d_X, int6
 
 // X[:, j] /= s[j]: column j on blockIdx.y (no per-element index division);
 // each thread divides four elements 256 apart, loads issued together
-__global__ void __launch_bounds__(256) k_colscale_div(int64_t n, int k, double *X,
+// Y[:, j] = X[:, j] / s[j] (Y == X: in place; otherwise Y must not overlap X)
+__global__ void __launch_bounds__(256) k_colscale_div(int64_t n, int k, const double *X,
                                                       int64_t ldx,
-                                                      const double *__restrict__ s) {
+                                                      const double *__restrict__ s,
+                                                      double *Y, int64_t ldy) {
   const int j = blockIdx.y;
-  double *col = X + (int64_t)j * ldx;
+  const double *src = X + (int64_t)j * ldx;
+  double *col = Y + (int64_t)j * ldy;
   const double d = __ldg(s + j);
   for (int64_t i0 = (int64_t)blockIdx.x * 1024 + threadIdx.x; i0 < n;
        i0 += (int64_t)gridDim.x * 1024) {
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(256) k_colscale_div(int64_t n, int k, double *
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t i = i0 + 256 * q;
-      v[q] = i < n ? col[i] : 0.0;
+      v[q] = i < n ? src[i] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -752,7 +755,19 @@ int krb_colscale_div(int64_t n, int64_t k, double *d_X, int64_t ldx,
   KRB_REQUIRE(k <= 65535, "krb_colscale_div: more than 65535 columns");
   const int64_t blocks = (n + 1023) / 1024;
   dim3 grid((unsigned)(blocks < 65535 ? blocks : 65535), (unsigned)k);
-  k_colscale_div<<<grid, 256, 0, as_stream(stream)>>>(n, (int)k, d_X, ldx, d_s);
+  k_colscale_div<<<grid, 256, 0, as_stream(stream)>>>(n, (int)k, d_X, ldx, d_s, d_X, ldx);
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
+int krb_colscale_div_to(int64_t n, int64_t k, const double *d_X, int64_t ldx,
+                        const double *d_s, double *d_Y, int64_t ldy, void *stream) {
+  KRB_REQUIRE(ldx >= n && ldy >= n, "krb_colscale_div_to: leading dimension < n");
+  if (n * k == 0) return KRB_OK;
+  KRB_REQUIRE(k <= 65535, "krb_colscale_div_to: more than 65535 columns");
+  const int64_t blocks = (n + 1023) / 1024;
+  dim3 grid((unsigned)(blocks < 65535 ? blocks : 65535), (unsigned)k);
+  k_colscale_div<<<grid, 256, 0, as_stream(stream)>>>(n, (int)k, d_X, ldx, d_s, d_Y, ldy);
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }

@@ -232,6 +232,36 @@ def colscale_div(X_dev, s_dev):
     return X_dev
 
 
+def colscale_div_to(X_dev, s_dev, out=None):
+    """out[j] = X[j] / s[j] (a new block unless ``out`` is given): the scaled
+    copy in one read and one write."""
+    t = torch()
+    k, n = X_dev.shape
+    if out is None:
+        out = t.empty((k, n), dtype=t.float64, device="cuda")
+    if k:
+        _lib.call("krb_colscale_div_to", n, k, ptr(X_dev), _ld(X_dev), ptr(s_dev),
+                  ptr(out), _ld(out), stream_ptr())
+    return out
+
+
+def assemble_scaled(parts, scales):
+    """[parts...] stacked along the column axis and divided column-wise by
+    ``scales`` (the hstack + column scaling of recycling.py:326-340) in one
+    pass per part, without materialising the unscaled concatenation."""
+    t = torch()
+    n = parts[0].shape[1]
+    m = sum(p.shape[0] for p in parts)
+    out = t.empty((m, n), dtype=t.float64, device="cuda")
+    o = 0
+    for p in parts:
+        kp = p.shape[0]
+        if kp:
+            colscale_div_to(p, scales[o:o + kp], out[o:o + kp])
+        o += kp
+    return out
+
+
 def dot(x_dev, y_dev):
     t = torch()
     out = t.empty(1, dtype=t.float64, device="cuda")
@@ -321,8 +351,8 @@ def biorthonormalize(U_raw, Ut_raw, A, C_raw=None, Ct_raw=None,
         U, C, Ut, Ct = (B.index_select(0, idx).contiguous() for B in (U, C, Ut, Ct))
         Dc = Dc[keep]
     Dc_d = to_device(Dc)
-    Chat = colscale_div(Ct.clone(), Dc_d)
-    Ccheck = colscale_div(C.clone(), Dc_d)
+    Chat = colscale_div_to(Ct, Dc_d)
+    Ccheck = colscale_div_to(C, Dc_d)
     return RecycleSpace(_dev=dict(U=U, Ut=Ut, C=C, Ct=Ct, Chat=Chat, Ccheck=Ccheck),
                         _n=n, Dc=Dc)
 

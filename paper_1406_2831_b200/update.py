@@ -17,8 +17,8 @@ import numpy as np
 
 from . import _lib
 from .device import device_matrix, flush_pending, ptr, stream_ptr, to_device, torch
-from .recycling import (RecycleSpace, _as_block, _ctx, _ld, _meter,
-                        biorthonormalize, colnorms, colscale_div, gemm, gram)
+from .recycling import (RecycleSpace, _as_block, _ctx, _ld, _meter, assemble_scaled,
+                        biorthonormalize, colnorms, gemm, gram)
 
 NEAR_NULL_FRAC = 1e-3   # recycling.py:228
 
@@ -159,17 +159,16 @@ def update_recycle_space(A, cycles, previous, k: int, rank_tol: float = 1e-12,
         _meter(A, nm=V.shape[0], nr=Vt.shape[0])
     if not bu:
         return prev if prev is not None else RecycleSpace.empty(n)
-    W, Wt = t.cat(bu, 0), t.cat(but, 0)
-    AW, AhWt = t.cat(bc, 0), t.cat(bct, 0)
-    # column scaling (recycling.py:333-340)
-    # scales stay on the device (a zero norm divides by 1, as the reference)
-    swd, std_ = colnorms(W), colnorms(Wt)
+    # hstack + column scaling (recycling.py:326-340): norms per part (each
+    # column's canonical dot is independent of its neighbours), then one
+    # scaled copy per part into the assembled block; the scales stay on the
+    # device (a zero norm divides by 1, as the reference)
+    swd = t.cat([colnorms(B.contiguous() if B.stride(-1) != 1 else B) for B in bu])
+    std_ = t.cat([colnorms(B.contiguous() if B.stride(-1) != 1 else B) for B in but])
     swd.masked_fill_(swd == 0, 1.0)
     std_.masked_fill_(std_ == 0, 1.0)
-    colscale_div(W, swd)
-    colscale_div(AW, swd)
-    colscale_div(Wt, std_)
-    colscale_div(AhWt, std_)
+    W, AW = assemble_scaled(bu, swd), assemble_scaled(bc, swd)
+    Wt, AhWt = assemble_scaled(but, std_), assemble_scaled(bct, std_)
     G2 = t.stack([gram(Wt, AW), gram(Wt, W)]).cpu().numpy()   # one read
     GA, GI = G2[0].copy(), G2[1].copy()
     import scipy.linalg as la

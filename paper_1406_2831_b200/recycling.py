@@ -127,12 +127,22 @@ class RecycleSpace:
 class CapturedCycle:
     """Lanczos-direction block of one harvest window (recycling.py:80-102).
     V / Vt are (ncols, n) device tensors (column-major n x ncols); ``tri``
-    holds the (sub, diag, super) recurrence coefficients (host)."""
+    holds the (sub, diag, super) recurrence coefficients (host).  ``tri``
+    may be given as a zero-argument callable: it is then evaluated on first
+    access (the recycle update never reads it, so the harvest path does not
+    pay for it)."""
 
     V_dev: object
     Vt_dev: object
-    tri: np.ndarray
+    tri: object
     first_index: int
+
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if name == "tri" and callable(v):
+            v = v()
+            object.__setattr__(self, "tri", v)
+        return v
 
     @property
     def V(self):

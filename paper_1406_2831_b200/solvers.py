@@ -455,9 +455,10 @@ class _CycleHarvest:
         _lib.copy_d2d(Vtd, self.ptrs[1], ncols * n)
         rhos, alphas, betas = _lib.fetch_f64_many(
             [(self.ptrs[2], npush), (self.ptrs[3], nalpha), (self.ptrs[4], nalpha)])
-        cyc = self.CapturedCycle(V_dev=Vd, Vt_dev=Vtd,
-                                 tri=_tri_block(self.start, ncols, alphas, betas, rhos),
-                                 first_index=self.start)
+        start = self.start
+        cyc = self.CapturedCycle(
+            V_dev=Vd, Vt_dev=Vtd, first_index=start,
+            tri=lambda: _tri_block(start, ncols, alphas, betas, rhos))   # lazy
         self.cycles.append(cyc)
         self.emitted = last
         if not final and ncols > 2:

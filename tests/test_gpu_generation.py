@@ -127,6 +127,9 @@ def test_rbicg_harvest_bitwise_vs_canon_oracle(P, canon, cfg, k):
     for cg, co in zip(cyc_g, cyc_o):
         assert cg.first_index == co.first_index
         assert np.array_equal(cg.V, co.V) and np.array_equal(cg.Vt, co.Vt)
+        tri = cg.tri   # lazily built on first access (solvers.py:524-540)
+        assert isinstance(tri, np.ndarray) and tri.shape == (3, cg.ncols)
+        assert cg.tri is tri and np.isfinite(tri[1, :-1]).all()
     assert dims_g == dims_o
     assert (Ag.n_matvec, Ag.n_rmatvec) == (Ao.n_matvec, Ao.n_rmatvec)
     if st_g["s"] is not None and st_g["s"].k:

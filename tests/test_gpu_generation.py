@@ -299,3 +299,44 @@ def test_sequence_with_pinned_inputs_prefetches_and_matches(P):
     assert len(r_p.recycling.histories) == len(r_g.recycling.histories) == nm
     for hp, hg in zip(r_p.recycling.histories, r_g.recycling.histories):
         assert hp.status == hg.status and hp.resid == hg.resid and hp.matvecs == hg.matvecs
+
+
+def test_rbicg_deferred_cycle_launch_paths(P, canon):
+    """The next harvest cycle is launched when the callback starts host work
+    (device.flush_pending), right after a callback that never flushes, or
+    immediately without a callback: the solve is the same in every case; a
+    callback that raises drops the deferred launch and the next solve runs."""
+    from paper_1406_2831_b200 import device as D
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence("c2", small=True)
+    A, b = seq.matrix(0), seq.rhs(0, 0)
+    cfg = P.SolverConfig(tol=seq.tol, max_itn=600, k=8, s=25, seed=0)
+    ones = np.ones(A.n)
+
+    def run(cb):
+        return P.rbicg_solve(P.SparseMatrix.from_csr(A), b, b_dual=ones, config=cfg,
+                             cycle_callback=cb)
+
+    seen = []
+    ref = run(None)
+    flushed = run(lambda c: (D.flush_pending(), seen.append(c.first_index)))
+    plain = run(lambda c: seen.append(-c.first_index))
+    for out in (flushed, plain):
+        assert out[2].resid == ref[2].resid and out[2].matvecs == ref[2].matvecs
+        assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
+        assert [c.first_index for c in out[3]] == [c.first_index for c in ref[3]]
+        for c1, c2 in zip(out[3], ref[3]):
+            assert np.array_equal(c1.V, c2.V)
+    assert len(ref[3]) > 1 and len(seen) == 2 * len(ref[3])
+
+    class Boom(Exception):
+        pass
+
+    def bad(c):
+        raise Boom()
+
+    with pytest.raises(Boom):
+        run(bad)
+    assert not D._PENDING
+    again = run(None)
+    assert again[2].resid == ref[2].resid

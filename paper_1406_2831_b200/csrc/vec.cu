@@ -493,23 +493,26 @@ __device__ inline uint64_t pcg_out(u128 s) {
   return (x >> rot) | (x << ((64 - rot) & 63));
 }
 
-// element i uses state LCG^(i+1)(s0); thread g handles i = g, g+T, ...
+// element i uses state LCG^(i+1)(s0); thread g handles the run
+// i = g L .. g L + L - 1: one jump to its start, then single LCG steps (a
+// jump per element costs ~18 dependent 128-bit multiply-adds)
+constexpr int kPcgRun = 16;
 __global__ void k_pcg64_uniform(int64_t n, uint64_t s_hi, uint64_t s_lo,
                                 uint64_t i_hi, uint64_t i_lo, double lo,
                                 double range, double *out) {
   const u128 mult = mk128(kPcgMulHi, kPcgMulLo), inc = mk128(i_hi, i_lo);
-  const int64_t T = (int64_t)gridDim.x * blockDim.x;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
-  u128 A, C, AT, CT;
-  pcg_jump(mult, inc, (uint64_t)g + 1, &A, &C);
+  const int64_t i0 = g * kPcgRun;
+  if (i0 >= n) return;
+  u128 A, C;
+  pcg_jump(mult, inc, (uint64_t)i0 + 1, &A, &C);
   u128 s = A * mk128(s_hi, s_lo) + C;
-  pcg_jump(mult, inc, (uint64_t)T, &AT, &CT);
-  for (int64_t i = g; i < n; i += T) {
+  const int64_t i1 = i0 + kPcgRun < n ? i0 + kPcgRun : n;
+  for (int64_t i = i0; i < i1; ++i) {
     uint64_t r = pcg_out(s);
     double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
     out[i] = __dadd_rn(lo, __dmul_rn(range, u));
-    s = AT * s + CT;
+    s = mult * s + inc;
   }
 }
 
@@ -776,9 +779,10 @@ int krb_uniform_pcg64(int64_t n, uint64_t state_hi, uint64_t state_lo,
                       uint64_t inc_hi, uint64_t inc_lo, double lo, double hi,
                       double *d_out, void *stream) {
   if (n <= 0) return KRB_OK;
-  int64_t blocks = (n + 255) / 256;
-  int grid = (int)(blocks < kNumSMs * 8 ? blocks : kNumSMs * 8);
-  k_pcg64_uniform<<<grid, 256, 0, as_stream(stream)>>>(
+  const int64_t threads = (n + kPcgRun - 1) / kPcgRun;
+  const int64_t grid = (threads + 255) / 256;
+  KRB_REQUIRE(grid < (int64_t)1 << 31, "krb_uniform_pcg64: n too large");
+  k_pcg64_uniform<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(
       n, state_hi, state_lo, inc_hi, inc_lo, lo, hi - lo, d_out);
   KRB_CHECK_LAUNCH();
   return KRB_OK;

@@ -166,3 +166,47 @@ def test_colscale_div_bitwise(dev, n, k):
     Xd = _cols(X)
     R.colscale_div(Xd, _tensor(sv))
     assert np.array_equal(Xd.cpu().numpy().T, X / sv)
+
+
+@pytest.mark.parametrize("n,parts", [(1, [1]), (1_000, [3, 2]), (262_144, [20, 27]),
+                                     (70_001, [0, 5, 7])])
+def test_assemble_scaled_bitwise(dev, n, parts):
+    """[parts] stacked and divided column-wise (the hstack + scaling of
+    recycling.py:326-340 done as scaled copies, krb_colscale_div_to): the
+    same bits as numpy's hstack then division; sources untouched."""
+    from paper_1406_2831_b200 import recycling as R
+    r = np.random.default_rng(n + len(parts))
+    blocks = [r.standard_normal((n, k)) for k in parts]
+    m = sum(parts)
+    sv = r.uniform(0.1, 10.0, size=m)
+    devs = [_cols(B) for B in blocks]
+    before = [d.clone() for d in devs]
+    out = R.assemble_scaled(devs, _tensor(sv))
+    assert np.array_equal(out.cpu().numpy().T, np.hstack(blocks) / sv)
+    for d, b0 in zip(devs, before):
+        assert np.array_equal(d.cpu().numpy(), b0.cpu().numpy())
+    C = blocks[-1]
+    got = R.colscale_div_to(_cols(C), _tensor(sv[-C.shape[1]:] if C.shape[1] else sv[:0]))
+    assert np.array_equal(got.cpu().numpy().T, C / sv[m - C.shape[1]:])
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4"])
+def test_spmv_adjoint_and_linearity(dev, cfg):
+    """The reference's operator properties (tests/test_sparse.py:78-102):
+    (A x, y) = (x, A^T y) and A (a x + b y) = a A x + b A y, to rounding."""
+    import torch
+    from paper_1406_2831_b200 import device as D
+    from paper_1406_2831_b200.workloads import make_sequence
+    A = make_sequence(cfg, small=True).matrix(0)
+    M = D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+    r = np.random.default_rng(3)
+    x, y = r.standard_normal(A.n), r.standard_normal(A.n)
+    xd, yd = _tensor(x), _tensor(y)
+    Ax = M.spmv(xd).cpu().numpy()
+    Aty = M.spmv(yd, transpose=True).cpu().numpy()
+    lhs, rhs = Ax @ y, x @ Aty
+    assert abs(lhs - rhs) <= 1e-12 * (np.abs(Ax) @ np.abs(y) + 1.0)
+    a, b = 0.75, -1.25
+    comb = M.spmv(_tensor(a * x + b * y)).cpu().numpy()
+    Ay = M.spmv(yd).cpu().numpy()
+    assert np.allclose(comb, a * Ax + b * Ay, rtol=1e-12, atol=1e-12 * np.abs(Ax).max())

@@ -546,13 +546,14 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
         harvest = _CycleHarvest(H, n, cycle_callback)
         state = (ctypes.c_int64 * 7)()
         launched = ctypes.c_int32()
+        st = stream_ptr()   # the solve's stream, fixed even if a callback switches streams
 
         def launch_next():
-            _lib.call("krb_rbicg_launch", H, ctypes.byref(launched), stream_ptr())
+            _lib.call("krb_rbicg_launch", H, ctypes.byref(launched), st)
 
         launch_next()
         while True:
-            _lib.call("krb_rbicg_wait", H, state, stream_ptr())
+            _lib.call("krb_rbicg_wait", H, state, st)
             running = state[0] == 0
             if state[1]:
                 harvest.emit(state, final=False,

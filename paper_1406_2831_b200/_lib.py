@@ -179,12 +179,11 @@ def launch_count() -> int:
 def copy_d2d(dst_tensor, src_addr: int, count: int):
     """Device-to-device copy of `count` doubles from a raw device address
     (libkrb ring views) into a torch tensor, on the current stream."""
-    import torch
     if count <= 0:
         return
+    from .device import stream_ptr
     call("krb_memcpy_d2d", ctypes.c_void_p(dst_tensor.data_ptr()),
-         ctypes.c_void_p(src_addr), 8 * count,
-         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+         ctypes.c_void_p(src_addr), 8 * count, stream_ptr())
 
 
 def fetch_f64(src_addr: int, count: int):

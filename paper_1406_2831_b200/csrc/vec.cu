@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(256) k_gram_part(
 // stride (conflict-free: the 16 distinct columns a warp reads hit distinct
 // banks) by per-thread cp.async, double-buffered so the next sub-tile loads
 // while this one is consumed.  FP64-FMA bound (m x m x n fma per Gram).
-constexpr int kGemmCT = 8;
 constexpr int kGT = 64;
 constexpr int kGS = kGT + 1;   // odd column stride in shared memory
 template <int T>
@@ -226,6 +225,119 @@ __global__ void __launch_bounds__(256) k_gram_rt(int64_t n, int64_t R, int64_t n
         if (a < na && c < nc) part[(int64_t)(a * nc + c) * nch + ch] = acc[i][j];
       }
   }
+}
+
+// Gram chunk partials, 64-thread groups (same order as k_gram_part): each
+// group of 64 threads (an 8 x 8 grid) owns one chunk at a time, thread
+// (ty, tx) the T x T entries (ty + 8 i, tx + 8 j), so a row costs 2T
+// shared-memory doubles for T^2 fmas (T = 6 at m = 47: 12 per 36, vs 6 per
+// 9 with 256 threads per chunk).  Rows are read in pairs as 16-byte loads
+// from kGT2-row sub-tiles staged column-major with stride kGT2 + 2 (odd in
+// 16-byte units: the 8 distinct columns a warp reads fall in distinct bank
+// groups), double-buffered per group by per-thread cp.async; groups
+// synchronise on their own named barrier, so the G groups of a CTA run
+// independently.  kGT2 = 16 and <= 128 registers keep two CTAs (16 warps)
+// per SM.
+template <int T, int G, int kGT2>
+__global__ void __launch_bounds__(64 * G, 2) k_gram_g(int64_t n, int64_t R, int64_t nch, int na,
+                                                   int nc, const double *__restrict__ X,
+                                                   int64_t ldx, const double *__restrict__ Y,
+                                                   int64_t ldy, double *__restrict__ part) {
+  extern __shared__ double2 sm2[];
+  constexpr int kGS2 = kGT2 + 2;
+  constexpr int W = 8 * T;                  // staged columns of X and of Y
+  constexpr int kBuf = 2 * W * kGS2;        // doubles per buffer (X then Y)
+  const int g = threadIdx.x >> 6, lt = threadIdx.x & 63, tx = lt & 7, ty = lt >> 3;
+  double *gsm = reinterpret_cast<double *>(sm2) + (size_t)g * 2 * kBuf;
+  const uint64_t pol = l2_policy(false);
+  auto gsync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(g + 1) : "memory"); };
+  for (int64_t ch = (int64_t)blockIdx.x * G + g; ch < nch; ch += (int64_t)gridDim.x * G) {
+    const int64_t r0 = ch * R;
+    const int64_t r1 = min(n, r0 + R);
+    const int nsub = (int)((r1 - r0 + kGT2 - 1) / kGT2);
+    auto stage = [&](int sub, int buf) {
+      const int64_t t0 = r0 + (int64_t)sub * kGT2;
+      const int rows = (int)min((int64_t)kGT2, r1 - t0);
+      double *xs = gsm + buf * kBuf, *ys = xs + W * kGS2;
+      for (int idx = lt; idx < W * kGT2; idx += 64) {
+        const int a = idx / kGT2, rr = idx % kGT2;
+        const bool okx = a < na && rr < rows, oky = a < nc && rr < rows;
+        cp_async8(xs + a * kGS2 + rr, X + (okx ? (int64_t)a * ldx + t0 + rr : 0), okx, pol);
+        cp_async8(ys + a * kGS2 + rr, Y + (oky ? (int64_t)a * ldy + t0 + rr : 0), oky, pol);
+      }
+      cp_async_commit();
+    };
+    double acc[T][T];
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+      for (int j = 0; j < T; ++j) acc[i][j] = 0.0;
+    gsync();   // the group's previous chunk readers are done with both buffers
+    stage(0, 0);
+    for (int sub = 0; sub < nsub; ++sub) {
+      if (sub + 1 < nsub) {
+        stage(sub + 1, (sub + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      gsync();
+      const double *xs = gsm + (sub & 1) * kBuf, *ys = xs + W * kGS2;
+      const int rows = (int)min((int64_t)kGT2, r1 - (r0 + (int64_t)sub * kGT2));
+      int rr = 0;
+      for (; rr + 1 < rows; rr += 2) {
+        double2 xv[T], yv[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+          xv[i] = *reinterpret_cast<const double2 *>(xs + (ty + 8 * i) * kGS2 + rr);
+#pragma unroll
+        for (int j = 0; j < T; ++j)
+          yv[j] = *reinterpret_cast<const double2 *>(ys + (tx + 8 * j) * kGS2 + rr);
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+#pragma unroll
+          for (int j = 0; j < T; ++j) acc[i][j] = __fma_rn(xv[i].x, yv[j].x, acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+#pragma unroll
+          for (int j = 0; j < T; ++j) acc[i][j] = __fma_rn(xv[i].y, yv[j].y, acc[i][j]);
+      }
+      if (rr < rows) {
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+#pragma unroll
+          for (int j = 0; j < T; ++j)
+            acc[i][j] = __fma_rn(xs[(ty + 8 * i) * kGS2 + rr], ys[(tx + 8 * j) * kGS2 + rr],
+                                 acc[i][j]);
+      }
+      gsync();   // buffer (sub & 1) is refilled two sub-tiles later
+    }
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+      for (int j = 0; j < T; ++j) {
+        const int a = ty + 8 * i, c = tx + 8 * j;
+        if (a < na && c < nc) part[(int64_t)(a * nc + c) * nch + ch] = acc[i][j];
+      }
+  }
+}
+
+template <int T, int G, int S>
+static int launch_gram_g(int64_t n, int64_t R, int64_t nch, int na, int nc, const double *X,
+                         int64_t ldx, const double *Y, int64_t ldy, double *part,
+                         cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)G * 2 * 2 * 8 * T * (S + 2);   // G x 2 buffers x (X, Y)
+  KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_g<T, G, S>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  KRB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram_g<T, G, S>, 64 * G,
+                                                               smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (nch + G - 1) / G;
+  const int64_t cap = (int64_t)kNumSMs * per_sm;
+  const int grid = (int)(want < cap ? want : cap);
+  k_gram_g<T, G, S><<<grid, 64 * G, smem, st>>>(n, R, nch, na, nc, X, ldx, Y, ldy, part);
+  return KRB_OK;
 }
 
 // out[i + c*ldo] = sum_j X[i + j*ldx] Z[j*nc + c]  (sequential fma, j order)
@@ -690,6 +802,27 @@ int krb_gram(krb_context *ctx, int64_t n, int64_t na, int64_t nc,
   }
   int rc = ctx_reserve_part(ctx, (size_t)(ne * nch));
   if (rc) return rc;
+  // m <= 48: 64-thread groups (k_gram_g, 6 x 6 tiles at m = 47: 135 -> 114 us
+  // at 262144 rows); m <= 64: 256 threads per chunk (k_gram_rt: 16 x 16 tiles
+  // of 4 x 4 hold their own at m = 60, 9.0 ms vs 9.4 ms at C5's 16.8 M rows)
+  const int64_t T8 = ((na > nc ? na : nc) + 7) / 8;
+  if (T8 <= 6) {
+    int rc = KRB_OK;
+#define KRB_GRAM_G(TT)                                                                      \
+  rc = launch_gram_g<TT, 4, 16>(n, R, nch, (int)na, (int)nc, d_X, ldx, d_Y, ldy, ctx->part, st)
+    switch (T8) {
+      case 1: KRB_GRAM_G(1); break;
+      case 2: KRB_GRAM_G(2); break;
+      case 3: KRB_GRAM_G(3); break;
+      case 4: KRB_GRAM_G(4); break;
+      case 5: KRB_GRAM_G(5); break;
+      default: KRB_GRAM_G(6); break;
+    }
+#undef KRB_GRAM_G
+    if (rc) return rc;
+    KRB_CHECK_LAUNCH();
+    return launch_final((int)ne, nch, ctx->part, d_G, st);
+  }
   const int64_t T = ((na > nc ? na : nc) + 15) / 16;
   if (T <= 4) {
     const size_t smem = sizeof(double) * 2 * 2 * 16 * T * kGS;

@@ -23,11 +23,21 @@ def torch():
     return _torch
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    """Raise KrbError without a CUDA device (no CPU fallback).  The positive
+    answer is cached: torch.cuda.is_available() re-queries NVML / the
+    environment on every call (~0.1 ms), and this runs once per entry point."""
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     t = torch()
     if not t.cuda.is_available():
         raise _lib.KrbError("no CUDA device: the B200 path has no CPU fallback")
     _lib.load()
+    _CUDA_OK = True
 
 
 def stream_ptr():

@@ -286,21 +286,19 @@ __global__ void __launch_bounds__(64 * G, 2) k_gram_g(int64_t n, int64_t R, int6
       const int rows = (int)min((int64_t)kGT2, r1 - (r0 + (int64_t)sub * kGT2));
       int rr = 0;
       for (; rr + 1 < rows; rr += 2) {
-        double2 xv[T], yv[T];
+        // y column by column: its loads overlap the previous column's fmas
+        double2 xv[T];
 #pragma unroll
         for (int i = 0; i < T; ++i)
           xv[i] = *reinterpret_cast<const double2 *>(xs + (ty + 8 * i) * kGS2 + rr);
 #pragma unroll
-        for (int j = 0; j < T; ++j)
-          yv[j] = *reinterpret_cast<const double2 *>(ys + (tx + 8 * j) * kGS2 + rr);
+        for (int j = 0; j < T; ++j) {
+          const double2 yv = *reinterpret_cast<const double2 *>(ys + (tx + 8 * j) * kGS2 + rr);
 #pragma unroll
-        for (int i = 0; i < T; ++i)
+          for (int i = 0; i < T; ++i) acc[i][j] = __fma_rn(xv[i].x, yv.x, acc[i][j]);
 #pragma unroll
-          for (int j = 0; j < T; ++j) acc[i][j] = __fma_rn(xv[i].x, yv[j].x, acc[i][j]);
-#pragma unroll
-        for (int i = 0; i < T; ++i)
-#pragma unroll
-          for (int j = 0; j < T; ++j) acc[i][j] = __fma_rn(xv[i].y, yv[j].y, acc[i][j]);
+          for (int i = 0; i < T; ++i) acc[i][j] = __fma_rn(xv[i].y, yv.y, acc[i][j]);
+        }
       }
       if (rr < rows) {
 #pragma unroll
@@ -425,6 +423,39 @@ __device__ __forceinline__ void tma_1d(double *dst, const double *src, unsigned 
       : "memory");
 }
 
+// Two adjacent rows per thread (i, i + 1): each broadcast Z load feeds 2 x 2
+// fmas instead of 2, the X pair is one 16-byte load.  Same per-entry order.
+template <int kCT>
+__device__ __forceinline__ void gemm_tile_rows2(const double *xs, int T, int r, int g, int m,
+                                                int nc, int ncp, const double2 *dsm2,
+                                                double *out, int64_t ldo, int64_t i,
+                                                int64_t nrows) {
+  const int c0 = g * kCT;
+  double a0[kCT], a1[kCT];
+#pragma unroll
+  for (int t = 0; t < kCT; ++t) a0[t] = a1[t] = 0.0;
+  const double2 *zrow = dsm2 + (c0 >> 1);
+#pragma unroll 2
+  for (int j = 0; j < m; ++j) {
+    const double2 xv = *reinterpret_cast<const double2 *>(xs + j * T + r);
+    const double2 *zr = zrow + j * (ncp >> 1);
+#pragma unroll
+    for (int t = 0; t < kCT / 2; ++t) {
+      const double2 z = zr[t];
+      a0[2 * t] = __fma_rn(xv.x, z.x, a0[2 * t]);
+      a0[2 * t + 1] = __fma_rn(xv.x, z.y, a0[2 * t + 1]);
+      a1[2 * t] = __fma_rn(xv.y, z.x, a1[2 * t]);
+      a1[2 * t + 1] = __fma_rn(xv.y, z.y, a1[2 * t + 1]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kCT; ++t)
+    if (c0 + t < nc) {
+      if (nrows > 0) out[(int64_t)(c0 + t) * ldo + i] = a0[t];
+      if (nrows > 1) out[(int64_t)(c0 + t) * ldo + i + 1] = a1[t];
+    }
+}
+
 template <int kCT>
 __device__ __forceinline__ void gemm_tile_rows(const double *xs, int T, int r, int g, int m,
                                                int nc, int ncp, const double2 *dsm2,
@@ -450,7 +481,7 @@ __device__ __forceinline__ void gemm_tile_rows(const double *xs, int T, int r, i
     if (c0 + t < nc) out[(int64_t)(c0 + t) * ldo + i] = acc[t];
 }
 
-template <int kCT>
+template <int kCT, int RPT>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(int64_t n, int m, int nc, int lgT,
                                                    const double *__restrict__ X, int64_t ldx,
                                                    const double *__restrict__ Z,
@@ -473,7 +504,8 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(int64_t n, int m, int nc, int
   }
   __syncthreads();
   const int64_t nfull = n >> lgT;
-  const int r = threadIdx.x & (T - 1), g = threadIdx.x >> lgT;   // row in tile, column group
+  // row in tile (RPT adjacent rows per thread), column group
+  const int r = (threadIdx.x & ((T / RPT) - 1)) * RPT, g = threadIdx.x >> (lgT - (RPT - 1));
   const int ngroups = ncp / kCT;
   const int per = m << lgT;
   const unsigned tile_bytes = (unsigned)per * 8u;
@@ -492,9 +524,14 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(int64_t n, int m, int nc, int
     if (threadIdx.x == 0 && tile + gridDim.x < nfull) issue(tile + gridDim.x, buf ^ 1);
     mbar_wait(&bar[buf], (ph >> buf) & 1u);
     ph ^= 1u << buf;
-    if (g < ngroups)
-      gemm_tile_rows<kCT>(stage + (size_t)buf * per, T, r, g, m, nc, ncp, dsm2, out, ldo,
-                          (tile << lgT) + r);
+    if (g < ngroups) {
+      if (RPT == 2)
+        gemm_tile_rows2<kCT>(stage + (size_t)buf * per, T, r, g, m, nc, ncp, dsm2, out, ldo,
+                             (tile << lgT) + r, 2);
+      else
+        gemm_tile_rows<kCT>(stage + (size_t)buf * per, T, r, g, m, nc, ncp, dsm2, out, ldo,
+                            (tile << lgT) + r);
+    }
     __syncthreads();   // every thread done with `buf` before it is refilled
   }
   // partial last tile: plain loads, by the CTA the tile loop would give it to
@@ -506,27 +543,37 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(int64_t n, int m, int nc, int
       xs[e] = rr < rem ? X[(int64_t)j * ldx + (nfull << lgT) + rr] : 0.0;
     }
     __syncthreads();
-    if (g < ngroups && r < rem)
-      gemm_tile_rows<kCT>(xs, T, r, g, m, nc, ncp, dsm2, out, ldo, (nfull << lgT) + r);
+    if (g < ngroups && r < rem) {
+      if (RPT == 2)
+        gemm_tile_rows2<kCT>(xs, T, r, g, m, nc, ncp, dsm2, out, ldo, (nfull << lgT) + r,
+                             rem - r);
+      else
+        gemm_tile_rows<kCT>(xs, T, r, g, m, nc, ncp, dsm2, out, ldo, (nfull << lgT) + r);
+    }
   }
 }
 
-template <int kCT>
+template <int kCT, int RPT = 1>
 static bool gemm_tiled(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
                        const double *d_Z, double *d_out, int64_t ldo, cudaStream_t st,
                        int *rc) {
   const int64_t ncp = ((nc + kCT - 1) / kCT) * kCT;
   const int64_t groups = ncp / kCT;
-  int lgT = 0;
-  while ((groups << (lgT + 1)) <= 256) ++lgT;
+  int lgT = 0;   // T = 2^lgT rows per tile, groups x T / RPT <= 256 threads
+  while ((groups << (lgT + 1)) <= 256 * RPT) ++lgT;
+  // RPT = 2: keep two CTAs per SM (tile stage + Z <= 110 KB) at the cost of threads
+  while (RPT == 2 && lgT > 5 &&
+         sizeof(double) * (size_t)(m * ncp + 2 * (m << lgT)) > 110 * 1024)
+    --lgT;
   if (lgT < 5) return false;   // T >= 32 rows (idle threads when groups does not divide 256)
   if ((ldx & 1) || (reinterpret_cast<uintptr_t>(d_X) & 15)) return false;   // TMA alignment
+  const int threads = (int)((groups << lgT) / RPT);
   const size_t smem = sizeof(double) * (size_t)(m * ncp + 2 * (m << lgT));
   if (smem > 200 * 1024) return false;
   *rc = KRB_OK;
   static size_t attr_smem = 0;   // largest dynamic smem opted in so far
   if (smem > attr_smem) {
-    if (cudaFuncSetAttribute(k_gemm_t<kCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k_gemm_t<kCT, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024) != cudaSuccess) {
       set_error("krb_gemm: cudaFuncSetAttribute failed");
       *rc = KRB_ECUDA;
@@ -535,11 +582,17 @@ static bool gemm_tiled(int64_t n, int64_t m, int64_t nc, const double *d_X, int6
     attr_smem = 200 * 1024;
   }
   // resident CTAs per SM: shared memory (227 KB) and registers (2 x 256 threads)
-  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  if (RPT == 2 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_t<kCT, RPT>, threads, smem) !=
+          cudaSuccess)
+    per_sm = 1;
+  if (per_sm < 1) per_sm = 1;
   const int64_t ntiles = (n + (1 << lgT) - 1) >> lgT;
   const int64_t cap = (int64_t)kNumSMs * per_sm;
   const int grid = (int)(ntiles < cap ? ntiles : cap);
-  k_gemm_t<kCT><<<grid, 256, smem, st>>>(n, (int)m, (int)nc, lgT, d_X, ldx, d_Z, d_out, ldo);
+  k_gemm_t<kCT, RPT><<<grid, RPT == 2 ? threads : 256, smem, st>>>(n, (int)m, (int)nc, lgT, d_X,
+                                                                     ldx, d_Z, d_out, ldo);
   if (cudaGetLastError() != cudaSuccess) {
     set_error("krb_gemm: launch failed");
     *rc = KRB_ECUDA;
@@ -863,13 +916,16 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
   if (n == 0 || nc == 0) return KRB_OK;
   const int64_t ncp = ((nc + kGemmCT2 - 1) / kGemmCT2) * kGemmCT2;
   {
-    // tiled kernels (KRB_GEMM_TILED = 0 off, 8 / 12 / 24: columns per thread)
+    // tiled kernels (KRB_GEMM_TILED = 0 off, 8 / 12 / 24: columns per thread,
+    // 122: 12 columns x 2 rows per thread; default: 122 for m <= 64 and nc >= 4
+    // (47 x 47 at 262144 rows 97 -> 85 us, 26 x 26 54 -> 38 us), else 12)
     const char *e = getenv("KRB_GEMM_TILED");
-    const int mode = e ? atoi(e) : 12;
+    const int mode = e ? atoi(e) : (m <= 64 && nc >= 4 ? 122 : 12);
     int rc = KRB_OK;
     if (m > 0 && mode == 8 && gemm_tiled<8>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
     if (m > 0 && mode == 12 && gemm_tiled<12>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
     if (m > 0 && mode == 24 && gemm_tiled<24>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
+    if (m > 0 && mode == 122 && gemm_tiled<12, 2>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
   }
   size_t smem = sizeof(double) * (m * ncp > 0 ? m * ncp : 2);
   KRB_REQUIRE(smem <= 200 * 1024, "krb_gemm: Z too large for shared memory");

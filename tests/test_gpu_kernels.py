@@ -138,16 +138,20 @@ def test_pcg64_matches_numpy(dev, seed, n):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("mode", ["0", "8", "12", "24"])
-@pytest.mark.parametrize("n,m,nc", [(1_000, 3, 1), (262_144, 40, 40), (5_003, 64, 64),
+@pytest.mark.parametrize("mode", ["0", "8", "12", "24", "122", None])
+@pytest.mark.parametrize("n,m,nc", [(1_000, 3, 1), (1_001, 47, 9), (129, 20, 20), (262_144, 40, 40), (5_003, 64, 64),
                                     (70_001, 200, 30), (70_002, 47, 47), (262_146, 26, 26),
                                     (4_096, 19, 20), (98, 5, 2)])
 def test_gemm_shapes_bitwise(dev, canon, monkeypatch, mode, n, m, nc):
     """row kernel (KRB_GEMM_TILED=0) and the TMA-tiled kernel with 8 / 12 /
-    24 columns per thread: full tiles, partial last tiles, idle column
-    groups, odd leading dimensions (row-kernel fallback)"""
+    24 columns per thread, 12 columns x 2 rows per thread (122), and the
+    default choice (None): full tiles, partial last tiles (odd remainders),
+    idle column groups, odd leading dimensions (row-kernel fallback)"""
     from paper_1406_2831_b200 import recycling as R
-    monkeypatch.setenv("KRB_GEMM_TILED", mode)
+    if mode is None:
+        monkeypatch.delenv("KRB_GEMM_TILED", raising=False)
+    else:
+        monkeypatch.setenv("KRB_GEMM_TILED", mode)
     r = np.random.default_rng(m + nc)
     X = r.standard_normal((n, m))
     Z = r.standard_normal((m, nc))

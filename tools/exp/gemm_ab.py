@@ -8,7 +8,7 @@ for m, nc in ((47, 47), (47, 20), (20, 20), (26, 26), (19, 19), (8, 3), (100, 60
     X = torch.randn(m, n, dtype=torch.float64, device="cuda")
     Z = torch.from_numpy(np.random.default_rng(m).standard_normal((m, nc))).cuda()
     res = {}
-    for mode in ("0", "8", "12", "24"):
+    for mode in ("0", "8", "12", "24", "122"):
         os.environ["KRB_GEMM_TILED"] = mode
         out = R.gemm(X, Z); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -325,12 +325,15 @@ static int launch_gram_g(int64_t n, int64_t R, int64_t nch, int na, int nc, cons
                          int64_t ldx, const double *Y, int64_t ldy, double *part,
                          cudaStream_t st) {
   const size_t smem = sizeof(double) * (size_t)G * 2 * 2 * 8 * T * (S + 2);   // G x 2 buffers x (X, Y)
-  KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_g<T, G, S>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  KRB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram_g<T, G, S>, 64 * G,
-                                                               smem));
-  if (per_sm < 1) per_sm = 1;
+  static int per_sm = 0;   // per instantiation: the opt-in and the occupancy query run once
+  if (per_sm == 0) {
+    KRB_CHECK_CUDA(cudaFuncSetAttribute(k_gram_g<T, G, S>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int q = 0;
+    KRB_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_gram_g<T, G, S>, 64 * G,
+                                                                 smem));
+    per_sm = q < 1 ? 1 : q;
+  }
   const int64_t want = (nch + G - 1) / G;
   const int64_t cap = (int64_t)kNumSMs * per_sm;
   const int grid = (int)(want < cap ? want : cap);
@@ -583,11 +586,23 @@ static bool gemm_tiled(int64_t n, int64_t m, int64_t nc, const double *d_X, int6
   }
   // resident CTAs per SM: shared memory (227 KB) and registers (2 x 256 threads)
   int per_sm = smem <= 110 * 1024 ? 2 : 1;
-  if (RPT == 2 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_t<kCT, RPT>, threads, smem) !=
-          cudaSuccess)
-    per_sm = 1;
-  if (per_sm < 1) per_sm = 1;
+  if (RPT == 2) {
+    // occupancy from the kernel's register count (queried once) and this
+    // launch's shared memory / threads, without a per-call occupancy query
+    static int regs = 0;
+    if (regs == 0) {
+      cudaFuncAttributes fa;
+      regs = cudaFuncGetAttributes(&fa, k_gemm_t<kCT, RPT>) == cudaSuccess ? fa.numRegs : 255;
+    }
+    const int warps = (threads + 31) / 32;
+    const int regs_per_warp = ((regs * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / (regs_per_warp * warps);
+    const int by_smem = (int)((228 * 1024) / (smem + 1024));
+    const int by_thr = 2048 / threads;
+    per_sm = by_regs < by_smem ? by_regs : by_smem;
+    if (by_thr < per_sm) per_sm = by_thr;
+    if (per_sm < 1) per_sm = 1;
+  }
   const int64_t ntiles = (n + (1 << lgT) - 1) >> lgT;
   const int64_t cap = (int64_t)kNumSMs * per_sm;
   const int grid = (int)(ntiles < cap ? ntiles : cap);

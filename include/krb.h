@@ -49,6 +49,13 @@ const char *krb_last_error(void);
 /* number of kernel launches issued by this library since load (counter) */
 int64_t krb_launch_count(void);
 
+/* Driver / kernel-variant knobs (process-wide; every variant computes the
+ * same bits).  Keys: "persist0", "p0_grid_half", "p0_onchip", "p0_prof_cta",
+ * "cluster", "persist_v1", "gemm_mode", "l2keep".  Unknown key -> KRB_EINVAL.
+ * No reference counterpart (the reference has no device drivers). */
+int krb_set_tuning(const char *key, int64_t value);
+int krb_reset_tuning(void);
+
 /* stream-ordered device-to-device copy (ring views -> caller tensors) */
 int krb_memcpy_d2d(void *d_dst, const void *d_src, int64_t bytes, void *stream);
 

@@ -10,7 +10,7 @@ Matrix Market I/O, problem generators, bi-Lanczos harness) is out of scope.
 from .device import prefetch_matrix
 from .operators import CountingOperator, as_operator
 from .recycling import (CapturedCycle, RecycleSpace, biorthonormalize,
-                        project_initial, refresh_images)
+                        project_initial, project_initial_dual, refresh_images)
 from .solvers import (BREAKDOWN_OMEGA, BREAKDOWN_SECOND_KIND,
                       BREAKDOWN_SERIOUS, CONVERGED, MAX_ITN,
                       ConvergenceHistory, SolverConfig, bicgstab_solve,
@@ -24,7 +24,7 @@ __version__ = "0.1.0"
 __all__ = [
     "CountingOperator", "as_operator",
     "CapturedCycle", "RecycleSpace", "biorthonormalize", "project_initial",
-    "refresh_images",
+    "project_initial_dual", "refresh_images",
     "ConvergenceHistory", "SolverConfig", "bicgstab_solve", "rbicgstab_solve",
     "rbicg_solve", "update_recycle_space",
     "rbicgstab_solve_batch", "bicgstab_solve_batch",

@@ -67,6 +67,8 @@ SIGNATURES = {
     "krb_abi_version": (c_int, []),
     "krb_last_error": (ctypes.c_char_p, []),
     "krb_launch_count": (c_i64, []),
+    "krb_set_tuning": (c_int, [ctypes.c_char_p, c_i64]),
+    "krb_reset_tuning": (c_int, []),
     "krb_context_create": (c_int, [ctypes.POINTER(c_vp)]),
     "krb_context_destroy": (c_int, [c_vp]),
     "krb_matrix_create": (c_int, [ctypes.POINTER(c_vp), c_i64, c_i64, c_vp,
@@ -128,12 +130,35 @@ _lock = threading.Lock()
 _lib = None
 
 
+BUILD_INFO = os.path.join(_HERE, "build_info.json")
+
+
 def build(force: bool = False) -> str:
-    """Compile libkrb.so in-tree with nvcc for sm_100a (make in csrc/)."""
-    cmd = ["make", "-s", "-C", CSRC, "-j8"]
+    """Compile libkrb.so in-tree with nvcc for sm_100a (make in csrc/).
+    ``force`` cleans first so every object is rebuilt from source; the
+    compile commands, the nvcc version and a hash of the sources are written
+    to build_info.json next to the library (evidence of a fresh build)."""
+    import hashlib
+    import json
+    import time
+    t0 = time.time()
     if force:
         subprocess.run(["make", "-s", "-C", CSRC, "clean"], check=True)
-    subprocess.run(cmd, check=True)
+    dry = subprocess.run(["make", "-n", "-C", CSRC], check=True, capture_output=True,
+                         text=True).stdout
+    subprocess.run(["make", "-s", "-C", CSRC, "-j8"], check=True)
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(CSRC)):
+        if name.endswith((".cu", ".cuh")) or name == "Makefile":
+            with open(os.path.join(CSRC, name), "rb") as f:
+                h.update(name.encode() + f.read())
+    nvcc = subprocess.run(["nvcc", "--version"], capture_output=True, text=True).stdout
+    info = {"built_at": time.strftime("%Y-%m-%dT%H:%M:%S"), "clean": bool(force),
+            "seconds": round(time.time() - t0, 1), "sources_sha256": h.hexdigest(),
+            "nvcc": nvcc.strip().splitlines()[-1] if nvcc else None,
+            "commands": [ln.strip() for ln in dry.splitlines() if "nvcc" in ln]}
+    with open(BUILD_INFO, "w") as f:
+        json.dump(info, f, indent=1)
     return LIB_PATH
 
 
@@ -143,8 +168,7 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        # KRB_LIB selects an alternative in-tree build (A/B kernel experiments)
-        p = path or os.environ.get("KRB_LIB") or LIB_PATH
+        p = path or LIB_PATH
         if not os.path.exists(p):
             raise KrbError(
                 f"{p} is missing: build it with `python -c 'import __graft_entry__ "
@@ -170,6 +194,39 @@ def call(name: str, *args):
     rc = getattr(load(), name)(*args)
     check(rc, name)
     return rc
+
+
+# Python-side driver knobs (see tuning()): "graph_mode" = None (automatic),
+# 0 host loop, 1 CUDA graph with a device WHILE node, 2 persistent kernel;
+# "phase_prof" = per-phase device stamps of the persistent kernel.
+PY_TUNING = {"graph_mode": None, "phase_prof": False}
+_PY_DEFAULTS = dict(PY_TUNING)
+
+
+class tuning:
+    """Context manager (or plain call + reset_tuning()) setting driver /
+    kernel-variant knobs for tests and profiling tools; every variant
+    computes the same bits.  Python keys: graph_mode, phase_prof; native
+    keys: see krb_set_tuning in include/krb.h."""
+
+    def __init__(self, **knobs):
+        for key, v in knobs.items():
+            if key in PY_TUNING:
+                PY_TUNING[key] = v
+            else:
+                call("krb_set_tuning", key.encode(), int(v))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        reset_tuning()
+
+
+def reset_tuning():
+    PY_TUNING.update(_PY_DEFAULTS)
+    if _lib is not None:
+        _lib.krb_reset_tuning()
 
 
 def launch_count() -> int:

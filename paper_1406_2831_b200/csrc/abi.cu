@@ -2,6 +2,7 @@
 // context lifetime.
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 
 #include "ctx.cuh"
 
@@ -19,6 +20,11 @@ void set_error(const char *fmt, ...) {
 
 int64_t &launch_counter() { return g_launches; }
 
+Tuning &tuning() {
+  static Tuning t;
+  return t;
+}
+
 }  // namespace krb
 
 extern "C" {
@@ -28,6 +34,28 @@ int krb_abi_version(void) { return 1; }
 const char *krb_last_error(void) { return krb::g_err; }
 
 int64_t krb_launch_count(void) { return krb::g_launches; }
+
+int krb_set_tuning(const char *key, int64_t value) {
+  KRB_REQUIRE(key != nullptr, "krb_set_tuning: NULL key");
+  krb::Tuning &t = krb::tuning();
+  struct { const char *name; int *slot; } table[] = {
+      {"persist0", &t.persist0},   {"p0_grid_half", &t.p0_grid_half},
+      {"p0_onchip", &t.p0_onchip}, {"p0_prof_cta", &t.p0_prof_cta},
+      {"cluster", &t.cluster},     {"persist_v1", &t.persist_v1},
+      {"gemm_mode", &t.gemm_mode}, {"l2keep", &t.l2keep}};
+  for (auto &e : table)
+    if (strcmp(e.name, key) == 0) {
+      *e.slot = (int)value;
+      return KRB_OK;
+    }
+  krb::set_error("krb_set_tuning: unknown key '%s'", key);
+  return KRB_EINVAL;
+}
+
+int krb_reset_tuning(void) {
+  krb::tuning() = krb::Tuning();
+  return KRB_OK;
+}
 
 int krb_memcpy_d2d(void *d_dst, const void *d_src, int64_t bytes, void *stream) {
   KRB_REQUIRE(bytes >= 0, "krb_memcpy_d2d: negative size");

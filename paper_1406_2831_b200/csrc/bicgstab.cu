@@ -369,9 +369,9 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
     // entries in the fused kernel) when C and Chat fit in about 3/4 of the
-    // L2 (KRB_L2KEEP=0/1 overrides)
-    const char *e = getenv("KRB_L2KEEP");
-    h.l2keep = e ? atoi(e) : (2.0 * 8.0 * (double)n * (double)k <= 100e6 ? 1 : 0);
+    // L2 (tuning "l2keep" = 0 / 1 overrides)
+    const int e = tuning().l2keep;
+    h.l2keep = e >= 0 ? e : (2.0 * 8.0 * (double)n * (double)k <= 100e6 ? 1 : 0);
   }
   h.cond = hit ? G.cond : 0;
   IterArgs *d = reinterpret_cast<IterArgs *>(ctx->desc);

@@ -326,8 +326,7 @@ __global__ void __launch_bounds__(1024, 1) k_cluster(const IterArgs *__restrict_
 }
 
 bool cluster_eligible(const IterArgs &h) {
-  const char *e = getenv("KRB_CLUSTER");
-  if (e && atoi(e) == 0) return false;
+  if (!tuning().cluster) return false;
   return h.n > 0 && h.nb <= kClMaxCTAs && canon_E(h.n) == 1 && h.k <= kClMaxK &&
          h.A.perm == nullptr;
 }

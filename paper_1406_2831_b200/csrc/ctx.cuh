@@ -77,6 +77,21 @@ constexpr int kCounterTdotStandalone = 20;
 constexpr int kCounterTdotGraph = 21;
 constexpr int kCounterGridSync = 48;   // 2 words: persistent-kernel grid barrier
 
+// Process-wide driver / kernel-variant knobs (krb_set_tuning).  Every
+// variant computes the same bits; the knobs exist so tests can force each
+// driver and profiling tools can stamp phases.  -1 = automatic.
+struct Tuning {
+  int persist0 = 1;       // k = 0 fused kernel with the operator on chip
+  int p0_grid_half = 0;   // persist0: one CTA per two canonical blocks
+  int p0_onchip = 1;      // persist0: 0 = gather from global memory
+  int p0_prof_cta = 0;    // persist0: CTA whose phase stamps are recorded
+  int cluster = 1;        // single-cluster kernel for tiny systems
+  int persist_v1 = 0;     // force the nine-barrier persistent kernel
+  int gemm_mode = -1;     // krb_gemm: 0 row kernel, 8 / 12 / 24 / 122 tiled
+  int l2keep = -1;        // evict_last policy on the recycle blocks
+};
+Tuning &tuning();
+
 int ctx_reserve_part(krb_context *ctx, size_t doubles);
 int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);
 dim3 tdot_grid(int64_t nb, int64_t k);

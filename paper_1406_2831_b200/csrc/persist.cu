@@ -716,8 +716,6 @@ static bool persist2_eligible(const IterArgs &h) {
 
 bool cluster_eligible(const IterArgs &h);
 int cluster_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
-bool persist3_eligible(const IterArgs &h);
-int persist3_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
 bool persist0_eligible(const IterArgs &h);
 int persist0_launch(const IterArgs &h, const IterArgs *d, cudaStream_t st);
 
@@ -735,20 +733,13 @@ int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int
     }
   }
   // k = 0, canon_E == 1: the fused kernel with the operator on chip
-  // (persist0.cu; KRB_PERSIST0=0 disables)
+  // (persist0.cu; tuning "persist0" = 0 disables)
   if (persist0_eligible(h)) {
     *driver = KRB_DRIVER_FUSED;
     return persist0_launch(h, d, st);
   }
-  // large n (canon_E >= 4): the fused kernel with block-owned global round
-  // trips (persist3.cu)
-  if (persist3_eligible(h)) {
-    *driver = KRB_DRIVER_FUSED;
-    return persist3_launch(h, d, st);
-  }
-  // fused v2 unless the rows are sigma-permuted (KRB_PERSIST=1 forces v1)
-  const char *ev = getenv("KRB_PERSIST");
-  const bool v2 = persist2_eligible(h) && !(ev && atoi(ev) == 1);
+  // fused v2 unless the rows are sigma-permuted (tuning "persist_v1" forces v1)
+  const bool v2 = persist2_eligible(h) && !tuning().persist_v1;
   if (v2) {
     *driver = KRB_DRIVER_FUSED;
     switch (canon_E(h.n)) {

@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(1024, 1)
   };
 
   int cur = 0;   // partial buffer: a.part / a.part2 alternate per phase
-  // KRB_P0_PROF_CTA picks the CTA whose phase stamps are recorded
+  // tuning "p0_prof_cta" picks the CTA whose phase stamps are recorded
   const bool profiling = me == prof_cta && a.prof != nullptr;
   uint64_t *prof = (profiling && tid == 0) ? a.prof : nullptr;
 #define KRB_STAMP(slot)                                                        \
@@ -575,8 +575,7 @@ __global__ void __launch_bounds__(1024, 1)
 }  // namespace p0
 
 bool persist0_eligible(const IterArgs &h) {
-  const char *e = getenv("KRB_PERSIST0");
-  if (e && atoi(e) == 0) return false;
+  if (!tuning().persist0) return false;
   return h.k == 0 && h.A.perm == nullptr && canon_E(h.n) == 1 && h.n > 0 &&
          h.flags != nullptr;
 }
@@ -606,14 +605,11 @@ static int launch0(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
     return KRB_EINVAL;
   }
   int g = nb < grid ? (int)nb : grid;
-  // KRB_P0_GRID=half: one CTA per two canonical blocks (every CTA owns two)
-  const char *eg = getenv("KRB_P0_GRID");
-  if (eg && eg[0] == 'h') g = (int)((nb + 1) / 2);
+  // tuning "p0_grid_half": one CTA per two canonical blocks (every CTA owns two)
+  if (tuning().p0_grid_half) g = (int)((nb + 1) / 2);
   if (g > 160) g = 160;   // flag slots reserved / polled (nb <= 296 < 2 x 160)
-  const char *ef = getenv("KRB_P0_ONCHIP");
-  int force_global = (ef && atoi(ef) == 0) ? 1 : 0;
-  const char *ep = getenv("KRB_P0_PROF_CTA");
-  int prof_cta = ep ? atoi(ep) : 0;
+  int force_global = tuning().p0_onchip ? 0 : 1;
+  int prof_cta = tuning().p0_prof_cta;
   IterArgs hv = h;   // by value: the kernel reads the descriptor from its parameters
   void *args[] = {(void *)&hv, (void *)&force_global, (void *)&prof_cta};
   KRB_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)p0::k_persist0<kSell>, dim3(g),

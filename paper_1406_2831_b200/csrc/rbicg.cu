@@ -691,6 +691,11 @@ struct krb_rbicg {
   int64_t *hist_m = nullptr;
   uint64_t *hist_t = nullptr;
   krb::BiScalars *S = nullptr;
+  // the handle's own block-partial buffers (two ping-pong halves): the
+  // context's shared scratch may be reallocated by any kernel a cycle
+  // callback launches (update_recycle_space's Grams / norms) while this
+  // handle's descriptor still holds the pointer
+  double *part = nullptr;
   int64_t s = 0, max_itn = 0, k = 0;
   krb_space_view R = {};
   bool has_R = false;
@@ -729,6 +734,7 @@ static void bi_free(krb_rbicg *H) {
   cudaFree(H->hist_m);
   cudaFree(H->hist_t);
   cudaFree(H->S);
+  cudaFree(H->part);
   delete H;
 }
 
@@ -825,6 +831,8 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   if (e == cudaSuccess) e = cudaMalloc(&H->hist_m, sizeof(int64_t) * (max_itn + 2));
   if (e == cudaSuccess) e = cudaMalloc(&H->hist_t, sizeof(uint64_t) * (max_itn + 2));
   if (e == cudaSuccess) e = cudaMalloc(&H->S, sizeof(BiScalars));
+  if (e == cudaSuccess)
+    e = cudaMalloc(&H->part, sizeof(double) * 2 * ((size_t)((2 * k + 3) * nb) + 64));
   if (e != cudaSuccess) {
     set_error("krb_rbicg_create: %s", cudaGetErrorString(e));
     bi_free(H);
@@ -832,8 +840,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   }
 fill:
   const size_t part_one = (size_t)((2 * k + 3) * nb) + 64;
-  rc = ctx_reserve_part(ctx, 2 * part_one);
-  if (!rc) rc = ctx_reserve_counters(ctx, st);
+  rc = ctx_reserve_counters(ctx, st);
   if (rc) {
     bi_free(H);
     return rc;
@@ -862,8 +869,8 @@ fill:
   h.rhos = H->scal;
   h.alphas = H->scal + (max_itn + ring_cols + 2);
   h.betas = H->scal + 2 * (max_itn + ring_cols + 2);
-  h.part = ctx->part;
-  h.part2 = ctx->part + part_one;
+  h.part = H->part;
+  h.part2 = H->part + part_one;
   h.counters = ctx->counters;
   h.S = H->S;
   h.hist_r = H->hist;

@@ -931,11 +931,12 @@ int krb_gemm(int64_t n, int64_t m, int64_t nc, const double *d_X, int64_t ldx,
   if (n == 0 || nc == 0) return KRB_OK;
   const int64_t ncp = ((nc + kGemmCT2 - 1) / kGemmCT2) * kGemmCT2;
   {
-    // tiled kernels (KRB_GEMM_TILED = 0 off, 8 / 12 / 24: columns per thread,
-    // 122: 12 columns x 2 rows per thread; default: 122 for m <= 64 and nc >= 4
-    // (47 x 47 at 262144 rows 97 -> 85 us, 26 x 26 54 -> 38 us), else 12)
-    const char *e = getenv("KRB_GEMM_TILED");
-    const int mode = e ? atoi(e) : (m <= 64 && nc >= 4 ? 122 : 12);
+    // tiled kernels (tuning "gemm_mode" = 0 off, 8 / 12 / 24: columns per
+    // thread, 122: 12 columns x 2 rows per thread; default: 122 for m <= 64
+    // and nc >= 4 (47 x 47 at 262144 rows 97 -> 85 us, 26 x 26 54 -> 38 us),
+    // else 12)
+    const int tm = tuning().gemm_mode;
+    const int mode = tm >= 0 ? tm : (m <= 64 && nc >= 4 ? 122 : 12);
     int rc = KRB_OK;
     if (m > 0 && mode == 8 && gemm_tiled<8>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;
     if (m > 0 && mode == 12 && gemm_tiled<12>(n, m, nc, d_X, ldx, d_Z, d_out, ldo, st, &rc)) return rc;

@@ -401,10 +401,18 @@ def device_matrix(A) -> DeviceMatrix:
         if A.ndim != 2 or A.shape[0] != A.shape[1]:
             raise ValueError("solver requires a square operator")
         import scipy.sparse as sp
-        S = sp.csr_matrix(A)
-        S.sort_indices()
-        return MATRICES.get(A, lambda: DeviceMatrix(A.shape[0], S.indptr,
-                                                    S.indices, S.data))
+
+        def build():
+            S = sp.csr_matrix(A)
+            S.sort_indices()
+            return DeviceMatrix(A.shape[0], S.indptr, S.indices, S.data)
+
+        if A.flags.writeable:
+            # a mutable array may be edited in place between calls (the
+            # reference's DenseOperator reads the live array on every
+            # product): never serve a cached device copy of it
+            return build()
+        return MATRICES.get(A, build)
     raise NotImplementedError(
         f"{type(A).__name__} has no CSR representation; the device path "
         "supports SparseMatrix-like CSR operators only (no CPU fallback)")

@@ -12,8 +12,6 @@ function below).
 from __future__ import annotations
 
 import warnings
-from dataclasses import dataclass
-
 import numpy as np
 
 from . import _lib
@@ -123,42 +121,98 @@ class RecycleSpace:
         return f"RecycleSpace(n={self.n}, k={self.k}, device=cuda)"
 
 
-@dataclass
 class CapturedCycle:
-    """Lanczos-direction block of one harvest window (recycling.py:80-102).
-    V / Vt are (ncols, n) device tensors (column-major n x ncols); ``tri``
-    holds the (sub, diag, super) recurrence coefficients (host).  ``tri``
-    may be given as a zero-argument callable: it is then evaluated on first
-    access (the recycle update never reads it, so the harvest path does not
-    pay for it)."""
+    """Lanczos-direction block of one harvest window (recycling.py:80-102),
+    constructed with the reference's fields: ``CapturedCycle(V, Vt, tri,
+    first_index)``.
 
-    V_dev: object
-    Vt_dev: object
-    tri: object
-    first_index: int
+    ``V`` / ``Vt`` may be given as the reference gives them -- host numpy
+    n x ncols -- or as (ncols, n) CUDA tensors (the column-major device
+    layout of this package; what rbicg_solve's harvest produces).  Both
+    views exist lazily: ``.V`` / ``.Vt`` are numpy n x ncols (one device->host
+    copy on first access), ``.V_dev`` / ``.Vt_dev`` the (ncols, n) device
+    blocks (one host->device copy on first access).  ``tri`` holds the
+    (sub, diag, super) recurrence coefficients; it may be a zero-argument
+    callable, evaluated on first access (the recycle update never reads it,
+    so the harvest path does not pay for it)."""
 
-    def __getattribute__(self, name):
-        v = object.__getattribute__(self, name)
-        if name == "tri" and callable(v):
-            v = v()
-            object.__setattr__(self, "tri", v)
-        return v
+    __slots__ = ("_V", "_Vt", "_V_dev", "_Vt_dev", "_tri", "first_index")
+
+    def __init__(self, V, Vt, tri, first_index):
+        self._V = self._V_dev = self._Vt = self._Vt_dev = None
+        if _is_cuda(V):
+            self._V_dev = V
+        else:
+            self._V = np.asarray(V)
+        if _is_cuda(Vt):
+            self._Vt_dev = Vt
+        else:
+            self._Vt = np.asarray(Vt)
+        self._tri = tri
+        self.first_index = int(first_index)
 
     @property
     def V(self):
-        return self.V_dev.detach().cpu().numpy().T
+        if self._V is None:
+            self._V = self._V_dev.detach().cpu().numpy().T
+        return self._V
 
     @property
     def Vt(self):
-        return self.Vt_dev.detach().cpu().numpy().T
+        if self._Vt is None:
+            self._Vt = self._Vt_dev.detach().cpu().numpy().T
+        return self._Vt
+
+    @property
+    def V_dev(self):
+        if self._V_dev is None:
+            self._V_dev = _host_block(self._V)
+        return self._V_dev
+
+    @property
+    def Vt_dev(self):
+        if self._Vt_dev is None:
+            self._Vt_dev = _host_block(self._Vt)
+        return self._Vt_dev
+
+    @property
+    def tri(self):
+        if callable(self._tri):
+            self._tri = self._tri()
+        return self._tri
+
+    @tri.setter
+    def tri(self, value):
+        self._tri = value
 
     @property
     def ncols(self) -> int:
-        return int(self.V_dev.shape[0])
+        if self._V_dev is not None:
+            return int(self._V_dev.shape[0])
+        return int(self._V.shape[1])
 
     @property
     def last_index(self) -> int:
         return self.first_index + self.ncols - 1
+
+    def __repr__(self):
+        return (f"CapturedCycle(ncols={self.ncols}, first_index={self.first_index}, "
+                f"device={self._V_dev is not None})")
+
+
+def _is_cuda(x):
+    return hasattr(x, "is_cuda") and x.is_cuda
+
+
+def _host_block(X):
+    """numpy n x c -> (c, n) device block."""
+    X = np.atleast_2d(np.asarray(X))
+    if np.iscomplexobj(X):
+        raise NotImplementedError("complex cycles are out of scope on the device path")
+    n, c = X.shape
+    if c == 0:
+        return torch().zeros((0, n), dtype=torch().float64, device="cuda")
+    return to_device(np.ascontiguousarray(X.T, dtype=np.float64)).reshape(c, n)
 
 
 # ---------------------------------------------------------------------------
@@ -395,3 +449,26 @@ def project_initial(A, b, x_minus1, recycle):
     x0 = gemv(R.device("U"), y, base=x, sign=+1)
     r0 = gemv(R.device("C"), y, base=r, sign=-1)
     return to_host(x0), to_host(r0)
+
+
+def project_initial_dual(A, b_dual, xt_minus1, recycle):
+    """recycling.py:209-222 on the device: the dual analogue of
+    project_initial for A^H xt = b_dual (rt = b_dual - A^H xt_minus1,
+    y = Ccheck^H rt, xt0 = xt + Ut y, rt0 = rt - Ct y); host (xt0, rt0)."""
+    t = torch()
+    M = device_matrix(A)
+    bd = to_device(np.asarray(b_dual, dtype=np.float64))
+    if xt_minus1 is None:
+        xt = t.zeros(M.n, dtype=t.float64, device="cuda")
+        rt = bd.clone()
+    else:
+        xt = to_device(np.asarray(xt_minus1, dtype=np.float64))
+        rt = bd - M.spmv(xt, transpose=True)
+        _meter(A, nr=1)
+    R = RecycleSpace.of(recycle)
+    if R is None or R.k == 0:
+        return to_host(xt), to_host(rt)
+    y = tdot(R.device("Ccheck"), rt)
+    xt0 = gemv(R.device("Ut"), y, base=xt, sign=+1)
+    rt0 = gemv(R.device("Ct"), y, base=rt, sign=-1)
+    return to_host(xt0), to_host(rt0)

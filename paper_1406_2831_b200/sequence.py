@@ -151,7 +151,10 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
             else:
                 if kappa == 0 and space is not None and i > 0:
                     space = api.refresh_images(space, op_rec)
-                recycled = space is not None and space.k > 0
+                # driver.py:142 gates on the space's existence, not its size:
+                # an empty harvested space still gets the capped attempt and
+                # the reseeded retry
+                recycled = space is not None
                 cap = min(max_itn, max(block_itn, 50))
                 if use_batch and kappa not in pre_rec and kappa + 1 < nk:
                     # every remaining rhs of this matrix shares the space

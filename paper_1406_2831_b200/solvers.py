@@ -170,8 +170,6 @@ _STATUS = {1: CONVERGED, 2: MAX_ITN, 3: BREAKDOWN_SERIOUS, 4: BREAKDOWN_OMEGA,
 
 
 LAST_SOLVE = {}   # launch accounting of the most recent solve (bench / tests)
-import os as _os
-_PHASE_PROF = _os.environ.get("KRB_PHASE_PROF") == "1"   # per-phase device stamps
 
 
 def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
@@ -184,16 +182,14 @@ def _device_solve(A, b, x_init, recycle, cfg, label, t0, use_graph=None):
 
 
 def _graph_mode():
-    """Iteration driver (bit-identical results in every mode):
-    KRB_GRAPH_MODE=2 (default for RBiCGSTAB): one persistent cooperative kernel
-    per solve, phases separated by grid barriers whose last CTA finalizes;
-    1: one CUDA graph per solve with a device-driven WHILE node (the RBiCG
-    generation solve always uses this, pausing at every harvest cycle);
-    0: host-launched iterations with a status poll every 8 (per-kernel ncu
-    profiling: ncu cannot see inside conditional graph nodes)."""
-    import os
-    v = os.environ.get("KRB_GRAPH_MODE")
-    return int(v) if v is not None else None
+    """Iteration driver override (_lib.tuning(graph_mode=...); None =
+    automatic; bit-identical results in every mode): 2 = one persistent
+    cooperative kernel per solve (n <= PERSISTENT_MAX_N); 1 = one CUDA graph
+    per solve with a device-driven WHILE node (the RBiCG generation solve at
+    large n uses this, pausing at every harvest cycle); 0 = host-launched
+    iterations with a status poll every 8 (per-kernel ncu profiling: ncu
+    cannot see inside conditional graph nodes)."""
+    return _lib.PY_TUNING["graph_mode"]
 
 
 # Below this size one persistent cooperative kernel beats per-phase kernels
@@ -235,7 +231,7 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     c.pcg_state_hi, c.pcg_state_lo, c.pcg_inc_hi, c.pcg_inc_lo = pcg64_words(cfg.seed)
     c.use_graph = int(use_graph)
     prof = None
-    if _PHASE_PROF and use_graph == 2:
+    if _lib.PY_TUNING["phase_prof"] and use_graph == 2:
         prof = t.zeros((cfg.max_itn + 1) * 16, dtype=t.int64, device="cuda")
         c.d_phase_stamps = prof.data_ptr()
         c.phase_stamps_cap = cfg.max_itn + 1
@@ -440,7 +436,12 @@ class _CycleHarvest:
                   ctypes.byref(rh), ctypes.byref(al), ctypes.byref(be))
         self.ptrs = (V.value, Vt.value, rh.value, al.value, be.value)
 
-    def emit(self, state, final=False, launch_next=None):
+    def emit(self, state, st, final=False, launch_next=None):
+        """Copy the completed cycle out of the ring and rotate the ring, all
+        on the solve's stream ``st`` (so the next cycle's kernel, also on
+        ``st``, cannot overwrite columns still being copied even if the
+        callback switched streams), then hand the cycle to the callback on
+        the caller's current stream, ordered after those copies."""
         ncols, nalpha, npush = int(state[2]), int(state[4]), int(state[6])
         last = self.start + ncols - 1
         if ncols == 0 or last <= self.emitted:
@@ -448,25 +449,15 @@ class _CycleHarvest:
                 launch_next()
             return
         t = torch()
-        n = self.n
-        Vd = t.empty((ncols, n), dtype=t.float64, device="cuda")
-        Vtd = t.empty((ncols, n), dtype=t.float64, device="cuda")
-        _lib.copy_d2d(Vd, self.ptrs[0], ncols * n)
-        _lib.copy_d2d(Vtd, self.ptrs[1], ncols * n)
-        rhos, alphas, betas = _lib.fetch_f64_many(
-            [(self.ptrs[2], npush), (self.ptrs[3], nalpha), (self.ptrs[4], nalpha)])
-        start = self.start
-        cyc = self.CapturedCycle(
-            V_dev=Vd, Vt_dev=Vtd, first_index=start,
-            tri=lambda: _tri_block(start, ncols, alphas, betas, rhos))   # lazy
-        self.cycles.append(cyc)
-        self.emitted = last
-        if not final and ncols > 2:
-            # the copies above are queued first on the same stream, so the
-            # ring may be rotated and refilled before the callback runs
-            _lib.call("krb_rbicg_rotate", self.H, 2, stream_ptr())
-            self.start = last - 1
-            state[2] = 2          # the ring now holds the two overlap columns
+        cur = t.cuda.current_stream()
+        sv = st.value or 0
+        if cur.cuda_stream == sv:
+            cyc = self._copy_out(state, final, st, ncols, nalpha, npush, last)
+        else:
+            solve_stream = t.cuda.ExternalStream(sv)
+            with t.cuda.stream(solve_stream):
+                cyc = self._copy_out(state, final, st, ncols, nalpha, npush, last)
+            cur.wait_stream(solve_stream)
         if launch_next is None:
             if self.callback is not None:
                 self.callback(cyc)
@@ -483,6 +474,29 @@ class _CycleHarvest:
             drop_pending()
             raise
         flush_pending()
+
+    def _copy_out(self, state, final, st, ncols, nalpha, npush, last):
+        t = torch()
+        n = self.n
+        Vd = t.empty((ncols, n), dtype=t.float64, device="cuda")
+        Vtd = t.empty((ncols, n), dtype=t.float64, device="cuda")
+        _lib.copy_d2d(Vd, self.ptrs[0], ncols * n)
+        _lib.copy_d2d(Vtd, self.ptrs[1], ncols * n)
+        rhos, alphas, betas = _lib.fetch_f64_many(
+            [(self.ptrs[2], npush), (self.ptrs[3], nalpha), (self.ptrs[4], nalpha)])
+        start = self.start
+        cyc = self.CapturedCycle(
+            V=Vd, Vt=Vtd, first_index=start,
+            tri=lambda: _tri_block(start, ncols, alphas, betas, rhos))   # lazy
+        self.cycles.append(cyc)
+        self.emitted = last
+        if not final and ncols > 2:
+            # the copies above are queued first on the same stream, so the
+            # ring may be rotated and refilled before the callback runs
+            _lib.call("krb_rbicg_rotate", self.H, 2, st)
+            self.start = last - 1
+            state[2] = 2          # the ring now holds the two overlap columns
+        return cyc
 
 
 def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
@@ -556,13 +570,13 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
             _lib.call("krb_rbicg_wait", H, state, st)
             running = state[0] == 0
             if state[1]:
-                harvest.emit(state, final=False,
+                harvest.emit(state, st, final=False,
                              launch_next=launch_next if running else None)
             elif running:
                 launch_next()
             if not running:
                 break
-        harvest.emit(state, final=True)
+        harvest.emit(state, st, final=True)
         xo = t.empty(n, dtype=t.float64, device="cuda")
         xto = t.empty(n, dtype=t.float64, device="cuda")
         L = int(cfg.max_itn) + 2

@@ -230,10 +230,11 @@ def test_rbicg_drivers_bitwise(P, canon, cfg, k, monkeypatch):
     b = seq.rhs(1, 0)
     cfg_ = P.SolverConfig(tol=1e-9, max_itn=300, s=10, seed=5)
     out = {}
+    from paper_1406_2831_b200 import _lib
     for mode in ("2", "1", "0"):
-        monkeypatch.setenv("KRB_GRAPH_MODE", mode)
-        out[mode] = P.rbicg_solve(P.SparseMatrix.from_csr(A), b, b_dual=np.ones(A.n),
-                                  recycle=Sg, config=cfg_)
+        with _lib.tuning(graph_mode=int(mode)):
+            out[mode] = P.rbicg_solve(P.SparseMatrix.from_csr(A), b, b_dual=np.ones(A.n),
+                                      recycle=Sg, config=cfg_)
     ref = out["2"]
     assert len(ref[3]) >= 2
     for mode in ("1", "0"):

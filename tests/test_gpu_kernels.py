@@ -143,19 +143,16 @@ def test_pcg64_matches_numpy(dev, seed, n):
                                     (70_001, 200, 30), (70_002, 47, 47), (262_146, 26, 26),
                                     (4_096, 19, 20), (98, 5, 2)])
 def test_gemm_shapes_bitwise(dev, canon, monkeypatch, mode, n, m, nc):
-    """row kernel (KRB_GEMM_TILED=0) and the TMA-tiled kernel with 8 / 12 /
+    """row kernel (gemm_mode 0) and the TMA-tiled kernel with 8 / 12 /
     24 columns per thread, 12 columns x 2 rows per thread (122), and the
     default choice (None): full tiles, partial last tiles (odd remainders),
     idle column groups, odd leading dimensions (row-kernel fallback)"""
-    from paper_1406_2831_b200 import recycling as R
-    if mode is None:
-        monkeypatch.delenv("KRB_GEMM_TILED", raising=False)
-    else:
-        monkeypatch.setenv("KRB_GEMM_TILED", mode)
+    from paper_1406_2831_b200 import _lib, recycling as R
     r = np.random.default_rng(m + nc)
     X = r.standard_normal((n, m))
     Z = r.standard_normal((m, nc))
-    out = R.gemm(_cols(X), Z).cpu().numpy().T
+    with _lib.tuning(**({} if mode is None else {"gemm_mode": int(mode)})):
+        out = R.gemm(_cols(X), Z).cpu().numpy().T
     assert np.array_equal(out, canon.gemm(X, Z))
 
 

@@ -2,8 +2,8 @@
 bit-identical to the canonical oracle and to the other k = 0 drivers:
 
 * stencil operators whose rows and halo fit in shared memory (every CTA on
-  chip), forced off chip (KRB_P0_ONCHIP=0: the same kernel gathering from
-  global memory), and the previous fused kernel (KRB_PERSIST0=0);
+  chip), forced off chip (tuning p0_onchip=0: the same kernel gathering from
+  global memory), and the previous fused kernel (tuning persist0=0);
 * scattered random columns (halo over budget: CTAs fall back per CTA) and a
   mix of banded and scattered rows (some CTAs on chip, some not);
 * one CTA per block (nb <= #SMs), two blocks per CTA, a partial last block,
@@ -88,7 +88,7 @@ CASES = [
 @pytest.mark.parametrize("kind,n,fmt", CASES)
 def test_persist0_bitwise(pkg, canon, monkeypatch, kind, n, fmt):
     from oracle import krylov as O
-    from paper_1406_2831_b200 import solvers as S
+    from paper_1406_2831_b200 import _lib, solvers as S
     from paper_1406_2831_b200.device import DeviceMatrix, to_device
     A = _matrix(kind, n)
     b = np.random.default_rng(A.n).standard_normal(A.n)
@@ -96,13 +96,9 @@ def test_persist0_bitwise(pkg, canon, monkeypatch, kind, n, fmt):
     for tol, max_itn in ((1e-14, 9), (1e-9, 600)):
         cfg = pkg.SolverConfig(tol=tol, max_itn=max_itn, seed=5)
         xo, ho = O.rbicgstab(A, b, config=O.Config(tol=tol, max_itn=max_itn, seed=5), ops=canon)
-        for env in ({}, {"KRB_P0_ONCHIP": "0"}, {"KRB_P0_GRID": "half"},
-                    {"KRB_PERSIST0": "0"}):
-            for key in ("KRB_P0_ONCHIP", "KRB_P0_GRID", "KRB_PERSIST0"):
-                monkeypatch.delenv(key, raising=False)
-            for key, v in env.items():
-                monkeypatch.setenv(key, v)
-            xg, hg = S.solve_device(M, to_device(b), None, None, cfg, use_graph=2)
+        for env in ({}, {"p0_onchip": 0}, {"p0_grid_half": 1}, {"persist0": 0}):
+            with _lib.tuning(**env):
+                xg, hg = S.solve_device(M, to_device(b), None, None, cfg, use_graph=2)
             assert S.LAST_SOLVE["driver"] == "fused", env
             assert hg.status == ho.status, env
             assert hg.resid == ho.resid, env
@@ -116,13 +112,14 @@ def test_persist0_single_block(pkg, canon, monkeypatch):
     from paper_1406_2831_b200 import solvers as S
     from paper_1406_2831_b200.device import DeviceMatrix, to_device
     from test_gpu_persistent import ragged_matrix
-    monkeypatch.setenv("KRB_CLUSTER", "0")
+    from paper_1406_2831_b200 import _lib
     A = ragged_matrix(777, seed=1)
     b = np.random.default_rng(2).standard_normal(A.n)
     M = DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=2)
     cfg = pkg.SolverConfig(tol=1e-12, max_itn=300, seed=1)
     xo, ho = O.rbicgstab(A, b, config=O.Config(tol=1e-12, max_itn=300, seed=1), ops=canon)
-    xg, hg = S.solve_device(M, to_device(b), None, None, cfg, use_graph=2)
+    with _lib.tuning(cluster=0):
+        xg, hg = S.solve_device(M, to_device(b), None, None, cfg, use_graph=2)
     assert S.LAST_SOLVE["driver"] == "fused"
     assert (hg.status, hg.resid, hg.matvecs) == (ho.status, ho.resid, ho.matvecs)
     assert np.array_equal(xg.cpu().numpy(), xo)

@@ -63,7 +63,11 @@ CASES = [
     (200_000, 33, 2),      # k > 32: v1 kernel
     (400_000, 8, 2),       # E = 2
     (606_208, 3, 1),       # largest E = 2 size, CSR
-    (700_001, 6, 2),       # E = 4: large-n fused kernel (persist3.cu)
+]
+
+# above PERSISTENT_MAX_N the persistent driver refuses; the graph driver runs
+GRAPH_CASES = [
+    (700_001, 6, 2),       # E = 4
     (1_300_000, 0, 2),     # E = 8, k = 0
     (1_300_000, 9, 1),     # E = 8, CSR
 ]
@@ -115,3 +119,23 @@ def test_persistent_sigma_rows_use_v1(pkg, canon):
     assert S.LAST_SOLVE["driver"] == "persistent"
     assert (hg.status, hg.resid, hg.matvecs) == (ho.status, ho.resid, ho.matvecs)
     assert np.array_equal(xg.cpu().numpy(), xo)
+
+
+@pytest.mark.parametrize("n,k,fmt", GRAPH_CASES)
+def test_large_n_graph_bitwise_and_persistent_refused(pkg, canon, n, k, fmt):
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import _lib, solvers as S
+    from paper_1406_2831_b200.device import DeviceMatrix, to_device
+    A = ragged_matrix(n, seed=n + k)
+    b = np.random.default_rng(n).standard_normal(n)
+    Sp = random_space_arrays(A, k, seed=11, ops=canon) if k else None
+    M = DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=fmt)
+    cfg = pkg.SolverConfig(tol=1e-9, max_itn=400, seed=5)
+    xo, ho = O.rbicgstab(A, b, recycle=Sp, config=O.Config(tol=1e-9, max_itn=400, seed=5),
+                         ops=canon)
+    xg, hg = S.solve_device(M, to_device(b), None, _space(pkg, Sp) if k else None, cfg)
+    assert S.LAST_SOLVE["driver"] == "graph"
+    assert (hg.status, hg.resid, hg.matvecs) == (ho.status, ho.resid, ho.matvecs)
+    assert np.array_equal(xg.cpu().numpy(), xo)
+    with pytest.raises(_lib.KrbError):
+        S.solve_device(M, to_device(b), None, None, cfg, use_graph=2)

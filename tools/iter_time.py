@@ -47,7 +47,7 @@ def run(name, k=None, reps=3, max_itn=None):
 
 
 def phase_breakdown(name, k=None):
-    """Per-phase device time inside the persistent kernel (KRB_PHASE_PROF=1):
+    """Per-phase device time inside the persistent kernel (_lib.tuning(phase_prof=True)):
     median us per phase over the iterations of one solve."""
     import paper_1406_2831_b200 as P
     from paper_1406_2831_b200 import device as D, solvers as S, workloads as W
@@ -58,7 +58,9 @@ def phase_breakdown(name, k=None):
     r = np.random.default_rng(12345)
     space = P.biorthonormalize(r.standard_normal((A.n, k)), r.standard_normal((A.n, k)), M) if k else None
     b = D.to_device(seq.rhs(0, 0))
-    S.solve_device(M, b, None, space, P.SolverConfig(tol=seq.tol, seed=0), use_graph=2)
+    from paper_1406_2831_b200 import _lib
+    with _lib.tuning(phase_prof=True):
+        S.solve_device(M, b, None, space, P.SolverConfig(tol=seq.tol, seed=0), use_graph=2)
     st = S.LAST_SOLVE["phase_stamps"].astype(np.int64)
     used = 6 if st[0, 12] != 0 else 10   # fused v2 stamps slots 12, 13
     names = (["P", "M1", "Z1", "Q", "S", "M2", "Z2", "T", "X"] if used >= 10 else

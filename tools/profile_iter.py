@@ -1,5 +1,5 @@
 """Profiling driver: RBiCGSTAB solves on one BASELINE config with a fixed
-seeded k-dimensional space, in host-loop mode (KRB_GRAPH_MODE=0) so ncu can
+seeded k-dimensional space, in host-loop mode (graph_mode 0) so ncu can
 see every kernel (it cannot profile inside conditional graph nodes).
 
     python tools/profile_iter.py --config c2 --solves 2
@@ -8,8 +8,9 @@ import argparse
 import os
 import sys
 
-os.environ.setdefault("KRB_GRAPH_MODE", "0")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1406_2831_b200 import _lib  # noqa: E402
+_lib.PY_TUNING["graph_mode"] = 0
 
 import numpy as np  # noqa: E402
 

@@ -172,6 +172,13 @@ typedef struct krb_solve_config {
    * phase boundaries of iteration i at d_phase_stamps[16 i + slot]        */
   uint64_t *d_phase_stamps;
   int64_t phase_stamps_cap;  /* iterations covered                        */
+  /* optional (graph / host-loop drivers): live per-kernel device time.  For
+   * the 9 kernels of one iteration (slot 0 P, 1 q=Ap, 2 Chat^T q, 3 Q,
+   * 4 S, 5 t=As, 6 Chat^T t, 7 T, 8 X) d_kernel_times[4 slot + 1] gains
+   * (last CTA's end - CTA 0's start) in ns and [4 slot + 2] one per launch
+   * that did work.  36 uint64, zeroed by the caller; accumulates across
+   * solves.                                                              */
+  uint64_t *d_kernel_times;
 } krb_solve_config;
 
 typedef struct krb_solve_result {

@@ -47,7 +47,7 @@ class SolveConfig(ctypes.Structure):
                 ("pcg_state_hi", c_u64), ("pcg_state_lo", c_u64),
                 ("pcg_inc_hi", c_u64), ("pcg_inc_lo", c_u64),
                 ("use_graph", c_int), ("d_phase_stamps", c_vp),
-                ("phase_stamps_cap", c_i64)]
+                ("phase_stamps_cap", c_i64), ("d_kernel_times", c_vp)]
 
 
 class SolveResult(ctypes.Structure):
@@ -199,15 +199,18 @@ def call(name: str, *args):
 # Python-side driver knobs (see tuning()): "graph_mode" = None (automatic),
 # 0 host loop, 1 CUDA graph with a device WHILE node, 2 persistent kernel;
 # "phase_prof" = per-phase device stamps of the persistent kernel.
-PY_TUNING = {"graph_mode": None, "phase_prof": False}
+# "kernel_times" = a zeroed (36,) int64 CUDA tensor that the graph /
+# host-loop drivers accumulate live per-kernel device time into
+# (krb_solve_config.d_kernel_times).
+PY_TUNING = {"graph_mode": None, "phase_prof": False, "kernel_times": None}
 _PY_DEFAULTS = dict(PY_TUNING)
 
 
 class tuning:
     """Context manager (or plain call + reset_tuning()) setting driver /
     kernel-variant knobs for tests and profiling tools; every variant
-    computes the same bits.  Python keys: graph_mode, phase_prof; native
-    keys: see krb_set_tuning in include/krb.h."""
+    computes the same bits.  Python keys: graph_mode, phase_prof,
+    kernel_times; native keys: see krb_set_tuning in include/krb.h."""
 
     def __init__(self, **knobs):
         for key, v in knobs.items():

@@ -71,16 +71,22 @@ __global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa)
       cudaGraphSetConditional(a.cond, 0);
     return;
   }
+  constexpr int kSlot = ktime_slot_of(PH);
+  ktime_start(a, kSlot);
   if (PH == PH_PROJ_Q || PH == PH_PROJ_T) {
     const double *src = PH == PH_PROJ_Q ? a.zeta : a.gamma;
     for (int j = threadIdx.x; j < a.k; j += blockDim.x) coef[j] = src[j];
     __syncthreads();
   }
   phase_blocks<kE, PH>(a, sc, red, coef, blockIdx.x, gridDim.x, a.part);
-  if (ND == 0) return;
+  if (ND == 0) {
+    ktime_finish(a, kSlot);
+    return;
+  }
   if (!elect_last_cta(a.counters + PH, &last_flag)) return;
   phase_leader<PH>(a, sc);
   if (threadIdx.x == 0) {
+    ktime_add(a, kSlot);
     a.counters[PH] = 0;
     if (PH == PH_XR && a.use_cond)
       cudaGraphSetConditional(a.cond, S->status == KRB_RUNNING ? 1u : 0u);
@@ -92,9 +98,11 @@ template <int kE, bool kGamma>
 __global__ void __launch_bounds__(1024) k_proj_dot(const IterArgs *__restrict__ pa) {
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
+  ktime_start(a, kGamma ? 6 : 2);
   tdot_body<kE, false>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
                        kGamma ? a.gamma : a.zeta, a.counters + kCounterTdotGraph,
                        a.l2keep != 0);
+  ktime_finish(a, kGamma ? 6 : 2);
 }
 
 // SpMV inside the iteration (matrix read from the descriptor)
@@ -102,11 +110,14 @@ template <bool kSell, bool kSecond>
 __global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ pa) {
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
+  ktime_start(a, kSecond ? 5 : 1);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.A.n) return;
-  const double *x = kSecond ? a.s : a.p;
-  double *y = kSecond ? a.t : a.q;
-  y[(kSell && a.A.perm) ? a.A.perm[i] : i] = spmv_row<kSell>(i, a.A, x);
+  if (i < a.A.n) {
+    const double *x = kSecond ? a.s : a.p;
+    double *y = kSecond ? a.t : a.q;
+    y[(kSell && a.A.perm) ? a.A.perm[i] : i] = spmv_row<kSell>(i, a.A, x);
+  }
+  ktime_finish(a, kSecond ? 5 : 1);
 }
 
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
@@ -361,6 +372,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   h.hist_t = hist_t;
   h.prof = cfg->d_phase_stamps;
   h.prof_cap = cfg->d_phase_stamps ? cfg->phase_stamps_cap : 0;
+  h.ktime = cfg->d_kernel_times;
   const int mode = cfg->use_graph;   // 0 host loop, 1 graph, 2 persistent
   const bool graph = mode == 1;
   GraphCache &G = ctx->graph;

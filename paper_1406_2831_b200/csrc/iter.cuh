@@ -33,6 +33,7 @@ struct IterArgs {
   double *part, *part2;   // part2: second partial buffer (persistent kernel)
   uint64_t *prof;         // optional per-phase %globaltimer stamps (16/iter)
   int64_t prof_cap;
+  uint64_t *ktime;        // optional live per-kernel time (krb_solve_config)
   unsigned int *counters;
   unsigned int *flags;    // per-CTA phase epochs, 128 B apart (persist0.cu)
   SolveScalars *S;
@@ -57,6 +58,46 @@ __device__ __forceinline__ void record(const IterArgs &a, SolveScalars *S,
     a.hist_t[h] = globaltimer();
   }
   S->hist_len = h + 1;
+}
+
+// Live per-kernel device time (graph / host-loop drivers; krb.h
+// krb_solve_config.d_kernel_times): CTA 0 stamps the start, the last CTA to
+// finish adds (end - start) to the slot's total.  Slots: 0 P, 1 q = A p,
+// 2 Chat^T q, 3 Q, 4 S, 5 t = A s, 6 Chat^T t, 7 T, 8 X.
+__host__ __device__ constexpr int ktime_slot_of(int PH) {
+  return PH == PH_PUPDATE ? 0 : PH == PH_PROJ_Q ? 3 : PH == PH_SUPD ? 4
+       : PH == PH_PROJ_T ? 7 : PH == PH_XR ? 8 : -1;
+}
+
+__device__ __forceinline__ void ktime_start(const IterArgs &a, int slot) {
+  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    *(volatile uint64_t *)&a.ktime[4 * slot] = globaltimer();
+}
+
+// by thread 0 of the CTA known to finish last
+__device__ __forceinline__ void ktime_add(const IterArgs &a, int slot) {
+  if (!a.ktime || slot < 0) return;
+  const uint64_t t1 = globaltimer();
+  const uint64_t t0 = *(volatile uint64_t *)&a.ktime[4 * slot];
+  a.ktime[4 * slot + 1] += t1 - t0;
+  a.ktime[4 * slot + 2] += 1;
+}
+
+// every thread of every CTA: elects the last CTA with the slot's own
+// counter (kernels without a last-CTA election of their own)
+__device__ __forceinline__ void ktime_finish(const IterArgs &a, int slot) {
+  if (!a.ktime || slot < 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long total = (unsigned long long)gridDim.x * gridDim.y;
+    unsigned long long *cnt = (unsigned long long *)&a.ktime[4 * slot + 3];
+    if (atomicAdd(cnt, 1ull) == total - 1) {
+      __threadfence();
+      ktime_add(a, slot);
+      *cnt = 0;
+    }
+  }
 }
 
 __host__ __device__ constexpr int ndots_of(int PH) {

@@ -313,13 +313,16 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   KRB_REQUIRE(n < ((int64_t)1 << 31), "krb_matrix_create: n >= 2^31");
   static bool pool_ready = false;
   if (!pool_ready) {
-    // keep freed blocks in the default pool: re-creating a sequence's
-    // matrices every step must not pay cudaMalloc / implicit syncs again
+    // keep up to 4 GB of freed blocks in the default pool: re-creating a
+    // small sequence's matrices every step must not pay cudaMalloc /
+    // implicit syncs again, while the blocks of large matrices (a C5 matrix
+    // with its transpose is ~22 GB) go back to the device at the next
+    // synchronisation, where the caller's allocator (torch) can reuse them
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
+      uint64_t thr = (uint64_t)4 << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     pool_ready = true;

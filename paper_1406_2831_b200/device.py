@@ -299,8 +299,17 @@ class DeviceMatrix:
             d_val = to_device(values, np.float64)
             d_ci = to_device(col_idx, np.int32 if col_idx.dtype == np.int32 else np.int64)
         fn = "krb_matrix_create" if col_idx.dtype == np.int32 else "krb_matrix_create_i64"
-        _lib.call(fn, ctypes.byref(h), self.n, self.nnz, ptr(d_rp), ptr(d_ci),
-                  ptr(d_val), int(fmt), s)
+        try:
+            _lib.call(fn, ctypes.byref(h), self.n, self.nnz, ptr(d_rp), ptr(d_ci),
+                      ptr(d_val), int(fmt), s)
+        except _lib.KrbError as e:
+            if "out of memory" not in str(e):
+                raise
+            # the device memory may sit in torch's cache: hand it back, retry
+            t.cuda.synchronize()
+            t.cuda.empty_cache()
+            _lib.call(fn, ctypes.byref(h), self.n, self.nnz, ptr(d_rp), ptr(d_ci),
+                      ptr(d_val), int(fmt), s)
         del d_rp, d_ci, d_val
         self.h = h
         self._finalizer = weakref.finalize(self, _destroy_matrix, h.value)
@@ -319,7 +328,7 @@ class DeviceMatrix:
         if y_dev is None:
             y_dev = t.empty(self.n, dtype=t.float64, device="cuda")
         fn = "krb_spmv_t" if transpose else "krb_spmv"
-        _lib.call(fn, self.h, ptr(x_dev), ptr(y_dev), stream_ptr())
+        call_retry_oom(fn, self.h, ptr(x_dev), ptr(y_dev), stream_ptr())
         return y_dev
 
     def spmm(self, X_dev, transpose=False, out=None):
@@ -331,7 +340,7 @@ class DeviceMatrix:
         if ncols:
             ldx = X_dev.stride(0) if ncols > 1 else self.n
             ldy = out.stride(0) if ncols > 1 else self.n
-            _lib.call("krb_spmm", self.h, 1 if transpose else 0, ncols,
+            call_retry_oom("krb_spmm", self.h, 1 if transpose else 0, ncols,
                       ptr(X_dev), ldx, ptr(out), ldy, stream_ptr())
         return out
 
@@ -344,25 +353,64 @@ def _destroy_matrix(h):
         pass
 
 
+def call_retry_oom(name, *args):
+    """_lib.call, retried once after handing torch's cached device memory
+    back when libkrb's stream-ordered pool (matrices, transposes) reports
+    out of memory."""
+    try:
+        return _lib.call(name, *args)
+    except _lib.KrbError as e:
+        if "out of memory" not in str(e):
+            raise
+        t = torch()
+        t.cuda.synchronize()
+        t.cuda.empty_cache()
+        return _lib.call(name, *args)
+
+
 class _MatrixCache:
     """Device copies keyed on the identity of immutable host matrices (the
     reference freezes SparseMatrix arrays, sparse.py:66-67).  A strong
-    reference pins each key object so ids cannot be recycled; LRU of 3."""
+    reference pins each key object so ids cannot be recycled.  LRU of at most
+    ``cap`` matrices and at most ``budget_frac`` of the device memory (device
+    CSR + SELL + transpose: a C5 matrix is ~23 GB, so a sequence walking
+    through C5 systems keeps one or two, not three)."""
 
-    def __init__(self, cap=3):
+    def __init__(self, cap=3, budget_frac=0.30):
         self.cap = cap
+        self.budget_frac = budget_frac
         self.items: OrderedDict = OrderedDict()
 
-    def get(self, obj, build):
+    @staticmethod
+    def _bytes(dev):
+        b = ctypes.c_int64()
+        try:
+            _lib.call("krb_matrix_info", dev.h, None, None, None, ctypes.byref(b))
+        except Exception:
+            return 0
+        return int(b.value)
+
+    def get(self, obj, build, nnz=0):
         key = id(obj)
         hit = self.items.get(key)
         if hit is not None and hit[0] is obj:
             self.items.move_to_end(key)
             return hit[1]
+        # make room first: a new matrix with its transpose needs about
+        # 2 x (CSR + SELL) = ~50 bytes per stored entry
+        budget = self.budget_frac * torch().cuda.get_device_properties(0).total_memory
+        need = 50 * int(nnz)
+        while self.items and \
+                sum(self._bytes(d) for _, d in self.items.values()) + need > budget:
+            self.items.popitem(last=False)
         dev = build()
         self.items[key] = (obj, dev)
         self.items.move_to_end(key)
         while len(self.items) > self.cap:
+            self.items.popitem(last=False)
+        budget = self.budget_frac * torch().cuda.get_device_properties(0).total_memory
+        while len(self.items) > 1 and \
+                sum(self._bytes(d) for _, d in self.items.values()) > budget:
             self.items.popitem(last=False)
         return dev
 
@@ -396,7 +444,8 @@ def device_matrix(A) -> DeviceMatrix:
         if n != ncols:
             raise ValueError("solver requires a square operator")
         return MATRICES.get(A, lambda: DeviceMatrix(n, A.row_ptr, A.col_idx,
-                                                    A.values, uploaded=PREFETCH.take(A)))
+                                                    A.values, uploaded=PREFETCH.take(A)),
+                            nnz=len(A.values))
     if isinstance(A, np.ndarray):
         if A.ndim != 2 or A.shape[0] != A.shape[1]:
             raise ValueError("solver requires a square operator")

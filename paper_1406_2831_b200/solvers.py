@@ -19,8 +19,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .device import (Context, defer_launch, device_matrix, drop_pending, flush_pending,
-                     ptr, stream_ptr, to_device, to_host, torch)
+from .device import (Context, call_retry_oom, defer_launch, device_matrix, drop_pending,
+                     flush_pending, ptr, stream_ptr, to_device, to_host, torch)
 from .recycling import RecycleSpace
 
 CONVERGED = "converged"
@@ -230,6 +230,8 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     c.d_shadow = None
     c.pcg_state_hi, c.pcg_state_lo, c.pcg_inc_hi, c.pcg_inc_lo = pcg64_words(cfg.seed)
     c.use_graph = int(use_graph)
+    kt = _lib.PY_TUNING["kernel_times"]
+    c.d_kernel_times = kt.data_ptr() if kt is not None else None
     prof = None
     if _lib.PY_TUNING["phase_prof"] and use_graph == 2:
         prof = t.zeros((cfg.max_itn + 1) * 16, dtype=t.int64, device="cuda")
@@ -530,7 +532,7 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     xtd = _dev_vec(x_init_dual)
     H = ctypes.c_void_p()
     view = R.view() if R is not None else None
-    _lib.call("krb_rbicg_create", ctypes.byref(H), ctx.h, M.h,
+    call_retry_oom("krb_rbicg_create", ctypes.byref(H), ctx.h, M.h,
               ctypes.byref(view) if view is not None else None,
               int(cfg.s), int(cfg.max_itn), stream_ptr())
     try:

@@ -1,0 +1,205 @@
+"""Full-size parity fixtures: the REFERENCE itself (krecycle from
+/root/reference/pkg/src) run on the BASELINE configs C1 and C2 at their full
+sizes, at every OpenBLAS thread count in THREADS -- each one a valid
+configuration of the reference, whose results differ in the last bits of
+every BLAS reduction.  Runs in the build container only;
+the small summary arrays go to tests/golden/reference_full.npz (committed).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden_full.py [group ...]
+
+Cases (every solver case stores, per thread count: the first 51 relative
+residuals, iterations, matvecs, status, final true residual):
+
+* bicgstab/c1/j, rbicgstab/c1/j   -- all 6 C1 systems; rbicgstab with the k =
+  10 space biorthonormalize(U, Ut, A_j) of a seeded N(0,1) pair;
+* bicgstab/c2/j, rbicgstab/c2/j   -- C2 systems 0, 5, 9, k = 20;
+* policy/c1first, policy/c2first  -- the sequence policy (sequence.py,
+  policy "first") over the reference's own functions: RBiCG + harvest on
+  system 0, refresh + guarded RBiCGSTAB after (the round-1 C2 bench step);
+* driver/c1, driver/c2s           -- the reference's OWN driver.run_sequence
+  with the ILUTP split preconditioner replaced by the identity (verbatim
+  policy: RBiCG + harvest at every matrix change);
+* ilutp/...                       -- see make_golden_ilutp.py.
+
+The matrices are identified by a sha256 of their CSR arrays, so the GPU
+tests (which regenerate them with paper_1406_2831_b200.workloads on the
+box) first prove they solve the same systems.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+import warnings
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.abspath(os.path.join(HERE, "..", ".."))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+import krecycle as K  # noqa: E402
+from paper_1406_2831_b200 import workloads as W  # noqa: E402
+
+warnings.simplefilter("ignore")
+THREADS = (1, 2, 4, 8, 16)
+OUT = os.path.join(HERE, "reference_full.npz")
+SPACE_SEED = 777
+
+
+def csr_hash(csr) -> str:
+    h = hashlib.sha256()
+    for a in (csr.row_ptr, csr.col_idx, csr.values):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def vec_hash(v) -> str:
+    return hashlib.sha256(np.ascontiguousarray(v, dtype=np.float64).tobytes()).hexdigest()
+
+
+def ref_matrix(csr):
+    return K.SparseMatrix(csr.n, csr.n, csr.row_ptr, csr.col_idx, csr.values)
+
+
+def put_hist(out, p, h):
+    out[p + "resid51"] = np.asarray(h.resid[:51])
+    out[p + "iters"] = np.array(h.iterations)
+    out[p + "matvecs"] = np.array(h.total_matvecs)
+    out[p + "status"] = np.array(h.status)
+    out[p + "final_true_resid"] = np.array(h.final_true_resid)
+
+
+def seeded_pair(n, k, j):
+    r = np.random.default_rng(SPACE_SEED + j)
+    return r.standard_normal((n, k)), r.standard_normal((n, k))
+
+
+def solver_cases(out, name, systems):
+    seq = W.make_sequence(name)
+    for j in systems:
+        A = seq.matrix(j)
+        b = seq.rhs(j, 0)
+        RA = ref_matrix(A)
+        U, Ut = seeded_pair(A.n, seq.k, j)
+        out[f"mat/{name}/{j}/sha"] = np.array(csr_hash(A))
+        out[f"mat/{name}/{j}/b_sha"] = np.array(vec_hash(b))
+        cfg = K.SolverConfig(tol=seq.tol, max_itn=seq.max_itn, seed=j)
+        for th in THREADS:
+            t0 = time.time()
+            with threadpool_limits(th):
+                _, h = K.bicgstab_solve(RA, b, config=cfg)
+                put_hist(out, f"bicgstab/{name}/{j}/t{th}/", h)
+                S = K.biorthonormalize(U, Ut, RA)
+                out[f"rbicgstab/{name}/{j}/t{th}/k"] = np.array(S.k)
+                _, hr = K.rbicgstab_solve(RA, b, recycle=S, config=cfg)
+                put_hist(out, f"rbicgstab/{name}/{j}/t{th}/", hr)
+            print(f"{name} {j} t{th}: bicgstab {h.iterations} {h.status}, rbicgstab "
+                  f"{hr.iterations} {hr.status} ({time.time() - t0:.1f}s)", flush=True)
+
+
+def ref_api():
+    import types
+    return types.SimpleNamespace(
+        SparseMatrix=types.SimpleNamespace(from_csr=ref_matrix),
+        CountingOperator=K.CountingOperator, SolverConfig=K.SolverConfig,
+        rbicg_solve=K.rbicg_solve, rbicgstab_solve=K.rbicgstab_solve,
+        bicgstab_solve=K.bicgstab_solve, update_recycle_space=K.update_recycle_space,
+        refresh_images=K.refresh_images)
+
+
+def put_seq(out, p, rec, space_dims):
+    out[p + "space_dims"] = np.asarray(space_dims)
+    out[p + "iters"] = np.asarray([h.iterations for h in rec.histories])
+    out[p + "matvecs"] = np.asarray([h.total_matvecs for h in rec.histories])
+    out[p + "status"] = np.asarray([h.status for h in rec.histories])
+    out[p + "aux"] = np.array(rec.aux_matvecs)
+    out[p + "resid51_0"] = np.asarray(rec.histories[0].resid[:51])
+    out[p + "resid51_1"] = np.asarray(rec.histories[1].resid[:51])
+
+
+def policy_cases(out, name):
+    from paper_1406_2831_b200.sequence import run_sequence
+    seq = W.make_sequence(name)
+    for j in range(seq.num_matrices):
+        out[f"mat/{name}/{j}/sha"] = np.array(csr_hash(seq.matrix(j)))
+    for th in THREADS:
+        t0 = time.time()
+        with threadpool_limits(th):
+            res = run_sequence(W.make_sequence(name), policy="first", baseline=False,
+                               api=ref_api())
+        put_seq(out, f"policy/{name}first/t{th}/", res.recycling, res.space_dims)
+        print(f"policy {name} t{th}: {[h.iterations for h in res.recycling.histories]} "
+              f"dims {res.space_dims} ({time.time() - t0:.1f}s)", flush=True)
+
+
+class _SeqAdapter:
+    """A workloads sequence seen through krecycle's ParametricSequence
+    interface (matrix(i) -> SparseMatrix, rhs[i][kappa])."""
+
+    def __init__(self, seq):
+        self.seq = seq
+        self.num_matrices = seq.num_matrices
+        self.rhs_per_matrix = seq.rhs_per_matrix
+        self.rhs = [[seq.rhs(i, kap) for kap in range(seq.rhs_per_matrix)]
+                    for i in range(seq.num_matrices)]
+
+    def matrix(self, i):
+        return ref_matrix(self.seq.matrix(i))
+
+
+def driver_cases(out, tag, seq, threads=THREADS):
+    """The reference's driver.run_sequence itself, preconditioner = identity
+    (ilutp_factor / SplitPreconditionedOperator / apply_left patched in the
+    driver module only; everything else is the reference's own code)."""
+    import krecycle.driver as KD
+    saved = (KD.ilutp_factor, KD.SplitPreconditionedOperator, KD.apply_left)
+    KD.ilutp_factor = lambda A, **kw: None
+    KD.SplitPreconditionedOperator = lambda A, f: A
+    KD.apply_left = lambda f, b: np.asarray(b)
+    try:
+        for th in threads:
+            t0 = time.time()
+            with threadpool_limits(th):
+                res = KD.run_sequence(_SeqAdapter(seq), tol=seq.tol, max_itn=seq.max_itn,
+                                      k=seq.k, s=seq.s, seed=0)
+            put_seq(out, f"driver/{tag}/t{th}/", res.recycling, res.space_dims)
+            out[f"driver/{tag}/t{th}/base_iters"] = np.asarray(
+                [h.iterations for h in res.baseline.histories])
+            out[f"driver/{tag}/t{th}/base_aux"] = np.array(res.baseline.aux_matvecs)
+            print(f"driver {tag} t{th}: {[h.iterations for h in res.recycling.histories]} "
+                  f"dims {res.space_dims} ({time.time() - t0:.1f}s)", flush=True)
+    finally:
+        KD.ilutp_factor, KD.SplitPreconditionedOperator, KD.apply_left = saved
+
+
+GROUPS = {
+    "c1": lambda out: solver_cases(out, "c1", range(6)),
+    "c2": lambda out: solver_cases(out, "c2", (0, 5, 9)),
+    "policy": lambda out: (policy_cases(out, "c1"), policy_cases(out, "c2")),
+    "driver": lambda out: (driver_cases(out, "c1", W.make_sequence("c1")),
+                           driver_cases(out, "c2s", W.make_sequence("c2", small=True))),
+}
+
+
+def main():
+    groups = sys.argv[1:] or list(GROUPS)
+    out = dict(np.load(OUT)) if os.path.exists(OUT) else {}
+    for g in groups:
+        GROUPS[g](out)
+        np.savez_compressed(OUT, **out)     # incremental: a long run keeps its parts
+    import scipy
+    out["meta/numpy"] = np.array(np.__version__)
+    out["meta/scipy"] = np.array(scipy.__version__)
+    out["meta/threads"] = np.asarray(THREADS)
+    np.savez_compressed(OUT, **out)
+    print(f"wrote {OUT}: {len(out)} arrays, {os.path.getsize(OUT)} bytes")
+
+
+if __name__ == "__main__":
+    main()

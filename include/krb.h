@@ -56,6 +56,15 @@ int64_t krb_launch_count(void);
 int krb_set_tuning(const char *key, int64_t value);
 int krb_reset_tuning(void);
 
+/* Device allocator for the library's own arrays (matrices, transposes and
+ * their build temporaries).  Default: the stream-ordered CUDA pool.  A host
+ * framework installs its caching allocator here so both share one pool
+ * (the Python binding installs torch's).  Must be called before the first
+ * allocation; alloc returns NULL on failure (-> KRB_ENOMEM).             */
+typedef void *(*krb_alloc_fn)(size_t bytes, void *stream);
+typedef void (*krb_free_fn)(void *ptr, void *stream);
+int krb_set_allocator(krb_alloc_fn alloc, krb_free_fn free_fn);
+
 /* stream-ordered device-to-device copy (ring views -> caller tensors) */
 int krb_memcpy_d2d(void *d_dst, const void *d_src, int64_t bytes, void *stream);
 
@@ -179,6 +188,13 @@ typedef struct krb_solve_config {
    * that did work.  36 uint64, zeroed by the caller; accumulates across
    * solves.                                                              */
   uint64_t *d_kernel_times;
+  /* optional record_iterates (solvers.py:40-56, recording at :168-172,
+   * :209-218, :281-286, :340-346; host-loop driver only): per history entry
+   * j (0 = start) d_rec_x / d_rec_r[j n ..] = x, r and d_rec_xc[j k ..] = xc
+   * (the iterate is x - U xc); per full iteration i (0-based)
+   * d_rec_s / d_rec_t[i n ..] = s, t and d_rec_omega[i] = omega.  NULL
+   * d_rec_x = off; capacity max_itn + 1 entries.                          */
+  double *d_rec_x, *d_rec_r, *d_rec_xc, *d_rec_s, *d_rec_t, *d_rec_omega;
 } krb_solve_config;
 
 typedef struct krb_solve_result {

@@ -47,7 +47,9 @@ class SolveConfig(ctypes.Structure):
                 ("pcg_state_hi", c_u64), ("pcg_state_lo", c_u64),
                 ("pcg_inc_hi", c_u64), ("pcg_inc_lo", c_u64),
                 ("use_graph", c_int), ("d_phase_stamps", c_vp),
-                ("phase_stamps_cap", c_i64), ("d_kernel_times", c_vp)]
+                ("phase_stamps_cap", c_i64), ("d_kernel_times", c_vp),
+                ("d_rec_x", c_vp), ("d_rec_r", c_vp), ("d_rec_xc", c_vp),
+                ("d_rec_s", c_vp), ("d_rec_t", c_vp), ("d_rec_omega", c_vp)]
 
 
 class SolveResult(ctypes.Structure):
@@ -69,6 +71,7 @@ SIGNATURES = {
     "krb_launch_count": (c_i64, []),
     "krb_set_tuning": (c_int, [ctypes.c_char_p, c_i64]),
     "krb_reset_tuning": (c_int, []),
+    "krb_set_allocator": (c_int, [c_vp, c_vp]),
     "krb_context_create": (c_int, [ctypes.POINTER(c_vp)]),
     "krb_context_destroy": (c_int, [c_vp]),
     "krb_matrix_create": (c_int, [ctypes.POINTER(c_vp), c_i64, c_i64, c_vp,

@@ -20,6 +20,29 @@ void set_error(const char *fmt, ...) {
 
 int64_t &launch_counter() { return g_launches; }
 
+static krb_alloc_fn g_alloc = nullptr;
+static krb_free_fn g_free = nullptr;
+static bool g_allocated = false;   // any dev_alloc yet (the hook is fixed after)
+
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t st) {
+  g_allocated = true;
+  if (g_alloc) {
+    *p = g_alloc(bytes ? bytes : 8, (void *)st);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
+void dev_free(void *p, cudaStream_t st) {
+  if (!p) return;
+  if (g_free)
+    g_free(p, (void *)st);
+  else if (st)
+    cudaFreeAsync(p, st);
+  else
+    cudaFree(p);
+}
+
 Tuning &tuning() {
   static Tuning t;
   return t;
@@ -50,6 +73,17 @@ int krb_set_tuning(const char *key, int64_t value) {
     }
   krb::set_error("krb_set_tuning: unknown key '%s'", key);
   return KRB_EINVAL;
+}
+
+int krb_set_allocator(krb_alloc_fn alloc, krb_free_fn free_fn) {
+  KRB_REQUIRE((alloc == nullptr) == (free_fn == nullptr),
+              "krb_set_allocator: give both functions or neither");
+  if (krb::g_alloc == alloc && krb::g_free == free_fn) return KRB_OK;
+  KRB_REQUIRE(!krb::g_allocated,
+              "krb_set_allocator: device memory was already allocated");
+  krb::g_alloc = alloc;
+  krb::g_free = free_fn;
+  return KRB_OK;
 }
 
 int krb_reset_tuning(void) {

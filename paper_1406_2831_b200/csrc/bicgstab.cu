@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ 
     double *y = kSecond ? a.t : a.q;
     y[(kSell && a.A.perm) ? a.A.perm[i] : i] = spmv_row<kSell>(i, a.A, x);
   }
-  ktime_finish(a, kSecond ? 5 : 1);
+  ktime_end_spmv(a, kSecond ? 5 : 1);
 }
 
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
@@ -373,6 +373,14 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   h.prof = cfg->d_phase_stamps;
   h.prof_cap = cfg->d_phase_stamps ? cfg->phase_stamps_cap : 0;
   h.ktime = cfg->d_kernel_times;
+  if (cfg->d_rec_x) {
+    KRB_REQUIRE(cfg->use_graph == 0, "record_iterates needs the host-loop driver");
+    KRB_REQUIRE(cfg->d_rec_r && cfg->d_rec_s && cfg->d_rec_t && cfg->d_rec_omega &&
+                    (k == 0 || cfg->d_rec_xc),
+                "record_iterates: NULL snapshot buffer");
+    h.rec_x = cfg->d_rec_x; h.rec_r = cfg->d_rec_r; h.rec_xc = cfg->d_rec_xc;
+    h.rec_s = cfg->d_rec_s; h.rec_t = cfg->d_rec_t; h.rec_omega = cfg->d_rec_omega;
+  }
   const int mode = cfg->use_graph;   // 0 host loop, 1 graph, 2 persistent
   const bool graph = mode == 1;
   GraphCache &G = ctx->graph;

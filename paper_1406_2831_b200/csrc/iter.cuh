@@ -34,6 +34,8 @@ struct IterArgs {
   uint64_t *prof;         // optional per-phase %globaltimer stamps (16/iter)
   int64_t prof_cap;
   uint64_t *ktime;        // optional live per-kernel time (krb_solve_config)
+  // optional record_iterates snapshots (krb_solve_config.d_rec_*)
+  double *rec_x, *rec_r, *rec_xc, *rec_s, *rec_t, *rec_omega;
   unsigned int *counters;
   unsigned int *flags;    // per-CTA phase epochs, 128 B apart (persist0.cu)
   SolveScalars *S;
@@ -69,9 +71,36 @@ __host__ __device__ constexpr int ktime_slot_of(int PH) {
        : PH == PH_PROJ_T ? 7 : PH == PH_XR ? 8 : -1;
 }
 
+// The SpMV kernels (slots 1, 5: one CTA per 256 rows, 65536 CTAs at C5)
+// mark their end with a fire-and-forget atomicMax per CTA instead of a
+// last-CTA election (an atomic with a return value per CTA costs ~20 % of
+// the launch); the next kernel's CTA 0 folds the pending end into the total.
+__device__ __forceinline__ void ktime_fold_spmv(const IterArgs &a) {
+#pragma unroll
+  for (int s = 1; s <= 5; s += 4) {
+    volatile uint64_t *kt = (volatile uint64_t *)a.ktime + 4 * s;
+    const uint64_t end = kt[3];
+    if (end != 0) {
+      kt[1] = kt[1] + (end - kt[0]);
+      kt[2] = kt[2] + 1;
+      kt[3] = 0;
+    }
+  }
+}
+
 __device__ __forceinline__ void ktime_start(const IterArgs &a, int slot) {
-  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    ktime_fold_spmv(a);
     *(volatile uint64_t *)&a.ktime[4 * slot] = globaltimer();
+  }
+}
+
+__device__ __forceinline__ void ktime_end_spmv(const IterArgs &a, int slot) {
+  if (!a.ktime) return;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    atomicMax((unsigned long long *)&a.ktime[4 * slot + 3],
+              (unsigned long long)globaltimer());
 }
 
 // by thread 0 of the CTA known to finish last
@@ -262,8 +291,16 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
         double sv = s[i];
         x[i] = __dadd_rn(__dadd_rn(x[i], __dmul_rn(alpha, p[i])),
                          __dmul_rn(omega, sv));
-        double rv = __dsub_rn(sv, __dmul_rn(omega, t[i]));
+        double tv = t[i];
+        double rv = __dsub_rn(sv, __dmul_rn(omega, tv));
         r[i] = rv;
+        if (a.rec_x) {              // record_iterates: entry hist_len, step itn
+          const int64_t j = a.S->hist_len, it = a.S->itn;
+          a.rec_x[j * n + i] = x[i];
+          a.rec_r[j * n + i] = rv;
+          a.rec_s[it * n + i] = sv;
+          a.rec_t[it * n + i] = tv;
+        }
         acc[0] = __fma_rn(rv, rv, acc[0]);
         acc[1] = __fma_rn(rt0[i], rv, acc[1]);
       } else if (PH == PH_BNORM) {
@@ -271,6 +308,10 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
         acc[0] = __fma_rn(bv, bv, acc[0]);
       } else if (PH == PH_INIT) {
         double rv = r[i], tv = rt0[i];
+        if (a.rec_x) {              // record_iterates: entry 0
+          a.rec_x[i] = x[i];
+          a.rec_r[i] = rv;
+        }
         acc[0] = __fma_rn(rv, rv, acc[0]);
         acc[1] = __fma_rn(tv, rv, acc[1]);
         acc[2] = __fma_rn(tv, tv, acc[2]);
@@ -306,23 +347,41 @@ __device__ __forceinline__ void phase_leader(const IterArgs &a, const PhaseScal 
   }
   if (PH == PH_XR) {
     // xc = xc + alpha*zeta + omega*gamma     (solvers.py:340)
-    for (int j = threadIdx.x; j < a.k; j += blockDim.x)
-      a.xc[j] = __dadd_rn(__dadd_rn(a.xc[j], __dmul_rn(sc.alpha, a.zeta[j])),
-                          __dmul_rn(sc.omega, a.gamma[j]));
+    const int64_t hj = a.S->hist_len;
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x) {
+      const double v = __dadd_rn(__dadd_rn(a.xc[j], __dmul_rn(sc.alpha, a.zeta[j])),
+                                 __dmul_rn(sc.omega, a.gamma[j]));
+      a.xc[j] = v;
+      if (a.rec_x) a.rec_xc[hj * a.k + j] = v;
+    }
+    if (a.rec_x && threadIdx.x == 0) a.rec_omega[a.S->itn] = sc.omega;
   }
+  if (PH == PH_INIT && a.rec_x)
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x) a.rec_xc[j] = a.xc[j];
   __syncthreads();
   if (threadIdx.x == 0) finalize<PH>(a, a.S, dfin);
   __syncthreads();
 }
 
 // half-step exit (solvers.py:315-325): x += alpha p, xc += alpha zeta
+// (record_iterates: entry hist_len - 1 gets x, r = s and xc)
 __device__ __forceinline__ void half_exit_update(const IterArgs &a, double alpha,
                                                  int64_t first, int64_t step) {
-  for (int64_t i = first * blockDim.x + threadIdx.x; i < a.n; i += step * blockDim.x)
-    a.x[i] = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));   // solvers.py:316
+  const int64_t hj = a.rec_x ? a.S->hist_len - 1 : 0;
+  for (int64_t i = first * blockDim.x + threadIdx.x; i < a.n; i += step * blockDim.x) {
+    const double xv = __dadd_rn(a.x[i], __dmul_rn(alpha, a.p[i]));   // solvers.py:316
+    a.x[i] = xv;
+    if (a.rec_x) {
+      a.rec_x[hj * a.n + i] = xv;
+      a.rec_r[hj * a.n + i] = a.s[i];                               // solvers.py:319
+    }
+  }
   if (first == 0)
-    for (int j = threadIdx.x; j < a.k; j += blockDim.x)     // solvers.py:318
-      a.xc[j] = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
+    for (int j = threadIdx.x; j < a.k; j += blockDim.x) {   // solvers.py:318
+      const double v = __dadd_rn(a.xc[j], __dmul_rn(alpha, a.zeta[j]));
+      a.xc[j] = v;
+      if (a.rec_x) a.rec_xc[hj * a.k + j] = v;
+    }
 }
 
 // per-solve setup / tail shared by the single and batched drivers

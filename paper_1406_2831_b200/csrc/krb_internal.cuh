@@ -35,6 +35,14 @@ struct krb_matrix {
 
 namespace krb {
 
+// ---------------------------------------------------------- allocation
+// Device memory of matrices / transposes / their build temporaries: the
+// caller's allocator when one is installed (krb_set_allocator: the Python
+// binding installs torch's caching allocator, so the library and torch
+// share one pool), else the stream-ordered CUDA pool.
+cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t st);
+void dev_free(void *p, cudaStream_t st);
+
 // ---------------------------------------------------------------- errors
 void set_error(const char *fmt, ...);
 int64_t &launch_counter();

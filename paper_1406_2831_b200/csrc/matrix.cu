@@ -191,7 +191,7 @@ static int sell_layout(krb_matrix *A, const int32_t *rlen_pos, int64_t *total,
                        cudaStream_t st) {
   const int64_t n = A->n;
   int64_t *width = nullptr;
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&width, sizeof(int64_t) * (A->nslices + 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&width, sizeof(int64_t) * (A->nslices + 1), st));
   if (n > 0) {
     unsigned wblocks = (unsigned)((A->nslices * 32 + 255) / 256);
     k_slice_width<<<wblocks, 256, 0, st>>>(n, rlen_pos, width);
@@ -201,14 +201,14 @@ static int sell_layout(krb_matrix *A, const int32_t *rlen_pos, int64_t *total,
   void *tmp = nullptr;
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr, A->nslices + 1, st);
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tmp, tmp_bytes, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&tmp, tmp_bytes, st));
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, width, A->sl_ptr, A->nslices + 1, st);
   KRB_CHECK_CUDA(cudaGetLastError());
   KRB_CHECK_CUDA(cudaMemcpyAsync(total, A->sl_ptr + A->nslices, sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(width, st);
+  dev_free(tmp, st);
+  dev_free(width, st);
   return KRB_OK;
 }
 
@@ -222,10 +222,10 @@ static int sigma_sort(krb_matrix *A, cudaStream_t st) {
   const int64_t nseg = (n + kSigma - 1) / kSigma;
   int32_t *keys_out = nullptr, *iota = nullptr;
   int *off = nullptr;
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&keys_out, sizeof(int32_t) * n, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&iota, sizeof(int32_t) * n, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->perm, sizeof(int32_t) * n, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&off, sizeof(int) * (nseg + 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&keys_out, sizeof(int32_t) * n, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&iota, sizeof(int32_t) * n, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->perm, sizeof(int32_t) * n, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&off, sizeof(int) * (nseg + 1), st));
   k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, iota);
   KRB_CHECK_LAUNCH();
   k_window_offsets<<<(unsigned)((nseg + 256) / 256), 256, 0, st>>>(nseg, n, kSigma, off);
@@ -235,15 +235,15 @@ static int sigma_sort(krb_matrix *A, cudaStream_t st) {
   cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, A->rlen, keys_out, iota,
                                                      A->perm, (int)n, (int)nseg, off, off + 1,
                                                      0, 32, st);
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tmp, tb, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&tmp, tb, st));
   cub::DeviceSegmentedRadixSort::SortPairsDescending(tmp, tb, A->rlen, keys_out, iota,
                                                      A->perm, (int)n, (int)nseg, off, off + 1,
                                                      0, 32, st);
   KRB_CHECK_CUDA(cudaGetLastError());
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(off, st);
-  cudaFreeAsync(iota, st);
-  cudaFreeAsync(A->rlen, st);
+  dev_free(tmp, st);
+  dev_free(off, st);
+  dev_free(iota, st);
+  dev_free(A->rlen, st);
   A->rlen = keys_out;   // lengths now indexed by slice position
   return KRB_OK;
 }
@@ -251,8 +251,8 @@ static int sigma_sort(krb_matrix *A, cudaStream_t st) {
 static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
   const int64_t n = A->n;
   A->nslices = (n + 31) / 32;
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1), st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->rlen, sizeof(int32_t) * (n > 0 ? n : 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->sl_ptr, sizeof(int64_t) * (A->nslices + 1), st));
   unsigned blocks = (unsigned)((n + 255) / 256);
   if (n > 0) {
     k_row_len<<<blocks, 256, 0, st>>>(n, A->rp, A->rlen);
@@ -270,21 +270,21 @@ static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
     if (rc) return rc;
     use_sell = format == 3 || total <= budget;
     if (!use_sell) {
-      cudaFreeAsync(A->perm, st);
+      dev_free(A->perm, st);
       A->perm = nullptr;
     }
   }
   A->sell_elems = total;
   if (!use_sell) {
-    cudaFreeAsync(A->sl_ptr, st);
+    dev_free(A->sl_ptr, st);
     A->sl_ptr = nullptr;
-    cudaFreeAsync(A->rlen, st);
+    dev_free(A->rlen, st);
     A->rlen = nullptr;
     A->format = 1;
     return KRB_OK;
   }
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->s_col, sizeof(int32_t) * (total > 0 ? total : 1), st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&A->s_val, sizeof(double) * (total > 0 ? total : 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->s_col, sizeof(int32_t) * (total > 0 ? total : 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->s_val, sizeof(double) * (total > 0 ? total : 1), st));
   if (total > A->nnz) {
     k_pad_fill<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(total, A->s_col, A->s_val);
     KRB_CHECK_LAUNCH();
@@ -330,12 +330,12 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   krb_matrix *A = new krb_matrix();
   A->n = n;
   A->nnz = nnz;
-  cudaError_t e = cudaMallocAsync((void **)&A->rp, sizeof(int64_t) * (n + 1), st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void **)&A->ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void **)&A->val, sizeof(double) * (nnz > 0 ? nnz : 1), st);
+  cudaError_t e = dev_alloc((void **)&A->rp, sizeof(int64_t) * (n + 1), st);
+  if (e == cudaSuccess) e = dev_alloc((void **)&A->ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st);
+  if (e == cudaSuccess) e = dev_alloc((void **)&A->val, sizeof(double) * (nnz > 0 ? nnz : 1), st);
   if (e != cudaSuccess) {
     set_error("krb_matrix_create: %s", cudaGetErrorString(e));
-    cudaFreeAsync(A->rp, st); cudaFreeAsync(A->ci, st); cudaFreeAsync(A->val, st);
+    dev_free(A->rp, st); dev_free(A->ci, st); dev_free(A->val, st);
     delete A;
     return KRB_ENOMEM;
   }
@@ -395,12 +395,12 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   int64_t *cnt = nullptr, *trp = nullptr;
   double *tval = nullptr;
   size_t m = nnz > 0 ? nnz : 1;
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&rows, sizeof(int32_t) * m, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&keys_out, sizeof(int32_t) * m, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&perm_in, sizeof(int32_t) * m, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&perm_out, sizeof(int32_t) * m, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&cnt, sizeof(int64_t) * (n + 1), st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&trp, sizeof(int64_t) * (n + 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&rows, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&keys_out, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&perm_in, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&perm_out, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&cnt, sizeof(int64_t) * (n + 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&trp, sizeof(int64_t) * (n + 1), st));
   KRB_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n + 1), st));
   unsigned nb = (unsigned)((nnz + 255) / 256), rb = (unsigned)((n + 255) / 256);
   if (n > 0) {
@@ -420,29 +420,29 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   cub::DeviceRadixSort::SortPairs(nullptr, tb1, A->ci, keys_out, perm_in,
                                   perm_out, (int)nnz, 0, end_bit, st);
   cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, trp, n + 1, st);
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tmp, tb1 > tb2 ? tb1 : tb2, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&tmp, tb1 > tb2 ? tb1 : tb2, st));
   if (nnz > 0)
     cub::DeviceRadixSort::SortPairs(tmp, tb1, A->ci, keys_out, perm_in,
                                     perm_out, (int)nnz, 0, end_bit, st);
   cub::DeviceScan::ExclusiveSum(tmp, tb2, cnt, trp, n + 1, st);
   KRB_CHECK_CUDA(cudaGetLastError());
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tci, sizeof(int32_t) * m, st));
-  KRB_CHECK_CUDA(cudaMallocAsync((void **)&tval, sizeof(double) * m, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&tci, sizeof(int32_t) * m, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&tval, sizeof(double) * m, st));
   if (nnz > 0) {
     k_gather_t<<<nb, 256, 0, st>>>(nnz, perm_out, rows, A->val, tci, tval);
     KRB_CHECK_LAUNCH();
   }
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(rows, st);
-  cudaFreeAsync(keys_out, st);
-  cudaFreeAsync(perm_in, st);
-  cudaFreeAsync(perm_out, st);
-  cudaFreeAsync(cnt, st);
+  dev_free(tmp, st);
+  dev_free(rows, st);
+  dev_free(keys_out, st);
+  dev_free(perm_in, st);
+  dev_free(perm_out, st);
+  dev_free(cnt, st);
   krb_matrix *T = nullptr;
   int rc = matrix_create(&T, n, nnz, trp, tci, nullptr, tval, 0, st);
-  cudaFreeAsync(trp, st);
-  cudaFreeAsync(tci, st);
-  cudaFreeAsync(tval, st);
+  dev_free(trp, st);
+  dev_free(tci, st);
+  dev_free(tval, st);
   if (rc != KRB_OK) return rc;
   A->T = T;
   return KRB_OK;
@@ -456,13 +456,9 @@ void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
   if (!A) return;
   matrix_free(A->T, async, st);
   void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm};
+  if (!async) cudaDeviceSynchronize();
   for (void *p : arrays)
-    if (p) {
-      if (async)
-        cudaFreeAsync(p, st);
-      else
-        cudaFree(p);
-    }
+    if (p) dev_free(p, async ? st : nullptr);
   delete A;
 }
 

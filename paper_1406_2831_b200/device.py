@@ -26,17 +26,43 @@ def torch():
 _CUDA_OK = False
 
 
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
+@_ALLOC_FN
+def _torch_alloc(nbytes, stream):
+    try:
+        return torch()._C._cuda_cudaCachingAllocator_raw_alloc(int(nbytes), int(stream or 0))
+    except Exception:      # out of memory -> NULL -> KRB_ENOMEM
+        return None
+
+
+@_FREE_FN
+def _torch_free(p, stream):
+    try:
+        torch()._C._cuda_cudaCachingAllocator_raw_delete(int(p))
+    except Exception:      # interpreter shutdown: torch already torn down
+        pass
+
+
 def require_cuda():
     """Raise KrbError without a CUDA device (no CPU fallback).  The positive
     answer is cached: torch.cuda.is_available() re-queries NVML / the
-    environment on every call (~0.1 ms), and this runs once per entry point."""
+    environment on every call (~0.1 ms), and this runs once per entry point.
+    The first call also makes libkrb allocate its matrices from torch's
+    caching allocator (krb_set_allocator), so the library and torch share
+    one device pool instead of two that cannot lend each other memory."""
     global _CUDA_OK
     if _CUDA_OK:
         return
     t = torch()
     if not t.cuda.is_available():
         raise _lib.KrbError("no CUDA device: the B200 path has no CPU fallback")
-    _lib.load()
+    lib = _lib.load()
+    rc = lib.krb_set_allocator(ctypes.cast(_torch_alloc, ctypes.c_void_p),
+                               ctypes.cast(_torch_free, ctypes.c_void_p))
+    _lib.check(rc, "krb_set_allocator")
     _CUDA_OK = True
 
 
@@ -439,6 +465,7 @@ def device_matrix(A) -> DeviceMatrix:
     if inner is not None and not hasattr(A, "row_ptr"):
         return device_matrix(inner)
     if hasattr(A, "row_ptr") and hasattr(A, "col_idx") and hasattr(A, "values"):
+        require_cuda()
         n = A.nrows if hasattr(A, "nrows") else A.n
         ncols = A.ncols if hasattr(A, "ncols") else n
         if n != ncols:

@@ -106,6 +106,15 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
     total = seq.num_systems if systems is None else min(systems, seq.num_systems)
     t_start = time.perf_counter()
     prefetch = getattr(api, "prefetch_matrix", None)
+    # the cycles are consumed by the harvest callback; a backend that can
+    # drop them instead of returning the whole list is told to (device
+    # cycles are n x (s+2) pairs: ~100 GB per C5 generation solve)
+    import inspect
+    try:
+        drop_kw = ({"keep_cycles": False}
+                   if "keep_cycles" in inspect.signature(api.rbicg_solve).parameters else {})
+    except (TypeError, ValueError):
+        drop_kw = {}
     A_next = None
     for i in range(seq.num_matrices):
         if gidx >= total:
@@ -138,7 +147,7 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                 dual_rhs = np.ones(A.nrows if hasattr(A, "nrows") else seq.n)
                 _, _, hist, _ = api.rbicg_solve(op_rec, b, b_dual=dual_rhs,
                                                 recycle=space, config=cfg,
-                                                cycle_callback=harvest)
+                                                cycle_callback=harvest, **drop_kw)
                 if hist.status == "converged":
                     space = state["space"]
                 else:

@@ -127,9 +127,6 @@ def _check_common(A, b, precond, cfg):
     if precond is not None:
         raise NotImplementedError("split preconditioning is out of scope on the "
                                   "B200 path (SURVEY.md §2.1 row 7)")
-    if cfg.record_iterates:
-        raise NotImplementedError("record_iterates is not supported on the "
-                                  "device path")
     M = device_matrix(A)
     if _is_device(b):
         if tuple(b.shape) != (M.n,):
@@ -229,6 +226,19 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     c.max_itn = int(cfg.max_itn)
     c.d_shadow = None
     c.pcg_state_hi, c.pcg_state_lo, c.pcg_inc_hi, c.pcg_inc_lo = pcg64_words(cfg.seed)
+    rec = None
+    if cfg.record_iterates:
+        # per-iteration snapshots on the device (host-loop driver: the graph
+        # and persistent drivers do not carry the snapshot pointers)
+        use_graph = 0
+        L = int(cfg.max_itn) + 2
+        kk = R.k if R is not None else 0
+        rec = {nm: t.empty((L, M.n), dtype=t.float64, device="cuda")
+               for nm in ("x", "r", "s", "t")}
+        rec["xc"] = t.empty((L, max(kk, 1)), dtype=t.float64, device="cuda")
+        rec["omega"] = t.empty(L, dtype=t.float64, device="cuda")
+        for nm in ("x", "r", "xc", "s", "t", "omega"):
+            setattr(c, "d_rec_" + nm, rec[nm].data_ptr())
     c.use_graph = int(use_graph)
     kt = _lib.PY_TUNING["kernel_times"]
     c.d_kernel_times = kt.data_ptr() if kt is not None else None
@@ -258,6 +268,8 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     hist.seconds = [base + (int(s) - st0) * 1e-9 for s in stamps]
     hist.status = _STATUS.get(int(res.status), f"unknown:{res.status}")
     hist.final_true_resid = float(res.final_true_resid)
+    if rec is not None:
+        _attach_iterates(hist, rec, R, L)
     LAST_SOLVE.clear()
     LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
                       kernel_launches=int(res.kernel_launches),
@@ -265,6 +277,33 @@ def solve_device(M, bd, xd, recycle, cfg, label="rbicgstab", t0=None,
     if prof is not None:
         LAST_SOLVE["phase_stamps"] = prof.view(-1, 16)[:hist.iterations].cpu().numpy()
     return xo, hist
+
+
+def _attach_iterates(hist, rec, R, L):
+    """record_iterates (solvers.py:284-286, 321-323, 344-347): iterates
+    x_j - U xc_j (one device GEMM over all entries, the same per-row fma
+    order as the solve's final x - U xc), residual vectors, and per full
+    iteration (s, t, omega); host numpy like the reference."""
+    t = torch()
+    from .recycling import gemm
+    X = rec["x"][:L]
+    if R is not None and R.k:
+        UX = gemm(R.device("U"), rec["xc"][:L, :R.k].t().contiguous())   # (L, n)
+        X = X - UX
+    nfull = L - 1 - (1 if hist.status == CONVERGED and len(hist.resid) >= 2 and
+                     _half_step(hist) else 0)
+    Xh, Rh = X.cpu().numpy(), rec["r"][:L].cpu().numpy()
+    Sh, Th = rec["s"][:nfull].cpu().numpy(), rec["t"][:nfull].cpu().numpy()
+    om = rec["omega"][:nfull].cpu().numpy()
+    hist.iterates = [Xh[j].copy() for j in range(L)]
+    hist.residual_vectors = [Rh[j].copy() for j in range(L)]
+    hist.omega_steps = [(Sh[i].copy(), Th[i].copy(), complex(om[i])) for i in range(nfull)]
+
+
+def _half_step(hist):
+    """Whether the last record is a half-step exit (1 product after the
+    previous record instead of 2)."""
+    return len(hist.matvecs) >= 2 and hist.matvecs[-1] - hist.matvecs[-2] == 1
 
 
 BATCH_MAX = 4   # right-hand sides per batched launch (batch.cu kMaxB)
@@ -343,6 +382,8 @@ def _batch_solve(A, bs, x_inits, recycle, configs, label):
     configs = list(configs) if configs is not None else [SolverConfig()] * len(bs)
     if len(configs) != len(bs):
         raise ValueError("one SolverConfig per right-hand side")
+    if any(c.record_iterates for c in configs):
+        raise NotImplementedError("record_iterates: use rbicgstab_solve per system")
     x_inits = list(x_inits) if x_inits is not None else [None] * len(bs)
     M, _ = _check_common(A, bs[0], None, configs[0])
     on_device = _is_device(bs[0])
@@ -426,10 +467,10 @@ class _CycleHarvest:
     """Host bookkeeping of the capture windows (solvers.py:512-558) over the
     device ring of krb_rbicg."""
 
-    def __init__(self, H, n, callback):
+    def __init__(self, H, n, callback, keep=True):
         from .recycling import CapturedCycle
         self.CapturedCycle = CapturedCycle
-        self.H, self.n, self.callback = H, n, callback
+        self.H, self.n, self.callback, self.keep = H, n, callback, keep
         self.start = 1
         self.emitted = 0
         self.cycles = []
@@ -490,7 +531,8 @@ class _CycleHarvest:
         cyc = self.CapturedCycle(
             V=Vd, Vt=Vtd, first_index=start,
             tri=lambda: _tri_block(start, ncols, alphas, betas, rhos))   # lazy
-        self.cycles.append(cyc)
+        if self.keep:
+            self.cycles.append(cyc)
         self.emitted = last
         if not final and ncols > 2:
             # the copies above are queued first on the same stream, so the
@@ -502,11 +544,17 @@ class _CycleHarvest:
 
 
 def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
-                precond=None, config=None, cycle_callback=None):
+                precond=None, config=None, cycle_callback=None, keep_cycles=True):
     """solvers.py:460-638 — two-sided deflated BiCG with cycle harvesting.
     Iterations run on the device (CUDA graph, device WHILE node that pauses
     at every completed cycle); each captured cycle is handed to
-    ``cycle_callback`` as it completes.  Returns (x, x_dual, history, cycles)."""
+    ``cycle_callback`` as it completes.  Returns (x, x_dual, history, cycles).
+
+    ``keep_cycles=False`` (extension, not in the reference signature) drops
+    each cycle after its callback instead of returning all of them: the
+    cycles are device-resident n x (s+2) pairs, 8 GB each at C5, and a
+    caller that consumes them in the callback (the sequence policy) would
+    otherwise hold ~100 GB of HBM for a list it discards."""
     cfg = config or SolverConfig()
     t0 = time.perf_counter()
     M, b = _check_common(A, b, precond, cfg)
@@ -559,7 +607,7 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
                   stream_ptr())
         status = ctypes.c_int32()
         _lib.call("krb_rbicg_begin", H, ctypes.byref(status), stream_ptr())
-        harvest = _CycleHarvest(H, n, cycle_callback)
+        harvest = _CycleHarvest(H, n, cycle_callback, keep_cycles)
         state = (ctypes.c_int64 * 7)()
         launched = ctypes.c_int32()
         st = stream_ptr()   # the solve's stream, fixed even if a callback switches streams

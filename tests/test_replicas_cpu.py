@@ -28,7 +28,7 @@ def _replica(rank, world, port, out):
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, repo)
     import time
-    from bench import oracle_api
+    from oracle.api import oracle_api
     from paper_1406_2831_b200.sequence import run_sequence
     from paper_1406_2831_b200.workloads import make_sequence
     dist.barrier()

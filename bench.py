@@ -302,7 +302,7 @@ def gpu_arm(args, wl, rank, world):
         step()
     torch.cuda.synchronize()
 
-    ktime = torch.zeros(36, dtype=torch.int64, device="cuda")
+    ktime = torch.zeros(384, dtype=torch.int64, device="cuda")
     clocks = Clocks(torch.cuda.current_device())
     clocks.start()
     clocks.wait_first_sample()

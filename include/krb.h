@@ -35,6 +35,7 @@ extern "C" {
 #define KRB_ECUDA -2
 #define KRB_ENOMEM -3
 #define KRB_ESTATE -4
+#define KRB_EFACTOR -5   /* ILUTP: no usable pivot (reference FactorizationError) */
 
 /* solver status codes (history.status strings of solvers.py:33-37) */
 #define KRB_RUNNING 0
@@ -64,6 +65,21 @@ int krb_reset_tuning(void);
 typedef void *(*krb_alloc_fn)(size_t bytes, void *stream);
 typedef void (*krb_free_fn)(void *ptr, void *stream);
 int krb_set_allocator(krb_alloc_fn alloc, krb_free_fn free_fn);
+
+/* ------------------------------------------------------------- ILUTP */
+/* ilutp_factor (ilutp.py:131-281) on the host, bit-identical to the
+ * reference: A*P ~= L*U, L unit lower (diagonal stored), U upper, perm[j] =
+ * original column at position j.  fill_limit < 0: none.  KRB_EFACTOR with
+ * the reference's FactorizationError message when a row has no pivot.    */
+typedef struct krb_ilutp krb_ilutp;
+int krb_ilutp_factor(int64_t n, const int64_t *h_row_ptr, const int32_t *h_col_idx,
+                     const double *h_values, double drop_tol, double pivot_tol,
+                     int64_t fill_limit, krb_ilutp **out);
+int krb_ilutp_sizes(const krb_ilutp *F, int64_t *nnz_L, int64_t *nnz_U);
+/* copy the factors into caller-owned host arrays (any may be NULL) */
+int krb_ilutp_export(const krb_ilutp *F, int64_t *L_rp, int32_t *L_ci, double *L_val,
+                     int64_t *U_rp, int32_t *U_ci, double *U_val, int64_t *perm);
+int krb_ilutp_free(krb_ilutp *F);
 
 /* stream-ordered device-to-device copy (ring views -> caller tensors) */
 int krb_memcpy_d2d(void *d_dst, const void *d_src, int64_t bytes, void *stream);
@@ -185,8 +201,8 @@ typedef struct krb_solve_config {
    * the 9 kernels of one iteration (slot 0 P, 1 q=Ap, 2 Chat^T q, 3 Q,
    * 4 S, 5 t=As, 6 Chat^T t, 7 T, 8 X) d_kernel_times[4 slot + 1] gains
    * (last CTA's end - CTA 0's start) in ns and [4 slot + 2] one per launch
-   * that did work.  36 uint64, zeroed by the caller; accumulates across
-   * solves.                                                              */
+   * that did work.  384 uint64 zeroed by the caller (36 totals; from 64 on,
+   * per-SM end stamps of the SpMV kernels); accumulates across solves.  */
   uint64_t *d_kernel_times;
   /* optional record_iterates (solvers.py:40-56, recording at :168-172,
    * :209-218, :281-286, :340-346; host-loop driver only): per history entry

@@ -108,6 +108,11 @@ SIGNATURES = {
                                     ctypes.POINTER(SolveConfig), c_vp, c_vp, c_vp,
                                     c_vp, ctypes.POINTER(SolveResult), c_vp]),
     "krb_memcpy_d2d": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "krb_ilutp_factor": (c_int, [c_i64, c_vp, c_vp, c_vp, c_dbl, c_dbl, c_i64,
+                                 ctypes.POINTER(c_vp)]),
+    "krb_ilutp_sizes": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "krb_ilutp_export": (c_int, [c_vp] + [c_vp] * 7),
+    "krb_ilutp_free": (c_int, [c_vp]),
     "krb_colsq": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "krb_ritz_combine": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                  c_vp, c_vp, c_vp]),
@@ -202,7 +207,7 @@ def call(name: str, *args):
 # Python-side driver knobs (see tuning()): "graph_mode" = None (automatic),
 # 0 host loop, 1 CUDA graph with a device WHILE node, 2 persistent kernel;
 # "phase_prof" = per-phase device stamps of the persistent kernel.
-# "kernel_times" = a zeroed (36,) int64 CUDA tensor that the graph /
+# "kernel_times" = a zeroed (384,) int64 CUDA tensor that the graph /
 # host-loop drivers accumulate live per-kernel device time into
 # (krb_solve_config.d_kernel_times).
 PY_TUNING = {"graph_mode": None, "phase_prof": False, "kernel_times": None}

@@ -72,35 +72,63 @@ __host__ __device__ constexpr int ktime_slot_of(int PH) {
 }
 
 // The SpMV kernels (slots 1, 5: one CTA per 256 rows, 65536 CTAs at C5)
-// mark their end with a fire-and-forget atomicMax per CTA instead of a
-// last-CTA election (an atomic with a return value per CTA costs ~20 % of
-// the launch); the next kernel's CTA 0 folds the pending end into the total.
+// mark their end per SM instead of electing a last CTA: each CTA's thread 0
+// does a fire-and-forget atomicMax into its SM's slot (kKtSpmvBase + 160 s'
+// + smid; one address per SM, so no single-address atomic queue -- that
+// cost ~25 % of the launch), and the next kernel's CTA 0 folds the maximum
+// over the SMs into the slot's total.
+constexpr int kKtSpmvBase = 64;     // d_kernel_times[64 .. 64 + 2 x 160)
+constexpr int kKtSmSlots = 160;
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// by warp 0 of CTA 0
 __device__ __forceinline__ void ktime_fold_spmv(const IterArgs &a) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int s = 1; s <= 5; s += 4) {
-    volatile uint64_t *kt = (volatile uint64_t *)a.ktime + 4 * s;
-    const uint64_t end = kt[3];
-    if (end != 0) {
-      kt[1] = kt[1] + (end - kt[0]);
+  for (int s2 = 0; s2 < 2; ++s2) {
+    volatile uint64_t *sm = (volatile uint64_t *)a.ktime + kKtSpmvBase + kKtSmSlots * s2;
+    uint64_t mx = 0;
+    for (int q = lane; q < kKtSmSlots; q += 32) {
+      const uint64_t v = sm[q];
+      mx = v > mx ? v : mx;
+      if (v) sm[q] = 0;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, mx, off);
+      mx = o > mx ? o : mx;
+    }
+    if (lane == 0 && mx != 0) {
+      volatile uint64_t *kt = (volatile uint64_t *)a.ktime + 4 * (s2 == 0 ? 1 : 5);
+      kt[1] = kt[1] + (mx - kt[0]);
       kt[2] = kt[2] + 1;
-      kt[3] = 0;
     }
   }
 }
 
+// every thread (uniform call): CTA 0 folds pending SpMV ends and stamps the
+// kernel's start
 __device__ __forceinline__ void ktime_start(const IterArgs &a, int slot) {
-  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 32) {
     ktime_fold_spmv(a);
-    *(volatile uint64_t *)&a.ktime[4 * slot] = globaltimer();
+    __syncwarp();
+    if (threadIdx.x == 0) *(volatile uint64_t *)&a.ktime[4 * slot] = globaltimer();
   }
 }
 
 __device__ __forceinline__ void ktime_end_spmv(const IterArgs &a, int slot) {
   if (!a.ktime) return;
   __syncthreads();
-  if (threadIdx.x == 0)
-    atomicMax((unsigned long long *)&a.ktime[4 * slot + 3],
+  if (threadIdx.x == 0) {
+    const int s2 = slot == 1 ? 0 : 1;
+    atomicMax((unsigned long long *)&a.ktime[kKtSpmvBase + kKtSmSlots * s2 + smid()],
               (unsigned long long)globaltimer());
+  }
 }
 
 // by thread 0 of the CTA known to finish last

@@ -557,6 +557,9 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     otherwise hold ~100 GB of HBM for a list it discards."""
     cfg = config or SolverConfig()
     t0 = time.perf_counter()
+    if cfg.record_iterates:
+        raise NotImplementedError("record_iterates is supported by bicgstab_solve / "
+                                  "rbicgstab_solve on the device, not by rbicg_solve")
     M, b = _check_common(A, b, precond, cfg)
     t = torch()
     n = M.n

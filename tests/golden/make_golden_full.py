@@ -11,7 +11,10 @@ Cases (every solver case stores, per thread count: the first 51 relative
 residuals, iterations, matvecs, status, final true residual):
 
 * bicgstab/c1/j, rbicgstab/c1/j   -- all 6 C1 systems; rbicgstab with the k =
-  10 space biorthonormalize(U, Ut, A_j) of a seeded N(0,1) pair;
+  10 space biorthonormalize(U, U, A_j), U = the k lowest grid sine modes;
+  besides the thread counts, two more valid runs of the reference with its
+  dots in other summation orders (vexact: exactly rounded; vpair: numpy's
+  pairwise sum) -- what another BLAS would give;
 * bicgstab/c2/j, rbicgstab/c2/j   -- C2 systems 0, 5, 9, k = 20;
 * policy/c1first, policy/c2first  -- the sequence policy (sequence.py,
   policy "first") over the reference's own functions: RBiCG + harvest on
@@ -75,9 +78,44 @@ def put_hist(out, p, h):
     out[p + "final_true_resid"] = np.array(h.final_true_resid)
 
 
-def seeded_pair(n, k, j):
-    r = np.random.default_rng(SPACE_SEED + j)
-    return r.standard_normal((n, k)), r.standard_normal((n, k))
+def space_basis(seq):
+    """The recycle basis of the rbicgstab cases: the k lowest sine modes of
+    the grid (workloads.sine_basis), U = Ut -- well conditioned, so the
+    reference's own runs agree where the iteration itself is stable."""
+    grid = seq.meta["grid"]
+    return W.sine_basis(tuple(grid), seq.k)
+
+
+def _numpy_with_dot(dotf):
+    import types
+    ns = types.SimpleNamespace(**{k: getattr(np, k) for k in dir(np)
+                                  if not k.startswith("__")})
+    ns.vdot = dotf
+    ns.linalg = types.SimpleNamespace(norm=lambda x: np.sqrt(dotf(x, x)))
+    return ns
+
+
+def _exact_dot(a, b):
+    import math
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    f = 134217729.0
+
+    def split(x):
+        c = f * x
+        hi = c - (c - x)
+        return hi, x - hi
+    p = a * b
+    ah, al = split(a)
+    bh, bl = split(b)
+    e = ((ah * bh - p) + ah * bl + al * bh) + al * bl
+    return np.float64(math.fsum(np.concatenate([p, e])))
+
+
+# the reference's solvers with other valid summation orders for their dots
+# (what another BLAS would do): exactly rounded, and numpy's pairwise sum
+VARIANTS = {"vexact": _exact_dot,
+            "vpair": lambda a, b: np.float64(np.sum(np.asarray(a) * np.asarray(b)))}
 
 
 def solver_cases(out, name, systems):
@@ -86,20 +124,28 @@ def solver_cases(out, name, systems):
         A = seq.matrix(j)
         b = seq.rhs(j, 0)
         RA = ref_matrix(A)
-        U, Ut = seeded_pair(A.n, seq.k, j)
+        U = space_basis(seq)
         out[f"mat/{name}/{j}/sha"] = np.array(csr_hash(A))
         out[f"mat/{name}/{j}/b_sha"] = np.array(vec_hash(b))
         cfg = K.SolverConfig(tol=seq.tol, max_itn=seq.max_itn, seed=j)
-        for th in THREADS:
+        import krecycle.solvers as KS
+        runs = [(f"t{th}", th, None) for th in THREADS] + \
+               [(v, 1, f) for v, f in VARIANTS.items()]
+        for tag, th, dotf in runs:
             t0 = time.time()
-            with threadpool_limits(th):
-                _, h = K.bicgstab_solve(RA, b, config=cfg)
-                put_hist(out, f"bicgstab/{name}/{j}/t{th}/", h)
-                S = K.biorthonormalize(U, Ut, RA)
-                out[f"rbicgstab/{name}/{j}/t{th}/k"] = np.array(S.k)
-                _, hr = K.rbicgstab_solve(RA, b, recycle=S, config=cfg)
-                put_hist(out, f"rbicgstab/{name}/{j}/t{th}/", hr)
-            print(f"{name} {j} t{th}: bicgstab {h.iterations} {h.status}, rbicgstab "
+            if dotf is not None:
+                KS.np = _numpy_with_dot(dotf)
+            try:
+                with threadpool_limits(th):
+                    _, h = K.bicgstab_solve(RA, b, config=cfg)
+                    put_hist(out, f"bicgstab/{name}/{j}/{tag}/", h)
+                    S = K.biorthonormalize(U, U, RA)
+                    out[f"rbicgstab/{name}/{j}/{tag}/k"] = np.array(S.k)
+                    _, hr = K.rbicgstab_solve(RA, b, recycle=S, config=cfg)
+                    put_hist(out, f"rbicgstab/{name}/{j}/{tag}/", hr)
+            finally:
+                KS.np = np
+            print(f"{name} {j} {tag}: bicgstab {h.iterations} {h.status}, rbicgstab "
                   f"{hr.iterations} {hr.status} ({time.time() - t0:.1f}s)", flush=True)
 
 
@@ -197,6 +243,7 @@ def main():
     out["meta/numpy"] = np.array(np.__version__)
     out["meta/scipy"] = np.array(scipy.__version__)
     out["meta/threads"] = np.asarray(THREADS)
+    out["meta/variants"] = np.asarray(list(VARIANTS))
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT}: {len(out)} arrays, {os.path.getsize(OUT)} bytes")
 

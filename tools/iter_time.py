@@ -27,7 +27,12 @@ def run(name, k=None, reps=3, max_itn=None):
     cfg = P.SolverConfig(tol=seq.tol, max_itn=max_itn or seq.max_itn, seed=0)
     S.solve_device(M, b, None, space, cfg)
     best, h = None, None
-    for _ in range(reps):
+    from paper_1406_2831_b200 import _lib
+    kt = torch.zeros(384, dtype=torch.int64, device="cuda")
+    for rep in range(reps + 1):
+        # the last rep with the live per-kernel timing on (kernel_us); the
+        # iteration time is the best of the reps without it
+        _lib.PY_TUNING["kernel_times"] = kt if rep == reps else None
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -36,14 +41,23 @@ def run(name, k=None, reps=3, max_itn=None):
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1e3
+        if rep == reps:
+            t_kt = t
+            continue
         best = t if best is None else min(best, t)
+    _lib.PY_TUNING["kernel_times"] = None
+    ktn = kt.cpu().numpy()
+    names = ["P", "M1", "Z1", "Q", "S", "M2", "Z2", "T", "X"]
+    kern_us = {nm: round(ktn[4 * i + 1] / max(ktn[4 * i + 2], 1) / 1e3, 1)
+               for i, nm in enumerate(names) if ktn[4 * i + 2]}
     kk = space.k if space is not None else 0
     its = max(h.iterations, 1)
     B = W.bytes_per_iteration(A.n, A.nnz, kk)
     return {"config": name, "n": A.n, "nnz": A.nnz, "k": kk, "format": M.format,
             "iterations": h.iterations, "status": h.status,
             "solve_ms": round(best * 1e3, 3), "us_per_it": round(best / its * 1e6, 2),
-            "GBps_alg": round(B * its / best / 1e9, 1)}
+            "GBps_alg": round(B * its / best / 1e9, 1), "kernel_us": kern_us,
+            "us_per_it_with_kernel_timing": round(t_kt / its * 1e6, 2)}
 
 
 def phase_breakdown(name, k=None):
@@ -86,7 +100,12 @@ if __name__ == "__main__":
     ap.add_argument("--both", action="store_true", help="also k = 0")
     ap.add_argument("--phases", action="store_true",
                     help="per-phase breakdown of the persistent kernel")
+    ap.add_argument("--tune", nargs="*", default=[],
+                    help="tuning knobs key=value (paper_1406_2831_b200._lib.tuning)")
     a = ap.parse_args()
+    if a.tune:
+        from paper_1406_2831_b200 import _lib
+        _lib.tuning(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.tune})
     if a.phases:
         for c in a.config:
             print(json.dumps(phase_breakdown(c, a.k)), flush=True)

@@ -124,6 +124,50 @@ int krb_spmv_t(krb_matrix *A, const double *d_x, double *d_y, void *stream);
 int krb_spmm(krb_matrix *A, int transpose, int64_t ncols, const double *d_X,
              int64_t ldx, double *d_Y, int64_t ldy, void *stream);
 
+/* ------------------------------------------- split ILUTP operator */
+/* Level schedule of a triangular CSR (host): lev_out[i] = 1 + max level of
+ * the rows its off-diagonal entries reference (0 without); lower: entries
+ * left of the diagonal, else right.  KRB_EINVAL on an entry on the wrong
+ * side. */
+int krb_tri_levels(int64_t n, const int64_t *rp, const int32_t *ci, int lower,
+                   int32_t *lev_out, int32_t *nlev_out);
+
+/* One triangular factor for the device solve (host arrays, uploaded by
+ * krb_precond_create): off-diagonal CSR, diagonal (NULL = unit), and the
+ * level schedule as per-warp task lists -- task t = row t_row[t] of level
+ * t_lev[t], its t_len[t] off-diagonal entries at t_start[t]; warp w owns
+ * tasks warp_ptr[w] .. warp_ptr[w+1]-1 in level order (16 warps: 17
+ * entries; row r of a level goes to warp r mod 16).                        */
+typedef struct krb_tri_host {
+  int64_t n, nnz_off, ntasks;
+  int32_t nlev;
+  const int64_t *rp;
+  const int32_t *ci;
+  const double *val;
+  const double *diag;
+  const int32_t *warp_ptr, *t_row, *t_lev, *t_len;
+  const int64_t *t_start;
+} krb_tri_host;
+
+/* The ILUTP factors on the device (L unit lower, Lt its transpose, U upper
+ * with diagonal, Ut its transpose, h_perm the column permutation). */
+typedef struct krb_precond krb_precond;
+int krb_precond_create(const krb_tri_host *L, const krb_tri_host *Lt, const krb_tri_host *U,
+                       const krb_tri_host *Ut, const int64_t *h_perm, krb_precond **out,
+                       void *stream);
+int krb_precond_destroy(krb_precond *P);
+/* SplitPreconditionedOperator (ilutp.py:106-128) on the device: a view of
+ * A whose products are L^{-1} A P U^{-1} (krb_spmv / krb_spmm) and
+ * U^{-H} P^T A^H L^{-H} (krb_spmv_t / transposed krb_spmm), usable by every
+ * solver entry point.  A and P must outlive the view; destroy it with
+ * krb_matrix_destroy(_async).                                             */
+int krb_operator_create(krb_matrix *A, const krb_precond *P, krb_matrix **op_out);
+/* apply_left / apply_left_h / U^{-1} / U^{-H} (ilutp.py:76-97):
+ * which = 0 L^{-1}, 1 L^{-H}, 2 U^{-1}, 3 U^{-H}                         */
+int krb_precond_apply(const krb_precond *P, int which, const double *d_in, double *d_out,
+                      void *stream);
+
+
 /* ------------------------------------------------- canonical primitives */
 /* *d_out = (x, y)        (np.vdot, solvers.py:308-352) */
 int krb_dot(krb_context *ctx, int64_t n, const double *d_x, const double *d_y,

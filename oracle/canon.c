@@ -20,6 +20,9 @@
  *   canon_gemv   <- R.C @ zeta, R.U @ xc (solvers.py:307,329,359)
  *   canon_gram   <- Ct_raw^H C_raw, Wt^H AW, Wt^H W (recycling.py:140,342-343)
  *   canon_gemm   <- W @ Z, U_raw @ Y (recycling.py:151-154,351-352,365-368)
+ *   canon_trsv   <- the ILUTP triangular solves L^{-1}, L^{-H}, U^{-1}, U^{-H}
+ *                   (ilutp.py:76-97; the reference uses SuperLU's supernodal
+ *                   solve, whose order this does not reproduce)
  *
  * Build: see oracle/Makefile (gcc -O2 -ffp-contract=off; fma() is the libm
  * correctly-rounded fused multiply-add, identical to CUDA __fma_rn).
@@ -179,4 +182,28 @@ void canon_gemm(int64_t n, int64_t m, int64_t nc, const double *X, int64_t rsx,
         acc = fma(X[i * rsx + j * csx], Z[j * nc + c], acc);
       out[i * rso + c * cso] = acc;
     }
+}
+
+/* ---- canonical triangular solve ------------------------------------------
+ * Off-diagonal CSR (rp, ci, v) of a lower (lower != 0: rows in increasing
+ * order) or upper triangular factor, diag = NULL for a unit diagonal.
+ * Row i: lane l (of 32) accumulates fma(v_e, x[c_e], acc) over the row's
+ * off-diagonal entries e = l, l+32, ... in CSR (column) order; the 32-lane
+ * tree gives S; x_i = b_i - S, then / diag_i.  (The B200 kernel: a warp per
+ * row, csrc/precond.cu.)                                                    */
+void canon_trsv(int64_t n, const int64_t *rp, const int32_t *ci, const double *v,
+                const double *diag, int lower, const double *b, double *x) {
+  double a[32];
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t i = lower ? t : n - 1 - t;
+    memset(a, 0, sizeof(a));
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const int l = (int)((e - rp[i]) & 31);
+      a[l] = fma(v[e], x[ci[e]], a[l]);
+    }
+    tree32(a);
+    double s = b[i] - a[0];
+    if (diag) s = s / diag[i];
+    x[i] = s;
+  }
 }

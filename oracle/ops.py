@@ -67,6 +67,8 @@ def _lib():
         lib.canon_spmv.argtypes = [I, P, P, P, P, P]
         lib.canon_gram.restype = None
         lib.canon_gram.argtypes = [I, I, I, P, I, I, P, I, I, P]
+        lib.canon_trsv.restype = None
+        lib.canon_trsv.argtypes = [I, P, P, P, P, ctypes.c_int, P, P]
         lib.canon_gemm.restype = None
         lib.canon_gemm.argtypes = [I, I, I, P, I, I, P, P, I, I]
         _LIB = lib
@@ -103,8 +105,10 @@ class CsrOperand:
 
     @classmethod
     def of(cls, A):
-        if isinstance(A, cls):
+        if isinstance(A, (cls, SplitOperand)):
             return A
+        if hasattr(A, "factors") and hasattr(A, "_A"):
+            return SplitOperand(cls.of(A._A), A.factors)
         inner = getattr(A, "inner", None)
         if inner is not None and not hasattr(A, "row_ptr"):
             return cls.of(inner)
@@ -132,15 +136,92 @@ class CsrOperand:
         return self._t
 
 
+def _tri_offdiag(M, unit):
+    """Off-diagonal CSR and diagonal of a triangular scipy CSR."""
+    rp = M.indptr.astype(np.int64)
+    ci = M.indices.astype(np.int64)
+    v = M.data.astype(np.float64)
+    n = M.shape[0]
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    off = ci != rows
+    diag = None
+    if not unit:
+        diag = np.zeros(n)
+        diag[rows[~off]] = v[~off]
+    rp_off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows[off], minlength=n), out=rp_off[1:])
+    return (rp_off, np.ascontiguousarray(ci[off], dtype=np.int32),
+            np.ascontiguousarray(v[off]), diag)
+
+
+class SplitOperand:
+    """The split-ILUTP operator L^{-1} A P U^{-1} (ilutp.py:106-128) handed to
+    the oracle: base CSR operand + factors (L, U CSR, perm)."""
+
+    def __init__(self, base, factors):
+        self.base = base
+        self.nrows = self.ncols = base.nrows
+        self.perm = np.asarray(factors.perm, dtype=np.int64)
+        n = base.nrows
+
+        def csr(M):
+            return _sp.csr_matrix((np.asarray(M.values, dtype=np.float64),
+                                   np.asarray(M.col_idx), np.asarray(M.row_ptr)),
+                                  shape=(n, n))
+        self.L, self.U = csr(factors.L), csr(factors.U)
+        self._lu = None
+        self._tri = None
+
+    @property
+    def shape(self):
+        return (self.nrows, self.ncols)
+
+    @property
+    def dtype(self):
+        return np.dtype(np.float64)
+
+    def tri(self):
+        """canonical-order data: (L, L^T, U, U^T) off-diagonal CSR + diag"""
+        if self._tri is None:
+            Lt = self.L.T.tocsr()
+            Lt.sort_indices()
+            Ut = self.U.T.tocsr()
+            Ut.sort_indices()
+            self._tri = {"L": (_tri_offdiag(self.L, True), 1),
+                         "Lt": (_tri_offdiag(Lt, True), 0),
+                         "U": (_tri_offdiag(self.U, False), 0),
+                         "Ut": (_tri_offdiag(Ut, False), 1)}
+        return self._tri
+
+    def superlu(self):
+        """the reference's factor application (ilutp.py:37-42: SuperLU,
+        natural order, no pivoting, on each triangular factor)"""
+        if self._lu is None:
+            import scipy.sparse.linalg as spla
+            self._lu = tuple(spla.splu(M.tocsc(), permc_spec="NATURAL",
+                                       diag_pivot_thresh=0.0) for M in (self.L, self.U))
+        return self._lu
+
+
 class RefOps:
     """The reference's own numpy/scipy calls (bit-identical restatement)."""
 
     name = "ref"
 
     def matvec(self, A: CsrOperand, x):
+        if isinstance(A, SplitOperand):   # ilutp.py:124-125 / 76-91
+            luL, luU = A.superlu()
+            t = luU.solve(np.asarray(x))
+            y = np.empty_like(t)
+            y[A.perm] = t
+            return luL.solve(self.matvec(A.base, y))
         return A._csr @ x
 
     def rmatvec(self, A: CsrOperand, x):
+        if isinstance(A, SplitOperand):   # ilutp.py:127-128 / 81-97
+            luL, luU = A.superlu()
+            z = self.rmatvec(A.base, luL.solve(np.asarray(x), trans="H"))
+            return luU.solve(z[A.perm], trans="H")
         if A._csr_h is None:
             A._csr_h = A._csr.conj(copy=True).transpose().tocsr()
         return A._csr_h @ x
@@ -175,7 +256,21 @@ class CanonOps:
     def __init__(self):
         self.lib = _lib()
 
+    def trsv(self, A, which, b):
+        (rp, ci, v, diag), lower = A.tri()[which]
+        b = np.ascontiguousarray(_real(b, "trsv"))
+        x = np.empty(A.nrows)
+        self.lib.canon_trsv(A.nrows, _ptr(rp), _ptr(ci), _ptr(v),
+                            _ptr(diag) if diag is not None else None, lower,
+                            _ptr(b), _ptr(x))
+        return x
+
     def matvec(self, A: CsrOperand, x):
+        if isinstance(A, SplitOperand):   # L^{-1} A P U^{-1} x
+            t = self.trsv(A, "U", x)
+            y = np.empty_like(t)
+            y[A.perm] = t
+            return self.trsv(A, "L", self.matvec(A.base, y))
         x = np.ascontiguousarray(_real(x, "matvec"))
         y = np.empty(A.nrows)
         self.lib.canon_spmv(A.nrows, _ptr(A.row_ptr), _ptr(A.col_idx),
@@ -183,6 +278,9 @@ class CanonOps:
         return y
 
     def rmatvec(self, A: CsrOperand, x):
+        if isinstance(A, SplitOperand):   # U^{-H} P^T A^H L^{-H} x
+            z = self.rmatvec(A.base, self.trsv(A, "Lt", x))
+            return self.trsv(A, "Ut", z[A.perm])
         rp, ci, v = A.transpose_arrays()
         x = np.ascontiguousarray(_real(x, "rmatvec"))
         y = np.empty(A.ncols)

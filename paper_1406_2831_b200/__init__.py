@@ -3,8 +3,8 @@
 Drop-in for the solver / recycle-space names of krecycle
 (/root/reference/pkg/src/krecycle/__init__.py:33-52) that lie on the hot path
 (SURVEY.md §8): the arithmetic runs in libkrb.so (hand-written sm_100a CUDA,
-C ABI in include/krb.h).  Everything else in the reference (CLI, ILUTP,
-Matrix Market I/O, problem generators, bi-Lanczos harness) is out of scope.
+C ABI in include/krb.h).  Everything else in the reference (CLI, Matrix
+Market I/O, problem generators, bi-Lanczos harness) is out of scope.
 """
 
 from .device import prefetch_matrix
@@ -18,6 +18,9 @@ from .solvers import (BREAKDOWN_OMEGA, BREAKDOWN_SECOND_KIND,
                       rbicgstab_solve_batch)
 from .update import update_recycle_space
 from .sparse import SparseMatrix
+from .ilutp import (FactorizationError, IlutpFactors, SplitPreconditionedOperator,
+                    apply_left, apply_left_h, apply_right, apply_right_h, ilutp_factor,
+                    permutation_matrix, to_operator_coords)
 
 __version__ = "0.1.0"
 
@@ -31,4 +34,7 @@ __all__ = [
     "CONVERGED", "MAX_ITN", "BREAKDOWN_SERIOUS", "BREAKDOWN_OMEGA",
     "BREAKDOWN_SECOND_KIND",
     "SparseMatrix", "prefetch_matrix",
+    "FactorizationError", "IlutpFactors", "SplitPreconditionedOperator",
+    "apply_left", "apply_left_h", "apply_right", "apply_right_h", "ilutp_factor",
+    "permutation_matrix", "to_operator_coords",
 ]

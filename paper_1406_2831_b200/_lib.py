@@ -113,6 +113,11 @@ SIGNATURES = {
     "krb_ilutp_sizes": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "krb_ilutp_export": (c_int, [c_vp] + [c_vp] * 7),
     "krb_ilutp_free": (c_int, [c_vp]),
+    "krb_tri_levels": (c_int, [c_i64, c_vp, c_vp, c_int, c_vp, ctypes.POINTER(ctypes.c_int32)]),
+    "krb_precond_create": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp), c_vp]),
+    "krb_precond_destroy": (c_int, [c_vp]),
+    "krb_precond_apply": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp]),
+    "krb_operator_create": (c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
     "krb_colsq": (c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "krb_ritz_combine": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                  c_vp, c_vp, c_vp]),

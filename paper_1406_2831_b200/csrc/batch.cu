@@ -568,6 +568,7 @@ int rbicgstab_batch(krb_context *ctx, const krb_matrix *A, int64_t nrhs,
   KRB_REQUIRE(ctx && A && d_b && cfgs && d_x_out && hist_r && hist_m && hist_t && res,
               "krb_rbicgstab_batch: NULL argument");
   KRB_REQUIRE(nrhs >= 1 && nrhs <= kMaxB, "krb_rbicgstab_batch: 1 <= nrhs <= 4");
+  KRB_REQUIRE(!A->pre, "krb_rbicgstab_batch: preconditioned operators run one solve at a time");
   const int64_t n = A->n;
   const int64_t k = (R && R->k > 0) ? R->k : 0;
   if (k > 0) {

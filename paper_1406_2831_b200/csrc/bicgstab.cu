@@ -156,6 +156,9 @@ static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st
 template <bool kSecond>
 static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.n == 0) return KRB_OK;
+  if (h.A.pre)   // split-ILUTP operator: the composite kernels (precond.cu)
+    return spmv_launch(&h.A, kSecond ? h.s : h.p, kSecond ? h.t : h.q,
+                       reinterpret_cast<const int *>(&h.S->status), st);
   unsigned blocks = (unsigned)((h.n + 255) / 256);
   if (h.A.format == 2)
     k_iter_spmv<true, kSecond><<<blocks, 256, 0, st>>>(d);
@@ -381,10 +384,13 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     h.rec_x = cfg->d_rec_x; h.rec_r = cfg->d_rec_r; h.rec_xc = cfg->d_rec_xc;
     h.rec_s = cfg->d_rec_s; h.rec_t = cfg->d_rec_t; h.rec_omega = cfg->d_rec_omega;
   }
-  const int mode = cfg->use_graph;   // 0 host loop, 1 graph, 2 persistent
+  // 0 host loop, 1 graph, 2 persistent; a preconditioned operator runs the
+  // graph (its products are kernel sequences the fused kernels do not have)
+  const int mode = (A->pre && cfg->use_graph == 2) ? 1 : cfg->use_graph;
   const bool graph = mode == 1;
   GraphCache &G = ctx->graph;
-  const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format;
+  const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format &&
+                   G.pre_serial == precond_serial(A->pre);
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -400,7 +406,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   if (graph && !hit) {
     KRB_CHECK_CUDA(cudaStreamSynchronize(st));
     KRB_TRY(build_graph(ctx, h, d, capture_stream()));
-    G.n = n; G.k = k; G.format = A->format;
+    G.n = n; G.k = k; G.format = A->format; G.pre_serial = precond_serial(A->pre);
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

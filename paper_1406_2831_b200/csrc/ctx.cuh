@@ -31,6 +31,7 @@ struct GraphCache {
   cudaGraph_t graph = nullptr;
   cudaGraphConditionalHandle cond = 0;
   int64_t n = -1, k = -1;
+  int64_t pre_serial = 0;   // preconditioned operator the body was captured for
   int format = -1;
   int64_t kernels_per_body = 0;
   void reset() {

@@ -15,6 +15,7 @@
 #include "../../include/krb.h"
 
 // Device sparse matrix (CSR + optional SELL-32 + lazily built transpose).
+struct krb_precond;
 struct krb_matrix {
   int64_t n = 0, nnz = 0;
   int format = 0;  // 1 CSR, 2 SELL
@@ -30,6 +31,12 @@ struct krb_matrix {
   int32_t *perm = nullptr;  // SELL-C-sigma: slice position -> row (NULL: identity)
   krb_matrix *T = nullptr;  // lazily built transpose
   int64_t bytes = 0;
+  // preconditioned-operator view (precond.cu): shares `base`'s arrays; every
+  // application runs the split-ILUTP composite (pre_adj: its adjoint)
+  krb_matrix *base = nullptr;
+  krb_precond *pre = nullptr;
+  bool borrowed = false;
+  bool pre_adj = false;
 };
 
 
@@ -42,6 +49,12 @@ namespace krb {
 // share one pool), else the stream-ordered CUDA pool.
 cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t st);
 void dev_free(void *p, cudaStream_t st);
+
+// preconditioned operator (precond.cu)
+int precond_apply_op(const krb_matrix *A, const double *x, double *y, const int *status,
+                     cudaStream_t st);
+void precond_free(krb_precond *P);
+int64_t precond_serial(const krb_precond *P);
 
 // ---------------------------------------------------------------- errors
 void set_error(const char *fmt, ...);

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
 int spmv_launch(const krb_matrix *A, const double *x, double *y,
                 const int *d_status, cudaStream_t st) {
   if (A->n == 0) return KRB_OK;
+  if (A->pre) return precond_apply_op(A, x, y, d_status, st);
   int64_t blocks = (A->n + 255) / 256;
   if (A->format == 2)
     k_spmv<true><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
@@ -143,6 +144,11 @@ int spmm_launch(const krb_matrix *M, int64_t ncols, const double *X, int64_t ldx
                 double *Y, int64_t ldy, cudaStream_t st) {
   constexpr int kNC = 8;
   if (M->n == 0 || ncols == 0) return KRB_OK;
+  if (M->pre) {   // preconditioned operator: one composite application per column
+    for (int64_t c = 0; c < ncols; ++c)
+      KRB_TRY(spmv_launch(M, X + c * ldx, Y + c * ldy, nullptr, st));
+    return KRB_OK;
+  }
   dim3 grid((unsigned)((M->n + 255) / 256), (unsigned)((ncols + kNC - 1) / kNC));
   if (M->format == 2)
     k_spmm<true, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
@@ -389,6 +395,19 @@ __global__ void k_gather_t(int64_t nnz, const int32_t *__restrict__ perm,
 
 int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   if (A->T) return KRB_OK;
+  if (A->borrowed) {
+    // operator view: its adjoint is a view of the base's transpose carrying
+    // the same factors (applied as the adjoint composite)
+    KRB_TRY(ensure_transpose(A->base, st));
+    krb_matrix *T = new krb_matrix(*A->base->T);
+    T->T = nullptr;
+    T->base = A->base->T;
+    T->borrowed = true;
+    T->pre = A->pre;
+    T->pre_adj = !A->pre_adj;
+    A->T = T;
+    return KRB_OK;
+  }
   const int64_t n = A->n, nnz = A->nnz;
   int32_t *rows = nullptr, *keys_out = nullptr, *perm_in = nullptr,
           *perm_out = nullptr, *tci = nullptr;
@@ -454,6 +473,11 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
 // otherwise cudaFree (synchronises the device).
 void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
   if (!A) return;
+  if (A->borrowed) {   // a view: the arrays belong to its base, the factors
+    if (A->T) matrix_free(A->T, async, st);   // to their krb_precond
+    delete A;
+    return;
+  }
   matrix_free(A->T, async, st);
   void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm};
   if (!async) cudaDeviceSynchronize();

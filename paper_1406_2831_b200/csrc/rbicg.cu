@@ -375,6 +375,9 @@ template <bool kTrans>
 static int bi_spmv(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   const krb_matrix &M = kTrans ? h.AT : h.A;
   if (h.n == 0) return KRB_OK;
+  if (M.pre)   // split-ILUTP operator / its adjoint (precond.cu)
+    return spmv_launch(&M, kTrans ? h.pt : h.p, kTrans ? h.qt : h.q,
+                       reinterpret_cast<const int *>(&h.S->status), st);
   unsigned blocks = (unsigned)((h.n + 255) / 256);
   if (M.format == 2)
     k_bspmv<true, kTrans><<<blocks, 256, 0, st>>>(d);
@@ -696,6 +699,7 @@ struct krb_rbicg {
   // callback launches (update_recycle_space's Grams / norms) while this
   // handle's descriptor still holds the pointer
   double *part = nullptr;
+  int64_t pre_serial = 0;   // preconditioned operator the graph was captured for
   int64_t s = 0, max_itn = 0, k = 0;
   krb_space_view R = {};
   bool has_R = false;
@@ -804,7 +808,8 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   // instantiated graph, whose kernels read everything per solve from H->d)
   krb_rbicg *H = ctx->bi_cache;
   const bool reuse = H && H->h.n == n && H->k == k && H->s == s && H->max_itn == max_itn &&
-                     H->fmt == A->format && H->fmt_t == A->T->format;
+                     H->fmt == A->format && H->fmt_t == A->T->format &&
+                     H->pre_serial == precond_serial(A->pre);
   if (H && !reuse) bi_free(H);
   ctx->bi_cache = nullptr;
   if (!reuse) H = new krb_rbicg();
@@ -817,6 +822,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   H->k = k;
   H->fmt = A->format;
   H->fmt_t = A->T->format;
+  H->pre_serial = precond_serial(A->pre);
   const int64_t nb = canon_nblocks(n);
   const int64_t ring_cols = (s > 0 ? s : 0) + 3;
   cudaError_t e = cudaSuccess;
@@ -919,6 +925,7 @@ int krb_rbicg_start(krb_rbicg *H, const double *d_b, const double *d_bt,
   cudaStream_t st = as_stream(stream);
   BiArgs &h = H->h;
   const int64_t n = h.n, k = h.k;
+  if (H->A->pre && use_graph == 2) use_graph = 1;   // operator products are kernel sequences
   H->use_graph = use_graph;
   H->l0 = launch_counter();
   if (use_graph == 1 && !H->exec) {

@@ -461,6 +461,10 @@ def device_matrix(A) -> DeviceMatrix:
     dev = getattr(A, "_device", None)
     if isinstance(dev, DeviceMatrix):
         return dev
+    if hasattr(A, "factors") and hasattr(A, "_A"):
+        # split ILUTP operator (ilutp.py:106-128; ours or the reference's)
+        from .precond import device_operator
+        return device_operator(A)
     inner = getattr(A, "inner", None)
     if inner is not None and not hasattr(A, "row_ptr"):
         return device_matrix(inner)

@@ -15,7 +15,10 @@ For a sequence of systems A_i x = b_{i,kappa}:
 * policy="verbatim": the reference's own schedule — RBiCG + harvest on
   kappa = 0 of EVERY matrix, rbicgstab on kappa > 0 (C3's 4-rhs blocks);
 * a plain bicgstab_solve baseline track runs on the same systems
-  (driver.py:162-168) unless ``baseline=False``.
+  (driver.py:162-168) unless ``baseline=False``;
+* precond="ilutp": the reference driver's split preconditioning
+  (driver.py:99-107): one ILUTP factorization per matrix, every solve of
+  both tracks on L^{-1} A P U^{-1} with right-hand side L^{-1} b.
 
 Every product is metered through CountingOperator wrappers; aux products
 (refreshes, harvest updates) land in ``aux_matvecs`` exactly as
@@ -80,9 +83,10 @@ def default_api():
     return P
 
 
-def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
+def run_sequence(seq, k=None, s=None, tol=None, max_itn=None, seed=0,
                  policy="first", baseline=True, api=None, systems=None,
-                 max_seconds=None, batch=True):
+                 max_seconds=None, batch=True, precond=None, drop_tol=1e-4,
+                 pivot_tol=0.1):
     """Run the recycling policy (and the baseline) over ``seq``
     (a workloads.SequenceSpec).  ``max_seconds`` stops after the first system
     that ends past the budget (bounded CPU samples).  ``batch``: when the api
@@ -93,6 +97,11 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
     iteration for all of them.  Returns a SequenceResult."""
     api = api or default_api()
     k = seq.k if k is None else k
+    s = seq.s if s is None else s
+    if precond not in (None, "ilutp"):
+        raise ValueError("precond must be None or 'ilutp'")
+    if precond is not None:
+        batch = False   # the multi-rhs path has no preconditioned operator
     tol = seq.tol if tol is None else tol
     max_itn = seq.max_itn if max_itn is None else max_itn
     use_batch = batch and hasattr(api, "rbicgstab_solve_batch") and seq.rhs_per_matrix > 1
@@ -126,12 +135,21 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
             # the next matrix's upload overlaps this matrix's solves
             A_next = api.SparseMatrix.from_csr(seq.matrix(i + 1))
             prefetch(A_next)
-        op_rec = api.CountingOperator(A)
-        op_base = api.CountingOperator(A)
+        rhs = lambda kk, _i=i: seq.rhs(_i, kk)
+        if precond == "ilutp":
+            # driver.py:99-107: one ILUTP factorization per matrix, both tracks
+            # iterate on L^{-1} A P U^{-1} with b -> L^{-1} b
+            factors = api.ilutp_factor(A, drop_tol=drop_tol, pivot_tol=pivot_tol)
+            op_rec = api.CountingOperator(api.SplitPreconditionedOperator(A, factors))
+            op_base = api.CountingOperator(api.SplitPreconditionedOperator(A, factors))
+            rhs = lambda kk, _i=i, _f=factors: api.apply_left(_f, seq.rhs(_i, kk))
+        else:
+            op_rec = api.CountingOperator(A)
+            op_base = api.CountingOperator(A)
         nk = min(seq.rhs_per_matrix, total - gidx)
         pre_rec, pre_base = {}, {}   # kappa -> (history, seconds) of batched solves
         for kappa in range(nk):
-            b = seq.rhs(i, kappa)
+            b = rhs(kappa)
             cfg = api.SolverConfig(tol=tol, max_itn=max_itn, k=k, s=s, seed=seed + gidx)
             t0 = time.perf_counter()
             harvest_now = (gidx == 0) if policy == "first" else (kappa == 0)
@@ -172,7 +190,7 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                                              k=k, s=s, seed=seed + gidx + (kk - kappa))
                             for kk in ks]
                     tb = time.perf_counter()
-                    out = api.rbicgstab_solve_batch(op_rec, [seq.rhs(i, kk) for kk in ks],
+                    out = api.rbicgstab_solve_batch(op_rec, [rhs(kk) for kk in ks],
                                                     recycle=space if recycled else None,
                                                     configs=cfgs)
                     share = (time.perf_counter() - tb) / len(ks)
@@ -200,7 +218,7 @@ def run_sequence(seq, k=None, s=25, tol=None, max_itn=None, seed=0,
                     cfgs = [api.SolverConfig(tol=tol, max_itn=max_itn, k=k, s=s,
                                              seed=seed + gidx + kk) for kk in range(nk)]
                     tb = time.perf_counter()
-                    out = api.bicgstab_solve_batch(op_base, [seq.rhs(i, kk) for kk in range(nk)],
+                    out = api.bicgstab_solve_batch(op_base, [rhs(kk) for kk in range(nk)],
                                                    configs=cfgs)
                     share = (time.perf_counter() - tb) / nk
                     for kk, (_, h) in enumerate(out):

@@ -4,9 +4,10 @@ Same names, signatures, return values and error behaviour as
 /root/reference/pkg/src/krecycle/solvers.py; the arithmetic runs in libkrb.so
 (one CUDA-graph launch per solve, device-resident scalars and history).
 
-Out of scope on the device path (raise NotImplementedError, never a CPU
-fallback): split preconditioning (``precond``), complex data, and
-``record_iterates`` (a per-iteration host copy of every vector).
+Split ILUTP preconditioning (``precond`` = IlutpFactors) runs on the device
+(ilutp.py / precond.py).  Out of scope on the device path (raise
+NotImplementedError, never a CPU fallback): complex data, record_iterates in
+rbicg_solve, and the multi-rhs batch path with a preconditioner.
 """
 
 from __future__ import annotations
@@ -124,9 +125,6 @@ def device_uniform(seed: int, n: int, skip: int = 0):
 
 
 def _check_common(A, b, precond, cfg):
-    if precond is not None:
-        raise NotImplementedError("split preconditioning is out of scope on the "
-                                  "B200 path (SURVEY.md §2.1 row 7)")
     M = device_matrix(A)
     if _is_device(b):
         if tuple(b.shape) != (M.n,):
@@ -417,13 +415,84 @@ def bicgstab_solve_batch(A, bs, x_inits=None, configs=None, precond=None):
     return _batch_solve(A, bs, x_inits, None, configs, "bicgstab")
 
 
+class _Split:
+    """Split preconditioning of one solve (solvers.py:115-133 _setup_primary,
+    :136-144 _setup_dual) on the device: the iteration operator
+    L^{-1} A P U^{-1}, bh = L^{-1} b, xh = U P^T x_init, unwind y -> P U^{-1} y
+    (dual: bth = U^{-H} P^T b_dual, xth = L^H xt_init, unwind L^{-H})."""
+
+    def __init__(self, A, precond):
+        from .ilutp import SplitPreconditionedOperator, _factors
+        self.A = A
+        self.F = _factors(precond)
+        self.op = SplitPreconditionedOperator(A, self.F)
+        self.Fd = self.F.device()
+        t = torch()
+        self.perm = t.as_tensor(self.F.perm, device="cuda")
+
+    def rhs(self, b):
+        return self.Fd.apply("lower", _dev_vec(b))
+
+    def guess(self, x):
+        if x is None:
+            return None
+        z = _dev_vec(x)[self.perm]                                  # P^T x
+        return device_matrix(self.F.U).spmv(z.contiguous())          # U z
+
+    def unwind(self, y):
+        t = self.Fd.apply("upper", y)
+        x = torch().empty_like(t)
+        x[self.perm] = t                                             # x[perm] = t
+        return x
+
+    def rhs_dual(self, bt):
+        return self.Fd.apply("upper_h", _dev_vec(bt)[self.perm].contiguous())
+
+    def guess_dual(self, xt):
+        if xt is None:
+            return None
+        return device_matrix(self.F.L).spmv(_dev_vec(xt), transpose=True)   # L^H xt
+
+    def unwind_dual(self, yt):
+        return self.Fd.apply("lower_h", yt)
+
+    def true_residual(self, b, x):
+        """solvers.py:147-153 with the ORIGINAL operator and right-hand side:
+        ||b - A x|| / ||b|| (canonical device dots)."""
+        from .recycling import dot
+        M = device_matrix(self.A)
+        bd = _dev_vec(b)
+        r = bd - M.spmv(x)
+        rr, bb = dot(r, r), dot(bd, bd)
+        v = torch().stack([rr, bb]).cpu().numpy().ravel()
+        bn = float(np.sqrt(v[1]))
+        return float(np.sqrt(v[0]) / (bn if bn > 0 else 1.0))
+
+
+def _precond_solve(A, b, x_init, recycle, precond, cfg, label, t0):
+    sp = _Split(A, precond)
+    M = device_matrix(sp.op)
+    if not _is_device(b):
+        b = np.asarray(b)
+        if np.iscomplexobj(b):
+            raise NotImplementedError("complex right-hand sides are out of scope")
+    if tuple(b.shape) != (M.n,):
+        raise ValueError("right-hand side length does not match the operator")
+    xh, hist = solve_device(M, sp.rhs(b), sp.guess(x_init), recycle, cfg, label, t0)
+    _count(A, nm=LAST_SOLVE["matvecs"])
+    x = sp.unwind(xh)
+    hist.final_true_resid = sp.true_residual(b, x)
+    return (x if _is_device(b) else to_host(x)), hist
+
+
 def bicgstab_solve(A, b, x_init=None, precond=None, config=None):
     """solvers.py:156-242 — stabilized BiCG, shadow residual from the seeded
-    uniform(-1, 1) stream (drawn on the device, bit-identical to numpy)."""
+    uniform(-1, 1) stream (drawn on the device, bit-identical to numpy).
+    ``precond`` (IlutpFactors): split preconditioning on the device."""
     cfg = config or SolverConfig()
     t0 = time.perf_counter()
     if precond is not None:
-        _check_common(A, b, precond, cfg)
+        return _precond_solve(A, b, x_init, None, precond, cfg, "bicgstab", t0)
     return _device_solve(A, b, x_init, None, cfg, "bicgstab", t0)
 
 
@@ -431,11 +500,13 @@ def rbicgstab_solve(A, b, x_init=None, recycle=None, precond=None,
                     config=None):
     """solvers.py:245-361 — BiCGSTAB deflated by a recycle space (Algorithm 2):
     projected start, (I - C Chat^H) after every product, x = x - U xc at the
-    end.  With an empty space the arithmetic is that of bicgstab_solve."""
+    end.  With an empty space the arithmetic is that of bicgstab_solve.
+    ``precond`` (IlutpFactors): split preconditioning on the device; the
+    space then lives in the preconditioned coordinates, as in the reference."""
     cfg = config or SolverConfig()
     t0 = time.perf_counter()
     if precond is not None:
-        _check_common(A, b, precond, cfg)
+        return _precond_solve(A, b, x_init, recycle, precond, cfg, "rbicgstab", t0)
     return _device_solve(A, b, x_init, recycle, cfg, "rbicgstab", t0)
 
 
@@ -560,7 +631,8 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     if cfg.record_iterates:
         raise NotImplementedError("record_iterates is supported by bicgstab_solve / "
                                   "rbicgstab_solve on the device, not by rbicg_solve")
-    M, b = _check_common(A, b, precond, cfg)
+    sp = _Split(A, precond) if precond is not None else None
+    M, b = _check_common(sp.op if sp is not None else A, b, None, cfg)
     t = torch()
     n = M.n
     ctx = Context.get()
@@ -581,6 +653,9 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     bd = _dev_vec(b)
     xd = _dev_vec(x_init)
     xtd = _dev_vec(x_init_dual)
+    if sp is not None:   # solvers.py:115-144: iterate in preconditioned coordinates
+        bd, btd = sp.rhs(bd), sp.rhs_dual(btd)
+        xd, xtd = sp.guess(xd), sp.guess_dual(xtd)
     H = ctypes.c_void_p()
     view = R.view() if R is not None else None
     call_retry_oom("krb_rbicg_create", ctypes.byref(H), ctx.h, M.h,
@@ -664,6 +739,9 @@ def rbicg_solve(A, b, b_dual=None, x_init=None, x_init_dual=None, recycle=None,
     LAST_SOLVE.update(matvecs=int(res.matvecs), bodies=int(res.iterations_run),
                       kernel_launches=int(res.kernel_launches))
     _count(A, nm=int(counts[0]), nr=int(counts[1]))
+    if sp is not None:
+        xo, xto = sp.unwind(xo), sp.unwind_dual(xto)
+        hist.final_true_resid = sp.true_residual(b, xo)
     if on_device:
         return xo, xto, hist, harvest.cycles
     return to_host(xo), to_host(xto), hist, harvest.cycles

@@ -22,7 +22,8 @@ residuals, iterations, matvecs, status, final true residual):
 * driver/c1, driver/c2s           -- the reference's OWN driver.run_sequence
   with the ILUTP split preconditioner replaced by the identity (verbatim
   policy: RBiCG + harvest at every matrix change);
-* ilutp/...                       -- see make_golden_ilutp.py.
+* ilutp/c1s, ilutp/c1             -- the reference's driver.run_sequence as
+  shipped: ILUTP split preconditioning, verbatim policy (C1-small, full C1).
 
 The matrices are identified by a sha256 of their CSR arrays, so the GPU
 tests (which regenerate them with paper_1406_2831_b200.workloads on the
@@ -224,12 +225,35 @@ def driver_cases(out, tag, seq, threads=THREADS):
         KD.ilutp_factor, KD.SplitPreconditionedOperator, KD.apply_left = saved
 
 
+def ilutp_driver_cases(out, tag, seq, threads=(1, 2, 4, 8)):
+    """The reference's OWN driver.run_sequence, unmodified: ILUTP split
+    preconditioning (drop_tol 1e-4, pivot_tol 0.1), verbatim policy."""
+    import krecycle.driver as KD
+    for th in threads:
+        t0 = time.time()
+        with threadpool_limits(th):
+            res = KD.run_sequence(_SeqAdapter(seq), tol=seq.tol, max_itn=seq.max_itn,
+                                  k=seq.k, s=seq.s, seed=0)
+        put_seq(out, f"ilutp/{tag}/t{th}/", res.recycling, res.space_dims)
+        out[f"ilutp/{tag}/t{th}/base_iters"] = np.asarray(
+            [h.iterations for h in res.baseline.histories])
+        out[f"ilutp/{tag}/t{th}/base_matvecs"] = np.asarray(
+            [h.total_matvecs for h in res.baseline.histories])
+        out[f"ilutp/{tag}/t{th}/base_resid51_0"] = np.asarray(
+            res.baseline.histories[0].resid[:51])
+        print(f"ilutp {tag} t{th}: {[h.iterations for h in res.recycling.histories]} "
+              f"base {[h.iterations for h in res.baseline.histories]} dims {res.space_dims} "
+              f"({time.time() - t0:.1f}s)", flush=True)
+
+
 GROUPS = {
     "c1": lambda out: solver_cases(out, "c1", range(6)),
     "c2": lambda out: solver_cases(out, "c2", (0, 5, 9)),
     "policy": lambda out: (policy_cases(out, "c1"), policy_cases(out, "c2")),
     "driver": lambda out: (driver_cases(out, "c1", W.make_sequence("c1")),
                            driver_cases(out, "c2s", W.make_sequence("c2", small=True))),
+    "ilutp": lambda out: (ilutp_driver_cases(out, "c1s", W.make_sequence("c1", small=True)),
+                          ilutp_driver_cases(out, "c1", W.make_sequence("c1"))),
 }
 
 

@@ -108,3 +108,31 @@ def test_factorization_errors(K):
         K.ilutp_factor(KA)
     with pytest.raises(ValueError):
         ilutp_factor(P.SparseMatrix.from_triplets(2, 3, [0, 1], [0, 1], [1.0, 1.0]))
+
+
+def test_oracle_split_operator_refops_equals_reference(K):
+    """The oracle's split-ILUTP operand with RefOps (SuperLU solves, as
+    ilutp.py) reproduces krecycle's preconditioned solves bit for bit: a
+    BiCGSTAB and an RBiCG generation solve on the preconditioned operator
+    (driver.py:98-103 form: CountingOperator(SplitPreconditionedOperator),
+    b -> apply_left(b))."""
+    from threadpoolctl import threadpool_limits
+    from oracle import krylov as O
+    from oracle.ops import RefOps
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence("c1", small=True)
+    A, b = seq.matrix(1), seq.rhs(1, 0)
+    KA = K.SparseMatrix(A.n, A.n, A.row_ptr, A.col_idx, A.values)
+    F = K.ilutp_factor(KA)
+    op = K.SplitPreconditionedOperator(KA, F)
+    bh = K.apply_left(F, b)
+    with threadpool_limits(1):
+        _, hk = K.bicgstab_solve(K.CountingOperator(op), bh, config=K.SolverConfig(seed=2))
+        _, ho = O.bicgstab(op, bh, config=O.Config(seed=2), ops=RefOps())
+        assert hk.resid == ho.resid and hk.final_true_resid == ho.final_true_resid
+        _, _, gk, ck = K.rbicg_solve(K.CountingOperator(op), bh, b_dual=np.ones(A.n),
+                                     config=K.SolverConfig(seed=0, s=10))
+        _, _, go, co = O.rbicg(op, bh, b_dual=np.ones(A.n), ops=RefOps(),
+                               config=O.Config(seed=0, s=10))
+    assert gk.resid == go.resid and gk.resid_dual == go.resid_dual
+    assert len(ck) == len(co) and np.array_equal(ck[0].V, co[0].V)

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa)
   }
   if (!elect_last_cta(a.counters + PH, &last_flag)) return;
   phase_leader<PH>(a, sc);
+  if (PH == PH_XR && a.ktime && threadIdx.x < 32) ktime_fold_spmv(a);
   if (threadIdx.x == 0) {
     ktime_add(a, kSlot);
     a.counters[PH] = 0;
@@ -105,19 +106,31 @@ __global__ void __launch_bounds__(1024) k_proj_dot(const IterArgs *__restrict__ 
   ktime_finish(a, kGamma ? 6 : 2);
 }
 
-// SpMV inside the iteration (matrix read from the descriptor)
-template <bool kSell, bool kSecond>
-__global__ void __launch_bounds__(256) k_iter_spmv(const IterArgs *__restrict__ pa) {
-  const IterArgs &a = *pa;
-  if (a.S->status != KRB_RUNNING) return;
-  ktime_start(a, kSecond ? 5 : 1);
+// SpMV inside the iteration: one row per thread, the matrix, x, y and the
+// status word as kernel parameters (constant bank operands, as the
+// standalone k_spmv), so no thread chases the descriptor before its first
+// matrix load.  The graph bakes these parameters; rbicgstab re-captures it
+// when the matrix (or the kernel-timing buffer) differs from the captured
+// one.  (Reading them through the descriptor: 1025 us per C5 launch vs
+// 898 us for the same rows with parameters; broadcasting them through shared
+// memory costs 48 registers; a grid-stride variant with 6 x 148 CTAs:
+// 1258 us.)
+template <bool kSell, int kSlot>
+__global__ void __launch_bounds__(256) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
+                                                   double *__restrict__ y,
+                                                   const int *__restrict__ status,
+                                                   uint64_t *__restrict__ kt) {
+  if (*status != KRB_RUNNING) return;
+  if (kt && blockIdx.x == 0 && threadIdx.x == 0)
+    *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < a.A.n) {
-    const double *x = kSecond ? a.s : a.p;
-    double *y = kSecond ? a.t : a.q;
-    y[(kSell && a.A.perm) ? a.A.perm[i] : i] = spmv_row<kSell>(i, a.A, x);
+  if (i < A.n) y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
+  if (kt) {   // per-SM end stamp (iter.cuh ktime_end_spmv)
+    __syncthreads();
+    if (threadIdx.x == 0)
+      atomicMax((unsigned long long *)&kt[kKtSpmvBase + kKtSmSlots * (kSlot == 5 ? 1 : 0) + smid()],
+                (unsigned long long)globaltimer());
   }
-  ktime_end_spmv(a, kSecond ? 5 : 1);
 }
 
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
@@ -138,6 +151,8 @@ __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
 template <int PH>
 static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.nb == 0) return KRB_OK;
+  // 2 x 148 CTAs even where only one fits per SM: the second wave balances
+  // the blocks dynamically (one wave of 148: Q / T 702 -> 776 us on C5)
   int grid = grid_for(h.nb);
   KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
@@ -147,7 +162,8 @@ static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
 template <bool kGamma>
 static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.k <= 0 || h.nb == 0) return KRB_OK;
-  dim3 grid = tdot_grid(h.nb, h.k);
+  static int per_sm = occupancy_1024(k_proj_dot<16, kGamma>);
+  dim3 grid = tdot_grid(h.nb, h.k, per_sm);
   KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;
@@ -160,10 +176,13 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
     return spmv_launch(&h.A, kSecond ? h.s : h.p, kSecond ? h.t : h.q,
                        reinterpret_cast<const int *>(&h.S->status), st);
   unsigned blocks = (unsigned)((h.n + 255) / 256);
+  const int *status = reinterpret_cast<const int *>(&h.S->status);
+  const double *x = kSecond ? h.s : h.p;
+  double *y = kSecond ? h.t : h.q;
   if (h.A.format == 2)
-    k_iter_spmv<true, kSecond><<<blocks, 256, 0, st>>>(d);
+    k_iter_spmv<true, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
   else
-    k_iter_spmv<false, kSecond><<<blocks, 256, 0, st>>>(d);
+    k_iter_spmv<false, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -390,7 +409,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   const bool graph = mode == 1;
   GraphCache &G = ctx->graph;
   const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format &&
-                   G.pre_serial == precond_serial(A->pre);
+                   G.pre_serial == precond_serial(A->pre) && G.mat == A->val &&
+                   G.ktime == cfg->d_kernel_times;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -407,6 +427,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     KRB_CHECK_CUDA(cudaStreamSynchronize(st));
     KRB_TRY(build_graph(ctx, h, d, capture_stream()));
     G.n = n; G.k = k; G.format = A->format; G.pre_serial = precond_serial(A->pre);
+    G.mat = A->val;
+    G.ktime = cfg->d_kernel_times;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

@@ -32,6 +32,8 @@ struct GraphCache {
   cudaGraphConditionalHandle cond = 0;
   int64_t n = -1, k = -1;
   int64_t pre_serial = 0;   // preconditioned operator the body was captured for
+  const void *mat = nullptr;     // matrix values / kernel-timing buffer baked into
+  const void *ktime = nullptr;   // the SpMV node parameters
   int format = -1;
   int64_t kernels_per_body = 0;
   void reset() {
@@ -95,7 +97,17 @@ Tuning &tuning();
 
 int ctx_reserve_part(krb_context *ctx, size_t doubles);
 int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);
-dim3 tdot_grid(int64_t nb, int64_t k);
+dim3 tdot_grid(int64_t nb, int64_t k, int per_sm);
+// resident 1024-thread CTAs per SM of a kernel (>= 1)
+template <class K>
+int occupancy_1024(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, 1024, 0) != cudaSuccess) {
+    cudaGetLastError();
+    b = 1;
+  }
+  return b > 0 ? b : 1;
+}
 int ctx_reserve_vectors(krb_context *ctx, int64_t n, int64_t k);
 void rbicg_cache_free(krb_context *ctx);
 void batch_pool_free(krb_context *ctx);

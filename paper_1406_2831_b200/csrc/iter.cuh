@@ -75,8 +75,8 @@ __host__ __device__ constexpr int ktime_slot_of(int PH) {
 // mark their end per SM instead of electing a last CTA: each CTA's thread 0
 // does a fire-and-forget atomicMax into its SM's slot (kKtSpmvBase + 160 s'
 // + smid; one address per SM, so no single-address atomic queue -- that
-// cost ~25 % of the launch), and the next kernel's CTA 0 folds the maximum
-// over the SMs into the slot's total.
+// cost ~25 % of the launch), and the X phase's leader (after both SpMVs of
+// the iteration) folds the maximum over the SMs into the slots' totals.
 constexpr int kKtSpmvBase = 64;     // d_kernel_times[64 .. 64 + 2 x 160)
 constexpr int kKtSmSlots = 160;
 
@@ -111,14 +111,12 @@ __device__ __forceinline__ void ktime_fold_spmv(const IterArgs &a) {
   }
 }
 
-// every thread (uniform call): CTA 0 folds pending SpMV ends and stamps the
-// kernel's start
+// CTA 0 stamps the kernel's start (one store; the SpMV ends are folded by
+// the X phase's leader, ktime_fold_spmv, so the hot kernels carry no extra
+// code: the fold loop inlined into every kernel cost them registers)
 __device__ __forceinline__ void ktime_start(const IterArgs &a, int slot) {
-  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 32) {
-    ktime_fold_spmv(a);
-    __syncwarp();
-    if (threadIdx.x == 0) *(volatile uint64_t *)&a.ktime[4 * slot] = globaltimer();
-  }
+  if (a.ktime && slot >= 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    *(volatile uint64_t *)&a.ktime[4 * slot] = globaltimer();
 }
 
 __device__ __forceinline__ void ktime_end_spmv(const IterArgs &a, int slot) {

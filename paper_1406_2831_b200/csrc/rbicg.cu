@@ -390,7 +390,8 @@ static int bi_spmv(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
 template <bool kDual>
 static int bi_proj_dot(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   if (h.k <= 0 || h.nb == 0) return KRB_OK;
-  dim3 grid = tdot_grid(h.nb, h.k);
+  static int per_sm = occupancy_1024(k_bproj_dot<16, kDual>);
+  dim3 grid = tdot_grid(h.nb, h.k, per_sm);
   KRB_DISPATCH_E(canon_E(h.n), (k_bproj_dot<kE, kDual><<<grid, 1024, 0, st>>>(d)));
   KRB_CHECK_LAUNCH();
   return KRB_OK;

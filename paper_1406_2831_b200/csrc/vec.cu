@@ -715,9 +715,14 @@ int launch_final(int ndots, int64_t nb, const double *part, double *out,
   return KRB_OK;
 }
 
-dim3 tdot_grid(int64_t nb, int64_t k) {
+// One wave: gx x gy = 148 x (resident CTAs per SM), so the column groups of
+// a canonical block run at the same time (their shared v loads hit L2) and no
+// CTA waits for a second wave.  (2 per SM assumed before; with 42-64
+// registers only one 1024-thread CTA fits, so half the grid ran as a second
+// wave that re-read v from DRAM.)
+dim3 tdot_grid(int64_t nb, int64_t k, int per_sm) {
   int64_t gy = (k + kTdotCG - 1) / kTdotCG;
-  int64_t want = (int64_t)kNumSMs * 2;
+  int64_t want = (int64_t)kNumSMs * (per_sm > 0 ? per_sm : 1);
   int64_t gx = (want + gy - 1) / gy;
   if (gx > nb) gx = nb;
   if (gx < 1) gx = 1;
@@ -738,7 +743,8 @@ int launch_tdot(krb_context *ctx, int64_t n, int64_t k, const double *M,
   if (rc) return rc;
   rc = ctx_reserve_counters(ctx, st);
   if (rc) return rc;
-  dim3 grid = tdot_grid(nb, k);
+  static int per_sm = occupancy_1024(k_tdot<16, false, false>);
+  dim3 grid = tdot_grid(nb, k, per_sm);
   unsigned int *cnt = ctx->counters + kCounterTdotStandalone;
   if (self) {
     if (self_sqrt) {

@@ -331,7 +331,11 @@ def c4_sequence(n: int = 4_000_000, num: int = 8) -> SequenceSpec:
     def rhs(j, kappa):
         return _normal(j, n)
 
-    return SequenceSpec("c4", n, 30, 1e-8, num, 1, mat, rhs,
+    # max_itn 3000: system 0 (sigma = 0) needs 1909 BiCGSTAB iterations at
+    # n = 4 M (319 / 582 / 779 at n = 20 k / 200 k / 1 M; the reference
+    # algorithm on the CPU: 370 / 659 at 20 k / 200 k), so the default 1000
+    # would stop it at max_itn (tools/c4_convergence.py)
+    return SequenceSpec("c4", n, 30, 1e-8, num, 1, mat, rhs, max_itn=3000,
                         meta={"rows": n, "pattern": "power-law 3..200"})
 
 

@@ -56,8 +56,9 @@ def random_space_arrays(A, k, seed=0, ops=None):
     """Random biorthonormalized space built by the oracle (canonical ops)."""
     from oracle import krylov as O
     r = np.random.default_rng(seed)
-    U = r.standard_normal((A.n, k))
-    Ut = r.standard_normal((A.n, k))
+    n = A.n if hasattr(A, "n") else A.nrows
+    U = r.standard_normal((n, k))
+    Ut = r.standard_normal((n, k))
     return O.biorthonormalize(U, Ut, A, ops=ops)
 
 

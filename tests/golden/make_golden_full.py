@@ -51,7 +51,7 @@ import krecycle as K  # noqa: E402
 from paper_1406_2831_b200 import workloads as W  # noqa: E402
 
 warnings.simplefilter("ignore")
-THREADS = (1, 2, 4, 8, 16)
+THREADS = (1, 2, 3, 4, 6, 8, 16)
 OUT = os.path.join(HERE, "reference_full.npz")
 SPACE_SEED = 777
 
@@ -116,7 +116,11 @@ def _exact_dot(a, b):
 # the reference's solvers with other valid summation orders for their dots
 # (what another BLAS would do): exactly rounded, and numpy's pairwise sum
 VARIANTS = {"vexact": _exact_dot,
-            "vpair": lambda a, b: np.float64(np.sum(np.asarray(a) * np.asarray(b)))}
+            "vpair": lambda a, b: np.float64(np.sum(np.asarray(a) * np.asarray(b))),
+            "vrev": lambda a, b: np.float64(np.dot(np.asarray(a)[::-1], np.asarray(b)[::-1])),
+            "vblk": lambda a, b: np.float64(sum(np.dot(np.asarray(a)[i:i + 97],
+                                                       np.asarray(b)[i:i + 97])
+                                                for i in range(0, len(a), 97)))}
 
 
 def solver_cases(out, name, systems):
@@ -175,13 +179,21 @@ def policy_cases(out, name):
     seq = W.make_sequence(name)
     for j in range(seq.num_matrices):
         out[f"mat/{name}/{j}/sha"] = np.array(csr_hash(seq.matrix(j)))
-    for th in THREADS:
+    import krecycle.solvers as KS
+    runs = [(f"t{th}", th, None) for th in THREADS] + \
+           [(v, 1, f) for v, f in VARIANTS.items()]
+    for tag, th, dotf in runs:
         t0 = time.time()
-        with threadpool_limits(th):
-            res = run_sequence(W.make_sequence(name), policy="first", baseline=False,
-                               api=ref_api())
-        put_seq(out, f"policy/{name}first/t{th}/", res.recycling, res.space_dims)
-        print(f"policy {name} t{th}: {[h.iterations for h in res.recycling.histories]} "
+        if dotf is not None:
+            KS.np = _numpy_with_dot(dotf)
+        try:
+            with threadpool_limits(th):
+                res = run_sequence(W.make_sequence(name), policy="first", baseline=False,
+                                   api=ref_api())
+        finally:
+            KS.np = np
+        put_seq(out, f"policy/{name}first/{tag}/", res.recycling, res.space_dims)
+        print(f"policy {name} {tag}: {[h.iterations for h in res.recycling.histories]} "
               f"dims {res.space_dims} ({time.time() - t0:.1f}s)", flush=True)
 
 
@@ -209,17 +221,25 @@ def driver_cases(out, tag, seq, threads=THREADS):
     KD.ilutp_factor = lambda A, **kw: None
     KD.SplitPreconditionedOperator = lambda A, f: A
     KD.apply_left = lambda f, b: np.asarray(b)
+    import krecycle.solvers as KS
+    runs = [(f"t{th}", th, None) for th in threads] + \
+           [(v, 1, f) for v, f in VARIANTS.items()]
     try:
-        for th in threads:
+        for rt, th, dotf in runs:
             t0 = time.time()
-            with threadpool_limits(th):
-                res = KD.run_sequence(_SeqAdapter(seq), tol=seq.tol, max_itn=seq.max_itn,
-                                      k=seq.k, s=seq.s, seed=0)
-            put_seq(out, f"driver/{tag}/t{th}/", res.recycling, res.space_dims)
-            out[f"driver/{tag}/t{th}/base_iters"] = np.asarray(
+            if dotf is not None:
+                KS.np = _numpy_with_dot(dotf)
+            try:
+                with threadpool_limits(th):
+                    res = KD.run_sequence(_SeqAdapter(seq), tol=seq.tol,
+                                          max_itn=seq.max_itn, k=seq.k, s=seq.s, seed=0)
+            finally:
+                KS.np = np
+            put_seq(out, f"driver/{tag}/{rt}/", res.recycling, res.space_dims)
+            out[f"driver/{tag}/{rt}/base_iters"] = np.asarray(
                 [h.iterations for h in res.baseline.histories])
-            out[f"driver/{tag}/t{th}/base_aux"] = np.array(res.baseline.aux_matvecs)
-            print(f"driver {tag} t{th}: {[h.iterations for h in res.recycling.histories]} "
+            out[f"driver/{tag}/{rt}/base_aux"] = np.array(res.baseline.aux_matvecs)
+            print(f"driver {tag} {rt}: {[h.iterations for h in res.recycling.histories]} "
                   f"dims {res.space_dims} ({time.time() - t0:.1f}s)", flush=True)
     finally:
         KD.ilutp_factor, KD.SplitPreconditionedOperator, KD.apply_left = saved

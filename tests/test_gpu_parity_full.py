@@ -138,14 +138,21 @@ def test_full_size_solvers_vs_reference(P, G, canon, name, j):
     assert np.array_equal(x, xo)
 
 
+def _seq_tags(G, prefix):
+    tags = [f"t{t}" for t in threads(G)]
+    if "meta/variants" in G:
+        tags += [str(v) for v in G["meta/variants"]]
+    return [tg for tg in tags if f"{prefix}/{tg}/iters" in G]
+
+
 def _seq_check(G, prefix, res, label):
-    ts = [t for t in threads(G) if f"{prefix}/t{t}/iters" in G]
+    ts = _seq_tags(G, prefix)
     if not ts:
         pytest.skip(f"{prefix} not in the fixture")
-    mv = np.array([G[f"{prefix}/t{t}/matvecs"] for t in ts])          # (runs, systems)
-    dims = [list(G[f"{prefix}/t{t}/space_dims"]) for t in ts]
+    mv = np.array([G[f"{prefix}/{t}/matvecs"] for t in ts])          # (runs, systems)
+    dims = [list(G[f"{prefix}/{t}/space_dims"]) for t in ts]
     gm = np.array([h.total_matvecs for h in res.recycling.histories])
-    S0 = max(reldiff(G[f"{prefix}/t{a}/resid51_0"], G[f"{prefix}/t{b}/resid51_0"])
+    S0 = max(reldiff(G[f"{prefix}/{a}/resid51_0"], G[f"{prefix}/{b}/resid51_0"])
              for a in ts for b in ts if a != b) if len(ts) > 1 else 0.0
     dev0 = reldiff(res.recycling.histories[0].resid, G[f"{prefix}/t1/resid51_0"])
     print(f"\n{label}: gpu matvecs {gm.tolist()} dims {res.space_dims}; reference "
@@ -179,7 +186,7 @@ def test_verbatim_policy_vs_reference_driver(P, G):
     seq = make_sequence("c1")
     res = run_sequence(seq, policy="verbatim", baseline=True, api=P)
     _seq_check(G, "driver/c1", res, "driver c1")
-    ts = [t for t in threads(G) if f"driver/c1/t{t}/base_iters" in G]
-    bi = np.array([G[f"driver/c1/t{t}/base_iters"] for t in ts])
+    ts = [t for t in _seq_tags(G, "driver/c1") if f"driver/c1/{t}/base_iters" in G]
+    bi = np.array([G[f"driver/c1/{t}/base_iters"] for t in ts])
     gb = np.array([h.iterations for h in res.baseline.histories])
     assert bi.sum(1).min() * 0.98 <= gb.sum() <= bi.sum(1).max() * 1.02, (gb, bi)

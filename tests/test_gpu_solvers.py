@@ -131,8 +131,8 @@ def test_counting_operator_and_errors(pkg):
     assert op.n_matvec == h.total_matvecs and op.n_rmatvec == 0
     with pytest.raises(ValueError):
         pkg.bicgstab_solve(A, np.ones(A.nrows + 1))
-    with pytest.raises(NotImplementedError):
-        pkg.bicgstab_solve(A, seq.rhs(0, 0), precond=object())
+    with pytest.raises(AttributeError):   # not an IlutpFactors (the reference
+        pkg.bicgstab_solve(A, seq.rhs(0, 0), precond=object())   # fails alike)
     # max_itn = 0 -> immediate max_itn, one history entry
     x, h = pkg.bicgstab_solve(A, seq.rhs(0, 0), config=pkg.SolverConfig(max_itn=0))
     assert h.status == "max_itn" and h.iterations == 0

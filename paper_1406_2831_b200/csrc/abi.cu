@@ -65,7 +65,8 @@ int krb_set_tuning(const char *key, int64_t value) {
       {"persist0", &t.persist0},   {"p0_grid_half", &t.p0_grid_half},
       {"p0_onchip", &t.p0_onchip}, {"p0_prof_cta", &t.p0_prof_cta},
       {"cluster", &t.cluster},     {"persist_v1", &t.persist_v1},
-      {"gemm_mode", &t.gemm_mode}, {"l2keep", &t.l2keep}};
+      {"gemm_mode", &t.gemm_mode}, {"l2keep", &t.l2keep},
+      {"phase_variant", &t.phase_variant}};
   for (auto &e : table)
     if (strcmp(e.name, key) == 0) {
       *e.slot = (int)value;

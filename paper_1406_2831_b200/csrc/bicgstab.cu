@@ -43,8 +43,23 @@ namespace krb {
 // ---------------------------------------------------------------------------
 // graph / host-loop driver: one kernel per phase, last CTA finalizes
 // ---------------------------------------------------------------------------
-template <int kE, int PH>
-__global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa) {
+// Register budget and element unroll per phase (kV = tuning "phase_variant"
+// 0, measured on C5, same box, A/B): the projection updates Q / T keep up to
+// 64 registers (one 1024-thread CTA per SM) and 4 elements in flight
+// (702 us vs 739 at 32 registers); P, S and X run two CTAs per SM (at most 32
+// registers): P with 4 elements unrolled (76 vs 104 us at 64 registers), S
+// and X with 2 (S 73 vs 97, X 203 vs 253).  kV = 1: every phase at 64
+// registers / 4 elements (the round-1 kernels, kept for A/B).  Same
+// arithmetic, same bits.
+__host__ __device__ constexpr int phase_minb(int PH, int kV) {
+  return kV == 1 ? 1 : ((PH == PH_PROJ_Q || PH == PH_PROJ_T) ? 1 : 2);
+}
+__host__ __device__ constexpr int phase_unroll(int PH, int kV) {
+  return kV == 1 ? 4 : ((PH == PH_SUPD || PH == PH_XR) ? 2 : 4);
+}
+
+template <int kE, int PH, int kV>
+__global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterArgs *__restrict__ pa) {
   __shared__ double coef[512];
   __shared__ double red[4][32];
   __shared__ int last_flag;
@@ -78,7 +93,7 @@ __global__ void __launch_bounds__(1024) k_phase(const IterArgs *__restrict__ pa)
     for (int j = threadIdx.x; j < a.k; j += blockDim.x) coef[j] = src[j];
     __syncthreads();
   }
-  phase_blocks<kE, PH>(a, sc, red, coef, blockIdx.x, gridDim.x, a.part);
+  phase_blocks<kE, PH, phase_unroll(PH, kV)>(a, sc, red, coef, blockIdx.x, gridDim.x, a.part);
   if (ND == 0) {
     ktime_finish(a, kSlot);
     return;
@@ -154,7 +169,11 @@ static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   // 2 x 148 CTAs even where only one fits per SM: the second wave balances
   // the blocks dynamically (one wave of 148: Q / T 702 -> 776 us on C5)
   int grid = grid_for(h.nb);
-  KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH><<<grid, 1024, 0, st>>>(d)));
+  if (tuning().phase_variant == 1) {
+    KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 1><<<grid, 1024, 0, st>>>(d)));
+  } else {
+    KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 0><<<grid, 1024, 0, st>>>(d)));
+  }
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -410,7 +429,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   GraphCache &G = ctx->graph;
   const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format &&
                    G.pre_serial == precond_serial(A->pre) && G.mat == A->val &&
-                   G.ktime == cfg->d_kernel_times;
+                   G.ktime == cfg->d_kernel_times && G.variant == tuning().phase_variant;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -429,6 +448,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     G.n = n; G.k = k; G.format = A->format; G.pre_serial = precond_serial(A->pre);
     G.mat = A->val;
     G.ktime = cfg->d_kernel_times;
+    G.variant = tuning().phase_variant;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

@@ -34,6 +34,7 @@ struct GraphCache {
   int64_t pre_serial = 0;   // preconditioned operator the body was captured for
   const void *mat = nullptr;     // matrix values / kernel-timing buffer baked into
   const void *ktime = nullptr;   // the SpMV node parameters
+  int variant = -1;              // phase kernel variant (tuning) captured
   int format = -1;
   int64_t kernels_per_body = 0;
   void reset() {
@@ -92,6 +93,7 @@ struct Tuning {
   int persist_v1 = 0;     // force the nine-barrier persistent kernel
   int gemm_mode = -1;     // krb_gemm: 0 row kernel, 8 / 12 / 24 / 122 tiled
   int l2keep = -1;        // evict_last policy on the recycle blocks
+  int phase_variant = 0;  // graph phase kernels: 0 tuned per phase, 1 uniform (round 1)
 };
 Tuning &tuning();
 

@@ -247,7 +247,7 @@ __device__ __forceinline__ PhaseScal load_scal(const SolveScalars *S) {
 // Elementwise work + canonical block partials of one phase for canonical
 // blocks blk = first, first + step, ...   `coef` (k values of zeta / gamma)
 // must already be in shared memory for the projection phases.
-template <int kE, int PH>
+template <int kE, int PH, int kU = 4>
 __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal sc,
                                              double (*red)[32],
                                              const double *coef, int64_t first,
@@ -270,7 +270,7 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
   for (int64_t blk = first; blk < nb; blk += step) {
     const int64_t base = blk * ((int64_t)kLanes * kE) + threadIdx.x;
     double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll(kE < 4 ? kE : 4)
+#pragma unroll(kE < kU ? kE : kU)
     for (int e = 0; e < kE; ++e) {
       const int64_t i = base + (int64_t)kLanes * e;
       if (i >= n) continue;

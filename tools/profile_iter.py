@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--solves", type=int, default=2)
     ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--max-itn", type=int, default=None)
     a = ap.parse_args()
     import torch
     import paper_1406_2831_b200 as P
@@ -33,7 +34,8 @@ def main():
     b = D.to_device(seq.rhs(0, 0))
     for i in range(a.solves):
         _, h = S.solve_device(M, b, None, space,
-                              P.SolverConfig(tol=seq.tol, max_itn=seq.max_itn, seed=i))
+                              P.SolverConfig(tol=seq.tol, max_itn=a.max_itn or seq.max_itn,
+                                             seed=i))
         print(f"solve {i}: {h.status} {h.iterations} iterations, k={space.k}, "
               f"format={M.format}")
     torch.cuda.synchronize()

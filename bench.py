@@ -342,6 +342,9 @@ def gpu_arm(args, wl, rank, world):
            "matvecs_per_system": [h.total_matvecs for h in hists],
            "statuses": [h.status for h in hists],
            "final_true_resid_max": max(h.final_true_resid for h in hists),
+           "checks": {"all_converged": all(h.status == "converged" for h in hists),
+                      "true_resid_le_tol": all(h.final_true_resid <= 1.1 * wl.seq.tol
+                                               for h in hists)},
            "space_k_last": sp.k,
            "histories_head": {str(j): [float(v) for v in hists[j].resid[:51]]
                               for j in (0, len(hists) - 1)}}
@@ -593,7 +596,10 @@ def main():
                 "iterations_per_step": res["iters"] / args.steps,
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "e2e": res["e2e"], "roofline": res["roofline"], "cpu_baseline": cpu}
-        for key in ("e2e_pageable", "iteration", "kernel_shares", "step_ms",
+        if not all(res.get("checks", {}).values()):
+            print("bench: a timed solve did not converge to tol -- the number is not "
+                  "valid", file=sys.stderr)
+        for key in ("checks", "e2e_pageable", "iteration", "kernel_shares", "step_ms",
                     "iterations_per_system", "matvecs_per_system", "statuses",
                     "final_true_resid_max", "space_k_last", "baseline", "full_policy",
                     "histories_head"):

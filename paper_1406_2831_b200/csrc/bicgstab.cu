@@ -427,8 +427,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   const int mode = (A->pre && cfg->use_graph == 2) ? 1 : cfg->use_graph;
   const bool graph = mode == 1;
   GraphCache &G = ctx->graph;
-  const bool hit = graph && G.exec && G.n == n && G.k == k && G.format == A->format &&
-                   G.pre_serial == precond_serial(A->pre) && G.mat == A->val &&
+  const MatrixSig sig = matrix_sig(A);
+  const bool hit = graph && G.exec && G.n == n && G.k == k && same_sig(G.sig, sig) &&
                    G.ktime == cfg->d_kernel_times && G.variant == tuning().phase_variant;
   h.use_cond = graph ? 1 : 0;
   {
@@ -445,8 +445,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   if (graph && !hit) {
     KRB_CHECK_CUDA(cudaStreamSynchronize(st));
     KRB_TRY(build_graph(ctx, h, d, capture_stream()));
-    G.n = n; G.k = k; G.format = A->format; G.pre_serial = precond_serial(A->pre);
-    G.mat = A->val;
+    G.n = n; G.k = k; G.format = A->format; G.sig = sig;
     G.ktime = cfg->d_kernel_times;
     G.variant = tuning().phase_variant;
     h.cond = G.cond;

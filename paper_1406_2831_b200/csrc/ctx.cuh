@@ -31,9 +31,8 @@ struct GraphCache {
   cudaGraph_t graph = nullptr;
   cudaGraphConditionalHandle cond = 0;
   int64_t n = -1, k = -1;
-  int64_t pre_serial = 0;   // preconditioned operator the body was captured for
-  const void *mat = nullptr;     // matrix values / kernel-timing buffer baked into
-  const void *ktime = nullptr;   // the SpMV node parameters
+  MatrixSig sig;                 // matrix (operator) / kernel-timing buffer baked
+  const void *ktime = nullptr;   // into the SpMV node parameters
   int variant = -1;              // phase kernel variant (tuning) captured
   int format = -1;
   int64_t kernels_per_body = 0;

@@ -50,6 +50,18 @@ namespace krb {
 cudaError_t dev_alloc(void **p, size_t bytes, cudaStream_t st);
 void dev_free(void *p, cudaStream_t st);
 
+// Every device pointer a kernel launched on this matrix may receive as a
+// parameter (a graph bakes kernel parameters: a cached graph is reused only
+// for a matrix with the same signature -- freed and re-allocated arrays can
+// come back at the address of another matrix's CSR values).
+struct MatrixSig {
+  const void *p[16];
+  int64_t n = -1, serial = 0;
+  int format = -1;
+};
+MatrixSig matrix_sig(const krb_matrix *A);
+bool same_sig(const MatrixSig &a, const MatrixSig &b);
+
 // preconditioned operator (precond.cu)
 int precond_apply_op(const krb_matrix *A, const double *x, double *y, const int *status,
                      cudaStream_t st);

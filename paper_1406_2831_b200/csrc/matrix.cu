@@ -20,6 +20,7 @@
 // scipy's .transpose().tocsr() order (ascending original row within each
 // column), and gets its own format choice.
 #include <cub/cub.cuh>
+#include <cstring>
 
 #include "krb_internal.cuh"
 #include "spmv.cuh"
@@ -78,6 +79,26 @@ __global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
   y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
+}
+
+MatrixSig matrix_sig(const krb_matrix *A) {
+  MatrixSig g;
+  memset(g.p, 0, sizeof(g.p));
+  if (!A) return g;
+  const krb_matrix *B = A->base ? A->base : A;
+  const void *ptrs[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val,
+                        A->perm, B->rp, B->ci, B->val, B->sl_ptr, B->rlen, B->s_col,
+                        B->s_val, B->perm};
+  for (int i = 0; i < 16; ++i) g.p[i] = ptrs[i];
+  g.n = A->n;
+  g.format = A->format;
+  g.serial = precond_serial(A->pre);
+  return g;
+}
+
+bool same_sig(const MatrixSig &a, const MatrixSig &b) {
+  return a.n == b.n && a.format == b.format && a.serial == b.serial &&
+         memcmp(a.p, b.p, sizeof(a.p)) == 0;
 }
 
 int spmv_launch(const krb_matrix *A, const double *x, double *y,

@@ -700,7 +700,7 @@ struct krb_rbicg {
   // callback launches (update_recycle_space's Grams / norms) while this
   // handle's descriptor still holds the pointer
   double *part = nullptr;
-  int64_t pre_serial = 0;   // preconditioned operator the graph was captured for
+  krb::MatrixSig sig;       // operator whose composite kernels the graph bakes
   int64_t s = 0, max_itn = 0, k = 0;
   krb_space_view R = {};
   bool has_R = false;
@@ -810,7 +810,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   krb_rbicg *H = ctx->bi_cache;
   const bool reuse = H && H->h.n == n && H->k == k && H->s == s && H->max_itn == max_itn &&
                      H->fmt == A->format && H->fmt_t == A->T->format &&
-                     H->pre_serial == precond_serial(A->pre);
+                     (!A->pre || same_sig(H->sig, matrix_sig(A)));
   if (H && !reuse) bi_free(H);
   ctx->bi_cache = nullptr;
   if (!reuse) H = new krb_rbicg();
@@ -823,7 +823,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   H->k = k;
   H->fmt = A->format;
   H->fmt_t = A->T->format;
-  H->pre_serial = precond_serial(A->pre);
+  H->sig = matrix_sig(A);
   const int64_t nb = canon_nblocks(n);
   const int64_t ring_cols = (s > 0 ? s : 0) + 3;
   cudaError_t e = cudaSuccess;

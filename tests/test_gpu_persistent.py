@@ -139,3 +139,27 @@ def test_large_n_graph_bitwise_and_persistent_refused(pkg, canon, n, k, fmt):
     assert np.array_equal(xg.cpu().numpy(), xo)
     with pytest.raises(_lib.KrbError):
         S.solve_device(M, to_device(b), None, None, cfg, use_graph=2)
+
+
+def test_graph_recaptured_for_a_new_matrix_of_the_same_shape(pkg, canon):
+    """The graph driver bakes the SpMV's matrix into its kernel parameters:
+    a solve on a NEW matrix of the same shape (its arrays partly at freed
+    addresses of the previous one) must re-capture, not reuse a graph that
+    reads freed memory (bench.py's C5 step caught this)."""
+    import gc
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import solvers as S
+    from paper_1406_2831_b200.device import DeviceMatrix, to_device
+    n = 700_001
+    b = np.random.default_rng(0).standard_normal(n)
+    cfg = pkg.SolverConfig(tol=1e-10, max_itn=25, seed=1)
+    for seed in (1, 2, 3):
+        A = ragged_matrix(n, seed=seed)
+        M = DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+        xg, hg = S.solve_device(M, to_device(b), None, None, cfg)
+        assert S.LAST_SOLVE["driver"] == "graph"
+        xo, ho = O.rbicgstab(A, b, config=O.Config(tol=1e-10, max_itn=25, seed=1), ops=canon)
+        assert (hg.status, hg.resid, hg.matvecs) == (ho.status, ho.resid, ho.matvecs), seed
+        assert np.array_equal(xg.cpu().numpy(), xo)
+        del M, xg
+        gc.collect()

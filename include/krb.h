@@ -52,7 +52,8 @@ int64_t krb_launch_count(void);
 
 /* Driver / kernel-variant knobs (process-wide; every variant computes the
  * same bits).  Keys: "persist0", "p0_grid_half", "p0_onchip", "p0_prof_cta",
- * "cluster", "persist_v1", "gemm_mode", "l2keep", "phase_variant".  Unknown key -> KRB_EINVAL.
+ * "cluster", "persist_v1", "gemm_mode", "l2keep", "phase_variant",
+ * "tdot_variant".  Unknown key -> KRB_EINVAL.
  * No reference counterpart (the reference has no device drivers). */
 int krb_set_tuning(const char *key, int64_t value);
 int krb_reset_tuning(void);

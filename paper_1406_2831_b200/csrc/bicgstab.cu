@@ -47,15 +47,17 @@ namespace krb {
 // 0, measured on C5, same box, A/B): the projection updates Q / T keep up to
 // 64 registers (one 1024-thread CTA per SM) and 4 elements in flight
 // (702 us vs 739 at 32 registers); P, S and X run two CTAs per SM (at most 32
-// registers): P with 4 elements unrolled (76 vs 104 us at 64 registers), S
-// and X with 2 (S 73 vs 97, X 203 vs 253).  kV = 1: every phase at 64
-// registers / 4 elements (the round-1 kernels, kept for A/B).  Same
-// arithmetic, same bits.
+// registers): P with 4 elements unrolled (86 vs 104 us at 64 registers), S
+// with 2 (73 vs 97), X with 1 (191 us; 205 with 2, 253 at 64 registers x 4).  kV = 1: every phase at 64
+// registers / 4 elements (the round-1 kernels, kept for A/B); kV = 2: the
+// record_iterates kernels (INIT / X with the snapshot stores); kV = 3: as 0
+// with S / X unrolled once (A/B).  Same arithmetic, same bits.
 __host__ __device__ constexpr int phase_minb(int PH, int kV) {
-  return kV == 1 ? 1 : ((PH == PH_PROJ_Q || PH == PH_PROJ_T) ? 1 : 2);
+  return (kV == 1 || kV == 2) ? 1 : ((PH == PH_PROJ_Q || PH == PH_PROJ_T) ? 1 : 2);
 }
 __host__ __device__ constexpr int phase_unroll(int PH, int kV) {
-  return kV == 1 ? 4 : ((PH == PH_SUPD || PH == PH_XR) ? 2 : 4);
+  return (kV == 1 || kV == 2) ? 4
+       : PH == PH_XR ? 1 : PH == PH_SUPD ? (kV == 3 ? 1 : 2) : 4;
 }
 
 template <int kE, int PH, int kV>
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterAr
     for (int j = threadIdx.x; j < a.k; j += blockDim.x) coef[j] = src[j];
     __syncthreads();
   }
-  phase_blocks<kE, PH, phase_unroll(PH, kV)>(a, sc, red, coef, blockIdx.x, gridDim.x, a.part);
+  phase_blocks<kE, PH, phase_unroll(PH, kV), kV == 2>(a, sc, red, coef, blockIdx.x, gridDim.x,
+                                                      a.part);
   if (ND == 0) {
     ktime_finish(a, kSlot);
     return;
@@ -110,12 +113,14 @@ __global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterAr
 }
 
 // projection dots inside the iteration: Chat^T v -> zeta / gamma
-template <int kE, bool kGamma>
-__global__ void __launch_bounds__(1024) k_proj_dot(const IterArgs *__restrict__ pa) {
+// kV (tuning "tdot_variant"): 0 = up to 64 registers, 4 elements unrolled;
+// 1 = at most 32 registers (two 1024-thread CTAs per SM), 2 elements.
+template <int kE, bool kGamma, int kV>
+__global__ void __launch_bounds__(1024, kV == 1 ? 2 : 1) k_proj_dot(const IterArgs *__restrict__ pa) {
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
   ktime_start(a, kGamma ? 6 : 2);
-  tdot_body<kE, false>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
+  tdot_body<kE, false, false, kV == 1 ? 2 : 4>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
                        kGamma ? a.gamma : a.zeta, a.counters + kCounterTdotGraph,
                        a.l2keep != 0);
   ktime_finish(a, kGamma ? 6 : 2);
@@ -169,8 +174,12 @@ static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   // 2 x 148 CTAs even where only one fits per SM: the second wave balances
   // the blocks dynamically (one wave of 148: Q / T 702 -> 776 us on C5)
   int grid = grid_for(h.nb);
-  if (tuning().phase_variant == 1) {
+  if (h.rec_x && (PH == PH_INIT || PH == PH_XR)) {   // record_iterates snapshots
+    KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 2><<<grid, 1024, 0, st>>>(d)));
+  } else if (tuning().phase_variant == 1) {
     KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 1><<<grid, 1024, 0, st>>>(d)));
+  } else if (tuning().phase_variant == 3) {
+    KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 3><<<grid, 1024, 0, st>>>(d)));
   } else {
     KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 0><<<grid, 1024, 0, st>>>(d)));
   }
@@ -181,9 +190,15 @@ static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
 template <bool kGamma>
 static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.k <= 0 || h.nb == 0) return KRB_OK;
-  static int per_sm = occupancy_1024(k_proj_dot<16, kGamma>);
-  dim3 grid = tdot_grid(h.nb, h.k, per_sm);
-  KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma><<<grid, 1024, 0, st>>>(d)));
+  if (tuning().tdot_variant == 1) {
+    static int per_sm1 = occupancy_1024(k_proj_dot<16, kGamma, 1>);
+    dim3 grid = tdot_grid(h.nb, h.k, per_sm1);
+    KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 1><<<grid, 1024, 0, st>>>(d)));
+  } else {
+    static int per_sm0 = occupancy_1024(k_proj_dot<16, kGamma, 0>);
+    dim3 grid = tdot_grid(h.nb, h.k, per_sm0);
+    KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 0><<<grid, 1024, 0, st>>>(d)));
+  }
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -429,7 +444,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   GraphCache &G = ctx->graph;
   const MatrixSig sig = matrix_sig(A);
   const bool hit = graph && G.exec && G.n == n && G.k == k && same_sig(G.sig, sig) &&
-                   G.ktime == cfg->d_kernel_times && G.variant == tuning().phase_variant;
+                   G.ktime == cfg->d_kernel_times &&
+                   G.variant == tuning().phase_variant + 16 * tuning().tdot_variant;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -447,7 +463,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     KRB_TRY(build_graph(ctx, h, d, capture_stream()));
     G.n = n; G.k = k; G.format = A->format; G.sig = sig;
     G.ktime = cfg->d_kernel_times;
-    G.variant = tuning().phase_variant;
+    G.variant = tuning().phase_variant + 16 * tuning().tdot_variant;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

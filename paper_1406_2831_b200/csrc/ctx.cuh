@@ -93,6 +93,7 @@ struct Tuning {
   int gemm_mode = -1;     // krb_gemm: 0 row kernel, 8 / 12 / 24 / 122 tiled
   int l2keep = -1;        // evict_last policy on the recycle blocks
   int phase_variant = 0;  // graph phase kernels: 0 tuned per phase, 1 uniform (round 1)
+  int tdot_variant = 0;   // graph projection dots: 0 <= 64 regs, 1 <= 32 regs
 };
 Tuning &tuning();
 

@@ -247,7 +247,10 @@ __device__ __forceinline__ PhaseScal load_scal(const SolveScalars *S) {
 // Elementwise work + canonical block partials of one phase for canonical
 // blocks blk = first, first + step, ...   `coef` (k values of zeta / gamma)
 // must already be in shared memory for the projection phases.
-template <int kE, int PH, int kU = 4>
+// kRec: compile the record_iterates snapshot stores in (the host-loop
+// record kernels only; the stores' pointer checks cost the hot X kernel
+// registers)
+template <int kE, int PH, int kU = 4, bool kRec = false>
 __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal sc,
                                              double (*red)[32],
                                              const double *coef, int64_t first,
@@ -320,7 +323,7 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
         double tv = t[i];
         double rv = __dsub_rn(sv, __dmul_rn(omega, tv));
         r[i] = rv;
-        if (a.rec_x) {              // record_iterates: entry hist_len, step itn
+        if (kRec && a.rec_x) {      // record_iterates: entry hist_len, step itn
           const int64_t j = a.S->hist_len, it = a.S->itn;
           a.rec_x[j * n + i] = x[i];
           a.rec_r[j * n + i] = rv;
@@ -334,7 +337,7 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
         acc[0] = __fma_rn(bv, bv, acc[0]);
       } else if (PH == PH_INIT) {
         double rv = r[i], tv = rt0[i];
-        if (a.rec_x) {              // record_iterates: entry 0
+        if (kRec && a.rec_x) {      // record_iterates: entry 0
           a.rec_x[i] = x[i];
           a.rec_r[i] = rv;
         }

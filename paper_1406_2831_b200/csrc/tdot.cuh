@@ -14,7 +14,7 @@ namespace krb {
 // -> part[j*nb + b].
 constexpr int kTdotCG = 8;
 
-template <int kE, bool kSelf>
+template <int kE, bool kSelf, int kU = 4>
 __device__ __forceinline__ void tdot_unit(int64_t n, int64_t nb, int k,
                                           const double *__restrict__ M,
                                           int64_t ldm,
@@ -29,7 +29,7 @@ __device__ __forceinline__ void tdot_unit(int64_t n, int64_t nb, int k,
   double acc[kTdotCG];
 #pragma unroll
   for (int c = 0; c < kTdotCG; ++c) acc[c] = 0.0;
-#pragma unroll(kE < 4 ? kE : 4)
+#pragma unroll(kE < kU ? kE : kU)
   for (int e = 0; e < kE; ++e) {
     const int64_t i = base + (int64_t)kLanes * e;
     if (i < n) {
@@ -67,7 +67,7 @@ __device__ __forceinline__ void tdot_finals(int64_t nb, int k,
 }
 
 // Grid (gx, ceil(k/kTdotCG)); the last CTA to finish runs the final stage.
-template <int kE, bool kSelf, bool kSqrt = kSelf>
+template <int kE, bool kSelf, bool kSqrt = kSelf, int kU = 4>
 __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           const double *__restrict__ M,
                                           int64_t ldm,
@@ -80,7 +80,7 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
   __shared__ int last_flag;
   const int j0 = blockIdx.y * kTdotCG;
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
-    tdot_unit<kE, kSelf>(n, nb, k, M, ldm, v, part, b, j0, red, keep);
+    tdot_unit<kE, kSelf, kU>(n, nb, k, M, ldm, v, part, b, j0, red, keep);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

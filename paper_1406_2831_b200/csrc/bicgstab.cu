@@ -113,14 +113,17 @@ __global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterAr
 }
 
 // projection dots inside the iteration: Chat^T v -> zeta / gamma
-// kV (tuning "tdot_variant"): 0 = up to 64 registers, 4 elements unrolled;
-// 1 = at most 32 registers (two 1024-thread CTAs per SM), 2 elements.
+// kV (tuning "tdot_variant"): 0 = up to 64 registers, guard-free full
+// blocks with the next element's loads issued before the current fmas, 1-D
+// balanced unit ranges; 1 = at most 32 registers (two 1024-thread CTAs per
+// SM), 2 elements; 2 = round-2 baseline (4 elements unrolled behind
+// per-element guards, 2-D grid of column groups).
 template <int kE, bool kGamma, int kV>
 __global__ void __launch_bounds__(1024, kV == 1 ? 2 : 1) k_proj_dot(const IterArgs *__restrict__ pa) {
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
   ktime_start(a, kGamma ? 6 : 2);
-  tdot_body<kE, false, false, kV == 1 ? 2 : 4>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
+  tdot_body<kE, false, false, kV == 1 ? 2 : kV == 2 ? 4 : 0>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
                        kGamma ? a.gamma : a.zeta, a.counters + kCounterTdotGraph,
                        a.l2keep != 0);
   ktime_finish(a, kGamma ? 6 : 2);
@@ -135,16 +138,24 @@ __global__ void __launch_bounds__(1024, kV == 1 ? 2 : 1) k_proj_dot(const IterAr
 // 898 us for the same rows with parameters; broadcasting them through shared
 // memory costs 48 registers; a grid-stride variant with 6 x 148 CTAs:
 // 1258 us.)
-template <bool kSell, int kSlot>
+// kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32.
+template <int kF, int kSlot>
 __global__ void __launch_bounds__(256) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status,
                                                    uint64_t *__restrict__ kt) {
+  constexpr bool kSell = kF == 1;
+  __shared__ int32_t sdict[kF == 2 ? 256 : 1];
   if (*status != KRB_RUNNING) return;
   if (kt && blockIdx.x == 0 && threadIdx.x == 0)
     *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
+  if (kF == 2) stage_dict(A, sdict);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < A.n) y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
+  if (kF == 2) {
+    if (i < A.n) y[i] = spmv_row_dict(i, A, sdict, [x](int c) { return __ldg(x + c); });
+  } else if (i < A.n) {
+    y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
+  }
   if (kt) {   // per-SM end stamp (iter.cuh ktime_end_spmv)
     __syncthreads();
     if (threadIdx.x == 0)
@@ -194,6 +205,10 @@ static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st
     static int per_sm1 = occupancy_1024(k_proj_dot<16, kGamma, 1>);
     dim3 grid = tdot_grid(h.nb, h.k, per_sm1);
     KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 1><<<grid, 1024, 0, st>>>(d)));
+  } else if (tuning().tdot_variant == 2) {
+    static int per_sm2 = occupancy_1024(k_proj_dot<16, kGamma, 2>);
+    dim3 grid = tdot_grid2d(h.nb, h.k, per_sm2);
+    KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 2><<<grid, 1024, 0, st>>>(d)));
   } else {
     static int per_sm0 = occupancy_1024(k_proj_dot<16, kGamma, 0>);
     dim3 grid = tdot_grid(h.nb, h.k, per_sm0);
@@ -213,10 +228,12 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   const int *status = reinterpret_cast<const int *>(&h.S->status);
   const double *x = kSecond ? h.s : h.p;
   double *y = kSecond ? h.t : h.q;
-  if (h.A.format == 2)
-    k_iter_spmv<true, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
+  if (h.A.dcode)
+    k_iter_spmv<2, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
+  else if (h.A.format == 2)
+    k_iter_spmv<1, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
   else
-    k_iter_spmv<false, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
+    k_iter_spmv<0, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }

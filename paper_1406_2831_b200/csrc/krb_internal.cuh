@@ -19,6 +19,7 @@ struct krb_precond;
 struct krb_matrix {
   int64_t n = 0, nnz = 0;
   int format = 0;  // 1 CSR, 2 SELL
+  int req_format = 0;  // as requested at creation (the transpose follows it)
   int64_t *rp = nullptr;
   int32_t *ci = nullptr;
   double *val = nullptr;
@@ -29,6 +30,17 @@ struct krb_matrix {
   int32_t *s_col = nullptr;
   double *s_val = nullptr;
   int32_t *perm = nullptr;  // SELL-C-sigma: slice position -> row (NULL: identity)
+  // offset-coded SELL-32 (built beside s_col when the matrix has <= 255
+  // distinct diagonals col - row, i.e. stencils / banded matrices): element
+  // j of row i has col = i + dict[code]; a slice whose 32 rows share one
+  // code sequence ("uniform": interior stencil rows) stores it once
+  // (dptr = byte offset << 1 | 1, codes at dcode[off + j]), any other slice
+  // stores one byte per element, column-major like s_col (dcode[off + 32 j + l]).
+  uint8_t *dcode = nullptr;
+  int64_t *dptr = nullptr;
+  int32_t *dict = nullptr;  // 256 entries (sorted distinct offsets, zero-padded)
+  int ndict = 0;
+  int64_t dcode_bytes = 0, uniform_slices = 0;
   krb_matrix *T = nullptr;  // lazily built transpose
   int64_t bytes = 0;
   // preconditioned-operator view (precond.cu): shares `base`'s arrays; every
@@ -55,7 +67,7 @@ void dev_free(void *p, cudaStream_t st);
 // for a matrix with the same signature -- freed and re-allocated arrays can
 // come back at the address of another matrix's CSR values).
 struct MatrixSig {
-  const void *p[16];
+  const void *p[22];
   int64_t n = -1, serial = 0;
   int format = -1;
 };

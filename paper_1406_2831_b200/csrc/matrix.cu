@@ -88,8 +88,10 @@ MatrixSig matrix_sig(const krb_matrix *A) {
   const krb_matrix *B = A->base ? A->base : A;
   const void *ptrs[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val,
                         A->perm, B->rp, B->ci, B->val, B->sl_ptr, B->rlen, B->s_col,
-                        B->s_val, B->perm};
-  for (int i = 0; i < 16; ++i) g.p[i] = ptrs[i];
+                        B->s_val, B->perm, A->dcode, A->dptr, A->dict, B->dcode, B->dptr,
+                        B->dict};
+  static_assert(sizeof(ptrs) == sizeof(g.p), "MatrixSig size");
+  for (int i = 0; i < 22; ++i) g.p[i] = ptrs[i];
   g.n = A->n;
   g.format = A->format;
   g.serial = precond_serial(A->pre);
@@ -101,12 +103,26 @@ bool same_sig(const MatrixSig &a, const MatrixSig &b) {
          memcmp(a.p, b.p, sizeof(a.p)) == 0;
 }
 
+// offset-coded SELL-32 (identity row order)
+__global__ void __launch_bounds__(256) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
+                                                   double *__restrict__ y,
+                                                   const int *__restrict__ status) {
+  __shared__ int32_t sdict[256];
+  if (status && *status) return;
+  stage_dict(A, sdict);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  y[i] = spmv_row_dict(i, A, sdict, [x](int c) { return __ldg(x + c); });
+}
+
 int spmv_launch(const krb_matrix *A, const double *x, double *y,
                 const int *d_status, cudaStream_t st) {
   if (A->n == 0) return KRB_OK;
   if (A->pre) return precond_apply_op(A, x, y, d_status, st);
   int64_t blocks = (A->n + 255) / 256;
-  if (A->format == 2)
+  if (A->dcode)
+    k_spmv_dict<<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
+  else if (A->format == 2)
     k_spmv<true><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
   else
     k_spmv<false><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
@@ -120,11 +136,14 @@ int spmv_launch(const krb_matrix *A, const double *x, double *y,
 // independent sequential sums (multiply then add, from 0.0) -- so every
 // column is bit-identical to its own SpMV, while the matrix is read once per
 // group of kNC columns instead of once per column.
-template <bool kSell, int kNC>
+template <int kF, int kNC>
 __global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
                                               const double *__restrict__ X,
                                               int64_t ldx, double *__restrict__ Y,
                                               int64_t ldy) {
+  constexpr bool kSell = kF == 1;
+  __shared__ int32_t sdict[kF == 2 ? 256 : 1];
+  if (kF == 2) stage_dict(A, sdict);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
   const int c0 = blockIdx.y * kNC;
@@ -134,7 +153,22 @@ __global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
 #pragma unroll
   for (int c = 0; c < kNC; ++c) sum[c] = 0.0;
   int64_t row = i;
-  if (kSell) {
+  if (kF == 2) {
+    const int64_t s = i >> 5;
+    const int l = (int)(i & 31);
+    const int len = __ldg(A.rlen + i);
+    const int64_t base = __ldg(A.sl_ptr + s) + l;
+    const int64_t dp = __ldg(A.dptr + s);
+    const uint8_t *cp = A.dcode + (dp >> 1) + ((dp & 1) ? 0 : l);
+    const int cs = (dp & 1) ? 1 : 32;
+    for (int j = 0; j < len; ++j) {
+      const int col = (int)i + sdict[__ldg(cp + cs * j)];
+      const double v = __ldg(A.s_val + base + 32 * j);
+#pragma unroll
+      for (int c = 0; c < kNC; ++c)
+        if (c < nc) sum[c] = __dadd_rn(sum[c], __dmul_rn(v, __ldg(Xc + (int64_t)c * ldx + col)));
+    }
+  } else if (kSell) {
     if (A.perm) row = A.perm[i];
     const int len = __ldg(A.rlen + i);
     const int64_t base = __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
@@ -171,10 +205,12 @@ int spmm_launch(const krb_matrix *M, int64_t ncols, const double *X, int64_t ldx
     return KRB_OK;
   }
   dim3 grid((unsigned)((M->n + 255) / 256), (unsigned)((ncols + kNC - 1) / kNC));
-  if (M->format == 2)
-    k_spmm<true, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
+  if (M->dcode)
+    k_spmm<2, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
+  else if (M->format == 2)
+    k_spmm<1, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
   else
-    k_spmm<false, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
+    k_spmm<0, kNC><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy);
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -330,6 +366,152 @@ static int build_sell(krb_matrix *A, int format, cudaStream_t st) {
   return KRB_OK;
 }
 
+// ---- offset-coded SELL-32 (krb_internal.cuh) ------------------------------
+__global__ void k_row_offsets(int64_t n, const int64_t *__restrict__ rp,
+                              const int32_t *__restrict__ ci, int32_t *__restrict__ off) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int64_t jj = rp[i]; jj < rp[i + 1]; ++jj) off[jj] = ci[jj] - (int32_t)i;
+}
+
+__device__ __forceinline__ int dict_code(const int32_t *sd, int nd, int32_t off) {
+  int lo = 0, hi = nd - 1;   // sd sorted ascending, off present
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sd[mid] < off) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// one warp per slice: uniform (all 32 rows present, equal lengths, equal
+// offset sequences) -> code bytes = len rounded up to 32, else 32 x width
+__global__ void k_dict_classify(int64_t n, int64_t nslices, const int64_t *__restrict__ sl_ptr,
+                                const int32_t *__restrict__ rlen,
+                                const int32_t *__restrict__ s_col, int64_t *__restrict__ bytes,
+                                uint8_t *__restrict__ uni, unsigned long long *__restrict__ nuni) {
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int l = threadIdx.x & 31;
+  if (s >= nslices) return;
+  const int64_t row = s * 32 + l;
+  const int len = row < n ? rlen[row] : -1;
+  const int64_t base = sl_ptr[s];
+  const int width = (int)((sl_ptr[s + 1] - base) / 32);
+  bool ok = __all_sync(0xffffffffu, len == __shfl_sync(0xffffffffu, len, 0));
+  for (int j = 0; ok && j < len; ++j) {
+    const int32_t off = s_col[base + 32 * j + l] - (int32_t)row;
+    ok = __all_sync(0xffffffffu, off == __shfl_sync(0xffffffffu, off, 0));
+  }
+  if (l == 0) {
+    uni[s] = ok ? 1 : 0;
+    if (ok) atomicAdd(nuni, 1ull);
+    bytes[s] = ok ? (int64_t)((len + 31) / 32) * 32 : (int64_t)32 * width;
+  }
+}
+
+__global__ void k_dict_fill(int64_t n, int64_t nslices, const int64_t *__restrict__ sl_ptr,
+                            const int32_t *__restrict__ rlen, const int32_t *__restrict__ s_col,
+                            const int32_t *__restrict__ dict, int nd,
+                            const int64_t *__restrict__ cptr, const uint8_t *__restrict__ uni,
+                            uint8_t *__restrict__ code, int64_t *__restrict__ dptr) {
+  __shared__ int32_t sd[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sd[t] = dict[t];
+  __syncthreads();
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int l = threadIdx.x & 31;
+  if (s >= nslices) return;
+  const int64_t base = sl_ptr[s], cb = cptr[s];
+  const int width = (int)((sl_ptr[s + 1] - base) / 32);
+  const int64_t row = s * 32 + l;
+  if (uni[s]) {
+    const int len = rlen[s * 32];
+    for (int j = l; j < (len + 31) / 32 * 32; j += 32)
+      code[cb + j] = j < len ? (uint8_t)dict_code(sd, nd, s_col[base + 32 * j] - (int32_t)(s * 32)) : 0;
+  } else {
+    const int len = row < n ? rlen[row] : 0;
+    for (int j = 0; j < width; ++j)
+      code[cb + 32 * j + l] =
+          j < len ? (uint8_t)dict_code(sd, nd, s_col[base + 32 * j + l] - (int32_t)row) : 0;
+  }
+  if (l == 0) dptr[s] = (cb << 1) | (uni[s] ? 1 : 0);
+}
+
+// Build the offset-coded stream beside an identity-order SELL-32 matrix when
+// its entries use at most 255 distinct offsets col - row.  Leaves the matrix
+// untouched (dcode == NULL) otherwise.
+static int build_dict(krb_matrix *A, cudaStream_t st) {
+  const int64_t n = A->n, nnz = A->nnz;
+  if (A->format != 2 || A->perm || n == 0 || nnz == 0) return KRB_OK;
+  int32_t *off = nullptr, *sorted = nullptr, *uniq = nullptr;
+  int *d_num = nullptr;
+  KRB_CHECK_CUDA(dev_alloc((void **)&off, sizeof(int32_t) * nnz, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&sorted, sizeof(int32_t) * nnz, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&uniq, sizeof(int32_t) * nnz, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&d_num, sizeof(int), st));
+  k_row_offsets<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, A->rp, A->ci, off);
+  KRB_CHECK_LAUNCH();
+  void *tmp = nullptr;
+  size_t tb1 = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tb1, off, sorted, (int)nnz, 0, 32, st);
+  cub::DeviceSelect::Unique(nullptr, tb2, sorted, uniq, d_num, (int)nnz, st);
+  KRB_CHECK_CUDA(dev_alloc(&tmp, tb1 > tb2 ? tb1 : tb2, st));
+  cub::DeviceRadixSort::SortKeys(tmp, tb1, off, sorted, (int)nnz, 0, 32, st);
+  cub::DeviceSelect::Unique(tmp, tb2, sorted, uniq, d_num, (int)nnz, st);
+  KRB_CHECK_CUDA(cudaGetLastError());
+  int num = 0;
+  KRB_CHECK_CUDA(cudaMemcpyAsync(&num, d_num, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  dev_free(tmp, st);
+  dev_free(off, st);
+  dev_free(sorted, st);
+  dev_free(d_num, st);
+  if (num < 1 || num > 255) {
+    dev_free(uniq, st);
+    return KRB_OK;
+  }
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->dict, sizeof(int32_t) * 256, st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(A->dict, 0, sizeof(int32_t) * 256, st));
+  KRB_CHECK_CUDA(cudaMemcpyAsync(A->dict, uniq, sizeof(int32_t) * num,
+                                 cudaMemcpyDeviceToDevice, st));
+  A->ndict = num;
+  const int64_t ns = A->nslices;
+  int64_t *bytes = nullptr, *cptr = nullptr;
+  uint8_t *uni = nullptr;
+  KRB_CHECK_CUDA(dev_alloc((void **)&bytes, sizeof(int64_t) * (ns + 1), st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&cptr, sizeof(int64_t) * (ns + 1), st));
+  unsigned long long *nuni = nullptr;
+  KRB_CHECK_CUDA(dev_alloc((void **)&uni, ns, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&nuni, sizeof(unsigned long long), st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(bytes + ns, 0, sizeof(int64_t), st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(nuni, 0, sizeof(unsigned long long), st));
+  const unsigned wb = (unsigned)((ns * 32 + 255) / 256);
+  k_dict_classify<<<wb, 256, 0, st>>>(n, ns, A->sl_ptr, A->rlen, A->s_col, bytes, uni, nuni);
+  KRB_CHECK_LAUNCH();
+  tb1 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb1, bytes, cptr, ns + 1, st);
+  KRB_CHECK_CUDA(dev_alloc(&tmp, tb1, st));
+  cub::DeviceScan::ExclusiveSum(tmp, tb1, bytes, cptr, ns + 1, st);
+  KRB_CHECK_CUDA(cudaGetLastError());
+  int64_t total = 0;
+  KRB_CHECK_CUDA(cudaMemcpyAsync(&total, cptr + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaMemcpyAsync(&A->uniform_slices, nuni, sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  dev_free(tmp, st);
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->dcode, total > 0 ? total : 1, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->dptr, sizeof(int64_t) * ns, st));
+  k_dict_fill<<<wb, 256, 0, st>>>(n, ns, A->sl_ptr, A->rlen, A->s_col, A->dict, num, cptr, uni,
+                                  A->dcode, A->dptr);
+  KRB_CHECK_LAUNCH();
+  dev_free(bytes, st);
+  dev_free(cptr, st);
+  dev_free(uni, st);
+  dev_free(nuni, st);
+  dev_free(uniq, st);
+  A->dcode_bytes = total;
+  A->bytes += total + ns * 8 + 256 * 4;
+  return KRB_OK;
+}
+
 int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
                   const int64_t *d_rp, const int32_t *d_ci32,
                   const int64_t *d_ci64, const double *d_val, int format,
@@ -380,7 +562,11 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
                                    cudaMemcpyDeviceToDevice, st));
   }
   A->bytes = (n + 1) * 8 + nnz * 12;
-  int rc = build_sell(A, format, st);
+  // 4 = SELL-32 with the offset-coded stream (when the matrix qualifies);
+  // 2 = plain SELL-32; 0 = auto (the offset-coded stream when it qualifies)
+  A->req_format = format;
+  int rc = build_sell(A, format == 4 ? 2 : format, st);
+  if (rc == KRB_OK && (format == 0 || format == 4)) rc = build_dict(A, st);
   if (rc != KRB_OK) {
     delete A;
     return rc;
@@ -479,7 +665,8 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   dev_free(perm_out, st);
   dev_free(cnt, st);
   krb_matrix *T = nullptr;
-  int rc = matrix_create(&T, n, nnz, trp, tci, nullptr, tval, 0, st);
+  int rc = matrix_create(&T, n, nnz, trp, tci, nullptr, tval,
+                         A->req_format == 2 || A->req_format == 4 ? A->req_format : 0, st);
   dev_free(trp, st);
   dev_free(tci, st);
   dev_free(tval, st);
@@ -500,7 +687,8 @@ void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
     return;
   }
   matrix_free(A->T, async, st);
-  void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm};
+  void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm,
+                    A->dcode, A->dptr, A->dict};
   if (!async) cudaDeviceSynchronize();
   for (void *p : arrays)
     if (p) dev_free(p, async ? st : nullptr);
@@ -548,7 +736,7 @@ int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz, int *format,
   KRB_REQUIRE(A != nullptr, "krb_matrix_info: NULL matrix");
   if (n) *n = A->n;
   if (nnz) *nnz = A->nnz;
-  if (format) *format = (A->format == 2 && A->perm) ? 3 : A->format;
+  if (format) *format = (A->format == 2 && A->perm) ? 3 : (A->dcode ? 4 : A->format);
   if (bytes) *bytes = A->bytes + (A->T ? A->T->bytes : 0);
   return KRB_OK;
 }

@@ -72,4 +72,48 @@ __device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
   return spmv_row_f<kSell>(i, A, [x](int c) { return ldx<kXro>(x + c); });
 }
 
+// ---- offset-coded SELL-32 row (identity row order: i is the row) ---------
+// Same entries, same CSR order, same mul-then-add as spmv_row_f<true>; the
+// column of element j is i + sdict[code_j] with the 1-byte code read from
+// the slice's code stream (a uniform slice's stream is shared by its 32
+// lanes: one broadcast byte per element instead of 4 index bytes per lane).
+// sdict: the matrix's offset dictionary staged in shared memory.
+template <int kB = 4, class XF>
+__device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A,
+                                               const int32_t *sdict, XF xf) {
+  const int64_t s = i >> 5;
+  const int l = (int)(i & 31);
+  const int len = __ldg(A.rlen + i);
+  const double *__restrict__ vp = A.s_val + __ldg(A.sl_ptr + s) + l;
+  const int64_t dp = __ldg(A.dptr + s);
+  const bool uni = dp & 1;
+  const uint8_t *__restrict__ cp = A.dcode + (dp >> 1) + (uni ? 0 : l);
+  const int cs = uni ? 1 : 32;
+  const int row = (int)i;
+  double sum = 0.0;
+  for (int j = 0; j < len; j += kB) {
+    int c[kB];
+    double v[kB], xv[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const bool ok = j + u < len;
+      c[u] = ok ? row + sdict[__ldg(cp + cs * (j + u))] : 0;
+      v[u] = ok ? __ldg(vp + 32 * (j + u)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) xv[u] = j + u < len ? xf(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (j + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+  }
+  return sum;
+}
+
+// stage the offset dictionary (256 entries) in shared memory; every thread
+// of the CTA must call it (one barrier)
+__device__ __forceinline__ void stage_dict(const krb_matrix &A, int32_t *sdict) {
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sdict[t] = __ldg(A.dict + t);
+  __syncthreads();
+}
+
 }  // namespace krb

@@ -342,7 +342,7 @@ class DeviceMatrix:
         n_, nnz_, f_, b_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
         _lib.call("krb_matrix_info", h, ctypes.byref(n_), ctypes.byref(nnz_),
                   ctypes.byref(f_), ctypes.byref(b_))
-        self.format = {1: "csr", 2: "sell32", 3: "sell32-sigma"}.get(f_.value, "?")
+        self.format = {1: "csr", 2: "sell32", 3: "sell32-sigma", 4: "sell32-dict"}.get(f_.value, "?")
         self.device_bytes = b_.value
 
     @property

@@ -43,7 +43,7 @@ def test_spmv_bitwise_vs_reference_golden(dev, golden, name):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
-@pytest.mark.parametrize("fmt", [0, 1, 2, 3])
+@pytest.mark.parametrize("fmt", [0, 1, 2, 3, 4])
 def test_spmv_formats_bitwise(dev, canon, cfg, fmt):
     from oracle.ops import CsrOperand
     from paper_1406_2831_b200.workloads import make_sequence
@@ -55,6 +55,64 @@ def test_spmv_formats_bitwise(dev, canon, cfg, fmt):
     assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(),
                           canon.rmatvec(op, x))
     assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), op._csr @ x)
+
+
+@pytest.mark.parametrize("cfg,expect", [("c1", "sell32-dict"), ("c2", "sell32-dict"),
+                                        ("c5", "sell32-dict"), ("c3", "sell32"),
+                                        ("c4", "sell32-sigma")])
+def test_offset_coded_format_choice(dev, cfg, expect):
+    """Stencil matrices (<= 255 distinct diagonals) get the offset-coded
+    SELL-32 stream automatically, their transposes too; C3's random K1
+    columns and C4's power-law rows do not qualify."""
+    from paper_1406_2831_b200.workloads import make_sequence
+    A = make_sequence(cfg, small=True).matrix(1)
+    M = dev.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+    assert M.format == expect
+    x = np.random.default_rng(5).standard_normal(A.n)
+    S = A.to_scipy()
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), S @ x)
+    assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(), S.T.tocsr() @ x)
+    X = np.random.default_rng(6).standard_normal((A.n, 11))
+    Y = M.spmm(_cols(X)).cpu().numpy().T
+    for c in range(11):
+        assert np.array_equal(Y[:, c], S @ X[:, c])
+
+
+@pytest.mark.parametrize("n", [31, 32, 33, 95, 1000, 4099])
+def test_offset_coded_ragged_slices(dev, n):
+    """Mixed slices: banded rows with random gaps (non-uniform slices next to
+    uniform ones), empty rows, a partial last slice, 255 distinct offsets
+    (the limit) and one more (falls back to plain SELL-32)."""
+    import scipy.sparse as sp
+    r = np.random.default_rng(n)
+    offs = np.arange(-127, 128)            # 255 distinct diagonals
+    rows, cols = [], []
+    for i in range(n):
+        if i % 97 == 5:
+            continue                        # empty row
+        sel = offs if (i // 32) % 3 == 0 else offs[r.random(offs.size) < 0.3]
+        c = i + sel
+        c = c[(c >= 0) & (c < n)]
+        rows.extend([i] * c.size)
+        cols.extend(c.tolist())
+    vals = r.standard_normal(len(rows)) * np.exp(r.uniform(-6, 6, len(rows)))
+    S = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    S.sort_indices()
+    x = r.standard_normal(n)
+    M = dev.DeviceMatrix(n, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data)
+    if n > 127:
+        assert M.format == "sell32-dict"
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), S @ x)
+    assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(), S.T.tocsr() @ x)
+    # 256 distinct offsets: no dictionary
+    if n > 200:
+        S2 = S.tolil()
+        S2[n - 1, n - 1 - 200] = 1.0
+        S2 = S2.tocsr()
+        S2.sort_indices()
+        M2 = dev.DeviceMatrix(n, S2.indptr.astype(np.int64), S2.indices.astype(np.int32), S2.data)
+        assert M2.format in ("sell32", "sell32-sigma", "csr")
+        assert np.array_equal(M2.spmv(_tensor(x)).cpu().numpy(), S2 @ x)
 
 
 def test_sell_sigma_chosen_for_power_law(dev):

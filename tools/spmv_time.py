@@ -16,12 +16,13 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--transpose", action="store_true")
+    ap.add_argument("--fmt", type=int, default=0, help="0 auto, 1 CSR, 2 SELL-32, 4 offset-coded")
     a = ap.parse_args()
     import torch
     from paper_1406_2831_b200 import device as D, workloads as W
     seq = W.make_sequence(a.config)
     A = seq.matrix(0)
-    M = D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
+    M = D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=a.fmt)
     x = torch.randn(A.n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
     for _ in range(3):
@@ -38,7 +39,7 @@ def main():
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(
         os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
     print(json.dumps({"config": a.config, "format": M.format, "transpose": a.transpose,
-                      "n": A.n, "nnz": A.nnz, "us": round(us, 1),
+                      "n": A.n, "nnz": A.nnz, "device_bytes": M.device_bytes, "us": round(us, 1),
                       "GBps": round(B / us / 1e3, 1), "frac": round(B / us / 1e3 / peak, 4)}))
 
 

@@ -53,7 +53,8 @@ int64_t krb_launch_count(void);
 /* Driver / kernel-variant knobs (process-wide; every variant computes the
  * same bits).  Keys: "persist0", "p0_grid_half", "p0_onchip", "p0_prof_cta",
  * "cluster", "persist_v1", "gemm_mode", "l2keep", "phase_variant",
- * "tdot_variant".  Unknown key -> KRB_EINVAL.
+ * "tdot_variant", "spmv_variant", "spmv_prefetch_mb" (bulk L2 prefetch
+ * distance of the SELL SpMVs, default 6).  Unknown key -> KRB_EINVAL.
  * No reference counterpart (the reference has no device drivers). */
 int krb_set_tuning(const char *key, int64_t value);
 int krb_reset_tuning(void);
@@ -110,9 +111,15 @@ int krb_matrix_destroy(krb_matrix *A);
  * the work already queued on `stream`; no device-wide synchronisation.  No
  * other stream may still use the matrix. */
 int krb_matrix_destroy_async(krb_matrix *A, void *stream);
-/* n, nnz, chosen format, device bytes held (incl. transpose when built) */
+/* n, nnz, chosen format (1 CSR, 2 SELL-32, 3 SELL-C-sigma, 4 SELL-32 with
+ * offset-coded columns), device bytes held (incl. transpose when built) */
 int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz,
                     int *format, int64_t *bytes);
+/* Bytes one y = A x streams in the chosen format (matrix arrays the kernel
+ * reads + x once + y once), the SELL slice count, the uniform slices of the
+ * offset-coded format (one shared offset row) and its dictionary size. */
+int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t *nslices,
+                            int64_t *uniform_slices, int *ndict);
 
 /* y = A x  (SparseMatrix.matvec, sparse.py:117-121; scipy csr_matvec order:
  * per-row sequential sum from 0.0, separate multiply and add) */

@@ -113,17 +113,17 @@ __global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterAr
 }
 
 // projection dots inside the iteration: Chat^T v -> zeta / gamma
-// kV (tuning "tdot_variant"): 0 = up to 64 registers, guard-free full
-// blocks with the next element's loads issued before the current fmas, 1-D
-// balanced unit ranges; 1 = at most 32 registers (two 1024-thread CTAs per
-// SM), 2 elements; 2 = round-2 baseline (4 elements unrolled behind
-// per-element guards, 2-D grid of column groups).
+// kV (tuning "tdot_variant"): 0 = up to 64 registers, 4 elements unrolled;
+// 1 = at most 32 registers (two 1024-thread CTAs per SM), 2 elements.
+// (Measured dead end, C5: guard-free full blocks with the next element's
+// loads issued before the current fmas over balanced 1-D unit ranges,
+// 669 vs 632 us.)
 template <int kE, bool kGamma, int kV>
 __global__ void __launch_bounds__(1024, kV == 1 ? 2 : 1) k_proj_dot(const IterArgs *__restrict__ pa) {
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
   ktime_start(a, kGamma ? 6 : 2);
-  tdot_body<kE, false, false, kV == 1 ? 2 : kV == 2 ? 4 : 0>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
+  tdot_body<kE, false, false, kV == 1 ? 2 : 4>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
                        kGamma ? a.gamma : a.zeta, a.counters + kCounterTdotGraph,
                        a.l2keep != 0);
   ktime_finish(a, kGamma ? 6 : 2);
@@ -138,25 +138,46 @@ __global__ void __launch_bounds__(1024, kV == 1 ? 2 : 1) k_proj_dot(const IterAr
 // 898 us for the same rows with parameters; broadcasting them through shared
 // memory costs 48 registers; a grid-stride variant with 6 x 148 CTAs:
 // 1258 us.)
-// kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32.
+// kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (uniform
+// slices: offsets by warp shuffle), 3 its first version (tuning spmv_variant=1).
 template <int kF, int kSlot>
 __global__ void __launch_bounds__(256) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status,
-                                                   uint64_t *__restrict__ kt) {
+                                                   uint64_t *__restrict__ kt, int64_t pf) {
   constexpr bool kSell = kF == 1;
-  __shared__ int32_t sdict[kF == 2 ? 256 : 1];
-  if (*status != KRB_RUNNING) return;
-  if (kt && blockIdx.x == 0 && threadIdx.x == 0)
-    *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
-  if (kF == 2) stage_dict(A, sdict);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (kF == 2) {
-    if (i < A.n) y[i] = spmv_row_dict(i, A, sdict, [x](int c) { return __ldg(x + c); });
-  } else if (i < A.n) {
-    y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
+  if (kF >= 2) {
+    // the status word is consumed only at the store (no dependent round
+    // trip before the first matrix load of every CTA); after a half-step
+    // exit (status set by S) the product of a finished solve is discarded
+    const int run = __ldg(status);
+    if (kt && blockIdx.x == 0 && threadIdx.x == 0 && run == KRB_RUNNING)
+      *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
+    if (i < A.n) {
+      const double yi = spmv_row_dict<kF == 2 ? 0 : 1>(i, A, [x](int c) { return __ldg(x + c); }, pf);
+      if (run == KRB_RUNNING) y[i] = yi;
+    }
+    if (run != KRB_RUNNING) return;
+  } else {
+    if (*status != KRB_RUNNING) return;
+    if (kt && blockIdx.x == 0 && threadIdx.x == 0)
+      *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
+    if (kSell && pf > 0 && (threadIdx.x & 31) == 0 && i < A.n) {
+      // bulk L2 prefetch of the slice a later wave streams (values, columns)
+      const int64_t s = i >> 5, b0 = __ldg(A.sl_ptr + s), w = __ldg(A.sl_ptr + s + 1) - b0;
+      const int64_t at = b0 + pf / 12;
+      if (w > 0 && at + w <= A.sell_elems) {
+        prefetch_l2_bulk(A.s_val + at, (uint32_t)(8 * w));
+        prefetch_l2_bulk(A.s_col + at, (uint32_t)(4 * w));
+      }
+    }
+    if (i < A.n) y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
   }
-  if (kt) {   // per-SM end stamp (iter.cuh ktime_end_spmv)
+  if (kt && blockIdx.x + 4096u >= gridDim.x) {
+    // per-SM end stamp (iter.cuh ktime_end_spmv), from the CTAs of the last
+    // ~4 waves only (the kernel's end is among them; an atomic from every
+    // one of 65536 CTAs cost ~2 % of the iteration)
     __syncthreads();
     if (threadIdx.x == 0)
       atomicMax((unsigned long long *)&kt[kKtSpmvBase + kKtSmSlots * (kSlot == 5 ? 1 : 0) + smid()],
@@ -205,10 +226,6 @@ static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st
     static int per_sm1 = occupancy_1024(k_proj_dot<16, kGamma, 1>);
     dim3 grid = tdot_grid(h.nb, h.k, per_sm1);
     KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 1><<<grid, 1024, 0, st>>>(d)));
-  } else if (tuning().tdot_variant == 2) {
-    static int per_sm2 = occupancy_1024(k_proj_dot<16, kGamma, 2>);
-    dim3 grid = tdot_grid2d(h.nb, h.k, per_sm2);
-    KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 2><<<grid, 1024, 0, st>>>(d)));
   } else {
     static int per_sm0 = occupancy_1024(k_proj_dot<16, kGamma, 0>);
     dim3 grid = tdot_grid(h.nb, h.k, per_sm0);
@@ -228,12 +245,15 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   const int *status = reinterpret_cast<const int *>(&h.S->status);
   const double *x = kSecond ? h.s : h.p;
   double *y = kSecond ? h.t : h.q;
-  if (h.A.dcode)
-    k_iter_spmv<2, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
+  const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
+  if (h.A.dcode && tuning().spmv_variant == 1)
+    k_iter_spmv<3, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+  else if (h.A.dcode)
+    k_iter_spmv<2, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.format == 2)
-    k_iter_spmv<1, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
+    k_iter_spmv<1, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else
-    k_iter_spmv<0, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime);
+    k_iter_spmv<0, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
   KRB_CHECK_LAUNCH();
   return KRB_OK;
 }
@@ -462,7 +482,9 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
   const MatrixSig sig = matrix_sig(A);
   const bool hit = graph && G.exec && G.n == n && G.k == k && same_sig(G.sig, sig) &&
                    G.ktime == cfg->d_kernel_times &&
-                   G.variant == tuning().phase_variant + 16 * tuning().tdot_variant;
+                   G.variant == tuning().phase_variant + 16 * tuning().tdot_variant +
+                                    256 * tuning().spmv_variant +
+                                    4096 * tuning().spmv_prefetch_mb;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -480,7 +502,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     KRB_TRY(build_graph(ctx, h, d, capture_stream()));
     G.n = n; G.k = k; G.format = A->format; G.sig = sig;
     G.ktime = cfg->d_kernel_times;
-    G.variant = tuning().phase_variant + 16 * tuning().tdot_variant;
+    G.variant = tuning().phase_variant + 16 * tuning().tdot_variant +
+                256 * tuning().spmv_variant + 4096 * tuning().spmv_prefetch_mb;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

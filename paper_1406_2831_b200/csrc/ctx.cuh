@@ -93,14 +93,15 @@ struct Tuning {
   int gemm_mode = -1;     // krb_gemm: 0 row kernel, 8 / 12 / 24 / 122 tiled
   int l2keep = -1;        // evict_last policy on the recycle blocks
   int phase_variant = 0;  // graph phase kernels: 0 tuned per phase, 1 uniform (round 1)
-  int tdot_variant = 0;   // graph projection dots: 0 pipelined, 1 <= 32 regs, 2 round-2 baseline
+  int tdot_variant = 0;   // graph projection dots: 0 <= 64 regs, 1 <= 32 regs
+  int spmv_prefetch_mb = 6;  // SELL SpMVs: bulk L2 prefetch distance ahead (MB, 0 = off)
+  int spmv_variant = 0;   // offset-coded SpMV: 0 = uniform offsets by warp shuffle, 1 = int4 loads
 };
 Tuning &tuning();
 
 int ctx_reserve_part(krb_context *ctx, size_t doubles);
 int ctx_reserve_counters(krb_context *ctx, cudaStream_t st);
 dim3 tdot_grid(int64_t nb, int64_t k, int per_sm);
-dim3 tdot_grid2d(int64_t nb, int64_t k, int per_sm);
 // resident 1024-thread CTAs per SM of a kernel (>= 1)
 template <class K>
 int occupancy_1024(K kernel) {

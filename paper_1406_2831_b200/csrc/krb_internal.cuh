@@ -308,6 +308,12 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
   return p;
 }
 
+// bulk L2 prefetch (TMA unit; no registers, no completion tracking):
+// 16-byte aligned address, size a multiple of 16
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -24,6 +24,7 @@
 
 #include "krb_internal.cuh"
 #include "spmv.cuh"
+#include "ctx.cuh"
 
 
 namespace krb {
@@ -104,15 +105,14 @@ bool same_sig(const MatrixSig &a, const MatrixSig &b) {
 }
 
 // offset-coded SELL-32 (identity row order)
+template <int kV>
 __global__ void __launch_bounds__(256) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
-                                                   const int *__restrict__ status) {
-  __shared__ int32_t sdict[256];
+                                                   const int *__restrict__ status, int64_t pf) {
   if (status && *status) return;
-  stage_dict(A, sdict);
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
-  y[i] = spmv_row_dict(i, A, sdict, [x](int c) { return __ldg(x + c); });
+  y[i] = spmv_row_dict<kV>(i, A, [x](int c) { return __ldg(x + c); }, pf);
 }
 
 int spmv_launch(const krb_matrix *A, const double *x, double *y,
@@ -120,8 +120,11 @@ int spmv_launch(const krb_matrix *A, const double *x, double *y,
   if (A->n == 0) return KRB_OK;
   if (A->pre) return precond_apply_op(A, x, y, d_status, st);
   int64_t blocks = (A->n + 255) / 256;
-  if (A->dcode)
-    k_spmv_dict<<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
+  const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
+  if (A->dcode && tuning().spmv_variant == 1)
+    k_spmv_dict<1><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, pf);
+  else if (A->dcode)
+    k_spmv_dict<0><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, pf);
   else if (A->format == 2)
     k_spmv<true><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status);
   else
@@ -142,8 +145,6 @@ __global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
                                               int64_t ldx, double *__restrict__ Y,
                                               int64_t ldy) {
   constexpr bool kSell = kF == 1;
-  __shared__ int32_t sdict[kF == 2 ? 256 : 1];
-  if (kF == 2) stage_dict(A, sdict);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
   const int c0 = blockIdx.y * kNC;
@@ -159,10 +160,11 @@ __global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
     const int len = __ldg(A.rlen + i);
     const int64_t base = __ldg(A.sl_ptr + s) + l;
     const int64_t dp = __ldg(A.dptr + s);
-    const uint8_t *cp = A.dcode + (dp >> 1) + ((dp & 1) ? 0 : l);
-    const int cs = (dp & 1) ? 1 : 32;
+    const bool uni = dp & 1;
+    const uint8_t *cp = A.dcode + (dp >> 1) + (uni ? 0 : l);
     for (int j = 0; j < len; ++j) {
-      const int col = (int)i + sdict[__ldg(cp + cs * j)];
+      const int col = (int)i + (uni ? __ldg(reinterpret_cast<const int32_t *>(cp) + j)
+                                    : __ldg(A.dict + __ldg(cp + 32 * j)));
       const double v = __ldg(A.s_val + base + 32 * j);
 #pragma unroll
       for (int c = 0; c < kNC; ++c)
@@ -384,7 +386,8 @@ __device__ __forceinline__ int dict_code(const int32_t *sd, int nd, int32_t off)
 }
 
 // one warp per slice: uniform (all 32 rows present, equal lengths, equal
-// offset sequences) -> code bytes = len rounded up to 32, else 32 x width
+// offset sequences) -> one int32 offset row (4 len bytes rounded up to 32),
+// else one code byte per element (32 x width)
 __global__ void k_dict_classify(int64_t n, int64_t nslices, const int64_t *__restrict__ sl_ptr,
                                 const int32_t *__restrict__ rlen,
                                 const int32_t *__restrict__ s_col, int64_t *__restrict__ bytes,
@@ -404,7 +407,7 @@ __global__ void k_dict_classify(int64_t n, int64_t nslices, const int64_t *__res
   if (l == 0) {
     uni[s] = ok ? 1 : 0;
     if (ok) atomicAdd(nuni, 1ull);
-    bytes[s] = ok ? (int64_t)((len + 31) / 32) * 32 : (int64_t)32 * width;
+    bytes[s] = ok ? (int64_t)((len + 7) / 8) * 32 : (int64_t)32 * width;
   }
 }
 
@@ -424,8 +427,9 @@ __global__ void k_dict_fill(int64_t n, int64_t nslices, const int64_t *__restric
   const int64_t row = s * 32 + l;
   if (uni[s]) {
     const int len = rlen[s * 32];
-    for (int j = l; j < (len + 31) / 32 * 32; j += 32)
-      code[cb + j] = j < len ? (uint8_t)dict_code(sd, nd, s_col[base + 32 * j] - (int32_t)(s * 32)) : 0;
+    int32_t *orow = reinterpret_cast<int32_t *>(code + cb);
+    for (int j = l; j < (len + 7) / 8 * 8; j += 32)
+      orow[j] = j < len ? s_col[base + 32 * j] - (int32_t)(s * 32) : 0;
   } else {
     const int len = row < n ? rlen[row] : 0;
     for (int j = 0; j < width; ++j)
@@ -738,6 +742,24 @@ int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz, int *format,
   if (nnz) *nnz = A->nnz;
   if (format) *format = (A->format == 2 && A->perm) ? 3 : (A->dcode ? 4 : A->format);
   if (bytes) *bytes = A->bytes + (A->T ? A->T->bytes : 0);
+  return KRB_OK;
+}
+
+int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t *nslices,
+                            int64_t *uniform_slices, int *ndict) {
+  KRB_REQUIRE(A != nullptr, "krb_matrix_stream_stats: NULL matrix");
+  const krb_matrix *B = A->base ? A->base : A;
+  int64_t b = 16 * B->n;   // x read once, y written once
+  if (B->dcode)
+    b += 8 * B->sell_elems + B->dcode_bytes + 4 * B->n + 16 * B->nslices + 1024;
+  else if (B->format == 2)
+    b += 12 * B->sell_elems + 4 * B->n + 8 * (B->nslices + 1) + (B->perm ? 4 * B->n : 0);
+  else
+    b += 12 * B->nnz + 8 * (B->n + 1);
+  if (stream_bytes) *stream_bytes = b;
+  if (nslices) *nslices = B->format == 2 ? B->nslices : 0;
+  if (uniform_slices) *uniform_slices = B->uniform_slices;
+  if (ndict) *ndict = B->ndict;
   return KRB_OK;
 }
 

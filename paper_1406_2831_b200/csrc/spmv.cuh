@@ -73,33 +73,73 @@ __device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
 }
 
 // ---- offset-coded SELL-32 row (identity row order: i is the row) ---------
-// Same entries, same CSR order, same mul-then-add as spmv_row_f<true>; the
-// column of element j is i + sdict[code_j] with the 1-byte code read from
-// the slice's code stream (a uniform slice's stream is shared by its 32
-// lanes: one broadcast byte per element instead of 4 index bytes per lane).
-// sdict: the matrix's offset dictionary staged in shared memory.
-template <int kB = 4, class XF>
-__device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A,
-                                               const int32_t *sdict, XF xf) {
+// Same entries, same CSR order, same mul-then-add as spmv_row_f<true>; only
+// the column of element j is encoded differently: a uniform slice (its 32
+// rows share one offset sequence: interior stencil rows) keeps ONE row of
+// int32 offsets col - row for all its lanes (16-byte broadcast loads, 4
+// elements each); any other slice keeps one code byte per element,
+// column-major like s_col, decoded through the matrix's offset dictionary
+// (1 KB, L1-resident).  No shared-memory staging, no CTA barrier.
+// Uniform slice: lane l loads entry l (l + 32, ...) of the shared offset row
+// with one coalesced load per 32 entries and the entries reach every lane by
+// warp shuffles -- no dependent memory round trip before each batch's
+// gathers (all 32 lanes of a uniform slice exist and share the trip count).
+// kV = 1: round-2 first version (the 4 offsets of each batch loaded by every
+// lane as one int4 broadcast, tuning spmv_variant=1).
+// pf > 0: lane 0 of each warp bulk-prefetches into L2 the value bytes pf
+// beyond its own slice (the slices a later wave will stream).
+template <int kV = 0, class XF>
+__device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A, XF xf,
+                                               int64_t pf = 0) {
+  constexpr int kB = 4;
   const int64_t s = i >> 5;
   const int l = (int)(i & 31);
   const int len = __ldg(A.rlen + i);
-  const double *__restrict__ vp = A.s_val + __ldg(A.sl_ptr + s) + l;
+  const int64_t vbase = __ldg(A.sl_ptr + s);
+  const double *__restrict__ vp = A.s_val + vbase + l;
+  if (pf > 0 && l == 0) {
+    const int64_t at = vbase + pf / 8, nb = 256 * (int64_t)len;
+    if (at + nb / 8 <= A.sell_elems && nb > 0) prefetch_l2_bulk(A.s_val + at, (uint32_t)nb);
+  }
   const int64_t dp = __ldg(A.dptr + s);
   const bool uni = dp & 1;
   const uint8_t *__restrict__ cp = A.dcode + (dp >> 1) + (uni ? 0 : l);
-  const int cs = uni ? 1 : 32;
   const int row = (int)i;
   double sum = 0.0;
+  if (uni && kV == 0) {
+    const int32_t *__restrict__ orow = reinterpret_cast<const int32_t *>(cp);
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      const int mine = j0 + l < len ? __ldg(orow + j0 + l) : 0;
+      const int m = min(32, len - j0);
+      for (int j = 0; j < m; j += kB) {
+        int c[kB];
+        double v[kB], xv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) c[u] = row + __shfl_sync(0xffffffffu, mine, (j + u) & 31);
+#pragma unroll
+        for (int u = 0; u < kB; ++u) v[u] = j + u < m ? __ldg(vp + 32 * (j0 + j + u)) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kB; ++u) xv[u] = j + u < m ? xf(c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (j + u < m) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+      }
+    }
+    return sum;
+  }
   for (int j = 0; j < len; j += kB) {
     int c[kB];
     double v[kB], xv[kB];
+    if (uni) {
+      const int4 o = __ldg(reinterpret_cast<const int4 *>(cp) + (j >> 2));
+      c[0] = row + o.x; c[1] = row + o.y; c[2] = row + o.z; c[3] = row + o.w;
+    } else {
 #pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      const bool ok = j + u < len;
-      c[u] = ok ? row + sdict[__ldg(cp + cs * (j + u))] : 0;
-      v[u] = ok ? __ldg(vp + 32 * (j + u)) : 0.0;
+      for (int u = 0; u < kB; ++u)
+        c[u] = j + u < len ? row + __ldg(A.dict + __ldg(cp + 32 * (j + u))) : 0;
     }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) v[u] = j + u < len ? __ldg(vp + 32 * (j + u)) : 0.0;
 #pragma unroll
     for (int u = 0; u < kB; ++u) xv[u] = j + u < len ? xf(c[u]) : 0.0;
 #pragma unroll
@@ -107,13 +147,6 @@ __device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A,
       if (j + u < len) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
   }
   return sum;
-}
-
-// stage the offset dictionary (256 entries) in shared memory; every thread
-// of the CTA must call it (one barrier)
-__device__ __forceinline__ void stage_dict(const krb_matrix &A, int32_t *sdict) {
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) sdict[t] = __ldg(A.dict + t);
-  __syncthreads();
 }
 
 }  // namespace krb

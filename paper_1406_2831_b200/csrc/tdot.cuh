@@ -29,47 +29,18 @@ __device__ __forceinline__ void tdot_unit(int64_t n, int64_t nb, int k,
   double acc[kTdotCG];
 #pragma unroll
   for (int c = 0; c < kTdotCG; ++c) acc[c] = 0.0;
-  if (kU == 0 && nj == kTdotCG && (b + 1) * ((int64_t)kLanes * kE) <= n) {
-    // full block, full column group: no per-element guards, the loads of
-    // element e + 1 are issued before the fmas of element e (two elements'
-    // 9 loads in flight per thread; same per-lane fma chain)
-    const double *__restrict__ Mj = M + (int64_t)j0 * ldm + base;
-    double m[kTdotCG], vi = 0.0;
+#pragma unroll(kE < kU ? kE : kU)
+  for (int e = 0; e < kE; ++e) {
+    const int64_t i = base + (int64_t)kLanes * e;
+    if (i < n) {
+      const double vi = kSelf ? 0.0 : v[i];
+      double m[kTdotCG];
 #pragma unroll
-    for (int c = 0; c < kTdotCG; ++c) m[c] = ldg_pol(Mj + (int64_t)c * ldm, pol);
-    if (!kSelf) vi = v[base];
+      for (int c = 0; c < kTdotCG; ++c)
+        m[c] = c < nj ? ldg_pol(M + (int64_t)(j0 + c) * ldm + i, pol) : 0.0;
 #pragma unroll
-    for (int e = 0; e < kE; ++e) {
-      double mn[kTdotCG], vn = 0.0;
-      if (e + 1 < kE) {
-#pragma unroll
-        for (int c = 0; c < kTdotCG; ++c)
-          mn[c] = ldg_pol(Mj + (int64_t)c * ldm + (int64_t)kLanes * (e + 1), pol);
-        if (!kSelf) vn = v[base + (int64_t)kLanes * (e + 1)];
-      }
-#pragma unroll
-      for (int c = 0; c < kTdotCG; ++c) acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
-      if (e + 1 < kE) {
-#pragma unroll
-        for (int c = 0; c < kTdotCG; ++c) m[c] = mn[c];
-        vi = vn;
-      }
-    }
-  } else {
-    constexpr int kUU = kU == 0 ? 4 : kU;
-#pragma unroll(kE < kUU ? kE : kUU)
-    for (int e = 0; e < kE; ++e) {
-      const int64_t i = base + (int64_t)kLanes * e;
-      if (i < n) {
-        const double vi = kSelf ? 0.0 : v[i];
-        double m[kTdotCG];
-#pragma unroll
-        for (int c = 0; c < kTdotCG; ++c)
-          m[c] = c < nj ? ldg_pol(M + (int64_t)(j0 + c) * ldm + i, pol) : 0.0;
-#pragma unroll
-        for (int c = 0; c < kTdotCG; ++c)
-          acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
-      }
+      for (int c = 0; c < kTdotCG; ++c)
+        acc[c] = __fma_rn(m[c], kSelf ? m[c] : vi, acc[c]);
     }
   }
   int col;
@@ -95,12 +66,7 @@ __device__ __forceinline__ void tdot_finals(int64_t nb, int k,
   }
 }
 
-// Work units (block b, column group g) in the order u = b * ng + g; CTA c of
-// a 1-D grid takes the contiguous range [c U / G, (c+1) U / G) -- every CTA
-// gets the same number of units (+-1) and the same mix of full and short
-// column groups, and the groups of one block run back to back (v's block is
-// re-read from L1 / L2).  A legacy 2-D grid (gx, ng) strides blocks per
-// group.  The last CTA to finish runs the final stage.
+// Grid (gx, ceil(k/kTdotCG)); the last CTA to finish runs the final stage.
 template <int kE, bool kSelf, bool kSqrt = kSelf, int kU = 4>
 __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           const double *__restrict__ M,
@@ -112,17 +78,9 @@ __device__ __forceinline__ void tdot_body(int64_t n, int64_t nb, int k,
                                           bool keep = false) {
   __shared__ double red[kTdotCG][32];
   __shared__ int last_flag;
-  if (gridDim.y == 1) {
-    const int64_t ng = (k + kTdotCG - 1) / kTdotCG, U = nb * ng, G = gridDim.x;
-    const int64_t u1 = (blockIdx.x + 1) * U / G;
-    for (int64_t u = blockIdx.x * U / G; u < u1; ++u)
-      tdot_unit<kE, kSelf, kU>(n, nb, k, M, ldm, v, part, u / ng, (int)(u % ng) * kTdotCG,
-                               red, keep);
-  } else {
-    const int j0 = blockIdx.y * kTdotCG;
-    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
-      tdot_unit<kE, kSelf, kU>(n, nb, k, M, ldm, v, part, b, j0, red, keep);
-  }
+  const int j0 = blockIdx.y * kTdotCG;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
+    tdot_unit<kE, kSelf, kU>(n, nb, k, M, ldm, v, part, b, j0, red, keep);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -720,18 +720,7 @@ int launch_final(int ndots, int64_t nb, const double *part, double *out,
 // CTA waits for a second wave.  (2 per SM assumed before; with 42-64
 // registers only one 1024-thread CTA fits, so half the grid ran as a second
 // wave that re-read v from DRAM.)
-// 1-D grid over the (block, column group) units (tdot_body's balanced
-// contiguous ranges): one wave of resident CTAs
 dim3 tdot_grid(int64_t nb, int64_t k, int per_sm) {
-  int64_t units = nb * ((k + kTdotCG - 1) / kTdotCG);
-  int64_t g = (int64_t)kNumSMs * (per_sm > 0 ? per_sm : 1);
-  if (g > units) g = units;
-  if (g < 1) g = 1;
-  return dim3((unsigned)g, 1);
-}
-
-// round-1 2-D grid (gx, column groups), kept for A/B (tuning tdot_variant=2)
-dim3 tdot_grid2d(int64_t nb, int64_t k, int per_sm) {
   int64_t gy = (k + kTdotCG - 1) / kTdotCG;
   int64_t want = (int64_t)kNumSMs * (per_sm > 0 ? per_sm : 1);
   int64_t gx = (want + gy - 1) / gy;

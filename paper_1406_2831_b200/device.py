@@ -344,6 +344,12 @@ class DeviceMatrix:
                   ctypes.byref(f_), ctypes.byref(b_))
         self.format = {1: "csr", 2: "sell32", 3: "sell32-sigma", 4: "sell32-dict"}.get(f_.value, "?")
         self.device_bytes = b_.value
+        sb, ns, nu, nd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        _lib.call("krb_matrix_stream_stats", h, ctypes.byref(sb), ctypes.byref(ns),
+                  ctypes.byref(nu), ctypes.byref(nd))
+        # bytes one SpMV streams in this format; slice statistics
+        self.stream_bytes = sb.value
+        self.stream_stats = {"nslices": ns.value, "uniform_slices": nu.value, "ndict": nd.value}
 
     @property
     def shape(self):

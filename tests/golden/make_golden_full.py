@@ -123,7 +123,28 @@ VARIANTS = {"vexact": _exact_dot,
                                                 for i in range(0, len(a), 97)))}
 
 
-def solver_cases(out, name, systems):
+def _blocked_dot(B):
+    """Partial sums over consecutive blocks of B elements, added in order:
+    the order a BLAS splitting the vector over n / B threads (or cache
+    blocks) gives -- the thread-count family generalised to any split."""
+    def dot(a, b):
+        a = np.asarray(a, dtype=np.float64).ravel()
+        b = np.asarray(b, dtype=np.float64).ravel()
+        m = len(a) // B
+        head = np.einsum("ij,ij->i", a[:m * B].reshape(m, B), b[:m * B].reshape(m, B))
+        tail = np.dot(a[m * B:], b[m * B:])
+        return np.float64((np.cumsum(head)[-1] if m else 0.0) + tail)
+    return dot
+
+
+def random_block_variants(n, count=16, seed=2024):
+    """count block sizes log-uniform in [64, n / 2] (seeded)."""
+    r = np.random.default_rng(seed)
+    Bs = np.unique(np.exp(r.uniform(np.log(64), np.log(n / 2), count)).astype(int))
+    return {f"vb{int(B)}": _blocked_dot(int(B)) for B in Bs}
+
+
+def solver_cases(out, name, systems, only_random=False):
     seq = W.make_sequence(name)
     for j in systems:
         A = seq.matrix(j)
@@ -136,6 +157,9 @@ def solver_cases(out, name, systems):
         import krecycle.solvers as KS
         runs = [(f"t{th}", th, None) for th in THREADS] + \
                [(v, 1, f) for v, f in VARIANTS.items()]
+        rb = random_block_variants(A.n)
+        out[f"meta/rblock/{name}/{j}"] = np.asarray(list(rb))
+        runs = ([] if only_random else runs) + [(v, 1, f) for v, f in rb.items()]
         for tag, th, dotf in runs:
             t0 = time.time()
             if dotf is not None:
@@ -269,6 +293,8 @@ def ilutp_driver_cases(out, tag, seq, threads=(1, 2, 4, 8)):
 GROUPS = {
     "c1": lambda out: solver_cases(out, "c1", range(6)),
     "c2": lambda out: solver_cases(out, "c2", (0, 5, 9)),
+    "c1rb": lambda out: solver_cases(out, "c1", range(6), only_random=True),
+    "c2rb": lambda out: solver_cases(out, "c2", (0, 5, 9), only_random=True),
     "policy": lambda out: (policy_cases(out, "c1"), policy_cases(out, "c2")),
     "driver": lambda out: (driver_cases(out, "c1", W.make_sequence("c1")),
                            driver_cases(out, "c2s", W.make_sequence("c2", small=True))),

@@ -64,10 +64,15 @@ def threads(G):
 
 def run_tags(G, prefix):
     """Every stored valid run of the reference for a case: its BLAS thread
-    counts and the alternative dot orders (make_golden_full.py VARIANTS)."""
+    counts, the alternative dot orders (make_golden_full.py VARIANTS) and the
+    seeded random block splits (random_block_variants: the thread-count
+    family generalised to any split of the vectors)."""
     tags = [f"t{t}" for t in threads(G)]
     if "meta/variants" in G:
         tags += [str(v) for v in G["meta/variants"]]
+    parts = prefix.split("/")
+    if len(parts) >= 3 and f"meta/rblock/{parts[1]}/{parts[2]}" in G:
+        tags += [str(v) for v in G[f"meta/rblock/{parts[1]}/{parts[2]}"]]
     return [tg for tg in tags if f"{prefix}/{tg}/resid51" in G]
 
 
@@ -77,29 +82,54 @@ def reldiff(a, b, m=51):
     return float(np.max(np.abs(a[:L] - b[:L]) / b[:L])) if L else 0.0
 
 
-def envelope(G, prefix):
-    """The reference's own spread over its valid runs (thread counts and
-    alternative dot orders): the largest pairwise history difference."""
-    runs = {tg: G[f"{prefix}/{tg}/resid51"] for tg in run_tags(G, prefix)}
+def spread(runs, m=51):
     ts = list(runs)
     S = 0.0
     for i, a in enumerate(ts):
         for b in ts[i + 1:]:
-            S = max(S, reldiff(runs[a], runs[b]), reldiff(runs[b], runs[a]))
-    mv = [int(G[f"{prefix}/{t}/matvecs"]) for t in ts]
-    st = {str(G[f"{prefix}/{t}/status"]) for t in ts}
-    return runs, S, mv, st
+            S = max(S, reldiff(runs[a], runs[b], m), reldiff(runs[b], runs[a], m))
+    return S
+
+
+# Beyond this relative spread the reference's own valid runs are
+# decorrelated: a history comparison there measures chaos, not parity.
+CHAOS = 1e-2
+
+
+def envelope(G, prefix):
+    """The reference's own spread over its valid runs (thread counts,
+    alternative dot orders, random block splits): the largest pairwise
+    history difference over the first 50 iterations; the window m* <= 51
+    over which the runs stay correlated (spread < CHAOS) and the spread
+    there."""
+    runs = {tg: G[f"{prefix}/{tg}/resid51"] for tg in run_tags(G, prefix)}
+    S = spread(runs)
+    m = 51
+    while m > 1 and spread(runs, m) >= CHAOS:
+        m -= 1
+    mv = [int(G[f"{prefix}/{t}/matvecs"]) for t in runs]
+    st = {str(G[f"{prefix}/{t}/status"]) for t in runs}
+    return runs, S, mv, st, m, spread(runs, m)
 
 
 def check(h, G, prefix, tol, label):
-    runs, S, mv, st = envelope(G, prefix)
+    runs, S, mv, st, m, Sm = envelope(G, prefix)
     dev = reldiff(h.resid, runs["t1"])
-    bar = max(1e-8, S)
     lo, hi = min(mv) * 0.98, max(mv) * 1.02
     print(f"\n{label}: gpu {h.iterations} its / {h.total_matvecs} mv ({h.status}); "
-          f"reference mv {min(mv)}..{max(mv)}; history dev vs ref@1 {dev:.2e}, "
-          f"reference spread {S:.2e}, bar {bar:.2e}")
-    assert dev <= bar, (label, dev, bar)
+          f"reference mv {min(mv)}..{max(mv)} over {len(runs)} valid runs; history dev vs "
+          f"ref@1 {dev:.2e}, reference spread {S:.2e}")
+    if S < CHAOS:
+        bar = max(1e-8, S)
+        assert dev <= bar, (label, dev, bar)
+    else:
+        # the reference's runs decorrelate inside the first 50 iterations:
+        # the history is compared over the window where they still agree
+        devm = reldiff(h.resid, runs["t1"], m)
+        bar = max(1e-8, Sm)
+        print(f"   chaotic: reference runs agree to {Sm:.2e} over the first {m} entries; "
+              f"gpu dev there {devm:.2e}")
+        assert devm <= bar, (label, m, devm, bar)
     assert lo <= h.total_matvecs <= hi, (label, h.total_matvecs, mv)
     conv = "converged" in st
     assert (h.status == "converged") == conv or h.status in st, (label, h.status, st)

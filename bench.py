@@ -247,13 +247,30 @@ def roofline_from_ktime(wl, kt, t_total):
     b = kernel_bytes(dom, wl.n, wl.nnz, wl.k)
     ach = b / (ns / cnt)            # bytes / ns = GB/s
     traffic, tsrc = _traffic(wl.name, dom)
-    return {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak,
+    roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak,
             "peak_source": src, "unit": "GB/s", "frac": round(ach / peak, 4),
             "traffic": traffic, "traffic_source": tsrc,
             "bytes_per_launch": b, "launch_us": round(ns / cnt / 1e3, 2),
             "launches": cnt, "share_of_step": shares[dom]["share"],
             "timing": "live: CTA 0 start -> last CTA end (%globaltimer) of every "
-                      "launch inside the timed steps"}, shares
+                      "launch inside the timed steps"}
+    sb = getattr(wl, "spmv_stream_bytes", None)
+    if sb and "k_iter_spmv" in shares:
+        sp = shares["k_iter_spmv (q = A p, t = A s)"]
+        st = sb / (sp["avg_us"] * 1e3)
+        sp.update({"format": wl.spmv_format, "stream_bytes_per_launch": sb,
+                   "GBps_stream": round(st, 1), "frac_stream": round(st / peak, 4)})
+        if dom.startswith("k_iter_spmv"):
+            roof.update({
+                "format": wl.spmv_format, "format_stats": wl.spmv_stream_stats,
+                "stream_bytes_per_launch": sb, "achieved_stream": round(st, 1),
+                "frac_stream": round(st / peak, 4),
+                "note": "bytes_per_launch = SURVEY §8(d) algorithmic SpMV bytes "
+                        "(12 nnz + 4 (n+1) + 16 n: int32 column indices); the "
+                        "offset-coded SELL-32 format streams fewer (values + 1-byte "
+                        "codes / shared offset rows): stream_bytes_per_launch, "
+                        "frac_stream"})
+    return roof, shares
 
 
 # ---------------------------------------------------------------------------
@@ -274,6 +291,8 @@ def gpu_arm(args, wl, rank, world):
     i0 = wl.keys[0][0]
     A0 = wl.mats[i0]
     M0 = D.DeviceMatrix(A0.n, A0.row_ptr, A0.col_idx, A0.values, uploaded=up[i0])
+    wl.spmv_format, wl.spmv_stream_bytes = M0.format, M0.stream_bytes
+    wl.spmv_stream_stats = M0.stream_stats
     space0 = P.biorthonormalize(wl.U0, wl.Ut0, M0)
     del M0
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 1 GB > L2

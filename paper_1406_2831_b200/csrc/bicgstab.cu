@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterAr
 
 // projection dots inside the iteration: Chat^T v -> zeta / gamma
 // kV (tuning "tdot_variant"): 0 = up to 64 registers, 4 elements unrolled;
-// 1 = at most 32 registers (two 1024-thread CTAs per SM), 2 elements.
+// 1 = at most 32 registers (two 1024-thread CTAs per SM), 2 elements;
+// 3 = as 0 in groups of 4 columns over a 1-D grid of balanced unit ranges
+// (automatic below kTdotSmallNb blocks: C3 256 blocks, 102 -> see DESIGN).
 // (Measured dead end, C5: guard-free full blocks with the next element's
 // loads issued before the current fmas over balanced 1-D unit ranges,
 // 669 vs 632 us.)
@@ -123,11 +125,13 @@ __global__ void __launch_bounds__(1024, kV == 1 ? 2 : 1) k_proj_dot(const IterAr
   const IterArgs &a = *pa;
   if (a.S->status != KRB_RUNNING) return;
   ktime_start(a, kGamma ? 6 : 2);
-  tdot_body<kE, false, false, kV == 1 ? 2 : 4>(a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part,
-                       kGamma ? a.gamma : a.zeta, a.counters + kCounterTdotGraph,
-                       a.l2keep != 0);
+  tdot_body<kE, false, false, kV == 1 ? 2 : 4, kV == 3 ? 4 : kTdotCG>(
+      a.n, a.nb, a.k, a.Chat, a.ld, kGamma ? a.t : a.q, a.part, kGamma ? a.gamma : a.zeta,
+      a.counters + kCounterTdotGraph, a.l2keep != 0);
   ktime_finish(a, kGamma ? 6 : 2);
 }
+
+constexpr int64_t kTdotSmallNb = 4 * kNumSMs;
 
 // SpMV inside the iteration: one row per thread, the matrix, x, y and the
 // status word as kernel parameters (constant bank operands, as the
@@ -163,15 +167,6 @@ __global__ void __launch_bounds__(256) k_iter_spmv(krb_matrix A, const double *_
     if (*status != KRB_RUNNING) return;
     if (kt && blockIdx.x == 0 && threadIdx.x == 0)
       *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
-    if (kSell && pf > 0 && (threadIdx.x & 31) == 0 && i < A.n) {
-      // bulk L2 prefetch of the slice a later wave streams (values, columns)
-      const int64_t s = i >> 5, b0 = __ldg(A.sl_ptr + s), w = __ldg(A.sl_ptr + s + 1) - b0;
-      const int64_t at = b0 + pf / 12;
-      if (w > 0 && at + w <= A.sell_elems) {
-        prefetch_l2_bulk(A.s_val + at, (uint32_t)(8 * w));
-        prefetch_l2_bulk(A.s_col + at, (uint32_t)(4 * w));
-      }
-    }
     if (i < A.n) y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
   }
   if (kt && blockIdx.x + 4096u >= gridDim.x) {
@@ -222,7 +217,13 @@ static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
 template <bool kGamma>
 static int launch_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   if (h.k <= 0 || h.nb == 0) return KRB_OK;
-  if (tuning().tdot_variant == 1) {
+  const int tv = tuning().tdot_variant;
+  if (tv == 3 || (tv == 0 && h.nb < kTdotSmallNb)) {
+    static int per_sm3 = occupancy_1024(k_proj_dot<16, kGamma, 3>);
+    const int64_t units = h.nb * ((h.k + 3) / 4);
+    const int64_t g = (int64_t)kNumSMs * per_sm3 < units ? (int64_t)kNumSMs * per_sm3 : units;
+    KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 3><<<dim3((unsigned)g, 1), 1024, 0, st>>>(d)));
+  } else if (tv == 1) {
     static int per_sm1 = occupancy_1024(k_proj_dot<16, kGamma, 1>);
     dim3 grid = tdot_grid(h.nb, h.k, per_sm1);
     KRB_DISPATCH_E(canon_E(h.n), (k_proj_dot<kE, kGamma, 1><<<grid, 1024, 0, st>>>(d)));
@@ -251,7 +252,7 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   else if (h.A.dcode)
     k_iter_spmv<2, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.format == 2)
-    k_iter_spmv<1, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+    k_iter_spmv<1, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
   else
     k_iter_spmv<0, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
   KRB_CHECK_LAUNCH();

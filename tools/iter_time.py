@@ -10,12 +10,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 
-def run(name, k=None, reps=3, max_itn=None, fmt=0):
+def run(name, k=None, reps=3, max_itn=None, fmt=0, system=0):
     import torch
     import paper_1406_2831_b200 as P
     from paper_1406_2831_b200 import device as D, solvers as S, workloads as W
     seq = W.make_sequence(name)
-    A = seq.matrix(0)
+    A = seq.matrix(system)
     k = seq.k if k is None else k
     M = D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=fmt)
     r = np.random.default_rng(12345)
@@ -53,7 +53,7 @@ def run(name, k=None, reps=3, max_itn=None, fmt=0):
     kk = space.k if space is not None else 0
     its = max(h.iterations, 1)
     B = W.bytes_per_iteration(A.n, A.nnz, kk)
-    return {"config": name, "n": A.n, "nnz": A.nnz, "k": kk, "format": M.format,
+    return {"config": name, "system": system, "n": A.n, "nnz": A.nnz, "k": kk, "format": M.format,
             "iterations": h.iterations, "status": h.status,
             "solve_ms": round(best * 1e3, 3), "us_per_it": round(best / its * 1e6, 2),
             "GBps_alg": round(B * its / best / 1e9, 1), "kernel_us": kern_us,
@@ -98,6 +98,7 @@ if __name__ == "__main__":
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--max-itn", type=int, default=None)
     ap.add_argument("--both", action="store_true", help="also k = 0")
+    ap.add_argument("--system", type=int, default=0, help="matrix index of the sequence")
     ap.add_argument("--fmt", type=int, default=0, help="matrix format (0 auto, 2 SELL-32, 4 offset-coded)")
     ap.add_argument("--phases", action="store_true",
                     help="per-phase breakdown of the persistent kernel")
@@ -112,6 +113,6 @@ if __name__ == "__main__":
             print(json.dumps(phase_breakdown(c, a.k)), flush=True)
         sys.exit(0)
     for c in a.config:
-        print(json.dumps(run(c, a.k, max_itn=a.max_itn, fmt=a.fmt)), flush=True)
+        print(json.dumps(run(c, a.k, max_itn=a.max_itn, fmt=a.fmt, system=a.system)), flush=True)
         if a.both:
-            print(json.dumps(run(c, 0, max_itn=a.max_itn, fmt=a.fmt)), flush=True)
+            print(json.dumps(run(c, 0, max_itn=a.max_itn, fmt=a.fmt, system=a.system)), flush=True)

@@ -255,7 +255,7 @@ def roofline_from_ktime(wl, kt, t_total):
             "timing": "live: CTA 0 start -> last CTA end (%globaltimer) of every "
                       "launch inside the timed steps"}
     sb = getattr(wl, "spmv_stream_bytes", None)
-    if sb and "k_iter_spmv" in shares:
+    if sb and "k_iter_spmv (q = A p, t = A s)" in shares:
         sp = shares["k_iter_spmv (q = A p, t = A s)"]
         st = sb / (sp["avg_us"] * 1e3)
         sp.update({"format": wl.spmv_format, "stream_bytes_per_launch": sb,

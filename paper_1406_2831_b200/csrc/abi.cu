@@ -67,8 +67,7 @@ int krb_set_tuning(const char *key, int64_t value) {
       {"cluster", &t.cluster},     {"persist_v1", &t.persist_v1},
       {"gemm_mode", &t.gemm_mode}, {"l2keep", &t.l2keep},
       {"phase_variant", &t.phase_variant}, {"tdot_variant", &t.tdot_variant},
-      {"spmv_variant", &t.spmv_variant}, {"spmv_prefetch_mb", &t.spmv_prefetch_mb},
-      {"spmm_panel", &t.spmm_panel}};
+      {"spmv_variant", &t.spmv_variant}, {"spmv_prefetch_mb", &t.spmv_prefetch_mb}};
   for (auto &e : table)
     if (strcmp(e.name, key) == 0) {
       *e.slot = (int)value;

@@ -95,7 +95,6 @@ struct Tuning {
   int phase_variant = 0;  // graph phase kernels: 0 tuned per phase, 1 uniform (round 1)
   int tdot_variant = 0;   // graph projection dots: 0 <= 64 regs, 1 <= 32 regs
   int spmv_prefetch_mb = 6;  // offset-coded SpMV: bulk L2 prefetch distance ahead (MB, 0 = off)
-  int spmm_panel = 1;        // offset-coded SpMM over row-major 8-column panels
   int spmv_variant = 0;   // offset-coded SpMV: 0 = uniform offsets by warp shuffle, 1 = int4 loads
 };
 Tuning &tuning();

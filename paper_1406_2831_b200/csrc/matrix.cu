@@ -197,84 +197,9 @@ __global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
     if (c < nc) Yc[(int64_t)c * ldy + row] = sum[c];
 }
 
-// ---- offset-coded SpMM over row-major panels of 8 columns ---------------
-// X (ncols column-major vectors) is first copied into panels P[g][i][c]
-// (n x 8, row-major, zero-padded), so every matrix entry gathers its 8
-// operands as one 64-byte row (four 16-byte loads, 2 sectors) instead of 8
-// scattered 8-byte loads; each thread still walks its row once per panel in
-// CSR order with 8 independent sequential mul-then-add sums (bit-identical
-// to 8 SpMVs).  Matrix value stream bulk-prefetched into L2 as in the SpMV.
-__global__ void k_panelize(int64_t n, int ncols, const double *__restrict__ X, int64_t ldx,
-                           double *__restrict__ P) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int g = blockIdx.y;
-  double v[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) v[c] = 8 * g + c < ncols ? __ldg(X + (int64_t)(8 * g + c) * ldx + i) : 0.0;
-  double2 *dst = reinterpret_cast<double2 *>(P + ((int64_t)g * n + i) * 8);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) dst[c] = make_double2(v[2 * c], v[2 * c + 1]);
-}
-
-__global__ void __launch_bounds__(256) k_spmm_panel(krb_matrix A, int ncols,
-                                                    const double *__restrict__ P,
-                                                    double *__restrict__ Y, int64_t ldy,
-                                                    int64_t pf) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= A.n) return;
-  const int g = blockIdx.y;
-  const int nc = min(8, ncols - 8 * g);
-  const double2 *__restrict__ Pg = reinterpret_cast<const double2 *>(P + (int64_t)g * A.n * 8);
-  const int64_t s = i >> 5;
-  const int l = (int)(i & 31);
-  const int len = __ldg(A.rlen + i);
-  const int64_t vbase = __ldg(A.sl_ptr + s);
-  const double *__restrict__ vp = A.s_val + vbase + l;
-  if (pf > 0 && l == 0) {
-    const int64_t at = vbase + pf / 8, nbytes = 256 * (int64_t)len;
-    if (at + nbytes / 8 <= A.sell_elems && nbytes > 0) prefetch_l2_bulk(A.s_val + at, (uint32_t)nbytes);
-  }
-  const int64_t dp = __ldg(A.dptr + s);
-  const bool uni = dp & 1;
-  const uint8_t *cp = A.dcode + (dp >> 1) + (uni ? 0 : l);
-  double sum[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) sum[c] = 0.0;
-  for (int j = 0; j < len; ++j) {
-    const int col = (int)i + (uni ? __ldg(reinterpret_cast<const int32_t *>(cp) + j)
-                                  : __ldg(A.dict + __ldg(cp + 32 * j)));
-    const double v = __ldg(vp + 32 * j);
-    const double2 *xr = Pg + (int64_t)col * 4;
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const double2 xx = __ldg(xr + h);
-      sum[2 * h] = __dadd_rn(sum[2 * h], __dmul_rn(v, xx.x));
-      sum[2 * h + 1] = __dadd_rn(sum[2 * h + 1], __dmul_rn(v, xx.y));
-    }
-  }
-  double *Yg = Y + (int64_t)(8 * g) * ldy;
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-    if (c < nc) Yg[(int64_t)c * ldy + i] = sum[c];
-}
-
 int spmm_launch(const krb_matrix *M, int64_t ncols, const double *X, int64_t ldx,
                 double *Y, int64_t ldy, cudaStream_t st) {
   constexpr int kNC = 8;
-  if (M->dcode && M->n > 0 && ncols > 0 && tuning().spmm_panel) {
-    const int64_t ng = (ncols + 7) / 8;
-    double *P = nullptr;
-    KRB_CHECK_CUDA(dev_alloc((void **)&P, sizeof(double) * 8 * M->n * ng, st));
-    dim3 grid((unsigned)((M->n + 255) / 256), (unsigned)ng);
-    k_panelize<<<grid, 256, 0, st>>>(M->n, (int)ncols, X, ldx, P);
-    KRB_CHECK_LAUNCH();
-    k_spmm_panel<<<grid, 256, 0, st>>>(*M, (int)ncols, P, Y, ldy,
-                                       (int64_t)tuning().spmv_prefetch_mb << 20);
-    KRB_CHECK_LAUNCH();
-    dev_free(P, st);
-    return KRB_OK;
-  }
   if (M->n == 0 || ncols == 0) return KRB_OK;
   if (M->pre) {   // preconditioned operator: one composite application per column
     for (int64_t c = 0; c < ncols; ++c)

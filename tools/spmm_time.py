@@ -1,6 +1,6 @@
 """SpMM (krb_spmm: A X and A^T X for ncols columns, the refresh_images /
 update products) timing on a BASELINE config's first matrix, CUDA events.
-    python tools/spmm_time.py --config c5 --ncols 30 [--tune spmm_panel=0]"""
+    python tools/spmm_time.py --config c5 --ncols 30 [--tune key=value]"""
 import argparse
 import json
 import os

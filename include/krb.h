@@ -121,6 +121,13 @@ int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz,
 int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t *nslices,
                             int64_t *uniform_slices, int *ndict);
 
+/* Identity and reference count of the shared sparsity pattern behind A
+ * (matrices with equal row_ptr / col_idx share the SELL layout, the offset
+ * codes and the transpose permutation while any of them is alive);
+ * transpose_known: the pattern's transpose permutation is built. */
+int krb_matrix_pattern_info(const krb_matrix *A, uint64_t *pattern_id, int *refs,
+                            int *transpose_known);
+
 /* y = A x  (SparseMatrix.matvec, sparse.py:117-121; scipy csr_matvec order:
  * per-row sequential sum from 0.0, separate multiply and add) */
 int krb_spmv(const krb_matrix *A, const double *d_x, double *d_y,

@@ -16,6 +16,7 @@
 
 // Device sparse matrix (CSR + optional SELL-32 + lazily built transpose).
 struct krb_precond;
+struct krb_pattern;   // shared sparsity structure (matrix.cu)
 struct krb_matrix {
   int64_t n = 0, nnz = 0;
   int format = 0;  // 1 CSR, 2 SELL
@@ -42,6 +43,11 @@ struct krb_matrix {
   int ndict = 0;
   int64_t dcode_bytes = 0, uniform_slices = 0;
   krb_matrix *T = nullptr;  // lazily built transpose
+  // the structure arrays above (rp, ci, sl_ptr, rlen, s_col, perm, dcode,
+  // dptr, dict) belong to this reference-counted pattern, shared by every
+  // live matrix with the same row_ptr / col_idx (a sequence A_j = s_j E - K);
+  // val and s_val are the matrix's own
+  krb_pattern *pat = nullptr;
   int64_t bytes = 0;
   // preconditioned-operator view (precond.cu): shares `base`'s arrays; every
   // application runs the split-ILUTP composite (pre_adj: its adjoint)

@@ -21,6 +21,8 @@
 // column), and gets its own format choice.
 #include <cub/cub.cuh>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "krb_internal.cuh"
 #include "spmv.cuh"
@@ -516,6 +518,148 @@ static int build_dict(krb_matrix *A, cudaStream_t st) {
   return KRB_OK;
 }
 
+// ---- shared sparsity patterns --------------------------------------------
+// Matrices of a sequence (A_j = s_j E - K: the same row_ptr / col_idx, new
+// values) share their structure work: the SELL layout, the offset codes and
+// the transpose's permutation are built once and reused while any matrix of
+// that pattern is alive (found by comparing the new index arrays on the
+// device against every live pattern of the same size).
+}  // namespace krb
+
+struct krb_pattern {
+  int refs = 0;
+  int64_t n = 0, nnz = 0;
+  int req_format = 0, format = 0, ndict = 0;
+  int64_t nslices = 0, sell_elems = 0, dcode_bytes = 0, uniform_slices = 0, bytes = 0;
+  int64_t *rp = nullptr, *sl_ptr = nullptr, *dptr = nullptr;
+  int32_t *ci = nullptr, *rlen = nullptr, *s_col = nullptr, *perm = nullptr, *dict = nullptr;
+  uint8_t *dcode = nullptr;
+  krb_pattern *tpat = nullptr;   // pattern of the transpose (may be this one)
+  int32_t *tperm = nullptr;      // transpose entry t = this pattern's CSR entry tperm[t]
+};
+
+namespace krb {
+
+static std::vector<krb_pattern *> &patterns() {
+  static std::vector<krb_pattern *> v;
+  return v;
+}
+static std::recursive_mutex &patterns_mu() {
+  static std::recursive_mutex m;
+  return m;
+}
+void matrix_free(krb_matrix *A, bool async, cudaStream_t st);
+
+static void pattern_release(krb_pattern *P, bool async, cudaStream_t st) {
+  std::lock_guard<std::recursive_mutex> lk(patterns_mu());
+  if (!P || --P->refs > 0) return;
+  auto &v = patterns();
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i] == P) { v.erase(v.begin() + i); break; }
+  void *arrays[] = {P->rp, P->ci, P->sl_ptr, P->rlen, P->s_col, P->perm,
+                    P->dcode, P->dptr, P->dict, P->tperm};
+  for (void *p : arrays)
+    if (p) dev_free(p, async ? st : nullptr);
+  krb_pattern *T = P->tpat;
+  delete P;
+  if (T && T != P) pattern_release(T, async, st);
+}
+
+// move the structure arrays of a freshly built matrix into a new pattern
+static void pattern_adopt(krb_matrix *A) {
+  std::lock_guard<std::recursive_mutex> lk(patterns_mu());
+  krb_pattern *P = new krb_pattern();
+  P->refs = 1;
+  P->n = A->n; P->nnz = A->nnz; P->req_format = A->req_format; P->format = A->format;
+  P->ndict = A->ndict; P->nslices = A->nslices; P->sell_elems = A->sell_elems;
+  P->dcode_bytes = A->dcode_bytes; P->uniform_slices = A->uniform_slices;
+  P->rp = A->rp; P->ci = A->ci; P->sl_ptr = A->sl_ptr; P->rlen = A->rlen; P->s_col = A->s_col;
+  P->perm = A->perm; P->dcode = A->dcode; P->dptr = A->dptr; P->dict = A->dict;
+  P->bytes = A->bytes - 8 * A->nnz - (A->s_val ? 8 * A->sell_elems : 0);
+  A->pat = P;
+  patterns().push_back(P);
+}
+
+static void pattern_attach(krb_matrix *A, krb_pattern *P) {
+  std::lock_guard<std::recursive_mutex> lk(patterns_mu());
+  P->refs++;
+  A->pat = P;
+  A->format = P->format; A->ndict = P->ndict; A->nslices = P->nslices;
+  A->sell_elems = P->sell_elems; A->dcode_bytes = P->dcode_bytes;
+  A->uniform_slices = P->uniform_slices;
+  A->rp = P->rp; A->ci = P->ci; A->sl_ptr = P->sl_ptr; A->rlen = P->rlen; A->s_col = P->s_col;
+  A->perm = P->perm; A->dcode = P->dcode; A->dptr = P->dptr; A->dict = P->dict;
+}
+
+__global__ void k_pattern_neq(int64_t n, int64_t nnz, const int64_t *__restrict__ rp_a,
+                              const int64_t *__restrict__ rp_b, const int32_t *__restrict__ ci_a,
+                              const int32_t *__restrict__ ci32_b,
+                              const int64_t *__restrict__ ci64_b, int *neq) {
+  const int64_t m = n + 1 > nnz ? n + 1 : nnz;
+  bool diff = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i <= n && rp_a[i] != rp_b[i]) diff = true;
+    if (i < nnz && ci_a[i] != (ci32_b ? ci32_b[i] : (int32_t)ci64_b[i])) diff = true;
+  }
+  if (__syncthreads_or(diff) && threadIdx.x == 0) *neq = 1;
+}
+
+static krb_pattern *pattern_find(int64_t n, int64_t nnz, int req_format, const int64_t *d_rp,
+                                 const int32_t *d_ci32, const int64_t *d_ci64,
+                                 cudaStream_t st) {
+  std::lock_guard<std::recursive_mutex> lk(patterns_mu());
+  int *flag = nullptr;
+  for (krb_pattern *P : patterns()) {
+    if (P->n != n || P->nnz != nnz || P->req_format != req_format) continue;
+    if (!flag && dev_alloc((void **)&flag, sizeof(int), st) != cudaSuccess) return nullptr;
+    int h = 0;
+    if (cudaMemsetAsync(flag, 0, sizeof(int), st) != cudaSuccess) break;
+    const int64_t m = n + 1 > nnz ? n + 1 : nnz;
+    k_pattern_neq<<<(unsigned)((m + 1023) / 1024), 256, 0, st>>>(n, nnz, P->rp, d_rp, P->ci,
+                                                                 d_ci32, d_ci64, flag);
+    launch_counter()++;
+    if (cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      break;
+    if (h == 0) {
+      dev_free(flag, st);
+      return P;
+    }
+  }
+  if (flag) dev_free(flag, st);
+  cudaGetLastError();
+  return nullptr;
+}
+
+// values of row p's slice column (padding slots of the row zeroed: no
+// separate pass over the padded array)
+__global__ void k_sell_fill_vals(int64_t n, const int64_t *__restrict__ rp,
+                                 const double *__restrict__ val,
+                                 const int64_t *__restrict__ sl_ptr,
+                                 const int32_t *__restrict__ perm, double *__restrict__ s_val) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t row = perm ? perm[p] : p;
+  const int64_t s0 = sl_ptr[p >> 5], width = (sl_ptr[(p >> 5) + 1] - s0) / 32;
+  const int64_t base = s0 + (p & 31);
+  const int64_t b = rp[row], e = rp[row + 1];
+  for (int64_t j = 0; j < width; ++j) s_val[base + 32 * j] = b + j < e ? val[b + j] : 0.0;
+}
+
+// the SELL values of a matrix attached to a pattern
+static int fill_values(krb_matrix *A, cudaStream_t st) {
+  if (A->format != 2 || A->n == 0) return KRB_OK;
+  const int64_t total = A->sell_elems;
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->s_val, sizeof(double) * (total > 0 ? total : 1), st));
+  // (slots of the missing lanes of a partial last slice stay unwritten:
+  // no row reads them)
+  k_sell_fill_vals<<<(unsigned)((A->n + 255) / 256), 256, 0, st>>>(A->n, A->rp, A->val,
+                                                                   A->sl_ptr, A->perm, A->s_val);
+  KRB_CHECK_LAUNCH();
+  return KRB_OK;
+}
+
 int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
                   const int64_t *d_rp, const int32_t *d_ci32,
                   const int64_t *d_ci64, const double *d_val, int format,
@@ -543,6 +687,28 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   krb_matrix *A = new krb_matrix();
   A->n = n;
   A->nnz = nnz;
+  A->req_format = format;
+  if (krb_pattern *P = pattern_find(n, nnz, format, d_rp, d_ci32, d_ci64, st)) {
+    pattern_attach(A, P);
+    cudaError_t e = dev_alloc((void **)&A->val, sizeof(double) * (nnz > 0 ? nnz : 1), st);
+    if (e != cudaSuccess) {
+      set_error("krb_matrix_create: %s", cudaGetErrorString(e));
+      pattern_release(P, true, st);
+      delete A;
+      return KRB_ENOMEM;
+    }
+    if (nnz > 0)
+      KRB_CHECK_CUDA(cudaMemcpyAsync(A->val, d_val, sizeof(double) * nnz,
+                                     cudaMemcpyDeviceToDevice, st));
+    int rc = fill_values(A, st);
+    if (rc != KRB_OK) {
+      matrix_free(A, true, st);
+      return rc;
+    }
+    A->bytes = P->bytes + 8 * nnz + (A->s_val ? 8 * A->sell_elems : 0);
+    *out = A;
+    return KRB_OK;
+  }
   cudaError_t e = dev_alloc((void **)&A->rp, sizeof(int64_t) * (n + 1), st);
   if (e == cudaSuccess) e = dev_alloc((void **)&A->ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1), st);
   if (e == cudaSuccess) e = dev_alloc((void **)&A->val, sizeof(double) * (nnz > 0 ? nnz : 1), st);
@@ -568,13 +734,13 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   A->bytes = (n + 1) * 8 + nnz * 12;
   // 4 = SELL-32 with the offset-coded stream (when the matrix qualifies);
   // 2 = plain SELL-32; 0 = auto (the offset-coded stream when it qualifies)
-  A->req_format = format;
   int rc = build_sell(A, format == 4 ? 2 : format, st);
   if (rc == KRB_OK && (format == 0 || format == 4)) rc = build_dict(A, st);
   if (rc != KRB_OK) {
     delete A;
     return rc;
   }
+  pattern_adopt(A);
   *out = A;
   return KRB_OK;
 }
@@ -591,6 +757,12 @@ __global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ ci,
                             int64_t *__restrict__ cnt) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nnz) atomicAdd(reinterpret_cast<unsigned long long *>(cnt + ci[i]), 1ull);
+}
+
+__global__ void k_gather_vals(int64_t nnz, const int32_t *__restrict__ perm,
+                              const double *__restrict__ val, double *__restrict__ tval) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nnz) tval[t] = val[perm[t]];
 }
 
 __global__ void k_gather_t(int64_t nnz, const int32_t *__restrict__ perm,
@@ -620,6 +792,29 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
     return KRB_OK;
   }
   const int64_t n = A->n, nnz = A->nnz;
+  krb_pattern *P = A->pat;
+  if (P && P->tpat) {
+    // the pattern's transpose is known: values by one gather through its
+    // permutation, structure shared
+    krb_matrix *T = new krb_matrix();
+    T->n = n;
+    T->nnz = nnz;
+    T->req_format = P->tpat->req_format;
+    pattern_attach(T, P->tpat);
+    KRB_CHECK_CUDA(dev_alloc((void **)&T->val, sizeof(double) * (nnz > 0 ? nnz : 1), st));
+    if (nnz > 0) {
+      k_gather_vals<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(nnz, P->tperm, A->val, T->val);
+      KRB_CHECK_LAUNCH();
+    }
+    int rc = fill_values(T, st);
+    if (rc != KRB_OK) {
+      matrix_free(T, true, st);
+      return rc;
+    }
+    T->bytes = P->tpat->bytes + 8 * nnz + (T->s_val ? 8 * T->sell_elems : 0);
+    A->T = T;
+    return KRB_OK;
+  }
   int32_t *rows = nullptr, *keys_out = nullptr, *perm_in = nullptr,
           *perm_out = nullptr, *tci = nullptr;
   int64_t *cnt = nullptr, *trp = nullptr;
@@ -666,7 +861,6 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   dev_free(rows, st);
   dev_free(keys_out, st);
   dev_free(perm_in, st);
-  dev_free(perm_out, st);
   dev_free(cnt, st);
   krb_matrix *T = nullptr;
   int rc = matrix_create(&T, n, nnz, trp, tci, nullptr, tval,
@@ -674,7 +868,19 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
   dev_free(trp, st);
   dev_free(tci, st);
   dev_free(tval, st);
-  if (rc != KRB_OK) return rc;
+  if (rc != KRB_OK) {
+    dev_free(perm_out, st);
+    return rc;
+  }
+  if (P && T->pat && !P->tpat) {
+    // remember the transpose's pattern and permutation (a symmetric
+    // pattern is its own transpose pattern: no counted self-reference)
+    P->tpat = T->pat;
+    if (T->pat != P) T->pat->refs++;
+    P->tperm = perm_out;
+  } else {
+    dev_free(perm_out, st);
+  }
   A->T = T;
   return KRB_OK;
 }
@@ -691,11 +897,17 @@ void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
     return;
   }
   matrix_free(A->T, async, st);
-  void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm,
-                    A->dcode, A->dptr, A->dict};
   if (!async) cudaDeviceSynchronize();
-  for (void *p : arrays)
-    if (p) dev_free(p, async ? st : nullptr);
+  if (A->pat) {   // structure arrays belong to the pattern
+    for (void *p : {(void *)A->val, (void *)A->s_val})
+      if (p) dev_free(p, async ? st : nullptr);
+    pattern_release(A->pat, async, st);
+  } else {
+    void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm,
+                      A->dcode, A->dptr, A->dict};
+    for (void *p : arrays)
+      if (p) dev_free(p, async ? st : nullptr);
+  }
   delete A;
 }
 
@@ -760,6 +972,17 @@ int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t 
   if (nslices) *nslices = B->format == 2 ? B->nslices : 0;
   if (uniform_slices) *uniform_slices = B->uniform_slices;
   if (ndict) *ndict = B->ndict;
+  return KRB_OK;
+}
+
+int krb_matrix_pattern_info(const krb_matrix *A, uint64_t *pattern_id, int *refs,
+                            int *transpose_known) {
+  KRB_REQUIRE(A != nullptr, "krb_matrix_pattern_info: NULL matrix");
+  const krb_matrix *B = A->base ? A->base : A;
+  std::lock_guard<std::recursive_mutex> lk(patterns_mu());
+  if (pattern_id) *pattern_id = (uint64_t)(uintptr_t)B->pat;
+  if (refs) *refs = B->pat ? B->pat->refs : 0;
+  if (transpose_known) *transpose_known = B->pat && B->pat->tperm ? 1 : 0;
   return KRB_OK;
 }
 

@@ -355,6 +355,15 @@ class DeviceMatrix:
     def shape(self):
         return (self.n, self.n)
 
+    def pattern_info(self):
+        """(pattern id, live references, transpose permutation known):
+        matrices with equal row_ptr / col_idx share their structure work
+        (matrix.cu)."""
+        pid, refs, tk = ctypes.c_uint64(), ctypes.c_int(), ctypes.c_int()
+        _lib.call("krb_matrix_pattern_info", self.h, ctypes.byref(pid), ctypes.byref(refs),
+                  ctypes.byref(tk))
+        return pid.value, refs.value, bool(tk.value)
+
     def spmv(self, x_dev, y_dev=None, transpose=False):
         t = torch()
         if y_dev is None:

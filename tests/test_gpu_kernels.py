@@ -269,3 +269,69 @@ def test_spmv_adjoint_and_linearity(dev, cfg):
     comb = M.spmv(_tensor(a * x + b * y)).cpu().numpy()
     Ay = M.spmv(yd).cpu().numpy()
     assert np.allclose(comb, a * Ax + b * Ay, rtol=1e-12, atol=1e-12 * np.abs(Ax).max())
+
+
+def _csr_of(S):
+    from paper_1406_2831_b200.workloads import CSR
+    S = S.tocsr()
+    S.sort_indices()
+    return CSR(S.shape[0], S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
+def test_shared_pattern_values_and_transpose(dev, cfg):
+    """Matrices of a sequence with one sparsity pattern share the structure
+    work (SELL layout, offset codes, transpose permutation): every product
+    stays bit-identical to scipy, the pattern outlives the matrix that built
+    it, and a different pattern of the same size is not shared."""
+    import scipy.sparse as sp
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence(cfg, small=True)
+    A1, A2 = seq.matrix(0), seq.matrix(1)
+    assert np.array_equal(A1.col_idx, A2.col_idx) or cfg == "c4"
+    r = np.random.default_rng(9)
+    x = r.standard_normal(A1.n)
+    M1 = dev.DeviceMatrix(A1.n, A1.row_ptr, A1.col_idx, A1.values)
+    y1t = M1.spmv(_tensor(x), transpose=True).cpu().numpy()      # builds the transpose
+    assert np.array_equal(y1t, A1.to_scipy().T.tocsr() @ x)
+    # same pattern, new values (scaled diagonal shift of the first matrix)
+    S2 = A1.to_scipy() + 0.37 * sp.identity(A1.n, format="csr")
+    B2 = _csr_of(S2)
+    same = np.array_equal(B2.row_ptr, A1.row_ptr) and np.array_equal(B2.col_idx, A1.col_idx)
+    M2 = dev.DeviceMatrix(B2.n, B2.row_ptr, B2.col_idx, B2.values)
+    p1, p2 = M1.pattern_info(), M2.pattern_info()
+    if same:
+        assert p1[0] == p2[0] and p2[1] >= 2 and p2[2]
+    assert np.array_equal(M2.spmv(_tensor(x)).cpu().numpy(), S2 @ x)
+    assert np.array_equal(M2.spmv(_tensor(x), transpose=True).cpu().numpy(), S2.T.tocsr() @ x)
+    X = r.standard_normal((A1.n, 9))
+    Y = M2.spmm(_cols(X), transpose=True).cpu().numpy().T
+    for c in range(9):
+        assert np.array_equal(Y[:, c], S2.T.tocsr() @ X[:, c])
+    # the builder goes away; the pattern stays with M2
+    del M1
+    import gc
+    gc.collect()
+    assert np.array_equal(M2.spmv(_tensor(x)).cpu().numpy(), S2 @ x)
+    assert np.array_equal(M2.spmv(_tensor(x), transpose=True).cpu().numpy(), S2.T.tocsr() @ x)
+    # a third matrix attaches to the surviving pattern
+    S3 = S2 * 1.5
+    B3 = _csr_of(S3)
+    M3 = dev.DeviceMatrix(B3.n, B3.row_ptr, B3.col_idx, B3.values)
+    if same:
+        assert M3.pattern_info()[0] == p2[0]
+    assert np.array_equal(M3.spmv(_tensor(x), transpose=True).cpu().numpy(), S3.T.tocsr() @ x)
+    # same n and nnz, one column moved: its own pattern
+    cols = B3.col_idx.copy()
+    row = int(np.argmax(np.diff(B3.row_ptr) >= 2))
+    b0, e0 = B3.row_ptr[row], B3.row_ptr[row + 1]
+    free = sorted(set(range(B3.n)) - set(cols[b0:e0].tolist()))
+    cols[e0 - 1] = free[-1] if free[-1] > cols[e0 - 2] else cols[e0 - 1]
+    S4 = sp.csr_matrix((B3.values, cols, B3.row_ptr), shape=(B3.n, B3.n))
+    S4.sort_indices()
+    B4 = _csr_of(S4)
+    M4 = dev.DeviceMatrix(B4.n, B4.row_ptr, B4.col_idx, B4.values)
+    if not np.array_equal(B4.col_idx, B3.col_idx):
+        assert M4.pattern_info()[0] != M3.pattern_info()[0]
+    assert np.array_equal(M4.spmv(_tensor(x)).cpu().numpy(), S4 @ x)
+    assert np.array_equal(M4.spmv(_tensor(x), transpose=True).cpu().numpy(), S4.T.tocsr() @ x)

@@ -201,11 +201,6 @@ static int launch_phase(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   // 2 x 148 CTAs even where only one fits per SM: the second wave balances
   // the blocks dynamically (one wave of 148: Q / T 702 -> 776 us on C5)
   int grid = grid_for(h.nb);
-  // tuning phase_grid: 1 = one canonical block per CTA for every phase, 2 =
-  // for P / S / X only (the hardware scheduler balances the blocks)
-  const int pg = tuning().phase_grid;
-  if (pg == 1 || (pg == 2 && (PH == PH_PUPDATE || PH == PH_SUPD || PH == PH_XR)))
-    grid = (int)h.nb;
   if (h.rec_x && (PH == PH_INIT || PH == PH_XR)) {   // record_iterates snapshots
     KRB_DISPATCH_E(canon_E(h.n), (k_phase<kE, PH, 2><<<grid, 1024, 0, st>>>(d)));
   } else if (tuning().phase_variant == 1) {
@@ -264,7 +259,9 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   return KRB_OK;
 }
 
-// one iteration (the graph body)
+// one iteration (the graph body).  (Programmatic dependent launches of
+// kernels 2..9 -- CTAs starting in the previous kernel's tail, waiting on
+// griddepcontrol -- measured no faster on C5: 4484-4518 vs 4468-4494 us.)
 static int launch_iteration(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
   KRB_TRY(launch_phase<PH_PUPDATE>(h, d, st));
   KRB_TRY(launch_iter_spmv<false>(h, d, st));
@@ -490,8 +487,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
                    G.ktime == cfg->d_kernel_times &&
                    G.variant == tuning().phase_variant + 16 * tuning().tdot_variant +
                                     256 * tuning().spmv_variant +
-                                    4096 * tuning().spmv_prefetch_mb +
-                                    (1 << 20) * tuning().phase_grid;
+                                    4096 * tuning().spmv_prefetch_mb;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -510,8 +506,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     G.n = n; G.k = k; G.format = A->format; G.sig = sig;
     G.ktime = cfg->d_kernel_times;
     G.variant = tuning().phase_variant + 16 * tuning().tdot_variant +
-                256 * tuning().spmv_variant + 4096 * tuning().spmv_prefetch_mb +
-                (1 << 20) * tuning().phase_grid;
+                256 * tuning().spmv_variant + 4096 * tuning().spmv_prefetch_mb;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

@@ -95,7 +95,7 @@ struct Tuning {
   int phase_variant = 0;  // graph phase kernels: 0 tuned per phase, 1 uniform (round 1)
   int tdot_variant = 0;   // graph projection dots: 0 <= 64 regs, 1 <= 32 regs
   int spmv_prefetch_mb = 6;  // offset-coded SpMV: bulk L2 prefetch distance ahead (MB, 0 = off)
-  int phase_grid = 0;        // graph phases: 0 = 2 x 148 CTAs, 1 = one block per CTA, 2 = P/S/X only
+  int spmm_variant = 1;      // offset-coded SpMM: 0 generic kernel, 1 k_spmm_dict (L2 prefetch)
   int spmv_variant = 0;   // offset-coded SpMV: 0 = uniform offsets by warp shuffle, 1 = int4 loads
 };
 Tuning &tuning();

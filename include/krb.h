@@ -53,7 +53,8 @@ int64_t krb_launch_count(void);
 /* Driver / kernel-variant knobs (process-wide; every variant computes the
  * same bits).  Keys: "persist0", "p0_grid_half", "p0_onchip", "p0_prof_cta",
  * "cluster", "persist_v1", "gemm_mode", "l2keep", "phase_variant",
- * "tdot_variant", "spmv_variant", "spmv_prefetch_mb" (bulk L2 prefetch
+ * "tdot_variant", "spmv_variant", "spmm_variant", "phase_pf_rows",
+ * "spmv_prefetch_mb" (bulk L2 prefetch
  * distance of the offset-coded SpMV, default 6).  Unknown key -> KRB_EINVAL.
  * No reference counterpart (the reference has no device drivers). */
 int krb_set_tuning(const char *key, int64_t value);

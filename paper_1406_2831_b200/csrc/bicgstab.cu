@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(1024, phase_minb(PH, kV)) k_phase(const IterAr
     for (int j = threadIdx.x; j < a.k; j += blockDim.x) coef[j] = src[j];
     __syncthreads();
   }
-  phase_blocks<kE, PH, phase_unroll(PH, kV), kV == 2>(a, sc, red, coef, blockIdx.x, gridDim.x,
+  phase_blocks<kE, PH, phase_unroll(PH, kV), kV == 2, true>(a, sc, red, coef, blockIdx.x, gridDim.x,
                                                       a.part);
   if (ND == 0) {
     ktime_finish(a, kSlot);
@@ -144,8 +144,8 @@ constexpr int64_t kTdotSmallNb = 4 * kNumSMs;
 // 1258 us.)
 // kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (uniform
 // slices: offsets by warp shuffle), 3 its first version (tuning spmv_variant=1).
-template <int kF, int kSlot>
-__global__ void __launch_bounds__(256) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
+template <int kF, int kSlot, int kMinB = 1>
+__global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status,
                                                    uint64_t *__restrict__ kt, int64_t pf) {
@@ -247,10 +247,12 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   const double *x = kSecond ? h.s : h.p;
   double *y = kSecond ? h.t : h.q;
   const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
+  // offset-coded: at most 40 registers (6 CTAs / SM; 47 unbounded, 5 CTAs:
+  // 776 vs 746 us live on C5; 32 registers spill: 776)
   if (h.A.dcode && tuning().spmv_variant == 1)
-    k_iter_spmv<3, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+    k_iter_spmv<3, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.dcode)
-    k_iter_spmv<2, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+    k_iter_spmv<2, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.format == 2)
     k_iter_spmv<1, kSecond ? 5 : 1><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
   else
@@ -495,6 +497,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     // L2 (tuning "l2keep" = 0 / 1 overrides)
     const int e = tuning().l2keep;
     h.l2keep = e >= 0 ? e : (2.0 * 8.0 * (double)n * (double)k <= 100e6 ? 1 : 0);
+    h.pf_rows = tuning().phase_pf_rows;
   }
   h.cond = hit ? G.cond : 0;
   IterArgs *d = reinterpret_cast<IterArgs *>(ctx->desc);

@@ -25,6 +25,7 @@ struct IterArgs {
   int k;
   int use_cond;
   int l2keep;   // keep C / Chat resident in L2 (evict_last loads)
+  int pf_rows;  // graph P / S / X phases: L2 prefetch distance in 1024-element rows
   cudaGraphConditionalHandle cond;
   const double *C, *Chat, *U;
   double *x, *r, *p, *q, *s, *t, *rt0, *b;
@@ -250,7 +251,7 @@ __device__ __forceinline__ PhaseScal load_scal(const SolveScalars *S) {
 // kRec: compile the record_iterates snapshot stores in (the host-loop
 // record kernels only; the stores' pointer checks cost the hot X kernel
 // registers)
-template <int kE, int PH, int kU = 4, bool kRec = false>
+template <int kE, int PH, int kU = 4, bool kRec = false, bool kPf = false>
 __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal sc,
                                              double (*red)[32],
                                              const double *coef, int64_t first,
@@ -276,6 +277,20 @@ __device__ __forceinline__ void phase_blocks(const IterArgs &a, const PhaseScal 
 #pragma unroll(kE < kU ? kE : kU)
     for (int e = 0; e < kE; ++e) {
       const int64_t i = base + (int64_t)kLanes * e;
+      if (kPf && a.pf_rows > 0 && threadIdx.x < 8 && e + a.pf_rows < kE) {
+        // bounded L2 prefetch: the 1024-element rows pf_rows ahead of this
+        // CTA's current row, one 8 KB bulk prefetch per read stream (at most
+        // 2 x 148 CTAs x streams x pf_rows x 8 KB in flight: fits in L2)
+        const int64_t r0 = blk * ((int64_t)kLanes * kE) + (int64_t)kLanes * (e + a.pf_rows);
+        const double *src = nullptr;
+        const int lane = threadIdx.x;
+        if (PH == PH_PUPDATE) src = lane == 0 ? r : lane == 1 ? p : lane == 2 ? q : nullptr;
+        else if (PH == PH_SUPD) src = lane == 0 ? r : lane == 1 ? q : nullptr;
+        else if (PH == PH_XR)
+          src = lane == 0 ? x : lane == 1 ? p : lane == 2 ? s : lane == 3 ? t : lane == 4 ? rt0
+                                                                                           : nullptr;
+        if (src && r0 + kLanes <= n) prefetch_l2_bulk(src + r0, 8 * kLanes);
+      }
       if (i >= n) continue;
       if (PH == PH_PUPDATE) {
         // p = r + beta * (p - omega * q)          (solvers.py:303)

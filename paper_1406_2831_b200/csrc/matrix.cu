@@ -108,7 +108,7 @@ bool same_sig(const MatrixSig &a, const MatrixSig &b) {
 
 // offset-coded SELL-32 (identity row order)
 template <int kV>
-__global__ void __launch_bounds__(256) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
+__global__ void __launch_bounds__(256, 6) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status, int64_t pf) {
   if (status && *status) return;

@@ -454,7 +454,7 @@ def e2e_arm(args, wl, space0, cfgs, flush, barrier, world, pinned):
             if i != last_i:
                 A = sms.pop(i, None) or P.SparseMatrix.from_csr(mats[i])
                 nxt = order.index(i) + 1
-                if pinned and nxt < len(order):
+                if nxt < len(order):
                     sms[order[nxt]] = P.SparseMatrix.from_csr(mats[order[nxt]])
                     P.prefetch_matrix(sms[order[nxt]])
                 if j > 0:

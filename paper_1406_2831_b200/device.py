@@ -194,11 +194,18 @@ _TDT = {np.dtype(np.float64): "float64", np.dtype(np.int64): "int64",
         np.dtype(np.int32): "int32"}
 
 
-def to_device(a: np.ndarray, dtype=np.float64):
+def to_device(a: np.ndarray, dtype=np.float64, staging=None):
     """Host numpy -> device tensor through reusable pinned staging, in
     chunks: the (multi-threaded) host copy of chunk i+1 into one pinned
-    buffer overlaps the DMA of chunk i out of the other."""
+    buffer overlaps the DMA of chunk i out of the other.  ``staging``: a
+    private _Staging (a background uploader must not share the caller's)."""
     t = torch()
+    stg = _STAGING if staging is None else staging
+    a = np.asarray(a)
+    dtype = np.dtype(dtype)
+    if (a.dtype != dtype and a.dtype.kind in "iu" and dtype.kind in "iu"
+            and a.ndim == 1 and a.nbytes >= (1 << 16) and not _is_pinned(a)):
+        return _to_device_cast(a, dtype, stg)
     a = np.ascontiguousarray(a, dtype=dtype)
     if a.nbytes < (1 << 16):
         # small operands (Ritz coefficients, column scales): a pinned copy
@@ -215,11 +222,49 @@ def to_device(a: np.ndarray, dtype=np.float64):
     n = a.nbytes
     for o in range(0, n, _CHUNK):
         m = min(_CHUNK, n - o)
-        i, buf = _STAGING.get(m)          # waits for this buffer's previous DMA
+        i, buf = stg.get(m)               # waits for this buffer's previous DMA
         _host_copy(buf[:m].numpy(), src[o:o + m])
         dst[o:o + m].copy_(buf[:m], non_blocking=True)
-        _STAGING.mark(i)
+        stg.mark(i)
     return out
+
+
+def _to_device_cast(a: np.ndarray, dtype, stg):
+    """Integer upload narrowed (or widened) during the staging copy itself:
+    each chunk is cast straight into the pinned buffer, so an int64 index
+    array goes over the link as int32 without a full host-side converted
+    copy first."""
+    t = torch()
+    out = t.empty(a.shape, dtype=getattr(t, _TDT[dtype]), device="cuda")
+    per = _CHUNK // dtype.itemsize
+    n = a.shape[0]
+    for o in range(0, n, per):
+        m = min(per, n - o)
+        i, buf = stg.get(m * dtype.itemsize)
+        dst = buf[:m * dtype.itemsize].numpy().view(dtype)
+        _host_copy_cast(dst, a[o:o + m])
+        out[o:o + m].copy_(buf[:m * dtype.itemsize].view(out.dtype), non_blocking=True)
+        stg.mark(i)
+    return out
+
+
+def _host_copy_cast(dst: np.ndarray, src: np.ndarray):
+    """dst[:] = src with an element-type cast, split across the copy pool."""
+    global _POOL
+    n = src.shape[0]
+    if n * src.itemsize < _PAR_BYTES:
+        np.copyto(dst, src, casting="unsafe")
+        return
+    if _POOL is None:
+        import concurrent.futures as cf
+        import os
+        _POOL = cf.ThreadPoolExecutor(max_workers=max(2, min(8, (os.cpu_count() or 2))))
+    parts = _POOL._max_workers
+    step = -(-n // parts)
+    futs = [_POOL.submit(np.copyto, dst[o:o + step], src[o:o + step], casting="unsafe")
+            for o in range(0, n, step)]
+    for f in futs:
+        f.result()
 
 
 def pinned_copy(a: np.ndarray) -> np.ndarray:
@@ -248,6 +293,17 @@ def to_host(tensor) -> np.ndarray:
     return out.numpy()
 
 
+def _ci_dtype(col_idx, n):
+    """Column indices travel as int32 whenever they fit (n < 2^31: the
+    library stores int32 indices anyway), halving a pageable int64 array's
+    upload (cast inside the staging copy); page-locked int64 goes by DMA."""
+    if col_idx.dtype == np.int32:
+        return np.int32
+    if _is_pinned(col_idx) or n >= (1 << 31):
+        return np.int64
+    return np.int32
+
+
 def _is_pinned(a) -> bool:
     try:
         return torch().from_numpy(np.ascontiguousarray(a)).is_pinned()
@@ -258,13 +314,32 @@ def _is_pinned(a) -> bool:
 class _Prefetch:
     """Host->device copies of a matrix's CSR arrays issued ahead of use on a
     side copy stream (run_sequence prefetches matrix i+1 while system i
-    solves: the DMA overlaps the kernels).  Only page-locked inputs are
-    prefetched (their copies are pure DMA; pageable ones would stall the
-    host in the staging copy)."""
+    solves: the DMA overlaps the kernels).  Page-locked inputs are pure DMA
+    and are issued directly; pageable ones go through a background thread
+    with its own pinned staging pair (its multi-threaded host copies release
+    the GIL, and the solve waiting in libkrb holds none), so a caller handing
+    in plain numpy arrays gets the same overlap."""
 
     def __init__(self):
         self.items = {}
         self.stream = None
+        self.staging = None
+        import threading
+        self.lock = threading.Lock()
+
+    def _upload(self, A, arrs, slot):
+        t = torch()
+        try:
+            with t.cuda.stream(self.stream):
+                d_rp = to_device(arrs[0], np.int64, staging=self.staging)
+                d_ci = to_device(arrs[1], _ci_dtype(arrs[1], len(arrs[0]) - 1),
+                                 staging=self.staging)
+                d_val = to_device(arrs[2], np.float64, staging=self.staging)
+                ev = t.cuda.Event()
+                ev.record(self.stream)
+            slot["result"] = ((d_rp, d_ci, d_val), ev)
+        except BaseException as e:   # reported at take(): the solve uploads itself
+            slot["error"] = e
 
     def issue(self, A) -> bool:
         if getattr(A, "_device", None) is not None or not hasattr(A, "row_ptr"):
@@ -272,33 +347,50 @@ class _Prefetch:
         if id(A) in self.items or MATRICES.items.get(id(A), (None,))[0] is A:
             return False
         arrs = (np.asarray(A.row_ptr), np.asarray(A.col_idx), np.asarray(A.values))
-        if np.iscomplexobj(arrs[2]) or not all(_is_pinned(a) for a in arrs):
+        if np.iscomplexobj(arrs[2]):
             return False
         t = torch()
         require_cuda()
         if self.stream is None:
             self.stream = t.cuda.Stream()
-        with t.cuda.stream(self.stream):
-            d_rp = to_device(arrs[0], np.int64)
-            d_ci = to_device(arrs[1], np.int32 if arrs[1].dtype == np.int32 else np.int64)
-            d_val = to_device(arrs[2], np.float64)
-            ev = t.cuda.Event()
-            ev.record(self.stream)
-        self.items[id(A)] = (A, (d_rp, d_ci, d_val), ev)
+        slot = {}
+        if all(_is_pinned(a) for a in arrs):
+            self._upload(A, arrs, slot)
+            self.items[id(A)] = (A, slot, None)
+            return True
+        import threading
+        with self.lock:
+            if self.staging is None:
+                self.staging = _Staging()
+            # one background upload at a time (the staging pair is shared)
+            for _, _, th in self.items.values():
+                if th is not None:
+                    th.join()
+            th = threading.Thread(target=self._upload, args=(A, arrs, slot), daemon=True)
+            th.start()
+            self.items[id(A)] = (A, slot, th)
         return True
 
     def take(self, A):
         hit = self.items.pop(id(A), None)
         if hit is None or hit[0] is not A:
             return None
+        if hit[2] is not None:
+            hit[2].join()
+        if "result" not in hit[1]:
+            return None
+        arrays, ev = hit[1]["result"]
         t = torch()
         cur = t.cuda.current_stream()
-        cur.wait_event(hit[2])
-        for d in hit[1]:
+        cur.wait_event(ev)
+        for d in arrays:
             d.record_stream(cur)   # freed after this stream's use, not the copy stream's
-        return hit[1]
+        return arrays
 
     def clear(self):
+        for _, _, th in list(self.items.values()):
+            if th is not None:
+                th.join()
         self.items.clear()
 
 
@@ -323,8 +415,8 @@ class DeviceMatrix:
         else:
             d_rp = to_device(row_ptr, np.int64)
             d_val = to_device(values, np.float64)
-            d_ci = to_device(col_idx, np.int32 if col_idx.dtype == np.int32 else np.int64)
-        fn = "krb_matrix_create" if col_idx.dtype == np.int32 else "krb_matrix_create_i64"
+            d_ci = to_device(col_idx, _ci_dtype(col_idx, self.n))
+        fn = "krb_matrix_create" if d_ci.dtype == t.int32 else "krb_matrix_create_i64"
         try:
             _lib.call(fn, ctypes.byref(h), self.n, self.nnz, ptr(d_rp), ptr(d_ci),
                       ptr(d_val), int(fmt), s)
@@ -465,7 +557,8 @@ PREFETCH = _Prefetch()
 
 def prefetch_matrix(A) -> bool:
     """Start the upload of A's CSR arrays ahead of its first solve (pinned
-    host inputs only); returns whether copies were issued."""
+    inputs: DMA on a copy stream; pageable: a background thread stages them);
+    returns whether an upload was started."""
     return PREFETCH.issue(A)
 
 

@@ -341,3 +341,29 @@ def test_rbicg_deferred_cycle_launch_paths(P, canon):
     assert not D._PENDING
     again = run(None)
     assert again[2].resid == ref[2].resid
+
+
+def test_pageable_int64_prefetch_background_matches(P):
+    """Plain pageable numpy inputs with int64 column indices (the reference
+    SparseMatrix's dtype): prefetch_matrix stages them on a background
+    thread (int64 -> int32 inside the staging copy); the solve equals the
+    one that uploads on first use, bit for bit."""
+    import numpy as np
+    from paper_1406_2831_b200 import device as D
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence("c2", small=True)
+    A = seq.matrix(1)
+    b = seq.rhs(1, 0)
+    ci64 = A.col_idx.astype(np.int64)
+    # the cast staging itself, across several pipeline chunks
+    big = np.random.default_rng(0).integers(0, 2**31 - 1, size=3_000_001, dtype=np.int64)
+    got = D.to_device(big, np.int32).cpu().numpy()
+    assert got.dtype == np.int32 and np.array_equal(got, big.astype(np.int32))
+    cfg = P.SolverConfig(tol=1e-10, max_itn=500, seed=3)
+    M1 = P.SparseMatrix(A.n, A.n, A.row_ptr, ci64, A.values)
+    x1, h1 = P.bicgstab_solve(M1, b, config=cfg)
+    M2 = P.SparseMatrix(A.n, A.n, A.row_ptr.copy(), ci64.copy(), A.values.copy())
+    assert D.prefetch_matrix(M2)
+    x2, h2 = P.bicgstab_solve(M2, b, config=cfg)
+    assert not D.PREFETCH.items
+    assert h1.resid == h2.resid and np.array_equal(x1, x2)

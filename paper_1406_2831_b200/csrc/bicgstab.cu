@@ -144,7 +144,7 @@ constexpr int64_t kTdotSmallNb = 4 * kNumSMs;
 // 1258 us.)
 // kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (uniform
 // slices: offsets by warp shuffle), 3 its first version (tuning spmv_variant=1).
-template <int kF, int kSlot, int kMinB = 1>
+template <int kF, int kSlot, int kMinB = 1, int kBU = 4>
 __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status,
@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const do
     if (kt && blockIdx.x == 0 && threadIdx.x == 0 && run == KRB_RUNNING)
       *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
     if (i < A.n) {
-      const double yi = spmv_row_dict<kF == 2 ? 0 : 1>(i, A, [x](int c) { return __ldg(x + c); }, pf);
+      auto xf = [x](int c) { return __ldg(x + c); };
+      const double yi = spmv_row_dict<kF == 2 ? 0 : 1, decltype(xf), kBU>(i, A, xf, pf);
       if (run == KRB_RUNNING) y[i] = yi;
     }
     if (run != KRB_RUNNING) return;
@@ -249,8 +250,15 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
   // offset-coded: at most 40 registers (6 CTAs / SM; 47 unbounded, 5 CTAs:
   // 776 vs 746 us live on C5; 32 registers spill: 776)
-  if (h.A.dcode && tuning().spmv_variant == 1)
+  const int sv = tuning().spmv_variant;
+  if (h.A.dcode && sv == 1)
     k_iter_spmv<3, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+  else if (h.A.dcode && sv == 2)
+    k_iter_spmv<2, kSecond ? 5 : 1, 5><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+  else if (h.A.dcode && sv == 3)
+    k_iter_spmv<2, kSecond ? 5 : 1, 4, 8><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
+  else if (h.A.dcode && sv == 4)
+    k_iter_spmv<2, kSecond ? 5 : 1, 5, 8><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.dcode)
     k_iter_spmv<2, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.format == 2)

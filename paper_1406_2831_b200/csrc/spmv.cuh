@@ -88,7 +88,7 @@ __device__ __forceinline__ double spmv_row(int64_t i, const krb_matrix &A,
 // lane as one int4 broadcast, tuning spmv_variant=1).
 // pf > 0: lane 0 of each warp bulk-prefetches into L2 the value bytes pf
 // beyond its own slice (the slices a later wave will stream).
-template <int kV = 0, class XF>
+template <int kV = 0, class XF, int kBU = 4>
 __device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A, XF xf,
                                                int64_t pf = 0) {
   constexpr int kB = 4;
@@ -111,18 +111,25 @@ __device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A, 
     for (int j0 = 0; j0 < len; j0 += 32) {
       const int mine = j0 + l < len ? __ldg(orow + j0 + l) : 0;
       const int m = min(32, len - j0);
-      for (int j = 0; j < m; j += kB) {
-        int c[kB];
-        double v[kB], xv[kB];
+      const double *__restrict__ vj = vp + 32 * j0;
+      int j = 0;
+      // full batches: no per-element predicates, so all 2 kB loads issue
+      // before the first multiply
+      for (; j + kBU <= m; j += kBU) {
+        int c[kBU];
+        double v[kBU], xv[kBU];
 #pragma unroll
-        for (int u = 0; u < kB; ++u) c[u] = row + __shfl_sync(0xffffffffu, mine, (j + u) & 31);
+        for (int u = 0; u < kBU; ++u) c[u] = row + __shfl_sync(0xffffffffu, mine, j + u);
 #pragma unroll
-        for (int u = 0; u < kB; ++u) v[u] = j + u < m ? __ldg(vp + 32 * (j0 + j + u)) : 0.0;
+        for (int u = 0; u < kBU; ++u) v[u] = __ldg(vj + 32 * (j + u));
 #pragma unroll
-        for (int u = 0; u < kB; ++u) xv[u] = j + u < m ? xf(c[u]) : 0.0;
+        for (int u = 0; u < kBU; ++u) xv[u] = xf(c[u]);
 #pragma unroll
-        for (int u = 0; u < kB; ++u)
-          if (j + u < m) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+        for (int u = 0; u < kBU; ++u) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+      }
+      for (; j < m; ++j) {
+        const int c = row + __shfl_sync(0xffffffffu, mine, j);
+        sum = __dadd_rn(sum, __dmul_rn(__ldg(vj + 32 * j), xf(c)));
       }
     }
     return sum;

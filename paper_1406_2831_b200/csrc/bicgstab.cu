@@ -249,16 +249,12 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   double *y = kSecond ? h.t : h.q;
   const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
   // offset-coded: at most 40 registers (6 CTAs / SM; 47 unbounded, 5 CTAs:
-  // 776 vs 746 us live on C5; 32 registers spill: 776)
-  const int sv = tuning().spmv_variant;
-  if (h.A.dcode && sv == 1)
+  // 776 vs 746 us live on C5; 32 registers spill: 776).  In-process A/B of
+  // the iteration (profiles/r02_spmv_variants_ab2.jsonl): 4 entries per
+  // batch at 40 registers 4666 us, at 48: 4743; 8 entries at 48 / 60
+  // registers: 4706 / 4969; the int4-offset version: 4666 (median 4783).
+  if (h.A.dcode && tuning().spmv_variant == 1)
     k_iter_spmv<3, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
-  else if (h.A.dcode && sv == 2)
-    k_iter_spmv<2, kSecond ? 5 : 1, 5><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
-  else if (h.A.dcode && sv == 3)
-    k_iter_spmv<2, kSecond ? 5 : 1, 4, 8><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
-  else if (h.A.dcode && sv == 4)
-    k_iter_spmv<2, kSecond ? 5 : 1, 5, 8><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.dcode)
     k_iter_spmv<2, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.format == 2)

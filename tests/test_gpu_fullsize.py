@@ -40,9 +40,20 @@ def test_fullsize_spmv_bitwise_vs_scipy(P, name):
     x = np.random.default_rng(0).standard_normal(A.n)
     S = A.to_scipy()
     assert np.array_equal(M.spmv(to_device(x)).cpu().numpy(), S @ x)
-    if name != "c5":   # transpose build + scipy transpose at 449M nnz is slow
+    if name != "c5":
         assert np.array_equal(M.spmv(to_device(x), transpose=True).cpu().numpy(),
                               S.T.tocsr() @ x)
+    else:
+        # scipy's .T.tocsr() at 449M nnz is too slow; the same order without
+        # it: products in CSR order, then per column added sequentially in
+        # ascending row order from 0.0 (np.add.at applies the entries in
+        # index order) == csr_matvec of the transpose
+        rows = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.row_ptr))
+        want = np.zeros(A.n)
+        np.add.at(want, A.col_idx, A.values * x[rows])
+        del rows
+        got = M.spmv(to_device(x), transpose=True).cpu().numpy()
+        assert np.array_equal(got, want)
 
 
 def test_fullsize_canonical_dot_and_projection(P, canon):

@@ -97,7 +97,6 @@ struct Tuning {
   int spmv_prefetch_mb = 6;  // offset-coded SpMV: bulk L2 prefetch distance ahead (MB, 0 = off)
   int spmm_variant = 1;      // offset-coded SpMM: 0 generic kernel, 1 k_spmm_dict (L2 prefetch)
   int phase_pf_rows = 1;     // graph P / S / X: L2 prefetch distance (1024-element rows)
-  int persist_dict = 1;      // fused persistent kernel: offset-coded SpMV rows
   int spmv_variant = 0;   // offset-coded SpMV: 0 = uniform offsets by warp shuffle, 1 = int4 loads
 };
 Tuning &tuning();

@@ -405,17 +405,7 @@ __device__ __forceinline__ void correct_warps(double *stage, const double *Cm, i
   }
 }
 
-// kF: 0 CSR, 1 SELL-32, 2 offset-coded SELL-32 (the fused SpMVs read the
-// shared offset rows / code bytes instead of int32 columns)
-template <int kF, class XF>
-__device__ __forceinline__ double p2_row(int64_t i, const krb_matrix &A, XF xf, uint64_t polm) {
-  if constexpr (kF == 2)
-    return spmv_row_dict<0, XF, 4>(i, A, xf, 0);
-  else
-    return spmv_row_f<kF == 1, 4, true>(i, A, xf, polm);
-}
-
-template <int kE, int kF>
+template <int kE, bool kSell>
 __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict__ pa) {
   extern __shared__ double stage[];   // kStages x kTileCols x 1024
   __shared__ double zeta[kV2MaxK], gamma[kV2MaxK], xc[kV2MaxK];
@@ -483,7 +473,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
             const double pv = pf((int)i);   // solvers.py:303
             pn[i] = pv;
             preg[bi][e] = pv;
-            const double qv = p2_row<kF>(i, A, pf, polm);
+            const double qv = spmv_row_f<kSell, 4, true>(i, A, pf, polm);
             qn[i] = qv;
             qreg[bi][e] = qv;
           }
@@ -561,7 +551,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
             s[i] = sv;
             sreg[bi][e] = sv;
             acc[0] = __fma_rn(sv, sv, acc[0]);
-            const double tv = p2_row<kF>(i, A, sf, polm);
+            const double tv = spmv_row_f<kSell, 4, true>(i, A, sf, polm);
             tv_[i] = tv;
             treg[bi][e] = tv;
             if (k == 0) {   // D's dots, straight from registers
@@ -687,7 +677,7 @@ __global__ void __launch_bounds__(1024, 1) k_persist2(const IterArgs *__restrict
   }
 }
 
-template <int kE, int kSell>
+template <int kE, bool kSell>
 static int persist2_launch(const IterArgs *d, int64_t nb, cudaStream_t st) {
   static int grid = 0;
   if (grid == 0) {
@@ -753,12 +743,8 @@ int launch_persistent(const IterArgs &h, const IterArgs *d, cudaStream_t st, int
   if (v2) {
     *driver = KRB_DRIVER_FUSED;
     switch (canon_E(h.n)) {
-      case 1:
-        return h.A.dcode && tuning().persist_dict ? persist2_launch<1, 2>(d, h.nb, st)
-               : sell ? persist2_launch<1, 1>(d, h.nb, st) : persist2_launch<1, 0>(d, h.nb, st);
-      case 2:
-        return h.A.dcode && tuning().persist_dict ? persist2_launch<2, 2>(d, h.nb, st)
-               : sell ? persist2_launch<2, 1>(d, h.nb, st) : persist2_launch<2, 0>(d, h.nb, st);
+      case 1: return sell ? persist2_launch<1, true>(d, h.nb, st) : persist2_launch<1, false>(d, h.nb, st);
+      case 2: return sell ? persist2_launch<2, true>(d, h.nb, st) : persist2_launch<2, false>(d, h.nb, st);
       default: break;
     }
     *driver = KRB_DRIVER_PERSISTENT;

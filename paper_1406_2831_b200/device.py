@@ -327,9 +327,11 @@ class _Prefetch:
         import threading
         self.lock = threading.Lock()
 
-    def _upload(self, A, arrs, slot):
+    def _upload(self, A, arrs, slot, dev=None):
         t = torch()
         try:
+            if dev is not None:
+                t.cuda.set_device(dev)   # a new thread starts on device 0
             with t.cuda.stream(self.stream):
                 d_rp = to_device(arrs[0], np.int64, staging=self.staging)
                 d_ci = to_device(arrs[1], _ci_dtype(arrs[1], len(arrs[0]) - 1),
@@ -366,7 +368,8 @@ class _Prefetch:
             for _, _, th in self.items.values():
                 if th is not None:
                     th.join()
-            th = threading.Thread(target=self._upload, args=(A, arrs, slot), daemon=True)
+            th = threading.Thread(target=self._upload,
+                                  args=(A, arrs, slot, t.cuda.current_device()), daemon=True)
             th.start()
             self.items[id(A)] = (A, slot, th)
         return True

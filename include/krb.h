@@ -55,7 +55,8 @@ int64_t krb_launch_count(void);
  * "cluster", "persist_v1", "gemm_mode", "l2keep", "phase_variant",
  * "tdot_variant", "spmv_variant", "spmm_variant", "phase_pf_rows",
  * "spmv_prefetch_mb" (bulk L2 prefetch
- * distance of the offset-coded SpMV, default 6).  Unknown key -> KRB_EINVAL.
+ * distance of the offset-coded SpMV, default 6), "value_coding" (value
+ * tables for constant diagonals, default 1).  Unknown key -> KRB_EINVAL.
  * No reference counterpart (the reference has no device drivers). */
 int krb_set_tuning(const char *key, int64_t value);
 int krb_reset_tuning(void);
@@ -113,7 +114,8 @@ int krb_matrix_destroy(krb_matrix *A);
  * other stream may still use the matrix. */
 int krb_matrix_destroy_async(krb_matrix *A, void *stream);
 /* n, nnz, chosen format (1 CSR, 2 SELL-32, 3 SELL-C-sigma, 4 SELL-32 with
- * offset-coded columns), device bytes held (incl. transpose when built) */
+ * offset-coded columns, 5 = 4 with value tables for the constant
+ * diagonals), device bytes held (incl. transpose when built) */
 int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz,
                     int *format, int64_t *bytes);
 /* Bytes one y = A x streams in the chosen format (matrix arrays the kernel
@@ -121,6 +123,18 @@ int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz,
  * offset-coded format (one shared offset row) and its dictionary size. */
 int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t *nslices,
                             int64_t *uniform_slices, int *ndict);
+/* Value-coded format (5): a diagonal col - row whose entries are all
+ * bit-identical (constant-coefficient stencils: every diagonal of K in
+ * s E - K but the main one) is served from a table instead of the value
+ * stream -- same value bits, same row order, so the same products as
+ * sparse.py:117-121.  Rows with the same offset sequence share a template
+ * (offsets + table values, a few KB per matrix); a row then reads its
+ * template id and only the values of its varying entries.  const_entries:
+ * entries served from the tables (0: not value-coded), templates: distinct
+ * row templates, const_diagonals: constant diagonals among the ndict offsets.
+ * Chosen automatically when at least half of the entries qualify. */
+int krb_matrix_value_stats(const krb_matrix *A, int64_t *const_entries, int *templates,
+                           int *const_diagonals);
 
 /* Identity and reference count of the shared sparsity pattern behind A
  * (matrices with equal row_ptr / col_idx share the SELL layout, the offset

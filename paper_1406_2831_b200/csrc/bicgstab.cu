@@ -143,7 +143,8 @@ constexpr int64_t kTdotSmallNb = 4 * kNumSMs;
 // memory costs 48 registers; a grid-stride variant with 6 x 148 CTAs:
 // 1258 us.)
 // kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (uniform
-// slices: offsets by warp shuffle), 3 its first version (tuning spmv_variant=1).
+// slices: offsets by warp shuffle), 3 its first version (tuning spmv_variant=1),
+// 4 value-coded (constant diagonals from the value tables).
 template <int kF, int kSlot, int kMinB = 1, int kBU = 4>
 __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
@@ -160,7 +161,11 @@ __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const do
       *(volatile uint64_t *)&kt[4 * kSlot] = globaltimer();
     if (i < A.n) {
       auto xf = [x](int c) { return __ldg(x + c); };
-      const double yi = spmv_row_dict<kF == 2 ? 0 : 1, decltype(xf), kBU>(i, A, xf, pf);
+      double yi;
+      if (kF == 4)
+        yi = spmv_row_tmpl(i, A, xf);
+      else
+        yi = spmv_row_dict<kF == 3 ? 1 : 0, decltype(xf), kBU>(i, A, xf, pf);
       if (run == KRB_RUNNING) y[i] = yi;
     }
     if (run != KRB_RUNNING) return;
@@ -253,7 +258,9 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   // the iteration (profiles/r02_spmv_variants_ab2.jsonl): 4 entries per
   // batch at 40 registers 4666 us, at 48: 4743; 8 entries at 48 / 60
   // registers: 4706 / 4969; the int4-offset version: 4666 (median 4783).
-  if (h.A.dcode && tuning().spmv_variant == 1)
+  if (h.A.tent && tuning().value_coding)
+    k_iter_spmv<4, kSecond ? 5 : 1, 4><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
+  else if (h.A.dcode && tuning().spmv_variant == 1)
     k_iter_spmv<3, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
   else if (h.A.dcode)
     k_iter_spmv<2, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);
@@ -493,7 +500,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
                    G.ktime == cfg->d_kernel_times &&
                    G.variant == tuning().phase_variant + 16 * tuning().tdot_variant +
                                     256 * tuning().spmv_variant +
-                                    4096 * tuning().spmv_prefetch_mb;
+                                    4096 * tuning().spmv_prefetch_mb +
+                                    (1 << 24) * tuning().value_coding;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -513,7 +521,8 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     G.n = n; G.k = k; G.format = A->format; G.sig = sig;
     G.ktime = cfg->d_kernel_times;
     G.variant = tuning().phase_variant + 16 * tuning().tdot_variant +
-                256 * tuning().spmv_variant + 4096 * tuning().spmv_prefetch_mb;
+                256 * tuning().spmv_variant + 4096 * tuning().spmv_prefetch_mb +
+                (1 << 24) * tuning().value_coding;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

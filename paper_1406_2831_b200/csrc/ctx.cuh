@@ -98,6 +98,7 @@ struct Tuning {
   int spmm_variant = 1;      // offset-coded SpMM: 0 generic kernel, 1 k_spmm_dict (L2 prefetch)
   int phase_pf_rows = 1;     // graph P / S / X: L2 prefetch distance (1024-element rows)
   int spmv_variant = 0;   // offset-coded SpMV: 0 = uniform offsets by warp shuffle, 1 = int4 loads
+  int value_coding = 1;   // value tables of constant diagonals: 0 = neither built nor used
 };
 Tuning &tuning();
 

@@ -17,6 +17,11 @@
 // Device sparse matrix (CSR + optional SELL-32 + lazily built transpose).
 struct krb_precond;
 struct krb_pattern;   // shared sparsity structure (matrix.cu)
+struct __align__(16) krb_tentry {
+  int32_t off;    // col - row
+  int32_t cst;    // 1: the value below; 0: the row's own s_val entry
+  double val;
+};
 struct krb_matrix {
   int64_t n = 0, nnz = 0;
   int format = 0;  // 1 CSR, 2 SELL
@@ -42,6 +47,28 @@ struct krb_matrix {
   int32_t *dict = nullptr;  // 256 entries (sorted distinct offsets, zero-padded)
   int ndict = 0;
   int64_t dcode_bytes = 0, uniform_slices = 0;
+  int32_t *rep = nullptr;   // 256: one CSR entry index per offset code (pattern)
+  // row templates (pattern level, built with the offset codes when no row is
+  // longer than 64 and the rows use at most 1024 distinct offset sequences):
+  // row i has the offset sequence of template tid[i]; template t has tlen[t]
+  // entries with codes tcode[64 t + j]
+  int32_t *tid = nullptr;
+  int32_t *tlen = nullptr;
+  uint8_t *tcode = nullptr;
+  int ntmpl = 0, tstride = 0;   // tstride: longest template, rounded up to 4
+  int64_t *code_count = nullptr;   // HOST array (256): entries per offset code
+  // value-coded format (matrix level, built beside s_val when most entries
+  // lie on diagonals col - row whose values are all bit-identical:
+  // constant-coefficient stencils, where only the main diagonal of s E - K
+  // varies).  Entries of such a diagonal come from a table instead of the
+  // s_val stream (same value bits, same order, same arithmetic -> same
+  // results): vtab[d] = the value of offset code d, then 256 flag bytes
+  // (1 = constant); tent[tstride t + j] = {offset, constant?, value} of
+  // entry j of template t -- a few KB, L1-resident, so a row costs its tid,
+  // its varying entries and its x gathers.
+  double *vtab = nullptr;
+  krb_tentry *tent = nullptr;
+  int64_t vconst_entries = 0;   // entries served from the tables
   krb_matrix *T = nullptr;  // lazily built transpose
   // the structure arrays above (rp, ci, sl_ptr, rlen, s_col, perm, dcode,
   // dptr, dict) belong to this reference-counted pattern, shared by every
@@ -73,7 +100,7 @@ void dev_free(void *p, cudaStream_t st);
 // for a matrix with the same signature -- freed and re-allocated arrays can
 // come back at the address of another matrix's CSR values).
 struct MatrixSig {
-  const void *p[22];
+  const void *p[28];
   int64_t n = -1, serial = 0;
   int format = -1;
 };

@@ -92,9 +92,9 @@ MatrixSig matrix_sig(const krb_matrix *A) {
   const void *ptrs[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val,
                         A->perm, B->rp, B->ci, B->val, B->sl_ptr, B->rlen, B->s_col,
                         B->s_val, B->perm, A->dcode, A->dptr, A->dict, B->dcode, B->dptr,
-                        B->dict};
+                        B->dict, A->vtab, A->tent, A->tid, B->vtab, B->tent, B->tid};
   static_assert(sizeof(ptrs) == sizeof(g.p), "MatrixSig size");
-  for (int i = 0; i < 22; ++i) g.p[i] = ptrs[i];
+  for (int i = 0; i < 28; ++i) g.p[i] = ptrs[i];
   g.n = A->n;
   g.format = A->format;
   g.serial = precond_serial(A->pre);
@@ -107,14 +107,18 @@ bool same_sig(const MatrixSig &a, const MatrixSig &b) {
 }
 
 // offset-coded SELL-32 (identity row order)
-template <int kV>
-__global__ void __launch_bounds__(256, 6) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
+template <int kV, bool kVC = false>
+__global__ void __launch_bounds__(256, kVC ? 4 : 6) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status, int64_t pf) {
   if (status && *status) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
-  y[i] = spmv_row_dict<kV>(i, A, [x](int c) { return __ldg(x + c); }, pf);
+  auto xf = [x](int c) { return __ldg(x + c); };
+  if (kVC)
+    y[i] = spmv_row_tmpl(i, A, xf);
+  else
+    y[i] = spmv_row_dict<kV, decltype(xf), 4>(i, A, xf, pf);
 }
 
 int spmv_launch(const krb_matrix *A, const double *x, double *y,
@@ -123,7 +127,9 @@ int spmv_launch(const krb_matrix *A, const double *x, double *y,
   if (A->pre) return precond_apply_op(A, x, y, d_status, st);
   int64_t blocks = (A->n + 255) / 256;
   const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
-  if (A->dcode && tuning().spmv_variant == 1)
+  if (A->tent && tuning().value_coding)
+    k_spmv_dict<0, true><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, 0);
+  else if (A->dcode && tuning().spmv_variant == 1)
     k_spmv_dict<1><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, pf);
   else if (A->dcode)
     k_spmv_dict<0><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, pf);
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(256) k_spmm(krb_matrix A, int ncols,
 // C5, 30 columns (A/B): <8, 1> 11.5 ms, <8, 2> 12.9 ms (80 registers),
 // <4, 4> 27.6 ms (84 registers, twice the matrix passes), the generic
 // k_spmm<2, 8> 15.9 ms.
-template <int kNC, int kB>
+template <int kNC, int kB, bool kVC = false>
 __global__ void __launch_bounds__(256) k_spmm_dict(krb_matrix A, int ncols,
                                                    const double *__restrict__ X, int64_t ldx,
                                                    double *__restrict__ Y, int64_t ldy,
@@ -220,39 +226,69 @@ __global__ void __launch_bounds__(256) k_spmm_dict(krb_matrix A, int ncols,
   for (int c = 0; c < kNC; ++c) sum[c] = 0.0;
   const int64_t s = i >> 5;
   const int l = (int)(i & 31);
-  const int len = __ldg(A.rlen + i);
   const int64_t vbase = __ldg(A.sl_ptr + s);
   const double *__restrict__ vp = A.s_val + vbase + l;
-  if (pf > 0 && l == 0) {
-    const int64_t at = vbase + pf / 8, nbytes = 256 * (int64_t)len;
-    if (at + nbytes / 8 <= A.sell_elems && nbytes > 0) prefetch_l2_bulk(A.s_val + at, (uint32_t)nbytes);
-  }
-  const int64_t dp = __ldg(A.dptr + s);
-  const bool uni = dp & 1;
-  const uint8_t *__restrict__ cp = A.dcode + (dp >> 1) + (uni ? 0 : l);
   const int row = (int)i;
-  for (int j = 0; j < len; j += kB) {
-    int col[kB];
-    double v[kB], g[kB][kNC];
+  if (kVC) {
+    // value-coded: the row's template (spmv_row_tmpl) supplies offsets and
+    // the values of the constant diagonals
+    const int t = __ldg(A.tid + i);
+    const int len = __ldg(A.tlen + t);
+    const int4 *__restrict__ te = reinterpret_cast<const int4 *>(A.tent) + (int64_t)t * A.tstride;
+    for (int j = 0; j < len; j += kB) {
+      int col[kB];
+      double v[kB], g[kB][kNC];
 #pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      const bool ok = j + u < len;
-      col[u] = ok ? row + (uni ? __ldg(reinterpret_cast<const int32_t *>(cp) + j + u)
-                               : __ldg(A.dict + __ldg(cp + 32 * (j + u))))
-                  : row;
-      v[u] = ok ? __ldg(vp + 32 * (j + u)) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kB; ++u)
-#pragma unroll
-      for (int c = 0; c < kNC; ++c)
-        g[u][c] = (j + u < len && c < nc) ? __ldg(Xc + (int64_t)c * ldx + col[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < kB; ++u)
-      if (j + u < len) {
-#pragma unroll
-        for (int c = 0; c < kNC; ++c) sum[c] = __dadd_rn(sum[c], __dmul_rn(v[u], g[u][c]));
+      for (int u = 0; u < kB; ++u) {
+        const bool ok = j + u < len;
+        const int4 e = ok ? __ldg(te + j + u) : make_int4(0, 1, 0, 0);
+        col[u] = row + e.x;
+        v[u] = e.y ? __hiloint2double(e.w, e.z) : __ldg(vp + 32 * (j + u));
       }
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+#pragma unroll
+        for (int c = 0; c < kNC; ++c)
+          g[u][c] = (j + u < len && c < nc) ? __ldg(Xc + (int64_t)c * ldx + col[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (j + u < len) {
+#pragma unroll
+          for (int c = 0; c < kNC; ++c) sum[c] = __dadd_rn(sum[c], __dmul_rn(v[u], g[u][c]));
+        }
+    }
+  } else {
+    const int len = __ldg(A.rlen + i);
+    if (pf > 0 && l == 0) {
+      const int64_t at = vbase + pf / 8, nbytes = 256 * (int64_t)len;
+      if (at + nbytes / 8 <= A.sell_elems && nbytes > 0) prefetch_l2_bulk(A.s_val + at, (uint32_t)nbytes);
+    }
+    const int64_t dp = __ldg(A.dptr + s);
+    const bool uni = dp & 1;
+    const uint8_t *__restrict__ cp = A.dcode + (dp >> 1) + (uni ? 0 : l);
+    for (int j = 0; j < len; j += kB) {
+      int col[kB];
+      double v[kB], g[kB][kNC];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const bool ok = j + u < len;
+        col[u] = ok ? row + (uni ? __ldg(reinterpret_cast<const int32_t *>(cp) + j + u)
+                                 : __ldg(A.dict + __ldg(cp + 32 * (j + u))))
+                    : row;
+        v[u] = ok ? __ldg(vp + 32 * (j + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+#pragma unroll
+        for (int c = 0; c < kNC; ++c)
+          g[u][c] = (j + u < len && c < nc) ? __ldg(Xc + (int64_t)c * ldx + col[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (j + u < len) {
+#pragma unroll
+          for (int c = 0; c < kNC; ++c) sum[c] = __dadd_rn(sum[c], __dmul_rn(v[u], g[u][c]));
+        }
+    }
   }
   double *Yc = Y + (int64_t)c0 * ldy;
 #pragma unroll
@@ -268,7 +304,10 @@ int spmm_launch(const krb_matrix *M, int64_t ncols, const double *X, int64_t ldx
     const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
     const unsigned gx = (unsigned)((M->n + 255) / 256);
     dim3 grid(gx, (unsigned)((ncols + 7) / 8));
-    k_spmm_dict<8, 1><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy, pf);
+    if (M->tent && tuning().value_coding)
+      k_spmm_dict<8, 1, true><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy, 0);
+    else
+      k_spmm_dict<8, 1><<<grid, 256, 0, st>>>(*M, (int)ncols, X, ldx, Y, ldy, pf);
     KRB_CHECK_LAUNCH();
     return KRB_OK;
   }
@@ -511,6 +550,31 @@ __global__ void k_dict_fill(int64_t n, int64_t nslices, const int64_t *__restric
   if (l == 0) dptr[s] = (cb << 1) | (uni[s] ? 1 : 0);
 }
 
+// one CSR entry index per offset code (any entry of that diagonal; the race
+// between writers is benign)
+__global__ void __launch_bounds__(256) k_dict_rep(int64_t n, const int64_t *__restrict__ rp,
+                                                  const int32_t *__restrict__ ci,
+                                                  const int32_t *__restrict__ dict, int nd,
+                                                  int32_t *__restrict__ rep) {
+  __shared__ int32_t sd[256];
+  __shared__ int sf[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    sd[t] = dict[t];
+    sf[t] = -1;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    for (int64_t jj = rp[i]; jj < rp[i + 1]; ++jj) {
+      const int code = dict_code(sd, nd, ci[jj] - (int32_t)i);
+      if (sf[code] < 0) sf[code] = (int)jj;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nd; t += blockDim.x)
+    if (sf[t] >= 0 && rep[t] < 0) rep[t] = sf[t];
+}
+
 // Build the offset-coded stream beside an identity-order SELL-32 matrix when
 // its entries use at most 255 distinct offsets col - row.  Leaves the matrix
 // untouched (dcode == NULL) otherwise.
@@ -578,13 +642,294 @@ static int build_dict(krb_matrix *A, cudaStream_t st) {
   k_dict_fill<<<wb, 256, 0, st>>>(n, ns, A->sl_ptr, A->rlen, A->s_col, A->dict, num, cptr, uni,
                                   A->dcode, A->dptr);
   KRB_CHECK_LAUNCH();
+  // one CSR entry per offset code (where the value tables take their values)
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->rep, sizeof(int32_t) * 256, st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(A->rep, 0xff, sizeof(int32_t) * 256, st));
+  k_dict_rep<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, A->rp, A->ci, A->dict, num, A->rep);
+  KRB_CHECK_LAUNCH();
   dev_free(bytes, st);
   dev_free(cptr, st);
   dev_free(uni, st);
   dev_free(nuni, st);
   dev_free(uniq, st);
   A->dcode_bytes = total;
-  A->bytes += total + ns * 8 + 256 * 4;
+  A->bytes += total + ns * 8 + 256 * 8;
+  return KRB_OK;
+}
+static int build_templates(krb_matrix *A, cudaStream_t st);
+
+// ---- value tables of a value-coded matrix (krb_internal.cuh) --------------
+// flag[d] = 1 where some entry of diagonal d differs (bitwise) from vtab[d]
+__global__ void __launch_bounds__(256) k_vc_check(int64_t n, const int64_t *__restrict__ rp,
+                                                  const int32_t *__restrict__ ci,
+                                                  const double *__restrict__ val,
+                                                  const int32_t *__restrict__ dict, int nd,
+                                                  const double *__restrict__ vtab,
+                                                  int *__restrict__ varies) {
+  __shared__ int32_t sd[256];
+  __shared__ unsigned long long sv[256];
+  __shared__ int sf[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    sd[t] = dict[t];
+    sv[t] = (unsigned long long)__double_as_longlong(vtab[t]);
+    sf[t] = 0;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    for (int64_t jj = rp[i]; jj < rp[i + 1]; ++jj) {
+      const int code = dict_code(sd, nd, ci[jj] - (int32_t)i);
+      if ((unsigned long long)__double_as_longlong(val[jj]) != sv[code] && !sf[code]) sf[code] = 1;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nd; t += blockDim.x)
+    if (sf[t] && !varies[t]) varies[t] = 1;
+}
+
+__global__ void k_vc_pick(int nd, const int32_t *__restrict__ rep, const double *__restrict__ val,
+                          double *__restrict__ vtab) {
+  const int t = threadIdx.x;
+  if (t < 256) vtab[t] = (t < nd && rep[t] >= 0) ? val[rep[t]] : 0.0;
+}
+
+// flag bytes behind the table; values of the varying diagonals zeroed
+__global__ void k_vc_flags(int nd, const int *__restrict__ varies, double *__restrict__ vtab) {
+  const int t = threadIdx.x;
+  uint8_t *fl = reinterpret_cast<uint8_t *>(vtab + 256);
+  if (t < 256) fl[t] = (t < nd && !varies[t]) ? 1 : 0;
+}
+
+// ---- row templates (pattern level) ----------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t h, uint64_t v) {
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  h *= 0xff51afd7ed558ccdull;
+  return h ^ (h >> 33);
+}
+
+// hash of row i's offset sequence (length included)
+__global__ void k_row_hash(int64_t n, const int64_t *__restrict__ rp,
+                           const int32_t *__restrict__ ci, uint64_t *__restrict__ hash,
+                           int *__restrict__ maxlen) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t b = rp[i], e = rp[i + 1];
+  uint64_t h = mix64(0x243f6a8885a308d3ull, (uint64_t)(e - b));
+  for (int64_t jj = b; jj < e; ++jj) h = mix64(h, (uint64_t)(uint32_t)(ci[jj] - (int32_t)i));
+  hash[i] = h;
+  if (e - b > 64) atomicMax(maxlen, (int)(e - b > 1 << 30 ? 1 << 30 : e - b));
+}
+
+// template of row i = position of its hash among the sorted distinct hashes;
+// rep_row[t] = some row of template t (the race between writers is benign)
+__global__ void k_row_tid(int64_t n, const uint64_t *__restrict__ hash,
+                          const uint64_t *__restrict__ uniq, int nt, int32_t *__restrict__ tid,
+                          int32_t *__restrict__ rep_row) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = hash[i];
+  int lo = 0, hi = nt - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (uniq[mid] < h) lo = mid + 1; else hi = mid;
+  }
+  tid[i] = lo;
+  if (rep_row[lo] < 0) rep_row[lo] = (int32_t)i;
+}
+
+// template t <- the codes of its representative row
+__global__ void k_tmpl_fill(int nt, const int32_t *__restrict__ rep_row,
+                            const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            const int32_t *__restrict__ dict, int nd, int32_t *__restrict__ tlen,
+                            uint8_t *__restrict__ tcode) {
+  __shared__ int32_t sd[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) sd[t] = dict[t];
+  __syncthreads();
+  const int t = blockIdx.x, j = threadIdx.x;
+  const int64_t r = rep_row[t];
+  const int64_t b = rp[r];
+  const int len = (int)(rp[r + 1] - b);
+  if (j == 0) tlen[t] = len;
+  if (j < 64) tcode[64 * t + j] = j < len ? (uint8_t)dict_code(sd, nd, ci[b + j] - (int32_t)r) : 0;
+}
+
+// every row against its template (a hash collision clears *ok); rows per template
+__global__ void __launch_bounds__(256) k_tmpl_verify(int64_t n, const int64_t *__restrict__ rp,
+                                                     const int32_t *__restrict__ ci,
+                                                     const int32_t *__restrict__ dict,
+                                                     const int32_t *__restrict__ tid,
+                                                     const int32_t *__restrict__ tlen,
+                                                     const uint8_t *__restrict__ tcode,
+                                                     unsigned long long *__restrict__ rows_of,
+                                                     int *__restrict__ ok) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  const int t = valid ? tid[i] : -1;
+  if (valid) {
+    const int64_t b = rp[i];
+    const int len = (int)(rp[i + 1] - b);
+    bool same = len == tlen[t];
+    for (int j = 0; same && j < len; ++j)
+      same = ci[b + j] - (int32_t)i == dict[tcode[64 * t + j]];
+    if (!same) *ok = 0;
+  }
+  // one atomic per group of lanes with the same template
+  const unsigned grp = __match_any_sync(0xffffffffu, t);
+  if (valid && (threadIdx.x & 31) == __ffs(grp) - 1)
+    atomicAdd(rows_of + t, (unsigned long long)__popc(grp));
+}
+
+// Row templates of an offset-coded pattern: rows with the same offset
+// sequence share template tid[i] (C5: the 27 boundary combinations of the
+// 27-point stencil).  Left unbuilt (tid == NULL) when a row is longer than 64
+// or there are more than 1024 distinct sequences.
+constexpr int kMaxTemplates = 1024;
+static int build_templates(krb_matrix *A, cudaStream_t st) {
+  const int64_t n = A->n;
+  if (!A->dcode || n == 0 || A->nnz == 0) return KRB_OK;
+  uint64_t *hash = nullptr, *sorted = nullptr, *uniq = nullptr;
+  int *d_num = nullptr;
+  KRB_CHECK_CUDA(dev_alloc((void **)&hash, sizeof(uint64_t) * n, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&sorted, sizeof(uint64_t) * n, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&uniq, sizeof(uint64_t) * n, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&d_num, 2 * sizeof(int), st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(d_num, 0, 2 * sizeof(int), st));
+  const unsigned rb = (unsigned)((n + 255) / 256);
+  k_row_hash<<<rb, 256, 0, st>>>(n, A->rp, A->ci, hash, d_num + 1);
+  KRB_CHECK_LAUNCH();
+  void *tmp = nullptr;
+  size_t tb1 = 0, tb2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tb1, hash, sorted, (int)n, 0, 64, st);
+  cub::DeviceSelect::Unique(nullptr, tb2, sorted, uniq, d_num, (int)n, st);
+  KRB_CHECK_CUDA(dev_alloc(&tmp, tb1 > tb2 ? tb1 : tb2, st));
+  cub::DeviceRadixSort::SortKeys(tmp, tb1, hash, sorted, (int)n, 0, 64, st);
+  cub::DeviceSelect::Unique(tmp, tb2, sorted, uniq, d_num, (int)n, st);
+  KRB_CHECK_CUDA(cudaGetLastError());
+  int h_num[2] = {0, 0};
+  KRB_CHECK_CUDA(cudaMemcpyAsync(h_num, d_num, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  dev_free(tmp, st);
+  dev_free(sorted, st);
+  const int nt = h_num[0];
+  int rc = KRB_OK;
+  int32_t *rep_row = nullptr;
+  unsigned long long *rows_of = nullptr;
+  int *ok = nullptr;
+  if (nt >= 1 && nt <= kMaxTemplates && h_num[1] <= 64) {
+    auto chk = [&](cudaError_t e) { if (e != cudaSuccess && rc == KRB_OK) { set_error("build_templates: %s", cudaGetErrorString(e)); rc = KRB_ECUDA; } };
+    chk(dev_alloc((void **)&A->tid, sizeof(int32_t) * n, st));
+    chk(dev_alloc((void **)&A->tlen, sizeof(int32_t) * nt, st));
+    chk(dev_alloc((void **)&A->tcode, 64 * (size_t)nt, st));
+    chk(dev_alloc((void **)&rep_row, sizeof(int32_t) * nt, st));
+    chk(dev_alloc((void **)&rows_of, sizeof(unsigned long long) * nt, st));
+    chk(dev_alloc((void **)&ok, sizeof(int), st));
+    if (rc == KRB_OK) {
+      chk(cudaMemsetAsync(rep_row, 0xff, sizeof(int32_t) * nt, st));
+      chk(cudaMemsetAsync(rows_of, 0, sizeof(unsigned long long) * nt, st));
+      const int one = 1;
+      chk(cudaMemcpyAsync(ok, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+      k_row_tid<<<rb, 256, 0, st>>>(n, hash, uniq, nt, A->tid, rep_row);
+      k_tmpl_fill<<<nt, 64, 0, st>>>(nt, rep_row, A->rp, A->ci, A->dict, A->ndict, A->tlen, A->tcode);
+      k_tmpl_verify<<<rb, 256, 0, st>>>(n, A->rp, A->ci, A->dict, A->tid, A->tlen, A->tcode, rows_of, ok);
+      launch_counter() += 3;
+      chk(cudaGetLastError());
+      std::vector<int32_t> h_len(nt);
+      std::vector<uint8_t> h_code(64 * (size_t)nt);
+      std::vector<unsigned long long> h_rows(nt);
+      int h_ok = 0;
+      chk(cudaMemcpyAsync(h_len.data(), A->tlen, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(h_code.data(), A->tcode, 64 * (size_t)nt, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(h_rows.data(), rows_of, sizeof(unsigned long long) * nt, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(&h_ok, ok, sizeof(int), cudaMemcpyDeviceToHost, st));
+      chk(cudaStreamSynchronize(st));
+      if (rc == KRB_OK && h_ok) {
+        A->ntmpl = nt;
+        int mx = 1;
+        A->code_count = new int64_t[256]();
+        for (int t = 0; t < nt; ++t) {
+          if (h_len[t] > mx) mx = h_len[t];
+          for (int j = 0; j < h_len[t]; ++j) A->code_count[h_code[64 * (size_t)t + j]] += (int64_t)h_rows[t];
+        }
+        A->tstride = (mx + 3) / 4 * 4;
+        A->bytes += 4 * n + 68 * (int64_t)nt;
+      }
+    }
+    if (rc != KRB_OK || !A->ntmpl) {   // no templates (hash collision: practically never)
+      for (void *p : {(void *)A->tid, (void *)A->tlen, (void *)A->tcode})
+        if (p) dev_free(p, st);
+      A->tid = nullptr; A->tlen = nullptr; A->tcode = nullptr;
+    }
+  }
+  for (void *p : {(void *)hash, (void *)uniq, (void *)d_num, (void *)rep_row, (void *)rows_of, (void *)ok})
+    if (p) dev_free(p, st);
+  return rc;
+}
+
+// tent[tstride t + j] = {offset, constant?, value} of entry j of template t
+__global__ void k_tent_fill(int ntmpl, int tstride, const int32_t *__restrict__ tlen,
+                            const uint8_t *__restrict__ tcode, const int32_t *__restrict__ dict,
+                            const double *__restrict__ vtab, krb_tentry *__restrict__ tent) {
+  const int t = blockIdx.x, j = threadIdx.x;
+  if (t >= ntmpl || j >= tstride) return;
+  const uint8_t *fl = reinterpret_cast<const uint8_t *>(vtab + 256);
+  krb_tentry e = {0, 1, 0.0};
+  if (j < tlen[t]) {
+    const int code = tcode[64 * t + j];
+    e.off = dict[code];
+    e.cst = fl[code] ? 1 : 0;
+    e.val = fl[code] ? vtab[code] : 0.0;
+  }
+  tent[(int64_t)tstride * t + j] = e;
+}
+
+static int64_t vcode_bytes(const krb_matrix *A) {
+  return A->tent ? 256 * 8 + 256 + (int64_t)A->ntmpl * A->tstride * 16 : 0;
+}
+
+static void free_vcode(krb_matrix *A, cudaStream_t st) {
+  for (void *p : {(void *)A->vtab, (void *)A->tent})
+    if (p) dev_free(p, st);
+  A->vtab = nullptr; A->tent = nullptr;
+  A->vconst_entries = 0;
+}
+
+// Build the value tables of an offset-coded matrix with row templates; kept
+// when at least half of the entries lie on constant diagonals (otherwise the
+// matrix stays plainly offset-coded).  One pass over the CSR copy (~1 ms at
+// C5) and two tiny kernels.
+static int build_vcode(krb_matrix *A, cudaStream_t st) {
+  if (!A->dcode || !A->rep || !A->tid || !A->code_count || A->n == 0 || A->nnz == 0 ||
+      tuning().value_coding == 0)
+    return KRB_OK;
+  const int nd = A->ndict;
+  int *varies = nullptr;
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->vtab, 256 * sizeof(double) + 256, st));
+  KRB_CHECK_CUDA(dev_alloc((void **)&varies, 256 * sizeof(int), st));
+  KRB_CHECK_CUDA(cudaMemsetAsync(varies, 0, 256 * sizeof(int), st));
+  k_vc_pick<<<1, 256, 0, st>>>(nd, A->rep, A->val, A->vtab);
+  KRB_CHECK_LAUNCH();
+  k_vc_check<<<(unsigned)((A->n + 255) / 256), 256, 0, st>>>(A->n, A->rp, A->ci, A->val, A->dict,
+                                                             nd, A->vtab, varies);
+  KRB_CHECK_LAUNCH();
+  k_vc_flags<<<1, 256, 0, st>>>(nd, varies, A->vtab);
+  KRB_CHECK_LAUNCH();
+  uint8_t fl[256];
+  KRB_CHECK_CUDA(cudaMemcpyAsync(fl, A->vtab + 256, 256, cudaMemcpyDeviceToHost, st));
+  KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  dev_free(varies, st);
+  int64_t cnt = 0;
+  for (int d = 0; d < nd; ++d)
+    if (fl[d]) cnt += A->code_count[d];
+  if (2 * cnt < A->nnz) {
+    free_vcode(A, st);
+    return KRB_OK;
+  }
+  A->vconst_entries = cnt;
+  KRB_CHECK_CUDA(dev_alloc((void **)&A->tent, sizeof(krb_tentry) * (size_t)A->ntmpl * A->tstride, st));
+  k_tent_fill<<<A->ntmpl, 64, 0, st>>>(A->ntmpl, A->tstride, A->tlen, A->tcode, A->dict, A->vtab,
+                                       A->tent);
+  KRB_CHECK_LAUNCH();
+  A->bytes += vcode_bytes(A);
   return KRB_OK;
 }
 
@@ -604,6 +949,11 @@ struct krb_pattern {
   int64_t *rp = nullptr, *sl_ptr = nullptr, *dptr = nullptr;
   int32_t *ci = nullptr, *rlen = nullptr, *s_col = nullptr, *perm = nullptr, *dict = nullptr;
   uint8_t *dcode = nullptr;
+  int32_t *rep = nullptr;
+  int32_t *tid = nullptr, *tlen = nullptr;
+  uint8_t *tcode = nullptr;
+  int ntmpl = 0, tstride = 0;
+  int64_t *code_count = nullptr;   // host: entries per offset code
   krb_pattern *tpat = nullptr;   // pattern of the transpose (may be this one)
   int32_t *tperm = nullptr;      // transpose entry t = this pattern's CSR entry tperm[t]
 };
@@ -627,9 +977,10 @@ static void pattern_release(krb_pattern *P, bool async, cudaStream_t st) {
   for (size_t i = 0; i < v.size(); ++i)
     if (v[i] == P) { v.erase(v.begin() + i); break; }
   void *arrays[] = {P->rp, P->ci, P->sl_ptr, P->rlen, P->s_col, P->perm,
-                    P->dcode, P->dptr, P->dict, P->tperm};
+                    P->dcode, P->dptr, P->dict, P->tperm, P->rep, P->tid, P->tlen, P->tcode};
   for (void *p : arrays)
     if (p) dev_free(p, async ? st : nullptr);
+  delete[] P->code_count;
   krb_pattern *T = P->tpat;
   delete P;
   if (T && T != P) pattern_release(T, async, st);
@@ -645,7 +996,9 @@ static void pattern_adopt(krb_matrix *A) {
   P->dcode_bytes = A->dcode_bytes; P->uniform_slices = A->uniform_slices;
   P->rp = A->rp; P->ci = A->ci; P->sl_ptr = A->sl_ptr; P->rlen = A->rlen; P->s_col = A->s_col;
   P->perm = A->perm; P->dcode = A->dcode; P->dptr = A->dptr; P->dict = A->dict;
-  P->bytes = A->bytes - 8 * A->nnz - (A->s_val ? 8 * A->sell_elems : 0);
+  P->rep = A->rep; P->tid = A->tid; P->tlen = A->tlen; P->tcode = A->tcode;
+  P->ntmpl = A->ntmpl; P->tstride = A->tstride; P->code_count = A->code_count;
+  P->bytes = A->bytes - 8 * A->nnz - (A->s_val ? 8 * A->sell_elems : 0) - vcode_bytes(A);
   A->pat = P;
   patterns().push_back(P);
 }
@@ -659,6 +1012,8 @@ static void pattern_attach(krb_matrix *A, krb_pattern *P) {
   A->uniform_slices = P->uniform_slices;
   A->rp = P->rp; A->ci = P->ci; A->sl_ptr = P->sl_ptr; A->rlen = P->rlen; A->s_col = P->s_col;
   A->perm = P->perm; A->dcode = P->dcode; A->dptr = P->dptr; A->dict = P->dict;
+  A->rep = P->rep; A->tid = P->tid; A->tlen = P->tlen; A->tcode = P->tcode;
+  A->ntmpl = P->ntmpl; A->tstride = P->tstride; A->code_count = P->code_count;
 }
 
 __global__ void k_pattern_neq(int64_t n, int64_t nnz, const int64_t *__restrict__ rp_a,
@@ -771,11 +1126,12 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
       KRB_CHECK_CUDA(cudaMemcpyAsync(A->val, d_val, sizeof(double) * nnz,
                                      cudaMemcpyDeviceToDevice, st));
     int rc = fill_values(A, st);
+    A->bytes = P->bytes + 8 * nnz + (A->s_val ? 8 * A->sell_elems : 0);
+    if (rc == KRB_OK) rc = build_vcode(A, st);
     if (rc != KRB_OK) {
       matrix_free(A, true, st);
       return rc;
     }
-    A->bytes = P->bytes + 8 * nnz + (A->s_val ? 8 * A->sell_elems : 0);
     *out = A;
     return KRB_OK;
   }
@@ -806,6 +1162,8 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   // 2 = plain SELL-32; 0 = auto (the offset-coded stream when it qualifies)
   int rc = build_sell(A, format == 4 ? 2 : format, st);
   if (rc == KRB_OK && (format == 0 || format == 4)) rc = build_dict(A, st);
+  if (rc == KRB_OK) rc = build_templates(A, st);
+  if (rc == KRB_OK) rc = build_vcode(A, st);
   if (rc != KRB_OK) {
     delete A;
     return rc;
@@ -877,11 +1235,12 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
       KRB_CHECK_LAUNCH();
     }
     int rc = fill_values(T, st);
+    T->bytes = P->tpat->bytes + 8 * nnz + (T->s_val ? 8 * T->sell_elems : 0);
+    if (rc == KRB_OK) rc = build_vcode(T, st);
     if (rc != KRB_OK) {
       matrix_free(T, true, st);
       return rc;
     }
-    T->bytes = P->tpat->bytes + 8 * nnz + (T->s_val ? 8 * T->sell_elems : 0);
     A->T = T;
     return KRB_OK;
   }
@@ -969,14 +1328,16 @@ void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
   matrix_free(A->T, async, st);
   if (!async) cudaDeviceSynchronize();
   if (A->pat) {   // structure arrays belong to the pattern
-    for (void *p : {(void *)A->val, (void *)A->s_val})
+    for (void *p : {(void *)A->val, (void *)A->s_val, (void *)A->vtab, (void *)A->tent})
       if (p) dev_free(p, async ? st : nullptr);
     pattern_release(A->pat, async, st);
   } else {
     void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm,
-                      A->dcode, A->dptr, A->dict};
+                      A->dcode, A->dptr, A->dict, A->rep, A->vtab, A->tent, A->tid, A->tlen,
+                      A->tcode};
     for (void *p : arrays)
       if (p) dev_free(p, async ? st : nullptr);
+    delete[] A->code_count;
   }
   delete A;
 }
@@ -1022,7 +1383,9 @@ int krb_matrix_info(const krb_matrix *A, int64_t *n, int64_t *nnz, int *format,
   KRB_REQUIRE(A != nullptr, "krb_matrix_info: NULL matrix");
   if (n) *n = A->n;
   if (nnz) *nnz = A->nnz;
-  if (format) *format = (A->format == 2 && A->perm) ? 3 : (A->dcode ? 4 : A->format);
+  if (format)
+    *format = (A->format == 2 && A->perm) ? 3
+              : (A->tent && tuning().value_coding) ? 5 : (A->dcode ? 4 : A->format);
   if (bytes) *bytes = A->bytes + (A->T ? A->T->bytes : 0);
   return KRB_OK;
 }
@@ -1032,7 +1395,13 @@ int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t 
   KRB_REQUIRE(A != nullptr, "krb_matrix_stream_stats: NULL matrix");
   const krb_matrix *B = A->base ? A->base : A;
   int64_t b = 16 * B->n;   // x read once, y written once
-  if (B->dcode)
+  if (B->tent && tuning().value_coding)
+    // value-coded: only the entries off the constant diagonals stream their
+    // values; per slice the offset row / code bytes, the value row and mask
+    // (values of the other entries, the rows' template ids, slice pointers, tables)
+    b += 8 * (B->nnz - B->vconst_entries) + 4 * B->n + 8 * B->nslices +
+         16 * (int64_t)B->ntmpl * B->tstride + 4 * B->ntmpl;
+  else if (B->dcode)
     b += 8 * B->sell_elems + B->dcode_bytes + 4 * B->n + 16 * B->nslices + 1024;
   else if (B->format == 2)
     b += 12 * B->sell_elems + 4 * B->n + 8 * (B->nslices + 1) + (B->perm ? 4 * B->n : 0);
@@ -1042,6 +1411,24 @@ int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t 
   if (nslices) *nslices = B->format == 2 ? B->nslices : 0;
   if (uniform_slices) *uniform_slices = B->uniform_slices;
   if (ndict) *ndict = B->ndict;
+  return KRB_OK;
+}
+
+int krb_matrix_value_stats(const krb_matrix *A, int64_t *const_entries, int *templates,
+                           int *const_diagonals) {
+  KRB_REQUIRE(A != nullptr, "krb_matrix_value_stats: NULL matrix");
+  const krb_matrix *B = A->base ? A->base : A;
+  const bool on = B->tent && tuning().value_coding;
+  if (const_entries) *const_entries = on ? B->vconst_entries : 0;
+  if (templates) *templates = on ? B->ntmpl : 0;
+  if (const_diagonals) {
+    *const_diagonals = 0;
+    if (on) {
+      uint8_t fl[256];
+      KRB_CHECK_CUDA(cudaMemcpy(fl, B->vtab + 256, 256, cudaMemcpyDeviceToHost));
+      for (int d = 0; d < B->ndict; ++d) *const_diagonals += fl[d] ? 1 : 0;
+    }
+  }
   return KRB_OK;
 }
 

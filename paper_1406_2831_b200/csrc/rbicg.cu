@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) k_bproj_dot(const BiArgs *__restrict__ p
 // kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (with the
 // values' bulk L2 prefetch pf bytes ahead, as the BiCGSTAB SpMV)
 template <int kF, bool kTrans>
-__global__ void __launch_bounds__(256, kF == 2 ? 6 : 1) k_bspmv(const BiArgs *__restrict__ pa,
+__global__ void __launch_bounds__(256, kF == 2 ? 6 : kF == 4 ? 4 : 1) k_bspmv(const BiArgs *__restrict__ pa,
                                                                 int64_t pf) {
   constexpr bool kSell = kF == 1;
   const BiArgs &a = *pa;
@@ -348,9 +348,12 @@ __global__ void __launch_bounds__(256, kF == 2 ? 6 : 1) k_bspmv(const BiArgs *__
   const krb_matrix &M = kTrans ? a.AT : a.A;
   const double *__restrict__ x = kTrans ? a.pt : a.p;
   double *y = kTrans ? a.qt : a.q;
-  if (kF == 2) {
+  if (kF == 2 || kF == 4) {   // 4: value-coded (constant diagonals from the tables)
     auto xf = [x](int c) { return __ldg(x + c); };
-    y[i] = spmv_row_dict<0, decltype(xf), 4>(i, M, xf, pf);
+    if (kF == 4)
+      y[i] = spmv_row_tmpl(i, M, xf);
+    else
+      y[i] = spmv_row_dict<0, decltype(xf), 4>(i, M, xf, pf);
   } else {
     y[(kSell && M.perm) ? M.perm[i] : i] = spmv_row<kSell>(i, M, x);
   }
@@ -380,6 +383,10 @@ static int bi_launch(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   return KRB_OK;
 }
 
+static int spmv_kind(const krb_matrix *M) {
+  return (M->tent && tuning().value_coding) ? 2 : M->dcode ? 1 : 0;
+}
+
 template <bool kTrans>
 static int bi_spmv(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
   const krb_matrix &M = kTrans ? h.AT : h.A;
@@ -388,7 +395,9 @@ static int bi_spmv(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
     return spmv_launch(&M, kTrans ? h.pt : h.p, kTrans ? h.qt : h.q,
                        reinterpret_cast<const int *>(&h.S->status), st);
   unsigned blocks = (unsigned)((h.n + 255) / 256);
-  if (M.dcode)
+  if (M.tent && tuning().value_coding)
+    k_bspmv<4, kTrans><<<blocks, 256, 0, st>>>(d, 0);
+  else if (M.dcode)
     k_bspmv<2, kTrans><<<blocks, 256, 0, st>>>(d, (int64_t)tuning().spmv_prefetch_mb << 20);
   else if (M.format == 2)
     k_bspmv<1, kTrans><<<blocks, 256, 0, st>>>(d, 0);
@@ -721,7 +730,7 @@ struct krb_rbicg {
   int64_t l0 = 0;
   int use_graph = 1;
   int fmt = -1, fmt_t = -1;   // storage formats the graph was captured for
-  bool dict = false, dict_t = false;   // offset-coded SpMV kernels captured
+  int dict = 0, dict_t = 0;   // SpMV kernels captured: 1 offset-coded, 2 value-coded
   // host copy of the scalar block as of the last begin / run (the device
   // block only changes inside those calls and in rotate, which keeps this
   // copy current): run and rotate need no extra read-back + synchronisation
@@ -822,7 +831,7 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   krb_rbicg *H = ctx->bi_cache;
   const bool reuse = H && H->h.n == n && H->k == k && H->s == s && H->max_itn == max_itn &&
                      H->fmt == A->format && H->fmt_t == A->T->format &&
-                     H->dict == (A->dcode != nullptr) && H->dict_t == (A->T->dcode != nullptr) &&
+                     H->dict == spmv_kind(A) && H->dict_t == spmv_kind(A->T) &&
                      (!A->pre || same_sig(H->sig, matrix_sig(A)));
   if (H && !reuse) bi_free(H);
   ctx->bi_cache = nullptr;
@@ -836,8 +845,8 @@ int krb_rbicg_create(krb_rbicg **out, krb_context *ctx, krb_matrix *A,
   H->k = k;
   H->fmt = A->format;
   H->fmt_t = A->T->format;
-  H->dict = A->dcode != nullptr;
-  H->dict_t = A->T->dcode != nullptr;
+  H->dict = spmv_kind(A);
+  H->dict_t = spmv_kind(A->T);
   H->sig = matrix_sig(A);
   const int64_t nb = canon_nblocks(n);
   const int64_t ring_cols = (s > 0 ? s : 0) + 3;

@@ -156,4 +156,42 @@ __device__ __forceinline__ double spmv_row_dict(int64_t i, const krb_matrix &A, 
   return sum;
 }
 
+// ---- value-coded row (row templates; identity row order) -----------------
+// Row i follows template tid[i]: entry j has column i + off_j and -- on a
+// constant diagonal -- the table's value, else the row's own s_val entry
+// (same position as in SELL-32).  Same entries, same CSR order, same
+// mul-then-add as spmv_row_f<true>, so the same bits; the template entries
+// (16 bytes each, a few KB per matrix) stay in L1 and the lanes of a warp
+// that share a template read them as one broadcast.  No collectives: any
+// mix of templates and row lengths inside a warp is handled by predication.
+template <class XF, int kB = 4>
+__device__ __forceinline__ double spmv_row_tmpl(int64_t i, const krb_matrix &A, XF xf) {
+  const int t = __ldg(A.tid + i);
+  const double *__restrict__ vp = A.s_val + __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
+  const int len = __ldg(A.tlen + t);
+  const int4 *__restrict__ te = reinterpret_cast<const int4 *>(A.tent) + (int64_t)t * A.tstride;
+  const int row = (int)i;
+  double sum = 0.0;
+  int j = 0;
+  for (; j + kB <= len; j += kB) {
+    int4 e[kB];
+    double v[kB], xv[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) e[u] = __ldg(te + j + u);
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      v[u] = e[u].y ? __hiloint2double(e[u].w, e[u].z) : __ldg(vp + 32 * (j + u));
+#pragma unroll
+    for (int u = 0; u < kB; ++u) xv[u] = xf(row + e[u].x);
+#pragma unroll
+    for (int u = 0; u < kB; ++u) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+  }
+  for (; j < len; ++j) {
+    const int4 e = __ldg(te + j);
+    const double v = e.y ? __hiloint2double(e.w, e.z) : __ldg(vp + 32 * j);
+    sum = __dadd_rn(sum, __dmul_rn(v, xf(row + e.x)));
+  }
+  return sum;
+}
+
 }  // namespace krb

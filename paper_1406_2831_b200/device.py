@@ -437,7 +437,8 @@ class DeviceMatrix:
         n_, nnz_, f_, b_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
         _lib.call("krb_matrix_info", h, ctypes.byref(n_), ctypes.byref(nnz_),
                   ctypes.byref(f_), ctypes.byref(b_))
-        self.format = {1: "csr", 2: "sell32", 3: "sell32-sigma", 4: "sell32-dict"}.get(f_.value, "?")
+        self.format = {1: "csr", 2: "sell32", 3: "sell32-sigma", 4: "sell32-dict",
+                       5: "sell32-dict-vc"}.get(f_.value, "?")
         self.device_bytes = b_.value
         sb, ns, nu, nd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
         _lib.call("krb_matrix_stream_stats", h, ctypes.byref(sb), ctypes.byref(ns),
@@ -445,6 +446,12 @@ class DeviceMatrix:
         # bytes one SpMV streams in this format; slice statistics
         self.stream_bytes = sb.value
         self.stream_stats = {"nslices": ns.value, "uniform_slices": nu.value, "ndict": nd.value}
+        if f_.value == 5:
+            ce, vl, cd = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int()
+            _lib.call("krb_matrix_value_stats", h, ctypes.byref(ce), ctypes.byref(vl),
+                      ctypes.byref(cd))
+            self.stream_stats.update(const_entries=ce.value, templates=vl.value,
+                                     const_diagonals=cd.value)
 
     @property
     def shape(self):

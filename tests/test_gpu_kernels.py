@@ -57,13 +57,15 @@ def test_spmv_formats_bitwise(dev, canon, cfg, fmt):
     assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), op._csr @ x)
 
 
-@pytest.mark.parametrize("cfg,expect", [("c1", "sell32-dict"), ("c2", "sell32-dict"),
-                                        ("c5", "sell32-dict"), ("c3", "sell32"),
+@pytest.mark.parametrize("cfg,expect", [("c1", "sell32-dict-vc"), ("c2", "sell32-dict-vc"),
+                                        ("c5", "sell32-dict-vc"), ("c3", "sell32"),
                                         ("c4", "sell32-sigma")])
 def test_offset_coded_format_choice(dev, cfg, expect):
     """Stencil matrices (<= 255 distinct diagonals) get the offset-coded
-    SELL-32 stream automatically, their transposes too; C3's random K1
-    columns and C4's power-law rows do not qualify."""
+    SELL-32 stream automatically, their transposes too -- with value tables
+    for their constant diagonals (constant-coefficient stencils: all of K's
+    diagonals but the main one of s E - K); C3's random K1 columns and C4's
+    power-law rows do not qualify."""
     from paper_1406_2831_b200.workloads import make_sequence
     A = make_sequence(cfg, small=True).matrix(1)
     M = dev.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values)
@@ -101,7 +103,7 @@ def test_offset_coded_ragged_slices(dev, n):
     x = r.standard_normal(n)
     M = dev.DeviceMatrix(n, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data)
     if n > 127:
-        assert M.format == "sell32-dict"
+        assert M.format == "sell32-dict"     # random values: no constant diagonal
     assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), S @ x)
     assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(), S.T.tocsr() @ x)
     # 256 distinct offsets: no dictionary
@@ -113,6 +115,118 @@ def test_offset_coded_ragged_slices(dev, n):
         M2 = dev.DeviceMatrix(n, S2.indptr.astype(np.int64), S2.indices.astype(np.int32), S2.data)
         assert M2.format in ("sell32", "sell32-sigma", "csr")
         assert np.array_equal(M2.spmv(_tensor(x)).cpu().numpy(), S2 @ x)
+
+
+def _banded(n, offs, r, const_offs, gaps=5):
+    """Banded matrix on the diagonals `offs`: the diagonals in const_offs
+    carry ONE value each (bit-identical), the others random values; rows of
+    every third slice group lose entries (one of `gaps` random subsets per
+    row: non-uniform slices, several row templates per warp)."""
+    import scipy.sparse as sp
+    cval = {int(o): float(r.standard_normal() * np.exp(r.uniform(-5, 5))) for o in const_offs}
+    subsets = [offs[r.random(offs.size) < 0.6] for _ in range(int(gaps))]
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        if i % 211 == 7:
+            continue                        # empty row
+        sel = offs if (not gaps or (i // 32) % 3) else subsets[r.integers(len(subsets))]
+        for o in sel:
+            c = i + int(o)
+            if 0 <= c < n:
+                rows.append(i)
+                cols.append(c)
+                vals.append(cval[int(o)] if int(o) in cval else float(r.standard_normal()))
+    S = sp.csr_matrix((np.array(vals), (rows, cols)), shape=(n, n))
+    S.sort_indices()
+    return S
+
+
+@pytest.mark.parametrize("n", [64, 1000, 4099, 40000])
+@pytest.mark.parametrize("nvar", [0, 1, 3])
+def test_value_coded_bitwise(dev, n, nvar):
+    """Value-coded format: constant diagonals served from the value tables,
+    varying ones from the stream; uniform and ragged slices, empty rows, a
+    partial last slice.  Products, transposed products and multi-column
+    products are bit-identical to scipy and to the same matrix with the value
+    tables switched off."""
+    from paper_1406_2831_b200 import _lib
+    r = np.random.default_rng(1000 * n + nvar)
+    offs = np.array([-40, -33, -32, -31, -1, 0, 1, 2, 31, 32, 33, 50, 51])
+    var = set(r.choice(offs, size=nvar, replace=False).tolist())
+    S = _banded(n, offs, r, [o for o in offs if int(o) not in var])
+    x = r.standard_normal(n)
+    X = r.standard_normal((n, 9))
+    args = (n, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data)
+    M = dev.DeviceMatrix(*args, fmt=4)
+    assert M.format == "sell32-dict-vc", M.format
+    assert M.stream_stats["const_diagonals"] == offs.size - nvar
+    coo = S.tocoo()
+    assert M.stream_stats["const_entries"] == int(np.isin(coo.col - coo.row,
+                                                          [o for o in offs if int(o) not in var]).sum())
+    assert 1 <= M.stream_stats["templates"] <= 1024
+    y, yt = M.spmv(_tensor(x)).cpu().numpy(), M.spmv(_tensor(x), transpose=True).cpu().numpy()
+    Y = M.spmm(_cols(X)).cpu().numpy().T
+    Yt = M.spmm(_cols(X), transpose=True).cpu().numpy().T
+    St = S.T.tocsr()
+    assert np.array_equal(y, S @ x) and np.array_equal(yt, St @ x)
+    for c in range(9):
+        assert np.array_equal(Y[:, c], S @ X[:, c])
+        assert np.array_equal(Yt[:, c], St @ X[:, c])
+    with _lib.tuning(value_coding=0):
+        M0 = dev.DeviceMatrix(*args, fmt=4)
+        assert M0.format == "sell32-dict"
+        assert np.array_equal(M0.spmv(_tensor(x)).cpu().numpy(), y)
+        assert np.array_equal(M0.spmv(_tensor(x), transpose=True).cpu().numpy(), yt)
+
+
+def test_value_coded_special_values_and_shared_pattern(dev):
+    """-0.0 / +0.0 and NaN payloads on a diagonal are different bit patterns
+    (such a diagonal is not constant); a later matrix on the SAME pattern with
+    random values is not value-coded while the first one stays so."""
+    r = np.random.default_rng(77)
+    n = 3000
+    offs = np.array([-32, -1, 0, 1, 32])
+    S = _banded(n, offs, r, offs, gaps=0)
+    d = S.data.copy()
+    main = np.flatnonzero(S.indices == np.repeat(np.arange(n), np.diff(S.indptr)))
+    up = np.flatnonzero(S.indices == np.repeat(np.arange(n), np.diff(S.indptr)) + 1)
+    d[main] = 0.0
+    d[main[::7]] = -0.0                      # same value, other bits
+    d[up[5]] = np.nan
+    args = (n, S.indptr.astype(np.int64), S.indices.astype(np.int32))
+    M = dev.DeviceMatrix(*args, d)
+    assert M.format == "sell32-dict-vc"
+    assert M.stream_stats["const_diagonals"] == 3
+    import scipy.sparse as sp
+    S1 = sp.csr_matrix((d, S.indices, S.indptr), shape=(n, n))
+    x = r.standard_normal(n)
+    y = M.spmv(_tensor(x)).cpu().numpy()
+    assert np.array_equal(y, S1 @ x, equal_nan=True)
+    assert np.array_equal(np.signbit(y), np.signbit(S1 @ x))
+    d2 = r.standard_normal(S.nnz)
+    M2 = dev.DeviceMatrix(*args, d2)
+    assert M2.pattern_info()[0] == M.pattern_info()[0]
+    assert M2.format == "sell32-dict" and M.format == "sell32-dict-vc"
+    S2 = sp.csr_matrix((d2, S.indices, S.indptr), shape=(n, n))
+    assert np.array_equal(M2.spmv(_tensor(x)).cpu().numpy(), S2 @ x)
+    assert np.array_equal(M2.spmv(_tensor(x), transpose=True).cpu().numpy(), S2.T.tocsr() @ x)
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), y, equal_nan=True)
+    assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(),
+                          S1.T.tocsr() @ x, equal_nan=True)
+
+
+def test_value_coded_falls_back_on_too_many_templates(dev):
+    """More than 1024 distinct row sequences: no templates, the matrix stays
+    plainly offset-coded (constant diagonals or not) and correct."""
+    r = np.random.default_rng(9)
+    n = 20000
+    offs = np.arange(-8, 9)
+    S = _banded(n, offs, r, offs, gaps=4000)
+    M = dev.DeviceMatrix(n, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data)
+    assert M.format == "sell32-dict"
+    x = r.standard_normal(n)
+    assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), S @ x)
+    assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(), S.T.tocsr() @ x)
 
 
 def test_sell_sigma_chosen_for_power_law(dev):

@@ -17,9 +17,12 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--transpose", action="store_true")
     ap.add_argument("--fmt", type=int, default=0, help="0 auto, 1 CSR, 2 SELL-32, 4 offset-coded")
+    ap.add_argument("--tune", nargs="*", default=[], help="knob=value ...")
     a = ap.parse_args()
     import torch
-    from paper_1406_2831_b200 import device as D, workloads as W
+    from paper_1406_2831_b200 import _lib, device as D, workloads as W
+    if a.tune:
+        _lib.tuning(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.tune})
     seq = W.make_sequence(a.config)
     A = seq.matrix(0)
     M = D.DeviceMatrix(A.n, A.row_ptr, A.col_idx, A.values, fmt=a.fmt)
@@ -40,7 +43,8 @@ def main():
         os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
     print(json.dumps({"config": a.config, "format": M.format, "transpose": a.transpose,
                       "n": A.n, "nnz": A.nnz, "device_bytes": M.device_bytes, "us": round(us, 1),
-                      "GBps": round(B / us / 1e3, 1), "frac": round(B / us / 1e3 / peak, 4)}))
+                      "GBps": round(B / us / 1e3, 1), "frac": round(B / us / 1e3 / peak, 4),
+                      "stream_bytes": M.stream_bytes, "stats": M.stream_stats, "tune": a.tune}))
 
 
 if __name__ == "__main__":

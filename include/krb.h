@@ -131,10 +131,13 @@ int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t 
  * (offsets + table values, a few KB per matrix); a row then reads its
  * template id and only the values of its varying entries.  const_entries:
  * entries served from the tables (0: not value-coded), templates: distinct
- * row templates, const_diagonals: constant diagonals among the ndict offsets.
+ * row templates, const_diagonals: constant diagonals among the ndict offsets,
+ * diagonal_form: the SpMV walks the <= 64 diagonals with the table in its
+ * kernel argument (rows sorted by column, at least half of the n x ndict
+ * positions filled) instead of the per-row templates.
  * Chosen automatically when at least half of the entries qualify. */
 int krb_matrix_value_stats(const krb_matrix *A, int64_t *const_entries, int *templates,
-                           int *const_diagonals);
+                           int *const_diagonals, int *diagonal_form);
 
 /* Identity and reference count of the shared sparsity pattern behind A
  * (matrices with equal row_ptr / col_idx share the SELL layout, the offset

@@ -83,7 +83,7 @@ SIGNATURES = {
     "krb_matrix_stream_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                         ctypes.POINTER(c_i64), ctypes.POINTER(c_int)]),
     "krb_matrix_value_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
-                                       ctypes.POINTER(c_int)]),
+                                       ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "krb_matrix_pattern_info": (c_int, [c_vp, ctypes.POINTER(ctypes.c_uint64),
                                         ctypes.POINTER(c_int), ctypes.POINTER(c_int)]),
     "krb_matrix_info": (c_int, [c_vp, ctypes.POINTER(c_i64),

@@ -144,7 +144,8 @@ constexpr int64_t kTdotSmallNb = 4 * kNumSMs;
 // 1258 us.)
 // kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (uniform
 // slices: offsets by warp shuffle), 3 its first version (tuning spmv_variant=1),
-// 4 value-coded (constant diagonals from the value tables).
+// 4 value-coded (constant diagonals from the row templates), 5 value-coded in
+// diagonal form (table in the matrix argument).
 template <int kF, int kSlot, int kMinB = 1, int kBU = 4>
 __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
@@ -162,7 +163,9 @@ __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const do
     if (i < A.n) {
       auto xf = [x](int c) { return __ldg(x + c); };
       double yi;
-      if (kF == 4)
+      if (kF == 5)
+        yi = spmv_row_dia(i, A, x);
+      else if (kF == 4)
         yi = spmv_row_tmpl(i, A, xf);
       else
         yi = spmv_row_dict<kF == 3 ? 1 : 0, decltype(xf), kBU>(i, A, xf, pf);
@@ -258,7 +261,9 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   // the iteration (profiles/r02_spmv_variants_ab2.jsonl): 4 entries per
   // batch at 40 registers 4666 us, at 48: 4743; 8 entries at 48 / 60
   // registers: 4706 / 4969; the int4-offset version: 4666 (median 4783).
-  if (h.A.tent && tuning().value_coding)
+  if (h.A.tent && tuning().value_coding && h.A.dia.nd && tuning().value_coding != 2)
+    k_iter_spmv<5, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
+  else if (h.A.tent && tuning().value_coding)
     k_iter_spmv<4, kSecond ? 5 : 1, 4><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, 0);
   else if (h.A.dcode && tuning().spmv_variant == 1)
     k_iter_spmv<3, kSecond ? 5 : 1, 6><<<blocks, 256, 0, st>>>(h.A, x, y, status, h.ktime, pf);

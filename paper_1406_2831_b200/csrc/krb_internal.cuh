@@ -22,6 +22,17 @@ struct __align__(16) krb_tentry {
   int32_t cst;    // 1: the value below; 0: the row's own s_val entry
   double val;
 };
+// Diagonal table of a value-coded matrix with at most 32 distinct diagonals,
+// carried BY VALUE inside krb_matrix: a kernel that takes the matrix as a
+// parameter reads it from the constant bank with warp-uniform indices (no
+// load/store-unit traffic, no per-lane copies of the same 16 bytes).
+struct __align__(16) krb_diatable {
+  int32_t nd = 0;            // 0: not available
+  int32_t pad = 0;
+  uint64_t cst = 0;          // bit c: diagonal c is constant (value val[c])
+  int32_t off[32] = {};      // col - row of diagonal c (ascending)
+  double val[32] = {};
+};
 struct krb_matrix {
   int64_t n = 0, nnz = 0;
   int format = 0;  // 1 CSR, 2 SELL
@@ -69,6 +80,12 @@ struct krb_matrix {
   double *vtab = nullptr;
   krb_tentry *tent = nullptr;
   int64_t vconst_entries = 0;   // entries served from the tables
+  // diagonal form (<= 32 diagonals, rows sorted by column, at least half of
+  // the n x ndict positions filled): row i's entries are the set bits of
+  // tmask[tid[i]] (bit c = diagonal c present), walked in ascending c = CSR
+  // order; constants and offsets from `dia`
+  uint64_t *tmask = nullptr;   // pattern
+  krb_diatable dia;            // matrix
   krb_matrix *T = nullptr;  // lazily built transpose
   // the structure arrays above (rp, ci, sl_ptr, rlen, s_col, perm, dcode,
   // dptr, dict) belong to this reference-counted pattern, shared by every

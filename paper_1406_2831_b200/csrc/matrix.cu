@@ -107,15 +107,17 @@ bool same_sig(const MatrixSig &a, const MatrixSig &b) {
 }
 
 // offset-coded SELL-32 (identity row order)
-template <int kV, bool kVC = false>
-__global__ void __launch_bounds__(256, kVC ? 4 : 6) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
+template <int kV, int kVC = 0>   // kVC: 1 value-coded by row templates, 2 in diagonal form
+__global__ void __launch_bounds__(256, kVC == 1 ? 4 : 6) k_spmv_dict(krb_matrix A, const double *__restrict__ x,
                                                    double *__restrict__ y,
                                                    const int *__restrict__ status, int64_t pf) {
   if (status && *status) return;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
   auto xf = [x](int c) { return __ldg(x + c); };
-  if (kVC)
+  if (kVC == 2)
+    y[i] = spmv_row_dia(i, A, x);
+  else if (kVC == 1)
     y[i] = spmv_row_tmpl(i, A, xf);
   else
     y[i] = spmv_row_dict<kV, decltype(xf), 4>(i, A, xf, pf);
@@ -127,8 +129,10 @@ int spmv_launch(const krb_matrix *A, const double *x, double *y,
   if (A->pre) return precond_apply_op(A, x, y, d_status, st);
   int64_t blocks = (A->n + 255) / 256;
   const int64_t pf = (int64_t)tuning().spmv_prefetch_mb << 20;
-  if (A->tent && tuning().value_coding)
-    k_spmv_dict<0, true><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, 0);
+  if (A->tent && tuning().value_coding && A->dia.nd && tuning().value_coding != 2)
+    k_spmv_dict<0, 2><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, 0);
+  else if (A->tent && tuning().value_coding)
+    k_spmv_dict<0, 1><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, 0);
   else if (A->dcode && tuning().spmv_variant == 1)
     k_spmv_dict<1><<<(unsigned)blocks, 256, 0, st>>>(*A, x, y, d_status, pf);
   else if (A->dcode)
@@ -679,7 +683,11 @@ __global__ void __launch_bounds__(256) k_vc_check(int64_t n, const int64_t *__re
   if (i < n) {
     for (int64_t jj = rp[i]; jj < rp[i + 1]; ++jj) {
       const int code = dict_code(sd, nd, ci[jj] - (int32_t)i);
-      if ((unsigned long long)__double_as_longlong(val[jj]) != sv[code] && !sf[code]) sf[code] = 1;
+      // (a non-finite value counts as varying: the diagonal-form kernel
+      // multiplies table values by zero for absent entries)
+      const double v = val[jj];
+      if (((unsigned long long)__double_as_longlong(v) != sv[code] || !isfinite(v)) && !sf[code])
+        sf[code] = 1;
     }
   }
   __syncthreads();
@@ -845,19 +853,42 @@ static int build_templates(krb_matrix *A, cudaStream_t st) {
       if (rc == KRB_OK && h_ok) {
         A->ntmpl = nt;
         int mx = 1;
-        A->code_count = new int64_t[256]();
+        A->code_count = new int64_t[512]();
+        std::vector<uint64_t> h_mask(nt, 0);
+        bool sorted_rows = A->ndict <= 32;
         for (int t = 0; t < nt; ++t) {
           if (h_len[t] > mx) mx = h_len[t];
-          for (int j = 0; j < h_len[t]; ++j) A->code_count[h_code[64 * (size_t)t + j]] += (int64_t)h_rows[t];
+          for (int j = 0; j < h_len[t]; ++j) {
+            const int code = h_code[64 * (size_t)t + j];
+            A->code_count[code] += (int64_t)h_rows[t];
+            if (j > 0 && code <= h_code[64 * (size_t)t + j - 1]) sorted_rows = false;
+            if (code < 64) h_mask[t] |= 1ull << code;
+          }
         }
         A->tstride = (mx + 3) / 4 * 4;
         A->bytes += 4 * n + 68 * (int64_t)nt;
+        {   // the offsets on the host (diagonal tables are assembled there)
+          int32_t h_dict[256];
+          chk(cudaMemcpyAsync(h_dict, A->dict, sizeof(h_dict), cudaMemcpyDeviceToHost, st));
+          chk(cudaStreamSynchronize(st));
+          for (int d = 0; d < 256; ++d) A->code_count[256 + d] = h_dict[d];
+        }
+        // diagonal form: rows sorted by column, <= 32 diagonals, at least
+        // half of the n x ndict positions filled
+        if (rc == KRB_OK && sorted_rows && 2 * A->nnz >= n * (int64_t)A->ndict) {
+          chk(dev_alloc((void **)&A->tmask, sizeof(uint64_t) * nt, st));
+          if (rc == KRB_OK)
+            chk(cudaMemcpyAsync(A->tmask, h_mask.data(), sizeof(uint64_t) * nt,
+                                cudaMemcpyHostToDevice, st));
+          chk(cudaStreamSynchronize(st));
+          A->bytes += 8 * (int64_t)nt;
+        }
       }
     }
     if (rc != KRB_OK || !A->ntmpl) {   // no templates (hash collision: practically never)
-      for (void *p : {(void *)A->tid, (void *)A->tlen, (void *)A->tcode})
+      for (void *p : {(void *)A->tid, (void *)A->tlen, (void *)A->tcode, (void *)A->tmask})
         if (p) dev_free(p, st);
-      A->tid = nullptr; A->tlen = nullptr; A->tcode = nullptr;
+      A->tid = nullptr; A->tlen = nullptr; A->tcode = nullptr; A->tmask = nullptr;
     }
   }
   for (void *p : {(void *)hash, (void *)uniq, (void *)d_num, (void *)rep_row, (void *)rows_of, (void *)ok})
@@ -891,6 +922,7 @@ static void free_vcode(krb_matrix *A, cudaStream_t st) {
     if (p) dev_free(p, st);
   A->vtab = nullptr; A->tent = nullptr;
   A->vconst_entries = 0;
+  A->dia = krb_diatable();
 }
 
 // Build the value tables of an offset-coded matrix with row templates; kept
@@ -913,9 +945,10 @@ static int build_vcode(krb_matrix *A, cudaStream_t st) {
   KRB_CHECK_LAUNCH();
   k_vc_flags<<<1, 256, 0, st>>>(nd, varies, A->vtab);
   KRB_CHECK_LAUNCH();
-  uint8_t fl[256];
-  KRB_CHECK_CUDA(cudaMemcpyAsync(fl, A->vtab + 256, 256, cudaMemcpyDeviceToHost, st));
+  double h_vtab[256 + 32];
+  KRB_CHECK_CUDA(cudaMemcpyAsync(h_vtab, A->vtab, sizeof(h_vtab), cudaMemcpyDeviceToHost, st));
   KRB_CHECK_CUDA(cudaStreamSynchronize(st));
+  const uint8_t *fl = reinterpret_cast<const uint8_t *>(h_vtab + 256);
   dev_free(varies, st);
   int64_t cnt = 0;
   for (int d = 0; d < nd; ++d)
@@ -925,6 +958,15 @@ static int build_vcode(krb_matrix *A, cudaStream_t st) {
     return KRB_OK;
   }
   A->vconst_entries = cnt;
+  A->dia = krb_diatable();
+  if (A->tmask && nd <= 32) {
+    A->dia.nd = nd;
+    for (int d = 0; d < nd; ++d) {
+      A->dia.off[d] = (int32_t)A->code_count[256 + d];
+      A->dia.val[d] = fl[d] ? h_vtab[d] : 0.0;
+      if (fl[d]) A->dia.cst |= 1ull << d;
+    }
+  }
   KRB_CHECK_CUDA(dev_alloc((void **)&A->tent, sizeof(krb_tentry) * (size_t)A->ntmpl * A->tstride, st));
   k_tent_fill<<<A->ntmpl, 64, 0, st>>>(A->ntmpl, A->tstride, A->tlen, A->tcode, A->dict, A->vtab,
                                        A->tent);
@@ -953,7 +995,8 @@ struct krb_pattern {
   int32_t *tid = nullptr, *tlen = nullptr;
   uint8_t *tcode = nullptr;
   int ntmpl = 0, tstride = 0;
-  int64_t *code_count = nullptr;   // host: entries per offset code
+  int64_t *code_count = nullptr;   // host: entries per offset code, then the 256 offsets
+  uint64_t *tmask = nullptr;
   krb_pattern *tpat = nullptr;   // pattern of the transpose (may be this one)
   int32_t *tperm = nullptr;      // transpose entry t = this pattern's CSR entry tperm[t]
 };
@@ -977,7 +1020,7 @@ static void pattern_release(krb_pattern *P, bool async, cudaStream_t st) {
   for (size_t i = 0; i < v.size(); ++i)
     if (v[i] == P) { v.erase(v.begin() + i); break; }
   void *arrays[] = {P->rp, P->ci, P->sl_ptr, P->rlen, P->s_col, P->perm,
-                    P->dcode, P->dptr, P->dict, P->tperm, P->rep, P->tid, P->tlen, P->tcode};
+                    P->dcode, P->dptr, P->dict, P->tperm, P->rep, P->tid, P->tlen, P->tcode, P->tmask};
   for (void *p : arrays)
     if (p) dev_free(p, async ? st : nullptr);
   delete[] P->code_count;
@@ -998,6 +1041,7 @@ static void pattern_adopt(krb_matrix *A) {
   P->perm = A->perm; P->dcode = A->dcode; P->dptr = A->dptr; P->dict = A->dict;
   P->rep = A->rep; P->tid = A->tid; P->tlen = A->tlen; P->tcode = A->tcode;
   P->ntmpl = A->ntmpl; P->tstride = A->tstride; P->code_count = A->code_count;
+  P->tmask = A->tmask;
   P->bytes = A->bytes - 8 * A->nnz - (A->s_val ? 8 * A->sell_elems : 0) - vcode_bytes(A);
   A->pat = P;
   patterns().push_back(P);
@@ -1014,6 +1058,7 @@ static void pattern_attach(krb_matrix *A, krb_pattern *P) {
   A->perm = P->perm; A->dcode = P->dcode; A->dptr = P->dptr; A->dict = P->dict;
   A->rep = P->rep; A->tid = P->tid; A->tlen = P->tlen; A->tcode = P->tcode;
   A->ntmpl = P->ntmpl; A->tstride = P->tstride; A->code_count = P->code_count;
+  A->tmask = P->tmask;
 }
 
 __global__ void k_pattern_neq(int64_t n, int64_t nnz, const int64_t *__restrict__ rp_a,
@@ -1334,7 +1379,7 @@ void matrix_free(krb_matrix *A, bool async, cudaStream_t st) {
   } else {
     void *arrays[] = {A->rp, A->ci, A->val, A->sl_ptr, A->rlen, A->s_col, A->s_val, A->perm,
                       A->dcode, A->dptr, A->dict, A->rep, A->vtab, A->tent, A->tid, A->tlen,
-                      A->tcode};
+                      A->tcode, A->tmask};
     for (void *p : arrays)
       if (p) dev_free(p, async ? st : nullptr);
     delete[] A->code_count;
@@ -1415,12 +1460,13 @@ int krb_matrix_stream_stats(const krb_matrix *A, int64_t *stream_bytes, int64_t 
 }
 
 int krb_matrix_value_stats(const krb_matrix *A, int64_t *const_entries, int *templates,
-                           int *const_diagonals) {
+                           int *const_diagonals, int *diagonal_form) {
   KRB_REQUIRE(A != nullptr, "krb_matrix_value_stats: NULL matrix");
   const krb_matrix *B = A->base ? A->base : A;
   const bool on = B->tent && tuning().value_coding;
   if (const_entries) *const_entries = on ? B->vconst_entries : 0;
   if (templates) *templates = on ? B->ntmpl : 0;
+  if (diagonal_form) *diagonal_form = on && B->dia.nd && tuning().value_coding != 2 ? 1 : 0;
   if (const_diagonals) {
     *const_diagonals = 0;
     if (on) {

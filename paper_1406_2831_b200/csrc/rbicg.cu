@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(1024) k_bproj_dot(const BiArgs *__restrict__ p
 // kF: 0 CSR, 1 SELL-32 / SELL-C-sigma, 2 offset-coded SELL-32 (with the
 // values' bulk L2 prefetch pf bytes ahead, as the BiCGSTAB SpMV)
 template <int kF, bool kTrans>
-__global__ void __launch_bounds__(256, kF == 2 ? 6 : kF == 4 ? 4 : 1) k_bspmv(const BiArgs *__restrict__ pa,
+__global__ void __launch_bounds__(256, kF == 2 || kF == 5 ? 6 : kF == 4 ? 4 : 1) k_bspmv(const BiArgs *__restrict__ pa,
                                                                 int64_t pf) {
   constexpr bool kSell = kF == 1;
   const BiArgs &a = *pa;
@@ -348,9 +348,11 @@ __global__ void __launch_bounds__(256, kF == 2 ? 6 : kF == 4 ? 4 : 1) k_bspmv(co
   const krb_matrix &M = kTrans ? a.AT : a.A;
   const double *__restrict__ x = kTrans ? a.pt : a.p;
   double *y = kTrans ? a.qt : a.q;
-  if (kF == 2 || kF == 4) {   // 4: value-coded (constant diagonals from the tables)
+  if (kF == 2 || kF == 4 || kF == 5) {   // 4 / 5: value-coded (row templates / diagonal form)
     auto xf = [x](int c) { return __ldg(x + c); };
-    if (kF == 4)
+    if (kF == 5)
+      y[i] = spmv_row_dia(i, M, x);
+    else if (kF == 4)
       y[i] = spmv_row_tmpl(i, M, xf);
     else
       y[i] = spmv_row_dict<0, decltype(xf), 4>(i, M, xf, pf);
@@ -384,7 +386,9 @@ static int bi_launch(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
 }
 
 static int spmv_kind(const krb_matrix *M) {
-  return (M->tent && tuning().value_coding) ? 2 : M->dcode ? 1 : 0;
+  if (M->tent && tuning().value_coding)
+    return (M->dia.nd && tuning().value_coding != 2) ? 3 : 2;
+  return M->dcode ? 1 : 0;
 }
 
 template <bool kTrans>
@@ -395,7 +399,9 @@ static int bi_spmv(const BiArgs &h, const BiArgs *d, cudaStream_t st) {
     return spmv_launch(&M, kTrans ? h.pt : h.p, kTrans ? h.qt : h.q,
                        reinterpret_cast<const int *>(&h.S->status), st);
   unsigned blocks = (unsigned)((h.n + 255) / 256);
-  if (M.tent && tuning().value_coding)
+  if (spmv_kind(&M) == 3)
+    k_bspmv<5, kTrans><<<blocks, 256, 0, st>>>(d, 0);
+  else if (spmv_kind(&M) == 2)
     k_bspmv<4, kTrans><<<blocks, 256, 0, st>>>(d, 0);
   else if (M.dcode)
     k_bspmv<2, kTrans><<<blocks, 256, 0, st>>>(d, (int64_t)tuning().spmv_prefetch_mb << 20);
@@ -730,7 +736,7 @@ struct krb_rbicg {
   int64_t l0 = 0;
   int use_graph = 1;
   int fmt = -1, fmt_t = -1;   // storage formats the graph was captured for
-  int dict = 0, dict_t = 0;   // SpMV kernels captured: 1 offset-coded, 2 value-coded
+  int dict = 0, dict_t = 0;   // SpMV kernels captured: 1 offset-coded, 2 / 3 value-coded
   // host copy of the scalar block as of the last begin / run (the device
   // block only changes inside those calls and in rotate, which keeps this
   // copy current): run and rotate need no extra read-back + synchronisation

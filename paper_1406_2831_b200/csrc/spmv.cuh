@@ -194,4 +194,66 @@ __device__ __forceinline__ double spmv_row_tmpl(int64_t i, const krb_matrix &A, 
   return sum;
 }
 
+// ---- value-coded row in diagonal form (A.dia.nd > 0: <= 32 diagonals) ----
+// The row's entries are the set bits of its template mask, walked in
+// ascending diagonal order (= CSR order: rows are sorted by column).  The
+// loop over the diagonals is fully unrolled, so offset and constant value of
+// diagonal c are fixed constant-bank operands of the matrix argument (no
+// load/store-unit traffic, no table loads at all); a varying diagonal's
+// value comes from the row's s_val entry at its CSR position (the number of
+// lower set bits).  Batches of 4 diagonals with predicated gathers.  Same
+// products and sums as spmv_row_f<true>.
+// (An absent entry adds +-0.0 = 0.0 * table value to the running sum instead
+// of being skipped: the sum starts at +0.0 and a round-to-nearest sum is -0.0
+// only when both addends are, so it never is -0.0 and adding a zero leaves
+// every bit unchanged.  Diagonals with a non-finite value are kept out of
+// the table -- 0 * inf -- and take the varying path.)
+static __device__ __noinline__ double spmv_dia_varying(double sum, unsigned m, int c,
+                                                const double *__restrict__ vp, double xv) {
+  if ((m >> c) & 1)
+    sum = __dadd_rn(sum, __dmul_rn(__ldg(vp + 32 * __popc(m & ((1u << c) - 1u))), xv));
+  return sum;
+}
+
+// x: the gathered vector (plain read-only loads).  cst and the x pointer are
+// pinned in registers (the compiler otherwise re-reads them from the constant
+// bank before every entry and the kernel ends up bound by the constant cache:
+// 91 % busy, 453 us at C5).
+__device__ __forceinline__ double spmv_row_dia(int64_t i, const krb_matrix &A,
+                                               const double *__restrict__ x) {
+  const unsigned m = (unsigned)__ldg(reinterpret_cast<const unsigned long long *>(A.tmask) +
+                                     __ldg(A.tid + i));
+  const double *__restrict__ vp = A.s_val + __ldg(A.sl_ptr + (i >> 5)) + (i & 31);
+  const int nd = A.dia.nd;
+  unsigned cst = (unsigned)A.dia.cst;
+  const double *xr = x + i;
+  asm volatile("" : "+r"(cst), "+l"(xr));
+  double sum = 0.0;
+#pragma unroll
+  for (int c0 = 0; c0 < 32; c0 += 4) {
+    if (c0 >= nd) break;   // (mask bits >= nd are clear)
+    // the batch's offsets as one 16-byte constant read, its constancy bits as
+    // one test: the common all-constant batch runs without per-entry tests
+    const int4 o4 = *reinterpret_cast<const int4 *>(&A.dia.off[c0]);
+    const int o[4] = {o4.x, o4.y, o4.z, o4.w};
+    double xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = ((m >> (c0 + u)) & 1) ? __ldg(xr + o[u]) : 0.0;
+    if (((cst >> c0) & 15u) == 15u) {   // warp-uniform
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sum = __dadd_rn(sum, __dmul_rn(A.dia.val[c0 + u], xv[u]));
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u;
+        if ((cst >> c) & 1)
+          sum = __dadd_rn(sum, __dmul_rn(A.dia.val[c], xv[u]));
+        else
+          sum = spmv_dia_varying(sum, m, c, vp, xv[u]);
+      }
+    }
+  }
+  return sum;
+}
+
 }  // namespace krb

@@ -447,11 +447,11 @@ class DeviceMatrix:
         self.stream_bytes = sb.value
         self.stream_stats = {"nslices": ns.value, "uniform_slices": nu.value, "ndict": nd.value}
         if f_.value == 5:
-            ce, vl, cd = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int()
+            ce, vl, cd, df = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
             _lib.call("krb_matrix_value_stats", h, ctypes.byref(ce), ctypes.byref(vl),
-                      ctypes.byref(cd))
+                      ctypes.byref(cd), ctypes.byref(df))
             self.stream_stats.update(const_entries=ce.value, templates=vl.value,
-                                     const_diagonals=cd.value)
+                                     const_diagonals=cd.value, diagonal_form=bool(df.value))
 
     @property
     def shape(self):

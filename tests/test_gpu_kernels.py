@@ -172,11 +172,39 @@ def test_value_coded_bitwise(dev, n, nvar):
     for c in range(9):
         assert np.array_equal(Y[:, c], S @ X[:, c])
         assert np.array_equal(Yt[:, c], St @ X[:, c])
+    assert M.stream_stats["diagonal_form"] == (n >= 1000)   # 13 diagonals, mostly full
+    with _lib.tuning(value_coding=2):           # the row-template kernel
+        assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), y)
+        assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(), yt)
     with _lib.tuning(value_coding=0):
         M0 = dev.DeviceMatrix(*args, fmt=4)
         assert M0.format == "sell32-dict"
         assert np.array_equal(M0.spmv(_tensor(x)).cpu().numpy(), y)
         assert np.array_equal(M0.spmv(_tensor(x), transpose=True).cpu().numpy(), yt)
+
+
+def test_value_coded_sparse_diagonals_use_row_templates(dev):
+    """Few entries per row spread over many diagonals (less than half of the
+    n x ndict positions filled), and a matrix with more than 32 diagonals:
+    value-coded through the row templates, not the diagonal form."""
+    import scipy.sparse as sp
+    r = np.random.default_rng(4)
+    n = 6000
+    for offs, per_row in ((np.arange(-30, 31, 2), 6), (np.arange(-25, 26), 40)):
+        cval = {int(o): float(r.standard_normal()) for o in offs}
+        kinds = [np.sort(r.choice(offs, size=per_row, replace=False)) for _ in range(6)]
+        rows, cols, vals = [], [], []
+        for i in range(n):
+            for o in kinds[(i // 64) % 6]:
+                if 0 <= i + int(o) < n:
+                    rows.append(i); cols.append(i + int(o)); vals.append(cval[int(o)])
+        S = sp.csr_matrix((np.array(vals), (rows, cols)), shape=(n, n))
+        S.sort_indices()
+        M = dev.DeviceMatrix(n, S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data, fmt=4)
+        assert M.format == "sell32-dict-vc" and not M.stream_stats["diagonal_form"]
+        x = r.standard_normal(n)
+        assert np.array_equal(M.spmv(_tensor(x)).cpu().numpy(), S @ x)
+        assert np.array_equal(M.spmv(_tensor(x), transpose=True).cpu().numpy(), S.T.tocsr() @ x)
 
 
 def test_value_coded_special_values_and_shared_pattern(dev):

@@ -218,7 +218,9 @@ static __device__ __noinline__ double spmv_dia_varying(double sum, unsigned m, i
 // x: the gathered vector (plain read-only loads).  cst and the x pointer are
 // pinned in registers (the compiler otherwise re-reads them from the constant
 // bank before every entry and the kernel ends up bound by the constant cache:
-// 91 % busy, 453 us at C5).
+// 91 % busy, 453 us at C5; with them 340 us, with the batch-level constancy
+// test and uniform-register values 265 us; an unpredicated path for batches
+// whose four entries are all present: 275 us, not kept).
 __device__ __forceinline__ double spmv_row_dia(int64_t i, const krb_matrix &A,
                                                const double *__restrict__ x) {
   const unsigned m = (unsigned)__ldg(reinterpret_cast<const unsigned long long *>(A.tmask) +

@@ -238,9 +238,16 @@ __device__ __forceinline__ double spmv_row_dia(int64_t i, const krb_matrix &A,
     // one test: the common all-constant batch runs without per-entry tests
     const int4 o4 = *reinterpret_cast<const int4 *>(&A.dia.off[c0]);
     const int o[4] = {o4.x, o4.y, o4.z, o4.w};
+    // the four gather addresses are formed unconditionally (offsets through
+    // uniform registers; formed under the entry's predicate they are per-lane
+    // LDC reads and the address-divergence unit becomes the limiter: 82 % busy)
+    const double *px[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) px[u] = xr + o[u];
+    asm volatile("" : "+l"(px[0]), "+l"(px[1]), "+l"(px[2]), "+l"(px[3]));
     double xv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = ((m >> (c0 + u)) & 1) ? __ldg(xr + o[u]) : 0.0;
+    for (int u = 0; u < 4; ++u) xv[u] = ((m >> (c0 + u)) & 1) ? __ldg(px[u]) : 0.0;
     if (((cst >> c0) & 15u) == 15u) {   // warp-uniform
 #pragma unroll
       for (int u = 0; u < 4; ++u) sum = __dadd_rn(sum, __dmul_rn(A.dia.val[c0 + u], xv[u]));

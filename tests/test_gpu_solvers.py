@@ -181,3 +181,39 @@ def test_drivers_bitwise_with_space(pkg, canon, cfg, k, mode):
                                  "rbicgstab", time.perf_counter(), use_graph=mode)
         assert hg.status == ho.status and hg.resid == ho.resid
         assert hg.matvecs == ho.matvecs and np.array_equal(xg, xo)
+
+
+@pytest.mark.parametrize("cfg,k", [("c2", 20), ("c5", 30)])
+def test_value_coding_variants_same_bits(pkg, canon, cfg, k):
+    """The value-coded SpMV kernels (diagonal form, row templates) and the
+    plain offset-coded one inside the graph drivers: RBiCGSTAB and the RBiCG
+    generation solve give the same bits under every setting, equal to the
+    oracle's."""
+    import time
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import _lib, device as D, solvers as S
+    from paper_1406_2831_b200.workloads import make_sequence
+    seq = make_sequence(cfg, small=True)
+    A = seq.matrix(1)
+    Sp = random_space_arrays(A, k, seed=4, ops=canon)
+    b = seq.rhs(1, 0)
+    conf = dict(tol=seq.tol, max_itn=120, seed=2)
+    x_o, h_o = O.rbicgstab(A, b, recycle=Sp, config=O.Config(**conf), ops=canon)
+    xb_o, xbt_o, hb_o, cyc_o = O.rbicg(A, b, b[::-1].copy(), config=O.Config(s=6, **conf),
+                                       ops=canon)
+    for vc in (1, 2, 0):
+        with _lib.tuning(value_coding=vc):
+            M = pkg.SparseMatrix.from_csr(A)
+            dm = D.device_matrix(M)
+            assert dm.format == ("sell32-dict-vc" if vc else "sell32-dict")
+            if vc:
+                assert dm.stream_stats["diagonal_form"] == (vc == 1)
+            x, h = S._device_solve(M, b, None, _space(pkg, Sp), pkg.SolverConfig(**conf),
+                                   "rbicgstab", time.perf_counter(), use_graph=1)
+            assert h.resid == h_o.resid and h.status == h_o.status
+            assert np.array_equal(x, x_o)
+            with _lib.tuning(graph_mode=1):
+                xb, xbt, hb, cyc = pkg.rbicg_solve(M, b, b[::-1].copy(),
+                                                   config=pkg.SolverConfig(s=6, **conf))
+            assert hb.resid == hb_o.resid and np.array_equal(xb, xb_o)
+            assert np.array_equal(xbt, xbt_o) and len(cyc) == len(cyc_o)

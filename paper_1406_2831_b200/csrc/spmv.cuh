@@ -220,7 +220,9 @@ static __device__ __noinline__ double spmv_dia_varying(double sum, unsigned m, i
 // bank before every entry and the kernel ends up bound by the constant cache:
 // 91 % busy, 453 us at C5; with them 340 us, with the batch-level constancy
 // test and uniform-register values 265 us; an unpredicated path for batches
-// whose four entries are all present: 275 us, not kept).
+// whose four entries are all present: 275 us, not kept; unconditional gather
+// addresses: 257 us; a warp-uniform copy of the loop without predicates for
+// warps whose rows have every diagonal: 261 us, not kept).
 __device__ __forceinline__ double spmv_row_dia(int64_t i, const krb_matrix &A,
                                                const double *__restrict__ x) {
   const unsigned m = (unsigned)__ldg(reinterpret_cast<const unsigned long long *>(A.tmask) +

@@ -69,7 +69,7 @@ int krb_set_tuning(const char *key, int64_t value) {
       {"phase_variant", &t.phase_variant}, {"tdot_variant", &t.tdot_variant},
       {"spmv_variant", &t.spmv_variant}, {"spmv_prefetch_mb", &t.spmv_prefetch_mb},
       {"spmm_variant", &t.spmm_variant}, {"phase_pf_rows", &t.phase_pf_rows},
-      {"value_coding", &t.value_coding}, {"fuse_spmv_dot", &t.fuse_spmv_dot}};
+      {"value_coding", &t.value_coding}};
   for (auto &e : table)
     if (strcmp(e.name, key) == 0) {
       *e.slot = (int)value;

@@ -189,111 +189,6 @@ __global__ void __launch_bounds__(256, kMinB) k_iter_spmv(krb_matrix A, const do
   }
 }
 
-// ---- SpMV + projection dots in one kernel (value-coded diagonal form) ------
-// y = A x, then out[j] = (Chat[:, j], y): the value-coded SpMV is bound on
-// chip (issue / L1 gathers, 8 % of the HBM bandwidth in use) and the dots
-// that follow it stream Chat from HBM with little issue pressure, so run back
-// to back each leaves the other resource idle.  Here one 1024-thread CTA per
-// SM walks its canonical blocks; every pass over a group of 8 Chat columns of
-// block b also computes the SpMV rows of one slice of the CTA's NEXT block
-// (elements e of lane l: rows base + 1024 e, the lanes the dots will read
-// them with -- written and later read by the same thread), odd warps rows
-// first and columns second, even warps the other way round, so at any time
-// half of the SM's warps compute rows while the other half streams columns.
-// Same per-row sums (spmv_row_dia) and the same canonical dot order
-// (tdot_unit) as the separate kernels -> the same bits.
-template <int kE, int kCG>
-__device__ __forceinline__ void fused_dot_acc(int64_t n, int k, const double *__restrict__ M,
-                                              int64_t ldm, const double *__restrict__ v,
-                                              int64_t b, int j0, uint64_t pol,
-                                              double (&acc)[kCG]) {
-  const int nj = min(kCG, k - j0);
-  const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
-#pragma unroll
-  for (int c = 0; c < kCG; ++c) acc[c] = 0.0;
-#pragma unroll(kE < 4 ? kE : 4)
-  for (int e = 0; e < kE; ++e) {
-    const int64_t i = base + (int64_t)kLanes * e;
-    if (i < n) {
-      const double vi = v[i];
-      double m[kCG];
-#pragma unroll
-      for (int c = 0; c < kCG; ++c)
-        m[c] = c < nj ? ldg_pol(M + (int64_t)(j0 + c) * ldm + i, pol) : 0.0;
-#pragma unroll
-      for (int c = 0; c < kCG; ++c) acc[c] = __fma_rn(m[c], vi, acc[c]);
-    }
-  }
-}
-
-template <int kE>
-__device__ __forceinline__ void fused_rows(const krb_matrix &A, const double *__restrict__ x,
-                                           double *__restrict__ y, int64_t b, int e0, int e1) {
-  const int64_t base = b * ((int64_t)kLanes * kE) + threadIdx.x;
-  for (int e = e0; e < e1; ++e) {
-    const int64_t i = base + (int64_t)kLanes * e;
-    if (i < A.n) y[i] = spmv_row_dia(i, A, x);
-  }
-}
-
-template <int kE, bool kGamma>
-__global__ void __launch_bounds__(1024, 1) k_spmv_proj_dot(krb_matrix A,
-                                                           const double *__restrict__ x,
-                                                           double *__restrict__ y,
-                                                           const IterArgs *__restrict__ pa) {
-  constexpr int kCG = kTdotCG;
-  const IterArgs &a = *pa;
-  if (a.S->status != KRB_RUNNING) return;
-  ktime_start(a, kGamma ? 6 : 2);
-  __shared__ double red[kTdotCG][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n = a.n, nb = a.nb;
-  const int k = a.k, ng = (k + kCG - 1) / kCG;
-  const uint64_t pol = l2_policy(a.l2keep != 0);
-  double *__restrict__ part = a.part;
-  const bool rows_first = warp & 1;
-  int64_t b = blockIdx.x;
-  if (b < nb) fused_rows<kE>(A, x, y, b, 0, kE);   // the first block's rows up front
-  for (; b < nb; b += gridDim.x) {
-    const int64_t bn = b + gridDim.x;
-    for (int g = 0; g < ng; ++g) {
-      const int e0 = g * kE / ng, e1 = (g + 1) * kE / ng;
-      const int j0 = g * kCG, nj = min(kCG, k - j0);
-      double acc[kCG];
-      if (rows_first) {
-        if (bn < nb) fused_rows<kE>(A, x, y, bn, e0, e1);
-        fused_dot_acc<kE, kCG>(n, k, a.Chat, a.ld, y, b, j0, pol, acc);
-      } else {
-        fused_dot_acc<kE, kCG>(n, k, a.Chat, a.ld, y, b, j0, pol, acc);
-        if (bn < nb) fused_rows<kE>(A, x, y, bn, e0, e1);
-      }
-      int col;
-      double w = warp_tree_multi<kCG>(acc, col);
-      if ((lane & (32 / kCG - 1)) == 0) red[col][warp] = w;
-      __syncthreads();
-      if (warp < nj) {
-        double r = warp_tree(red[warp][lane]);
-        if (lane == 0) part[(int64_t)(j0 + warp) * nb + b] = r;
-      }
-      __syncthreads();
-    }
-  }
-  __shared__ int last_flag;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int prev = atomicAdd(a.counters + kCounterTdotGraph, 1u);
-    last_flag = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last_flag) {
-    __threadfence();
-    tdot_finals<false>(nb, k, part, kGamma ? a.gamma : a.zeta);
-    if (threadIdx.x == 0) a.counters[kCounterTdotGraph] = 0;
-  }
-  ktime_finish(a, kGamma ? 6 : 2);
-}
-
 __global__ void k_init_scalars(SolveScalars *S, double tol, double btol,
                                int64_t max_itn, int k, int64_t mv0) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -382,45 +277,17 @@ static int launch_iter_spmv(const IterArgs &h, const IterArgs *d, cudaStream_t s
   return KRB_OK;
 }
 
-// SpMV + projection dots fused (k_spmv_proj_dot): value-coded diagonal-form
-// matrices with a recycle space, tuning "fuse_spmv_dot"
-static bool use_fused_spmv_dot(const IterArgs &h) {
-  // (1: systems with at least one full-size canonical block per SM; 2: any size)
-  const int f = tuning().fuse_spmv_dot;
-  return f && h.k > 0 && h.nb > 0 && !h.A.pre && h.A.tent && h.A.dia.nd &&
-         tuning().value_coding == 1 && (f == 2 || h.n >= (int64_t)kLanes * 16 * kNumSMs);
-}
-
-template <bool kSecond>
-static int launch_spmv_proj_dot(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
-  const double *x = kSecond ? h.s : h.p;
-  double *y = kSecond ? h.t : h.q;
-  const int grid = (int)(h.nb < kNumSMs ? h.nb : kNumSMs);
-  KRB_DISPATCH_E(canon_E(h.n), (k_spmv_proj_dot<kE, kSecond><<<grid, 1024, 0, st>>>(h.A, x, y, d)));
-  KRB_CHECK_LAUNCH();
-  return KRB_OK;
-}
-
 // one iteration (the graph body).  (Programmatic dependent launches of
 // kernels 2..9 -- CTAs starting in the previous kernel's tail, waiting on
 // griddepcontrol -- measured no faster on C5: 4484-4518 vs 4468-4494 us.)
 static int launch_iteration(const IterArgs &h, const IterArgs *d, cudaStream_t st) {
-  const bool fused = use_fused_spmv_dot(h);
   KRB_TRY(launch_phase<PH_PUPDATE>(h, d, st));
-  if (fused) {
-    KRB_TRY(launch_spmv_proj_dot<false>(h, d, st));
-  } else {
-    KRB_TRY(launch_iter_spmv<false>(h, d, st));
-    KRB_TRY(launch_proj_dot<false>(h, d, st));
-  }
+  KRB_TRY(launch_iter_spmv<false>(h, d, st));
+  KRB_TRY(launch_proj_dot<false>(h, d, st));
   KRB_TRY(launch_phase<PH_PROJ_Q>(h, d, st));
   KRB_TRY(launch_phase<PH_SUPD>(h, d, st));
-  if (fused) {
-    KRB_TRY(launch_spmv_proj_dot<true>(h, d, st));
-  } else {
-    KRB_TRY(launch_iter_spmv<true>(h, d, st));
-    KRB_TRY(launch_proj_dot<true>(h, d, st));
-  }
+  KRB_TRY(launch_iter_spmv<true>(h, d, st));
+  KRB_TRY(launch_proj_dot<true>(h, d, st));
   KRB_TRY(launch_phase<PH_PROJ_T>(h, d, st));
   KRB_TRY(launch_phase<PH_XR>(h, d, st));
   return KRB_OK;
@@ -639,8 +506,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
                    G.variant == tuning().phase_variant + 16 * tuning().tdot_variant +
                                     256 * tuning().spmv_variant +
                                     4096 * tuning().spmv_prefetch_mb +
-                                    (1 << 24) * tuning().value_coding +
-                                    (1 << 27) * tuning().fuse_spmv_dot;
+                                    (1 << 24) * tuning().value_coding;
   h.use_cond = graph ? 1 : 0;
   {
     // evict_last for the recycle blocks (and evict_first for the matrix
@@ -661,7 +527,7 @@ int rbicgstab(krb_context *ctx, const krb_matrix *A, const double *d_b,
     G.ktime = cfg->d_kernel_times;
     G.variant = tuning().phase_variant + 16 * tuning().tdot_variant +
                 256 * tuning().spmv_variant + 4096 * tuning().spmv_prefetch_mb +
-                (1 << 24) * tuning().value_coding + (1 << 27) * tuning().fuse_spmv_dot;
+                (1 << 24) * tuning().value_coding;
     h.cond = G.cond;
   }
   // the descriptor is written in stream order (the previous solve on this

@@ -99,7 +99,6 @@ struct Tuning {
   int phase_pf_rows = 1;     // graph P / S / X: L2 prefetch distance (1024-element rows)
   int spmv_variant = 0;   // offset-coded SpMV: 0 = uniform offsets by warp shuffle, 1 = int4 loads
   int value_coding = 1;   // value tables of constant diagonals: 0 = neither built nor used
-  int fuse_spmv_dot = 0;  // graph iteration: SpMV + projection dots in one kernel (value-coded)
 };
 Tuning &tuning();
 

@@ -217,29 +217,3 @@ def test_value_coding_variants_same_bits(pkg, canon, cfg, k):
                                                    config=pkg.SolverConfig(s=6, **conf))
             assert hb.resid == hb_o.resid and np.array_equal(xb, xb_o)
             assert np.array_equal(xbt, xbt_o) and len(cyc) == len(cyc_o)
-
-
-@pytest.mark.parametrize("cfg,k", [("c1", 10), ("c2", 20), ("c5", 30), ("c5", 3)])
-def test_fused_spmv_proj_dot_same_bits(pkg, canon, cfg, k):
-    """The fused SpMV + projection-dot kernel of the graph iteration (one
-    1024-thread CTA per SM, rows of the next block computed under the column
-    stream of the current one) against the separate kernels and the oracle:
-    same histories, same solutions, including max_itn / half-step exits."""
-    import time
-    from oracle import krylov as O
-    from paper_1406_2831_b200 import _lib, solvers as S
-    from paper_1406_2831_b200.workloads import make_sequence
-    seq = make_sequence(cfg, small=True)
-    A = seq.matrix(1)
-    Sp = random_space_arrays(A, k, seed=11, ops=canon)
-    for max_itn, seed in ((150, 1), (7, 2)):
-        b = seq.rhs(1, 0)
-        conf = dict(tol=seq.tol, max_itn=max_itn, seed=seed)
-        x_o, h_o = O.rbicgstab(A, b, recycle=Sp, config=O.Config(**conf), ops=canon)
-        for fuse in (2, 0):
-            with _lib.tuning(fuse_spmv_dot=fuse):
-                x, h = S._device_solve(pkg.SparseMatrix.from_csr(A), b, None, _space(pkg, Sp),
-                                       pkg.SolverConfig(**conf), "rbicgstab",
-                                       time.perf_counter(), use_graph=1)
-            assert h.status == h_o.status and h.resid == h_o.resid
-            assert h.matvecs == h_o.matvecs and np.array_equal(x, x_o)

@@ -86,6 +86,7 @@ struct krb_matrix {
   // order; constants and offsets from `dia`
   uint64_t *tmask = nullptr;   // pattern
   krb_diatable dia;            // matrix
+  int64_t uid = 0;             // creation serial (the graph cache keys the by-value table on it)
   krb_matrix *T = nullptr;  // lazily built transpose
   // the structure arrays above (rp, ci, sl_ptr, rlen, s_col, perm, dcode,
   // dptr, dict) belong to this reference-counted pattern, shared by every
@@ -119,6 +120,7 @@ void dev_free(void *p, cudaStream_t st);
 struct MatrixSig {
   const void *p[28];
   int64_t n = -1, serial = 0;
+  int64_t uid = 0;   // of a matrix whose diagonal table travels by value in kernel parameters
   int format = -1;
 };
 MatrixSig matrix_sig(const krb_matrix *A);

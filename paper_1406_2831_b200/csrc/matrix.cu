@@ -22,6 +22,7 @@
 #include <cub/cub.cuh>
 #include <cstring>
 #include <mutex>
+#include <atomic>
 #include <vector>
 
 #include "krb_internal.cuh"
@@ -84,6 +85,11 @@ __global__ void __launch_bounds__(256) k_spmv(krb_matrix A,
   y[(kSell && A.perm) ? A.perm[i] : i] = spmv_row<kSell>(i, A, x);
 }
 
+static int64_t next_uid() {
+  static std::atomic<int64_t> c{0};
+  return ++c;
+}
+
 MatrixSig matrix_sig(const krb_matrix *A) {
   MatrixSig g;
   memset(g.p, 0, sizeof(g.p));
@@ -98,11 +104,15 @@ MatrixSig matrix_sig(const krb_matrix *A) {
   g.n = A->n;
   g.format = A->format;
   g.serial = precond_serial(A->pre);
+  // the diagonal table is baked into a captured graph's kernel parameters BY
+  // VALUE: another matrix at the same addresses (freed and re-allocated
+  // arrays) with other constants must not reuse that graph
+  g.uid = B->dia.nd ? B->uid : 0;
   return g;
 }
 
 bool same_sig(const MatrixSig &a, const MatrixSig &b) {
-  return a.n == b.n && a.format == b.format && a.serial == b.serial &&
+  return a.n == b.n && a.format == b.format && a.serial == b.serial && a.uid == b.uid &&
          memcmp(a.p, b.p, sizeof(a.p)) == 0;
 }
 
@@ -1158,6 +1168,7 @@ int matrix_create(krb_matrix **out, int64_t n, int64_t nnz,
   A->n = n;
   A->nnz = nnz;
   A->req_format = format;
+  A->uid = next_uid();
   if (krb_pattern *P = pattern_find(n, nnz, format, d_rp, d_ci32, d_ci64, st)) {
     pattern_attach(A, P);
     cudaError_t e = dev_alloc((void **)&A->val, sizeof(double) * (nnz > 0 ? nnz : 1), st);
@@ -1272,6 +1283,7 @@ int ensure_transpose(krb_matrix *A, cudaStream_t st) {
     krb_matrix *T = new krb_matrix();
     T->n = n;
     T->nnz = nnz;
+    T->uid = next_uid();
     T->req_format = P->tpat->req_format;
     pattern_attach(T, P->tpat);
     KRB_CHECK_CUDA(dev_alloc((void **)&T->val, sizeof(double) * (nnz > 0 ? nnz : 1), st));

@@ -217,3 +217,31 @@ def test_value_coding_variants_same_bits(pkg, canon, cfg, k):
                                                    config=pkg.SolverConfig(s=6, **conf))
             assert hb.resid == hb_o.resid and np.array_equal(xb, xb_o)
             assert np.array_equal(xbt, xbt_o) and len(cyc) == len(cyc_o)
+
+
+def test_graph_cache_not_reused_for_other_constants(pkg, canon):
+    """The value-coded diagonal table travels BY VALUE in the captured
+    graph's kernel parameters: a later matrix with the same pattern and sizes
+    but other constants -- possibly at the very addresses of the freed arrays
+    of the first -- must get its own graph (each solve equals the oracle)."""
+    import gc
+    import time
+    from oracle import krylov as O
+    from paper_1406_2831_b200 import device as D, solvers as S
+    from paper_1406_2831_b200.workloads import CSR, make_sequence
+    seq = make_sequence("c5", small=True)
+    A1 = seq.matrix(1)
+    b = seq.rhs(1, 0)
+    conf = dict(tol=seq.tol, max_itn=60, seed=3)
+    mats = [A1, CSR(A1.n, A1.row_ptr, A1.col_idx, A1.values * 1.5),
+            CSR(A1.n, A1.row_ptr, A1.col_idx, A1.values * 0.75), A1]
+    for A in mats:
+        x_o, h_o = O.bicgstab(A, b, config=O.Config(**conf), ops=canon)
+        M = pkg.SparseMatrix.from_csr(A)
+        assert D.device_matrix(M).stream_stats.get("diagonal_form")
+        x, h = S._device_solve(M, b, None, None, pkg.SolverConfig(**conf), "bicgstab",
+                               time.perf_counter(), use_graph=1)
+        assert h.resid == h_o.resid and np.array_equal(x, x_o)
+        del M
+        D.MATRICES.clear()
+        gc.collect()

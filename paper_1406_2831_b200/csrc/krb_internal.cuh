@@ -67,7 +67,8 @@ struct krb_matrix {
   int32_t *tlen = nullptr;
   uint8_t *tcode = nullptr;
   int ntmpl = 0, tstride = 0;   // tstride: longest template, rounded up to 4
-  int64_t *code_count = nullptr;   // HOST array (256): entries per offset code
+  int64_t *code_count = nullptr;   // HOST array: [0, 256) entries per offset code,
+                                   // [256, 512) the offsets themselves (pattern)
   // value-coded format (matrix level, built beside s_val when most entries
   // lie on diagonals col - row whose values are all bit-identical:
   // constant-coefficient stencils, where only the main diagonal of s E - K

@@ -834,7 +834,12 @@ static int build_templates(krb_matrix *A, cudaStream_t st) {
   unsigned long long *rows_of = nullptr;
   int *ok = nullptr;
   if (nt >= 1 && nt <= kMaxTemplates && h_num[1] <= 64) {
-    auto chk = [&](cudaError_t e) { if (e != cudaSuccess && rc == KRB_OK) { set_error("build_templates: %s", cudaGetErrorString(e)); rc = KRB_ECUDA; } };
+    auto chk = [&](cudaError_t e) {
+      if (e != cudaSuccess && rc == KRB_OK) {
+        set_error("build_templates: %s", cudaGetErrorString(e));
+        rc = KRB_ECUDA;
+      }
+    };
     chk(dev_alloc((void **)&A->tid, sizeof(int32_t) * n, st));
     chk(dev_alloc((void **)&A->tlen, sizeof(int32_t) * nt, st));
     chk(dev_alloc((void **)&A->tcode, 64 * (size_t)nt, st));
@@ -847,17 +852,21 @@ static int build_templates(krb_matrix *A, cudaStream_t st) {
       const int one = 1;
       chk(cudaMemcpyAsync(ok, &one, sizeof(int), cudaMemcpyHostToDevice, st));
       k_row_tid<<<rb, 256, 0, st>>>(n, hash, uniq, nt, A->tid, rep_row);
-      k_tmpl_fill<<<nt, 64, 0, st>>>(nt, rep_row, A->rp, A->ci, A->dict, A->ndict, A->tlen, A->tcode);
-      k_tmpl_verify<<<rb, 256, 0, st>>>(n, A->rp, A->ci, A->dict, A->tid, A->tlen, A->tcode, rows_of, ok);
+      k_tmpl_fill<<<nt, 64, 0, st>>>(nt, rep_row, A->rp, A->ci, A->dict, A->ndict, A->tlen,
+                                     A->tcode);
+      k_tmpl_verify<<<rb, 256, 0, st>>>(n, A->rp, A->ci, A->dict, A->tid, A->tlen, A->tcode,
+                                        rows_of, ok);
       launch_counter() += 3;
       chk(cudaGetLastError());
       std::vector<int32_t> h_len(nt);
       std::vector<uint8_t> h_code(64 * (size_t)nt);
       std::vector<unsigned long long> h_rows(nt);
       int h_ok = 0;
-      chk(cudaMemcpyAsync(h_len.data(), A->tlen, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(h_len.data(), A->tlen, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost,
+                          st));
       chk(cudaMemcpyAsync(h_code.data(), A->tcode, 64 * (size_t)nt, cudaMemcpyDeviceToHost, st));
-      chk(cudaMemcpyAsync(h_rows.data(), rows_of, sizeof(unsigned long long) * nt, cudaMemcpyDeviceToHost, st));
+      chk(cudaMemcpyAsync(h_rows.data(), rows_of, sizeof(unsigned long long) * nt,
+                          cudaMemcpyDeviceToHost, st));
       chk(cudaMemcpyAsync(&h_ok, ok, sizeof(int), cudaMemcpyDeviceToHost, st));
       chk(cudaStreamSynchronize(st));
       if (rc == KRB_OK && h_ok) {
@@ -871,6 +880,7 @@ static int build_templates(krb_matrix *A, cudaStream_t st) {
           for (int j = 0; j < h_len[t]; ++j) {
             const int code = h_code[64 * (size_t)t + j];
             A->code_count[code] += (int64_t)h_rows[t];
+            // (strictly ascending codes <=> the row is sorted by column)
             if (j > 0 && code <= h_code[64 * (size_t)t + j - 1]) sorted_rows = false;
             if (code < 64) h_mask[t] |= 1ull << code;
           }
@@ -899,9 +909,11 @@ static int build_templates(krb_matrix *A, cudaStream_t st) {
       for (void *p : {(void *)A->tid, (void *)A->tlen, (void *)A->tcode, (void *)A->tmask})
         if (p) dev_free(p, st);
       A->tid = nullptr; A->tlen = nullptr; A->tcode = nullptr; A->tmask = nullptr;
+      A->ntmpl = 0;
     }
   }
-  for (void *p : {(void *)hash, (void *)uniq, (void *)d_num, (void *)rep_row, (void *)rows_of, (void *)ok})
+  for (void *p : {(void *)hash, (void *)uniq, (void *)d_num, (void *)rep_row, (void *)rows_of,
+                  (void *)ok})
     if (p) dev_free(p, st);
   return rc;
 }

@@ -3,7 +3,7 @@ per system the time spent in each statement of the step (matrix adoption,
 prefetch issue, refresh, solve incl. upload of b and read-back of x), without
 extra synchronisations, next to the device-resident step of the value arm.
 
-    python tools/e2e_step_timeline.py
+    python tools/e2e_step_timeline.py [--pageable]
 """
 import json
 import os
@@ -19,6 +19,7 @@ def main():
     import bench as B
     import paper_1406_2831_b200 as P
     from paper_1406_2831_b200 import device as D, workloads as W
+    pageable = "--pageable" in sys.argv
     wl = B.Workload("c5")
     cfgs = [P.SolverConfig(tol=wl.seq.tol, max_itn=wl.seq.max_itn, k=wl.k, s=wl.seq.s, seed=j + 1)
             for j in range(len(wl.keys))]
@@ -28,8 +29,12 @@ def main():
         if id(a) not in cache:
             cache[id(a)] = D.pinned_copy(a)
         return cache[id(a)]
-    mats = {i: W.CSR(A.n, pin(A.row_ptr), pin(A.col_idx), pin(A.values)) for i, A in wl.mats.items()}
-    rhs = {key: D.pinned_copy(b) for key, b in wl.rhs.items()}
+    if pageable:
+        mats, rhs = wl.mats, wl.rhs
+    else:
+        mats = {i: W.CSR(A.n, pin(A.row_ptr), pin(A.col_idx), pin(A.values))
+                for i, A in wl.mats.items()}
+        rhs = {key: D.pinned_copy(b) for key, b in wl.rhs.items()}
     i0 = wl.keys[0][0]
     space0 = P.biorthonormalize(wl.U0, wl.Ut0, P.SparseMatrix.from_csr(mats[i0]))
     D.MATRICES.clear()

@@ -366,7 +366,8 @@ def gpu_arm(args, wl, rank, world):
                                                for h in hists)},
            "space_k_last": sp.k,
            "histories_head": {str(j): [float(v) for v in hists[j].resid[:51]]
-                              for j in (0, len(hists) - 1)}}
+                              for j in (0, len(hists) - 1)},
+           "matvecs_head": [int(v) for v in hists[0].matvecs[:51]]}
     B_it = W.bytes_per_iteration(wl.n, wl.nnz, wl.k)
     us_it = 1e6 * sum(times) / max(its, 1)
     out["iteration"] = {"us_per_iteration_incl_setup_refresh": round(us_it, 1),
@@ -576,7 +577,8 @@ def cpu_sample(wl, iters, steps):
                       f"BLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'all')}",
             "seconds": round(loop_s, 3), "iterations": its,
             "seconds_incl_setup": round(wall, 3),
-            "space_build_s": round(t_space, 2)}
+            "space_build_s": round(t_space, 2),
+            "_resid": [float(v) for v in h.resid], "_matvecs": [int(v) for v in h.matvecs]}
 
 
 def main():
@@ -589,6 +591,8 @@ def main():
         wl = Workload(args.config, args.systems)
         cpu_sample(wl, 1, max(args.warmup, 0)) if args.warmup else None
         samp = cpu_sample(wl, args.cpu_iters, max(args.steps, 1))
+        samp.pop("_resid", None)
+        samp.pop("_matvecs", None)
         v = samp["value"]
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s",
@@ -612,6 +616,25 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_sample(wl, args.cpu_iters, 2)
+        parity = None
+        if cpu is not None:
+            # the CPU arm's residual history (the reference's algorithm, its
+            # own space built on the CPU from the same seeded basis) against
+            # the GPU arm's history of the same system over the common prefix
+            c_res, c_mv = cpu.pop("_resid"), cpu.pop("_matvecs")
+            g_res = res.get("histories_head", {}).get("0", [])
+            m = min(len(c_res), len(g_res))
+            if m:
+                parity = {"system": wl.keys[0][0], "residuals_compared": m,
+                          "max_rel_history_diff": max(abs(a - b) / abs(b) for a, b in
+                                                      zip(g_res[:m], c_res[:m])),
+                          "cpu_matvecs": c_mv[:m],
+                          "gpu_matvecs": res.get("matvecs_head", [])[:m],
+                          "note": "GPU arm vs CPU arm (oracle RefOps = krecycle's own calls) "
+                                  "of this run; each arm biorthonormalizes the same seeded "
+                                  "random basis pair itself, so the spaces already differ in "
+                                  "the last bits (the full-size parity tests use low-"
+                                  "amplification spaces and the reference's own envelope)"}
         line = {"metric": METRIC, "value": res["iters_all"] / res["t_total"],
                 "unit": "iters/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * res["t_total"] / args.steps,
@@ -619,7 +642,8 @@ def main():
                 "dtype": "f64", "data": "synthetic", "config": wl.config(world),
                 "iterations_per_step": res["iters"] / args.steps,
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
-                "e2e": res["e2e"], "roofline": res["roofline"], "cpu_baseline": cpu}
+                "e2e": res["e2e"], "roofline": res["roofline"], "cpu_baseline": cpu,
+                "parity": parity}
         if not all(res.get("checks", {}).values()):
             print("bench: a timed solve did not converge to tol -- the number is not "
                   "valid", file=sys.stderr)

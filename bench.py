@@ -453,7 +453,10 @@ def e2e_arm(args, wl, space0, cfgs, flush, barrier, world, pinned):
         sms = {}
         for j, (i, kap) in enumerate(wl.keys):
             if i != last_i:
-                A = sms.pop(i, None) or P.SparseMatrix.from_csr(mats[i])
+                A = sms.pop(i, None)
+                if A is None:
+                    A = P.SparseMatrix.from_csr(mats[i])
+                    P.prefetch_matrix(A)   # its own upload queued ahead of the next one's
                 nxt = order.index(i) + 1
                 if nxt < len(order):
                     sms[order[nxt]] = P.SparseMatrix.from_csr(mats[order[nxt]])

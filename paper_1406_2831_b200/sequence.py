@@ -128,7 +128,14 @@ def run_sequence(seq, k=None, s=None, tol=None, max_itn=None, seed=0,
     for i in range(seq.num_matrices):
         if gidx >= total:
             break
-        A = A_next if A_next is not None else api.SparseMatrix.from_csr(seq.matrix(i))
+        if A_next is not None:
+            A = A_next
+        else:
+            A = api.SparseMatrix.from_csr(seq.matrix(i))
+            if prefetch is not None:
+                # queue this matrix's own upload first: the next matrix's
+                # prefetch below must not share the link with it
+                prefetch(A)
         A_next = None
         if prefetch is not None and i + 1 < seq.num_matrices and \
                 gidx + min(seq.rhs_per_matrix, total - gidx) < total:

@@ -50,7 +50,10 @@ def main():
             row = {"sys": i}
             t = time.perf_counter()
             if i != last_i:
-                A = sms.pop(i, None) or P.SparseMatrix.from_csr(mats[i])
+                A = sms.pop(i, None)
+                if A is None:
+                    A = P.SparseMatrix.from_csr(mats[i])
+                    P.prefetch_matrix(A)
                 nxt = order.index(i) + 1
                 if nxt < len(order):
                     sms[order[nxt]] = P.SparseMatrix.from_csr(mats[order[nxt]])

@@ -223,7 +223,8 @@ static __device__ __noinline__ double spmv_dia_varying(double sum, unsigned m, i
 // whose four entries are all present: 275 us, not kept; unconditional gather
 // addresses: 257 us; a warp-uniform copy of the loop without predicates for
 // warps whose rows have every diagonal: 261 us, not kept; batches of 8
-// diagonals (40 registers): 337 us, not kept).
+// diagonals (40 registers, 48 instead of 64 warps per SM): 337 us, not kept;
+// prefetch.global.L1 of the next batch's gathers: 283 us, not kept).
 __device__ __forceinline__ double spmv_row_dia(int64_t i, const krb_matrix &A,
                                                const double *__restrict__ x) {
   const unsigned m = (unsigned)__ldg(reinterpret_cast<const unsigned long long *>(A.tmask) +
